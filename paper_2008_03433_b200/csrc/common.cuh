@@ -1,0 +1,90 @@
+// Shared device helpers: deterministic warp/block reductions and the
+// "last block finalizes" ticket used by every two-stage reduction.
+//
+// Determinism contract (the device analogue of the reference's fixed
+// 64-block partition + pairwise tree, proj/include/tron/parallel.hpp:14-34):
+// every reduction's shape depends only on the problem size and the launch
+// configuration (fixed per device), never on timing, so repeated runs are
+// bit-identical.  No floating-point atomics anywhere.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tb {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;  // valid in lane 0
+}
+
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;  // identical in every lane (fixed butterfly order)
+}
+
+// Sum over a power-of-two lane group of width G (G <= 32), result in the
+// group's first lane.
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, G);
+  return v;
+}
+
+// Block-wide sum; result valid in thread 0 (and returned to all threads
+// when `broadcast`).  `sh` needs BLOCK/32 + 1 doubles.
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v, double* sh, bool broadcast = false) {
+  constexpr int NW = BLOCK / kWarp;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < NW ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[NW] = t;
+  }
+  __syncthreads();
+  double r = broadcast ? sh[NW] : (threadIdx.x == 0 ? sh[NW] : 0.0);
+  if (broadcast) __syncthreads();
+  return r;
+}
+
+// Ticket: returns true in exactly one block (the last to arrive) after all
+// blocks have published their partials.  The ticket is reset for reuse.
+__device__ __forceinline__ bool last_block_arrive(unsigned int* ticket) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(ticket, 1u);
+    am_last = (t == gridDim.x - 1);
+    if (am_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last;
+}
+
+// Fixed-order reduction of `count` partials laid out with stride `stride`
+// (component c of block b at partials[b*stride + c]).  Called by one block.
+template <int BLOCK>
+__device__ __forceinline__ double reduce_partials(const double* partials, int count, int stride,
+                                                  int c, double* sh) {
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < count; b += BLOCK) acc += __ldcg(partials + (size_t)b * stride + c);
+  return block_sum<BLOCK>(acc, sh, true);
+}
+
+#define TB_LAUNCH_CHECK() \
+  do {                    \
+  } while (0)
+
+}  // namespace tb

@@ -1,0 +1,975 @@
+// Host orchestration of the B200 TRON hot path: device layout, the
+// evaluator operations (backend.cpp:136-306 semantics), the device-resident
+// truncated CG captured as a CUDA graph with a while node, and the
+// device-mode outer trust-region loop (tron.cpp:127-217 control flow with
+// only scalars crossing PCIe).
+#include "engine.h"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+namespace tb {
+
+[[noreturn]] void raise(int status, const std::string& msg) { throw StatusError(status, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();  // clear sticky-less errors
+  const int st = (e == cudaErrorMemoryAllocation) ? TRON_ERR_OOM : TRON_ERR_CUDA;
+  raise(st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ----------------------------------------------------------------------------
+// NCCL (dlopen'd so single-GPU use never needs it)
+// ----------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      lib = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+      if (lib) break;
+    }
+    if (!lib) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
+    AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(lib, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && AllReduce && CommDestroy;
+  }
+};
+NcclApi g_nccl;
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return;
+  raise(TRON_ERR_NCCL, std::string(what) + ": " +
+                           (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
+}
+}  // namespace
+
+int nccl_unique_id(void* out128) {
+  if (!g_nccl.load()) raise(TRON_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out128, &id, sizeof(id));
+  return TRON_OK;
+}
+
+void Comm::init(int rank_, int world_, const void* unique_id, int device) {
+  rank = rank_;
+  world = world_;
+  if (world <= 1) return;
+  if (!unique_id) raise(TRON_ERR_ARGUMENT, "world > 1 requires an nccl_unique_id");
+  if (!g_nccl.load()) raise(TRON_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  ncclComm_t c;
+  nccl_check(g_nccl.CommInitRank(&c, world, id, rank), "ncclCommInitRank");
+  comm_ = c;
+}
+
+Comm::~Comm() {
+  if (comm_ && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)comm_);
+}
+
+void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
+  if (world <= 1 || count == 0) return;
+  nccl_check(g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)comm_, s),
+             "ncclAllReduce");
+}
+
+// ----------------------------------------------------------------------------
+// creation + validation (FeatureMatrix::csr linalg.cpp:34-73; Problem::validate loss.cpp:20-33)
+// ----------------------------------------------------------------------------
+namespace {
+
+void validate_labels_C(uint64_t l, const double* y, double C) {
+  for (uint64_t i = 0; i < l; ++i) {
+    const double v = y[i];
+    if (v != 1.0 && v != -1.0)
+      raise(TRON_ERR_DIMENSION, "problem: label " + std::to_string(v) + " not in {-1,+1}");
+  }
+  if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");
+}
+
+void validate_csr(uint64_t l, uint64_t n, const int64_t* ro, const int32_t* ci) {
+  if (ro[0] != 0) raise(TRON_ERR_DIMENSION, "csr matrix: offsets/indices/values disagree");
+  for (uint64_t i = 0; i < l; ++i) {
+    if (ro[i] > ro[i + 1])
+      raise(TRON_ERR_DIMENSION, "csr matrix: decreasing row offset at row " + std::to_string(i));
+    int32_t prev = -1;
+    for (int64_t k = ro[i]; k < ro[i + 1]; ++k) {
+      const int32_t c = ci[k];
+      if (c < 0 || static_cast<uint64_t>(c) >= n)
+        raise(TRON_ERR_BOUNDS, "csr matrix: column " + std::to_string(c) + " out of range in row " +
+                                   std::to_string(i));
+      if (c <= prev)
+        raise(TRON_ERR_DIMENSION,
+              "csr matrix: column indices not strictly ascending in row " + std::to_string(i));
+      prev = c;
+    }
+  }
+}
+
+void check_options(int loss, const tron_gpu_options& opt) {
+  if (loss != TRON_LOSS_LOGISTIC && loss != TRON_LOSS_L2SVM)
+    raise(TRON_ERR_ARGUMENT, "unknown loss kind");
+  if (opt.svm_strategy != TRON_SVM_GATHERED && opt.svm_strategy != TRON_SVM_INDIRECT)
+    raise(TRON_ERR_DIMENSION, "plan: unknown svm strategy");
+  if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world)
+    raise(TRON_ERR_ARGUMENT, "invalid rank/world");
+}
+
+}  // namespace
+
+void Engine::common_alloc() {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "cudaStreamCreate");
+  sc_partials_.alloc(kMaxPartialBlocks * 4);
+  sc_tickets_.alloc(kNumTickets);
+  cuda_check(cudaMemset(sc_tickets_.p, 0, sc_tickets_.bytes()), "memset");
+  sc_.partials = sc_partials_.p;
+  sc_.tickets = sc_tickets_.p;
+  cuda_check(cudaMalloc(&obj_d_, sizeof(ObjScalars)), "cudaMalloc");
+  cuda_check(cudaMemset(obj_d_, 0, sizeof(ObjScalars)), "memset");
+  cuda_check(cudaMallocHost(&obj_h_, sizeof(ObjScalars)), "cudaMallocHost");
+  cuda_check(cudaMalloc(&st_d_, sizeof(CgState)), "cudaMalloc");
+  cuda_check(cudaMemset(st_d_, 0, sizeof(CgState)), "memset");
+  cuda_check(cudaMallocHost(&st_h_, sizeof(CgState)), "cudaMallocHost");
+  std::memset(obj_h_, 0, sizeof(ObjScalars));
+  std::memset(st_h_, 0, sizeof(CgState));
+
+  const size_t nn = n_ > 0 ? n_ : 1, ll = l_ > 0 ? l_ : 1;
+  for (auto& S : slot_) {
+    S.w.alloc(nn);
+    S.z.alloc(ll);
+    if (loss_ == TRON_LOSS_LOGISTIC) {
+      S.zhat.alloc(ll);
+      S.dvec.alloc(ll);
+    } else {
+      S.mask.alloc(ll);
+    }
+  }
+  for (DevBuf<double>* b : {&g_, &M_, &d_, &r0_, &r1_, &p_, &hp_, &vtmp_, &otmp_}) b->alloc(nn);
+  if (comm_.active()) raw_.alloc(nn);
+  if (!dense_) a_.alloc(ll);
+  if (dense_) parts_.alloc((size_t)dense_grid(l_) * nn);
+  small_engine_ = dense_ || n_ <= kSmallCgMaxN;
+  use_graphs_ = !comm_.active();
+}
+
+std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, const int64_t* ro,
+                                           const int32_t* ci, const double* vals, const double* y,
+                                           double C, const tron_gpu_options& opt) {
+  check_options(loss, opt);
+  if (!ro || !y || (l > 0 && ro[l] > 0 && (!ci || !vals)))
+    raise(TRON_ERR_ARGUMENT, "null problem array");
+  validate_csr(l, n, ro, ci);
+  validate_labels_C(l, y, C);
+  const int64_t nnz = ro[l];
+  if (nnz >= (int64_t{1} << 31) || n >= (uint64_t{1} << 31) || l >= (uint64_t{1} << 31))
+    raise(TRON_ERR_DIMENSION,
+          "csr shard exceeds int32 indexing (nnz, rows, cols < 2^31 per GPU); shard across more "
+          "GPUs");
+  if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
+    raise(TRON_ERR_STRATEGY,
+          "gathered L2-SVM strategy needs dense features on the GPU backend; use Indirect "
+          "(masked CSR/CSC traversal)");
+  std::unique_ptr<Engine> e(new Engine());
+  e->loss_ = loss;
+  e->dense_ = false;
+  e->l_ = (int64_t)l;
+  e->n_ = (int64_t)n;
+  e->C_ = C;
+  e->device_ = opt.device;
+  e->svm_strategy_ = opt.svm_strategy;
+  e->budget_ = opt.gathered_budget_bytes;
+  e->row_begin_ = opt.row_begin;
+  e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
+  e->common_alloc();
+  cudaStream_t s = e->s_;
+
+  e->rptr_.alloc(l + 1);
+  e->cidx_.alloc(nnz);
+  e->rval_.alloc(nnz);
+  e->cptr_.alloc(n + 1);
+  e->ridx_.alloc(nnz);
+  e->cval_.alloc(nnz);
+  e->y_.alloc(l > 0 ? l : 1);
+  {
+    DevBuf<int64_t> ro64;
+    ro64.alloc(l + 1);
+    cuda_check(cudaMemcpy(ro64.p, ro, (l + 1) * sizeof(int64_t), cudaMemcpyHostToDevice), "H2D");
+    narrow_offsets(ro64.p, e->rptr_.p, (int64_t)(l + 1), s);
+    if (nnz > 0) {
+      cuda_check(cudaMemcpyAsync(e->cidx_.p, ci, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s),
+                 "H2D");
+      cuda_check(cudaMemcpyAsync(e->rval_.p, vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s),
+                 "H2D");
+    }
+    if (l > 0)
+      cuda_check(cudaMemcpyAsync(e->y_.p, y, l * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaStreamSynchronize(s), "upload");
+  }
+  e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
+  const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
+  if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
+  e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
+  const int32_t tiles = merge_num_tiles(n, nnz);
+  e->tile_row_.alloc(tiles + 1);
+  e->tile_nz_.alloc(tiles + 1);
+  e->fix_chain_.alloc(tiles > 0 ? tiles : 1);
+  e->head_.alloc(tiles > 0 ? tiles : 1);
+  e->carry_.alloc(tiles > 0 ? tiles : 1);
+  merge_plan_build(e->Xt_, e->tile_row_.p, e->tile_nz_.p, e->fix_chain_.p, tiles, s);
+  e->plan_ = MergeView{tiles, e->tile_row_.p, e->tile_nz_.p, e->fix_chain_.p, e->head_.p,
+                       e->carry_.p};
+  e->group_ = choose_group((int64_t)l, nnz);
+  cuda_check(cudaStreamSynchronize(s), "csc build");
+  cuda_check(cudaGetLastError(), "csc build");
+  return e;
+}
+
+std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
+                                             const double* row_major, const double* y, double C,
+                                             const tron_gpu_options& opt) {
+  check_options(loss, opt);
+  if (!y || (l * n > 0 && !row_major)) raise(TRON_ERR_ARGUMENT, "null problem array");
+  validate_labels_C(l, y, C);
+  if (n > (uint64_t)kDenseMaxN) {
+    // Wide dense problems run through the sparse kernels (explicit entries).
+    if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
+      raise(TRON_ERR_STRATEGY, "gathered L2-SVM strategy supports n <= 64 dense features on GPU");
+    std::vector<int64_t> ro(l + 1);
+    std::vector<int32_t> ci(l * n);
+    for (uint64_t i = 0; i <= l; ++i) ro[i] = (int64_t)(i * n);
+    for (uint64_t i = 0; i < l; ++i)
+      for (uint64_t j = 0; j < n; ++j) ci[i * n + j] = (int32_t)j;
+    return create_csr(loss, l, n, ro.data(), ci.data(), row_major, y, C, opt);
+  }
+  if (l >= (uint64_t{1} << 31)) raise(TRON_ERR_DIMENSION, "dense shard exceeds 2^31 rows per GPU");
+  std::unique_ptr<Engine> e(new Engine());
+  e->loss_ = loss;
+  e->dense_ = true;
+  e->l_ = (int64_t)l;
+  e->n_ = (int64_t)n;
+  e->C_ = C;
+  e->device_ = opt.device;
+  e->svm_strategy_ = opt.svm_strategy;
+  e->budget_ = opt.gathered_budget_bytes;
+  e->row_begin_ = opt.row_begin;
+  e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
+  e->common_alloc();
+  cudaStream_t s = e->s_;
+  e->ld_ = (int64_t)((l + 3) / 4 * 4);
+  e->Xc_.alloc((size_t)e->ld_ * (n > 0 ? n : 1));
+  e->y_.alloc(l > 0 ? l : 1);
+  if (l > 0) {
+    cuda_check(cudaMemcpyAsync(e->y_.p, y, l * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    // chunked row-major upload + on-device transpose to column-major
+    const int64_t chunk_rows =
+        std::max<int64_t>(1, (int64_t{64} << 20) / (int64_t)(sizeof(double) * std::max<uint64_t>(n, 1)));
+    DevBuf<double> stage[2];
+    stage[0].alloc((size_t)chunk_rows * n);
+    stage[1].alloc((size_t)chunk_rows * n);
+    cudaEvent_t ev[2];
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    int k = 0;
+    bool used[2] = {false, false};
+    for (int64_t r0 = 0; r0 < (int64_t)l; r0 += chunk_rows, k ^= 1) {
+      const int64_t rows = std::min<int64_t>(chunk_rows, (int64_t)l - r0);
+      if (used[k]) cudaEventSynchronize(ev[k]);
+      cuda_check(cudaMemcpyAsync(stage[k].p, row_major + (size_t)r0 * n, rows * n * sizeof(double),
+                                 cudaMemcpyHostToDevice, s),
+                 "H2D");
+      dense_transpose_chunk(stage[k].p, rows, n, e->Xc_.p, e->ld_, r0, s);
+      cudaEventRecord(ev[k], s);
+      used[k] = true;
+    }
+    cuda_check(cudaStreamSynchronize(s), "dense upload");
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  }
+  if (loss == TRON_LOSS_L2SVM) {
+    e->idx_.alloc(l > 0 ? l : 1);
+    e->idx_tmp_.alloc((l + 1023) / 1024 + 2);
+    e->count_.alloc(1);
+  }
+  cuda_check(cudaGetLastError(), "dense create");
+  return e;
+}
+
+Engine::~Engine() {
+  if (s_) cudaStreamSynchronize(s_);
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      if (graph_exec_[a][b]) cudaGraphExecDestroy(graph_exec_[a][b]);
+      if (graph_[a][b]) cudaGraphDestroy(graph_[a][b]);
+    }
+  if (obj_d_) cudaFree(obj_d_);
+  if (obj_h_) cudaFreeHost(obj_h_);
+  if (st_d_) cudaFree(st_d_);
+  if (st_h_) cudaFreeHost(st_h_);
+  if (s_) cudaStreamDestroy(s_);
+}
+
+uint64_t Engine::memory_bytes() const {
+  uint64_t b = rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
+               cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes();
+  for (const auto& S : slot_)
+    b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes();
+  b += g_.bytes() * 9 + a_.bytes() + parts_.bytes();
+  return b;
+}
+
+void Engine::synchronize() { cuda_check(cudaStreamSynchronize(s_), "synchronize"); }
+
+void Engine::read_obj() {
+  cuda_check(cudaMemcpyAsync(obj_h_, obj_d_, sizeof(ObjScalars), cudaMemcpyDeviceToHost, s_),
+             "D2H");
+  cuda_check(cudaStreamSynchronize(s_), "sync");
+}
+
+void Engine::read_cg(CgState* out) {
+  cuda_check(cudaMemcpyAsync(st_h_, st_d_, sizeof(CgState), cudaMemcpyDeviceToHost, s_), "D2H");
+  cuda_check(cudaStreamSynchronize(s_), "sync");
+  *out = *st_h_;
+}
+
+// ----------------------------------------------------------------------------
+// fun: fused margin pass (loss.cpp:35-58 / :94-122)
+// ----------------------------------------------------------------------------
+void Engine::forward(Slot& S) {
+  const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
+  if (dense_) {
+    dense_forward(l_, n_, ld_, Xc_.p, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
+                  obj_d_, sc_, s_);
+  } else {
+    csr_forward(X_, group_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_,
+                s_);
+  }
+  count_launch(1);
+}
+
+double Engine::eval_candidate_dev(const double* d_step) {
+  Slot& S = slot_[cand_];
+  const Slot& W = slot_[cand_ ^ 1];
+  if (d_step) {
+    vec_axpy_dot(n_, W.w.p, d_step, S.w.p, obj_d_, sc_, s_);
+    count_launch(1);
+  } else if (!dense_) {
+    vec_axpy_dot(n_, S.w.p, nullptr, S.w.p, obj_d_, sc_, s_);
+    count_launch(1);
+  }
+  forward(S);
+  if (comm_.active()) comm_.allreduce_sum(obj_d_->red, 2, s_);  // per-shard loss sums, |I|
+  read_obj();
+  double f = obj_h_->f;
+  long long nact = obj_h_->nact;
+  if (comm_.active()) {
+    f = 0.5 * obj_h_->ww + C_ * obj_h_->red[0];  // loss.cpp:57 over the global sum
+    nact = (long long)obj_h_->red[1];
+  }
+  S.f = f;
+  S.nact = obj_h_->nact;
+  S.valid = true;
+  ledger.margin_passes++;
+  ledger.scalar_returns++;
+  if (loss_ == TRON_LOSS_L2SVM)
+    ledger.index_set_bytes = std::max<uint64_t>(ledger.index_set_bytes, (uint64_t)nact * 8);
+  return f;
+}
+
+double Engine::eval_candidate_host(const double* w) {
+  if (n_ > 0)
+    cuda_check(cudaMemcpyAsync(slot_[cand_].w.p, w, n_ * sizeof(double), cudaMemcpyHostToDevice, s_),
+               "H2D");
+  return eval_candidate_dev(nullptr);
+}
+
+// ----------------------------------------------------------------------------
+// transposed products: X^T u with epilogue, world-aware
+// ----------------------------------------------------------------------------
+void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out) {
+  if (!comm_.active()) {
+    csc_spmv(Xt_, plan_, u, squared, epi, out, s_);
+    count_launch(2);
+    return;
+  }
+  EpiView raw;
+  raw.kind = EPI_RAW;
+  csc_spmv(Xt_, plan_, u, squared, raw, raw_.p, s_);
+  comm_.allreduce_sum(raw_.p, n_, s_);
+  vec_epilogue(n_, raw_.p, epi, out, s_);
+  count_launch(3);
+}
+
+void Engine::dense_vector(int kind, const double* v, const EpiView& epi, double* out) {
+  const Slot& S = slot_[cand_ ^ 1];
+  const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
+  const bool gathered = kind == DA_HV && gathered_valid_;
+  if (gathered) {
+    dense_accum(DA_HV, nI_, n_, ldg_, Xg_.p, kLossSvm, v, nullptr, nullptr, nullptr, nullptr,
+                nullptr, parts_.p, s_);
+  } else {
+    dense_accum(kind, l_, n_, ld_, Xc_.p, loss, v, S.zhat.p, S.dvec.p, S.mask.p, S.z.p, y_.p,
+                parts_.p, s_);
+  }
+  const int nparts = dense_grid(gathered ? nI_ : l_);
+  if (!comm_.active()) {
+    dense_finalize(n_, parts_.p, nparts, epi, out, s_);
+    count_launch(2);
+    return;
+  }
+  EpiView raw;
+  raw.kind = EPI_RAW;
+  dense_finalize(n_, parts_.p, nparts, raw, raw_.p, s_);
+  comm_.allreduce_sum(raw_.p, n_, s_);
+  vec_epilogue(n_, raw_.p, epi, out, s_);
+  count_launch(3);
+}
+
+// ----------------------------------------------------------------------------
+// commit + gradient (backend.cpp:165-183 / :249-277; loss.cpp:74-80 / :129-137)
+// ----------------------------------------------------------------------------
+void Engine::gradient_dev() {
+  const Slot& S = slot_[cand_ ^ 1];
+  EpiView epi;
+  epi.kind = EPI_VEC;
+  epi.base = S.w.p;
+  epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+  if (dense_) {
+    dense_vector(DA_GRAD, nullptr, epi, g_.p);
+  } else {
+    UView u;
+    if (loss_ == TRON_LOSS_LOGISTIC) {
+      u.kind = U_VEC;
+      u.u = S.zhat.p;
+    } else {
+      u.kind = U_SVM_RESID;
+      u.mask = S.mask.p;
+      u.z = S.z.p;
+      u.y = y_.p;
+    }
+    transposed_raw_or_epi(u, false, epi, g_.p);
+  }
+  vec_norm_check(n_, g_.p, obj_d_, sc_, s_);
+  count_launch(1);
+}
+
+int Engine::compact(const Slot& S, DevBuf<int32_t>& idx) {
+  compact_mask(l_, S.mask.p, idx.p, idx_tmp_.p, count_.p, s_);
+  count_launch(3);
+  long long cnt = 0;
+  cuda_check(cudaMemcpyAsync(&cnt, count_.p, sizeof(cnt), cudaMemcpyDeviceToHost, s_), "D2H");
+  synchronize();
+  return (int)cnt;
+}
+
+void Engine::gather_active() {
+  const Slot& S = slot_[cand_ ^ 1];
+  const uint64_t projected = (uint64_t)S.nact * (uint64_t)n_ * sizeof(double);
+  if (projected > budget_) {
+    raise(TRON_ERR_BUDGET, "gathered submatrix would need " + std::to_string(projected) +
+                               " bytes, exceeding the " + std::to_string(budget_) +
+                               "-byte budget; use the mix backend (MixedActiveSet), which "
+                               "answers Hessian products by index-indirect traversal instead");
+  }
+  const int nI = compact(S, idx_);
+  const int64_t ldg = (int64_t)((nI + 3) / 4 * 4);
+  if ((size_t)ldg * n_ > Xg_.n) Xg_.alloc((size_t)std::max<int64_t>(ldg, 4) * n_);
+  if (nI > 0) {
+    dense_gather(nI, n_, Xc_.p, ld_, idx_.p, Xg_.p, ldg, s_);
+    count_launch(1);
+  }
+  nI_ = nI;
+  ldg_ = ldg;
+  gathered_valid_ = true;
+  ledger.gathered_submatrix_bytes =
+      std::max<uint64_t>(ledger.gathered_submatrix_bytes, (uint64_t)nI * n_ * sizeof(double));
+}
+
+void Engine::commit(double* gnorm) {
+  if (!slot_[cand_].valid) raise(TRON_ERR_LOGIC, "commit() without a pending candidate");
+  cand_ ^= 1;  // the candidate becomes the committed slot
+  slot_[cand_].valid = false;
+  committed_valid_ = true;
+  precond_valid_ = false;
+  gathered_valid_ = false;
+  if (loss_ == TRON_LOSS_L2SVM && svm_strategy_ == TRON_SVM_GATHERED) gather_active();
+  gradient_dev();
+  read_obj();
+  gnorm_ = obj_h_->gnorm;
+  ledger.gradient_materializations++;
+  if (gnorm) *gnorm = gnorm_;
+}
+
+void Engine::gradient_host(double* g) {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "gradient() before the first commit()");
+  if (n_ > 0)
+    cuda_check(cudaMemcpyAsync(g, g_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
+  synchronize();
+}
+
+// ----------------------------------------------------------------------------
+// Hv (loss.cpp:82-92 / :139-174) and preconditioner (loss.cpp:176-188)
+// ----------------------------------------------------------------------------
+void Engine::hv_kernels(const double* v, double* out) {
+  const Slot& S = slot_[cand_ ^ 1];
+  EpiView epi;
+  epi.kind = EPI_VEC;
+  epi.base = v;
+  epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+  if (dense_) {
+    dense_vector(DA_HV, v, epi, out);
+    return;
+  }
+  if (loss_ == TRON_LOSS_LOGISTIC)
+    csr_dv(X_, group_, v, S.dvec.p, nullptr, a_.p, s_);
+  else
+    csr_dv(X_, group_, v, nullptr, S.mask.p, a_.p, s_);
+  count_launch(1);
+  UView u;
+  u.kind = U_VEC;
+  u.u = a_.p;
+  transposed_raw_or_epi(u, false, epi, out);
+}
+
+void Engine::hessian_vec_dev(const double* v, double* out) {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "hessian_vec() before the first commit()");
+  hv_kernels(v, out);
+}
+
+void Engine::hessian_vec_host(const double* v, double* out) {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "hessian_vec() before the first commit()");
+  if (n_ > 0)
+    cuda_check(cudaMemcpyAsync(vtmp_.p, v, n_ * sizeof(double), cudaMemcpyHostToDevice, s_), "H2D");
+  hv_kernels(vtmp_.p, otmp_.p);
+  if (n_ > 0)
+    cuda_check(cudaMemcpyAsync(out, otmp_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, s_),
+               "D2H");
+  synchronize();
+  ledger.concealed_vector_returns++;
+}
+
+void Engine::ensure_precond() {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "precond_diagonal() before the first commit()");
+  if (precond_valid_) return;
+  const Slot& S = slot_[cand_ ^ 1];
+  EpiView epi;
+  epi.kind = EPI_CONST;
+  epi.cbase = 1.0;
+  epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+  if (dense_) {
+    dense_vector(DA_PRECOND, nullptr, epi, M_.p);
+  } else {
+    UView u;
+    if (loss_ == TRON_LOSS_LOGISTIC) {
+      u.kind = U_VEC;
+      u.u = S.dvec.p;
+    } else {
+      u.kind = U_MASK;
+      u.mask = S.mask.p;
+    }
+    transposed_raw_or_epi(u, true, epi, M_.p);
+  }
+  precond_valid_ = true;
+}
+
+void Engine::precond_host(double* m) {
+  ensure_precond();
+  if (n_ > 0)
+    cuda_check(cudaMemcpyAsync(m, M_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
+  synchronize();
+}
+
+// ----------------------------------------------------------------------------
+// state probes
+// ----------------------------------------------------------------------------
+void Engine::state_lr(int which, double* z, double* zhat, double* dvec) {
+  if (loss_ != TRON_LOSS_LOGISTIC) raise(TRON_ERR_LOGIC, "not a logistic evaluator");
+  const Slot& S = which == 0 ? slot_[cand_] : slot_[cand_ ^ 1];
+  if (!(which == 0 ? S.valid : committed_valid_)) raise(TRON_ERR_LOGIC, "state slot is empty");
+  if (l_ > 0) {
+    if (z) cuda_check(cudaMemcpyAsync(z, S.z.p, l_ * 8, cudaMemcpyDeviceToHost, s_), "D2H");
+    if (zhat) cuda_check(cudaMemcpyAsync(zhat, S.zhat.p, l_ * 8, cudaMemcpyDeviceToHost, s_), "D2H");
+    if (dvec) cuda_check(cudaMemcpyAsync(dvec, S.dvec.p, l_ * 8, cudaMemcpyDeviceToHost, s_), "D2H");
+  }
+  synchronize();
+}
+
+void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint64_t* n_active) {
+  if (loss_ != TRON_LOSS_L2SVM) raise(TRON_ERR_LOGIC, "not an L2-SVM evaluator");
+  const Slot& S = which == 0 ? slot_[cand_] : slot_[cand_ ^ 1];
+  if (!(which == 0 ? S.valid : committed_valid_)) raise(TRON_ERR_LOGIC, "state slot is empty");
+  if (z && l_ > 0) cuda_check(cudaMemcpyAsync(z, S.z.p, l_ * 8, cudaMemcpyDeviceToHost, s_), "D2H");
+  if (idx_.n == 0) {
+    idx_.alloc(l_ > 0 ? l_ : 1);
+    idx_tmp_.alloc((l_ + 1023) / 1024 + 2);
+    count_.alloc(1);
+  }
+  DevBuf<int32_t> idx;
+  idx.alloc(l_ > 0 ? l_ : 1);
+  const int cnt = compact(S, idx);
+  if (n_active) *n_active = (uint64_t)cnt;
+  if (active && cnt > 0) {
+    std::vector<int32_t> h(cnt);
+    cuda_check(cudaMemcpy(h.data(), idx.p, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    const uint64_t m = std::min<uint64_t>(cap, (uint64_t)cnt);
+    for (uint64_t k = 0; k < m; ++k) active[k] = (int64_t)h[k] + (int64_t)row_begin_;
+  }
+  synchronize();
+}
+
+// ----------------------------------------------------------------------------
+// device-resident truncated CG (tron.cpp:37-108)
+// ----------------------------------------------------------------------------
+void Engine::build_graph(int k, bool use_m) {
+  // Captured against committed slot k; CG vectors are fixed buffers.
+  cudaGraph_t graph;
+  cuda_check(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
+  cudaGraphConditionalHandle handle;
+  cuda_check(cudaGraphConditionalHandleCreate(&handle, graph, 0, 0), "conditional handle");
+  Cond cond;
+  cond.h = (unsigned long long)handle;
+  cond.on = 1;
+  CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
+
+  const int saved_cand = cand_;
+  cand_ = k ^ 1;  // so that slot_[cand_^1] == committed slot k during capture
+  const uint64_t saved_launches = launches;
+
+  cuda_check(cudaStreamBeginCaptureToGraph(s_, graph, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal),
+             "begin capture");
+  if (small_engine_)
+    cg_small_init(v, st_d_, cond, s_);
+  else
+    cg_large_init(v, st_d_, sc_, cond, s_);
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t capg = nullptr;
+  cuda_check(cudaStreamGetCaptureInfo(s_, &cs, nullptr, &capg, &deps, &ndeps), "capture info");
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond_node;
+  cuda_check(cudaGraphAddNode(&cond_node, capg, deps, ndeps, &cp), "add conditional node");
+  cuda_check(cudaStreamUpdateCaptureDependencies(s_, &cond_node, 1,
+                                                 cudaStreamSetCaptureDependencies),
+             "update deps");
+  if (!small_engine_) cg_large_post(v, st_d_, sc_, s_);
+  cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
+
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cuda_check(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal),
+             "begin body capture");
+  const uint64_t before = launches;
+  if (small_engine_) {
+    if (dense_) {
+      const Slot& S = slot_[k];
+      const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
+      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, loss, p_.p, S.zhat.p, S.dvec.p, S.mask.p, S.z.p, y_.p,
+                  parts_.p, s_);
+      cg_small_step(v, parts_.p, dense_grid(l_), loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_,
+                    st_d_, cond, s_);
+      count_launch(2);
+    } else {
+      hv_kernels(p_.p, hp_.p);
+      cg_small_step(v, nullptr, 0, 0.0, st_d_, cond, s_);
+      count_launch(1);
+    }
+  } else {
+    hv_kernels(p_.p, hp_.p);
+    cg_large_php(v, st_d_, sc_, cond, s_);
+    cg_large_update(v, st_d_, sc_, cond, s_);
+    cg_large_direction(v, st_d_, sc_, cond, s_);
+    count_launch(3);
+  }
+  body_kernels_ = launches - before;
+  cuda_check(cudaStreamEndCapture(s_, &body), "end body capture");
+  launches = saved_launches;
+  cand_ = saved_cand;
+
+  cudaGraphExec_t exec;
+  cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+  graph_[k][use_m] = graph;
+  graph_exec_[k][use_m] = exec;
+}
+
+void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "truncated CG before the first commit()");
+  const bool use_m = cfg.use_preconditioner != 0;
+  if (use_m) ensure_precond();
+  uint64_t max_iters = cfg.max_cg_iters;
+  if (max_iters == 0) max_iters = (uint64_t)n_ < 1000 ? (uint64_t)n_ : 1000;  // tron.cpp:40-41
+  CgState init{};
+  init.delta = delta;
+  init.stop = cfg.cg_tol * gnorm_;  // tron.cpp:55
+  init.max_iters = (long long)max_iters;
+  init.use_m = use_m;
+  *st_h_ = init;
+  cuda_check(cudaMemcpyAsync(st_d_, st_h_, sizeof(CgState), cudaMemcpyHostToDevice, s_), "H2D");
+  const int k = cand_ ^ 1;
+  CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
+  if (use_graphs_) {
+    if (!graph_exec_[k][use_m]) build_graph(k, use_m);
+    cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
+    read_cg(out);
+    launches += 1 + (uint64_t)out->iters * body_kernels_ + (small_engine_ ? 0 : 1);
+    return;
+  }
+  // host-driven loop (multi-GPU: NCCL between phases)
+  Cond none;
+  if (small_engine_)
+    cg_small_init(v, st_d_, none, s_);
+  else
+    cg_large_init(v, st_d_, sc_, none, s_);
+  count_launch(1);
+  read_cg(out);
+  while (out->cont) {
+    hv_kernels(p_.p, hp_.p);
+    if (small_engine_) {
+      cg_small_step(v, nullptr, 0, 0.0, st_d_, none, s_);
+      count_launch(1);
+    } else {
+      cg_large_php(v, st_d_, sc_, none, s_);
+      cg_large_update(v, st_d_, sc_, none, s_);
+      cg_large_direction(v, st_d_, sc_, none, s_);
+      count_launch(3);
+    }
+    read_cg(out);
+  }
+  if (!small_engine_) {
+    cg_large_post(v, st_d_, sc_, s_);
+    count_launch(1);
+    read_cg(out);
+  }
+}
+
+void Engine::truncated_cg(double delta, const tron_config& cfg, double* d, int32_t* exit_kind,
+                          uint64_t* iters, double* q) {
+  CgState st;
+  run_cg(delta, cfg, &st);
+  if (st.fail)
+    raise(TRON_ERR_NUMERICAL,
+          "conjugate gradients met non-positive curvature (" + std::to_string(st.php) + ")");
+  if (d && n_ > 0) {
+    cuda_check(cudaMemcpyAsync(d, d_.p, n_ * 8, cudaMemcpyDeviceToHost, s_), "D2H");
+    synchronize();
+  }
+  if (exit_kind) *exit_kind = st.exit_kind;
+  if (iters) *iters = (uint64_t)st.iters;
+  if (q) *q = st.q;
+}
+
+// ----------------------------------------------------------------------------
+// device-mode solve: tron.cpp:127-217 with device w/g/d and host scalars
+// ----------------------------------------------------------------------------
+namespace {
+void validate_config(const tron_config& c) {  // tron.cpp:19-29
+  if (!(c.eps > 0.0)) raise(TRON_ERR_DIMENSION, "config: eps must be positive");
+  if (!(c.sigma0 > 0.0 && c.sigma0 < 1.0)) raise(TRON_ERR_DIMENSION, "config: sigma0 must be in (0,1)");
+  if (!(0.0 < c.eta1 && c.eta1 < c.eta2 && c.eta2 < 1.0))
+    raise(TRON_ERR_DIMENSION, "config: need 0 < eta1 < eta2 < 1");
+  if (!(0.0 < c.gamma1 && c.gamma1 < c.gamma2 && c.gamma2 < 1.0 && c.gamma3 > 1.0))
+    raise(TRON_ERR_DIMENSION, "config: need 0 < gamma1 < gamma2 < 1 < gamma3");
+  if (!(c.cg_tol > 0.0 && c.cg_tol < 1.0)) raise(TRON_ERR_DIMENSION, "config: cg_tol must be in (0,1)");
+}
+
+struct NumericalAbort {
+  std::string what;
+};
+}  // namespace
+
+void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_out,
+                          tron_solve_info* info, tron_iteration* trace, uint64_t cap) {
+  validate_config(cfg);
+  std::memset(info, 0, sizeof(*info));
+  const uint64_t launches0 = launches;
+  uint64_t hv_count = 0;
+  auto finish = [&](int status) {
+    if (w_out && n_ > 0) {
+      cuda_check(cudaMemcpyAsync(w_out, slot_[cand_ ^ 1].w.p, n_ * 8, cudaMemcpyDeviceToHost, s_),
+                 "D2H");
+      synchronize();
+    }
+    info->status = status;
+    info->hessian_products = hv_count;
+    (void)launches0;
+  };
+  Slot& C0 = slot_[cand_];
+  if (n_ > 0) {
+    if (w0)
+      cuda_check(cudaMemcpyAsync(C0.w.p, w0, n_ * 8, cudaMemcpyHostToDevice, s_), "H2D");
+    else
+      cuda_check(cudaMemsetAsync(C0.w.p, 0, n_ * 8, s_), "memset");
+  }
+  double f = eval_candidate_dev(nullptr);
+  info->objective_evaluations = 1;
+  if (!std::isfinite(f)) {
+    // w_out must reflect the starting point like the reference's result.w
+    if (w_out && n_ > 0) {
+      if (w0) std::memcpy(w_out, w0, n_ * 8); else std::memset(w_out, 0, n_ * 8);
+    }
+    info->status = TRON_ERR_NUMERICAL;
+    raise(TRON_ERR_NUMERICAL, "objective is not finite at the starting point");
+  }
+  commit(nullptr);
+  info->gradient_materializations = 1;
+  if (obj_h_->grad_nonfinite) {
+    finish(TRON_ERR_NUMERICAL);
+    raise(TRON_ERR_NUMERICAL, "gradient is not finite at the starting point");
+  }
+  info->f_initial = f;
+  const double gnorm0 = gnorm_;
+  info->gradient_norm_initial = gnorm0;
+  double gnorm = gnorm0;
+  info->objective = f;
+  if (gnorm <= cfg.eps * gnorm0) {
+    info->converged = 1;
+    finish(TRON_OK);
+    return;
+  }
+  double delta = gnorm0;
+  while (info->n_iterations < cfg.max_outer_iters) {
+    CgState st;
+    run_cg(delta, cfg, &st);
+    hv_count += (uint64_t)st.iters;
+    if (st.fail) {
+      finish(TRON_ERR_NUMERICAL);
+      raise(TRON_ERR_NUMERICAL,
+            "conjugate gradients met non-positive curvature (" + std::to_string(st.php) + ")");
+    }
+    const double step_norm = st.dnorm;
+    const double f_cand = eval_candidate_dev(d_.p);
+    info->objective_evaluations++;
+    if (!std::isfinite(f_cand)) {
+      finish(TRON_ERR_NUMERICAL);
+      raise(TRON_ERR_NUMERICAL, "objective is not finite at a candidate step");
+    }
+    const double sigma = (f_cand - f) / st.q;
+    // trust_region_update (tron.cpp:110-125)
+    const bool accept = sigma > cfg.sigma0;
+    double next_delta;
+    if (!accept)
+      next_delta = cfg.gamma1 * step_norm;
+    else if (sigma < cfg.eta1)
+      next_delta = cfg.gamma2 * step_norm;
+    else if (sigma < cfg.eta2)
+      next_delta = delta;
+    else {
+      const double grown = cfg.gamma3 * step_norm;
+      next_delta = grown > delta ? grown : delta;
+    }
+    if (trace && info->n_iterations < cap) {
+      tron_iteration& rec = trace[info->n_iterations];
+      rec.f_candidate = f_cand;
+      rec.gradient_norm = gnorm;
+      rec.delta = delta;
+      rec.sigma = sigma;
+      rec.accepted = accept;
+      rec.cg_iters = (uint64_t)st.iters;
+      rec.cg_exit = st.exit_kind;
+    }
+    info->n_iterations++;
+    delta = next_delta;
+    if (accept) {
+      f = f_cand;
+      info->objective = f;
+      commit(nullptr);
+      info->accepted_steps++;
+      info->gradient_materializations++;
+      if (obj_h_->grad_nonfinite) {
+        finish(TRON_ERR_NUMERICAL);
+        raise(TRON_ERR_NUMERICAL, "gradient is not finite after an accepted step");
+      }
+      gnorm = gnorm_;
+      if (gnorm <= cfg.eps * gnorm0) {
+        info->converged = 1;
+        break;
+      }
+    }
+  }
+  finish(TRON_OK);
+}
+
+// ----------------------------------------------------------------------------
+// per-kernel timing for the roofline figures of bench.py
+// ----------------------------------------------------------------------------
+void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "bench_kernels() needs a committed state");
+  if (flush_l2 && flush_.n == 0) flush_.alloc((size_t)(256u << 20) / 8);  // 256 MiB > L2
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto time_it = [&](auto&& fn) {
+    double total = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      if (flush_l2) cudaMemsetAsync(flush_.p, r & 0xff, flush_.bytes(), s_);
+      cudaEventRecord(a, s_);
+      fn();
+      cudaEventRecord(b, s_);
+      cudaEventSynchronize(b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      total += ms;
+    }
+    return total / std::max(reps, 1);
+  };
+  cuda_check(cudaMemcpyAsync(vtmp_.p, g_.p, n_ * 8, cudaMemcpyDeviceToDevice, s_), "D2D");
+  out->hv_ms = time_it([&] { hv_kernels(vtmp_.p, otmp_.p); });
+  const Slot& S = slot_[cand_ ^ 1];
+  if (!dense_) {
+    UView u;
+    u.kind = U_VEC;
+    u.u = a_.p;
+    EpiView epi;
+    epi.kind = EPI_VEC;
+    epi.base = vtmp_.p;
+    epi.scale = C_;
+    out->transposed_ms = time_it([&] { csc_spmv(Xt_, plan_, u, false, epi, otmp_.p, s_); });
+    Slot& Cd = slot_[cand_];
+    out->forward_ms = time_it([&] {
+      csr_forward(X_, group_, loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm, S.w.p, y_.p,
+                  C_, Cd.z.p, Cd.zhat.p, Cd.dvec.p, Cd.mask.p, obj_d_, sc_, s_);
+    });
+  } else {
+    const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
+    out->transposed_ms = time_it([&] {
+      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, loss, vtmp_.p, S.zhat.p, S.dvec.p, S.mask.p, S.z.p,
+                  y_.p, parts_.p, s_);
+    });
+    out->forward_ms = time_it([&] {
+      dense_forward(l_, n_, ld_, Xc_.p, loss, S.w.p, y_.p, C_, slot_[cand_].z.p,
+                    slot_[cand_].zhat.p, slot_[cand_].dvec.p, slot_[cand_].mask.p, obj_d_, sc_, s_);
+    });
+  }
+  out->grad_ms = time_it([&] { gradient_dev(); });
+  slot_[cand_].valid = false;  // forward timing overwrote the candidate slot
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  synchronize();
+}
+
+}  // namespace tb

@@ -1,0 +1,179 @@
+// Device-resident state of one TRON problem shard and the host-side
+// orchestration of the hot path (the B200 counterpart of the reference's
+// LogisticEvaluator / SvmEvaluator, proj/src/backend.cpp:136-306).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "tron_b200.h"
+
+namespace tb {
+
+struct StatusError : std::runtime_error {
+  int status;
+  StatusError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] void raise(int status, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Lazily-loaded NCCL (libnccl.so.2) for the row-sharded multi-GPU layout.
+class Comm {
+ public:
+  int rank = 0, world = 1;
+  void init(int rank, int world, const void* unique_id, int device);
+  ~Comm();
+  void allreduce_sum(double* buf, size_t count, cudaStream_t s);
+  bool active() const { return world > 1; }
+
+ private:
+  void* comm_ = nullptr;
+};
+int nccl_unique_id(void* out128);
+
+struct KernelTimes {
+  double hv_ms = 0, transposed_ms = 0, forward_ms = 0, grad_ms = 0;
+};
+
+class Engine {
+ public:
+  static std::unique_ptr<Engine> create_csr(int loss, uint64_t l, uint64_t n, const int64_t* ro,
+                                            const int32_t* ci, const double* vals, const double* y,
+                                            double C, const tron_gpu_options& opt);
+  static std::unique_ptr<Engine> create_dense(int loss, uint64_t l, uint64_t n,
+                                              const double* row_major, const double* y, double C,
+                                              const tron_gpu_options& opt);
+  ~Engine();
+
+  int64_t dimension() const { return n_; }
+  int loss() const { return loss_; }
+  bool dense() const { return dense_; }
+
+  // LossEvaluator surface (host vectors).
+  double eval_candidate_host(const double* w);
+  void commit(double* gnorm);
+  void gradient_host(double* g);
+  void hessian_vec_host(const double* v, double* out);
+  void precond_host(double* m);
+  void state_lr(int which, double* z, double* zhat, double* dvec);
+  void state_svm(int which, double* z, int64_t* active, uint64_t cap, uint64_t* n_active);
+  void truncated_cg(double delta, const tron_config& cfg, double* d, int32_t* exit_kind,
+                    uint64_t* iters, double* q);
+  void solve_device(const tron_config& cfg, const double* w0, double* w_out, tron_solve_info* info,
+                    tron_iteration* trace, uint64_t cap);
+  void bench_kernels(int reps, bool flush_l2, KernelTimes* out);
+
+  tron_ledger ledger{};
+  uint64_t launches = 0;
+  uint64_t memory_bytes() const;
+  void synchronize();
+
+  // Device-side building blocks (also used by the host-CG adapter).
+  double eval_candidate_dev(const double* d_step);  // slot[cand].w (+ d_step) -> f
+  void hessian_vec_dev(const double* v, double* out);
+  void ensure_precond();
+  void run_cg(double delta, const tron_config& cfg, CgState* out);
+
+ private:
+  Engine() = default;
+  struct Slot {
+    DevBuf<double> w, z, zhat, dvec;
+    DevBuf<uint8_t> mask;
+    double f = 0.0;
+    long long nact = 0;
+    bool valid = false;
+  };
+  void common_alloc();
+  void forward(Slot& S);
+  void gradient_dev();
+  void transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out);
+  void dense_vector(int kind, const double* v, const EpiView& epi, double* out);
+  void hv_kernels(const double* v, double* out);  // enqueue only
+  void gather_active();
+  int compact(const Slot& S, DevBuf<int32_t>& idx);
+  void read_obj();
+  void read_cg(CgState* out);
+  void build_graph(int slot, bool use_m);
+  void count_launch(uint64_t k) { launches += k; }
+
+  int loss_ = 0;
+  bool dense_ = false;
+  int64_t l_ = 0, n_ = 0;
+  double C_ = 1.0;
+  int device_ = 0;
+  int svm_strategy_ = TRON_SVM_INDIRECT;
+  uint64_t budget_ = 0;
+  uint64_t row_begin_ = 0;
+  Comm comm_;
+  cudaStream_t s_ = nullptr;
+
+  // CSR + CSC (sparse layout)
+  DevBuf<int32_t> rptr_, cidx_, cptr_, ridx_;
+  DevBuf<double> rval_, cval_;
+  DevBuf<int32_t> tile_row_, tile_nz_, fix_chain_;
+  DevBuf<double> head_, carry_;
+  CsrView X_{}, Xt_{};
+  MergeView plan_{};
+  int group_ = 4;
+  // dense column-major
+  DevBuf<double> Xc_;
+  int64_t ld_ = 0;
+  DevBuf<double> Xg_;  // gathered panel X_{I,:} (Gathered strategy)
+  int64_t ldg_ = 0, nI_ = 0;
+  bool gathered_valid_ = false;
+  DevBuf<int32_t> idx_, idx_tmp_;
+  DevBuf<long long> count_;
+
+  DevBuf<double> y_;
+  Slot slot_[2];
+  int cand_ = 0;       // candidate slot index; committed = cand_ ^ 1
+  bool committed_valid_ = false;
+  DevBuf<double> g_, M_, d_, r0_, r1_, p_, hp_, a_, raw_, vtmp_, otmp_, parts_;
+  bool precond_valid_ = false;
+  double gnorm_ = 0.0;
+
+  DevBuf<double> sc_partials_;
+  DevBuf<unsigned int> sc_tickets_;
+  Scratch sc_{};
+  ObjScalars* obj_d_ = nullptr;
+  ObjScalars* obj_h_ = nullptr;  // pinned
+  CgState* st_d_ = nullptr;
+  CgState* st_h_ = nullptr;  // pinned
+  DevBuf<double> flush_;
+
+  // CUDA graphs of the device CG loop: [committed slot][preconditioned]
+  cudaGraphExec_t graph_exec_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  cudaGraph_t graph_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t body_kernels_ = 0;
+  bool small_engine_ = false;
+  bool use_graphs_ = true;
+};
+
+}  // namespace tb

@@ -1,0 +1,186 @@
+// Host-callable launchers for the sm_100a kernels of the TRON hot path.
+// Everything here is FP64; indices are int32 (checked at creation:
+// nnz and n below 2^31 per shard).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tb {
+
+constexpr int kLossLogistic = 0;
+constexpr int kLossSvm = 1;
+
+// Compressed rows (CSR of X) or compressed columns (CSC of X, i.e. CSR of
+// X^T): ptr has `rows+1` entries, idx/val `nnz`.
+struct CsrView {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  const int32_t* ptr = nullptr;
+  const int32_t* idx = nullptr;
+  const double* val = nullptr;
+};
+
+// Merge-path tiling of a compressed matrix (fixed per matrix structure).
+struct MergeView {
+  int32_t num_tiles = 0;
+  const int32_t* tile_row = nullptr;   // [num_tiles+1] rows ended before tile start
+  const int32_t* tile_nz = nullptr;    // [num_tiles+1] nonzeros consumed before tile start
+  const int32_t* fix_chain = nullptr;  // [num_tiles] first carry tile of the head row, or -1
+  double* head = nullptr;              // [num_tiles] partial of a tile's first (split) row
+  double* carry = nullptr;             // [num_tiles] carry-out toward the next tile
+};
+
+// Per-source-row weight u_i used by the transposed product sum_i u_i x_ij.
+enum UKind : int {
+  U_VEC = 0,        // u[i]
+  U_SVM_RESID = 1,  // mask[i] ? z[i] - y[i] : 0   (svm_gradient, loss.cpp:129-137)
+  U_MASK = 2,       // mask[i] ? 1 : 0              (masked_sq_col_sums, linalg.cpp:257-265)
+};
+struct UView {
+  int kind = U_VEC;
+  const double* u = nullptr;
+  const uint8_t* mask = nullptr;
+  const double* z = nullptr;
+  const double* y = nullptr;
+};
+
+// out_j = base_j + scale*sum_j (VEC), cbase + scale*sum_j (CONST), or sum_j (RAW)
+enum EpiKind : int { EPI_VEC = 0, EPI_CONST = 1, EPI_RAW = 2 };
+struct EpiView {
+  int kind = EPI_VEC;
+  const double* base = nullptr;
+  double cbase = 0.0;
+  double scale = 1.0;
+};
+
+constexpr int kCgConverged = 0;  // CgExit, tron.hpp:29
+constexpr int kCgBoundary = 1;
+constexpr int kCgMaxIters = 2;
+
+// Trust-region CG state kept in device memory (tron.cpp:37-108 scalars).
+struct CgState {
+  double delta, stop, rz, rnorm, alpha, beta, php, tau, q, dnorm;
+  long long iters, max_iters;
+  int exit_kind, boundary, cont, fail, rpar, use_m;
+};
+
+// Scalars of the objective / gradient passes.
+struct ObjScalars {
+  double ww;          // w_cand . w_cand
+  double f;           // candidate objective
+  double gnorm;       // ||grad|| of the committed iterate
+  long long nact;     // |I| of the candidate (SVM)
+  int grad_nonfinite; // any non-finite gradient entry
+  int pad;
+  double red[2];      // {sum of loss terms, |I|} of this shard (allreduced when sharded)
+};
+
+// Optional CUDA-graph while-loop handle set by the CG kernels.
+struct Cond {
+  unsigned long long h = 0;
+  int on = 0;
+};
+
+struct Scratch {
+  double* partials = nullptr;  // >= kMaxPartialBlocks * 4 doubles
+  unsigned int* tickets = nullptr;  // kNumTickets counters, zero-initialized
+};
+constexpr int kMaxPartialBlocks = 4096;
+constexpr int kNumTickets = 16;
+enum Ticket : int { T_FUN = 0, T_AXPY = 1, T_NORM = 2, T_CG_INIT = 3, T_CG_PHP = 4, T_CG_UPD = 5,
+                    T_CG_P = 6, T_CG_POST = 7, T_DENSE_FIN = 8, T_COUNT = 9 };
+
+int device_sm_count();
+
+// ---- CSR forward passes (csr_kernels.cu) -----------------------------------
+int choose_group(int64_t rows, int64_t nnz);
+// Fused margin pass: z = Xw; LR: zhat, dvec; SVM: mask (+ active count).
+// f = 0.5*ww + C*sum(loss terms) is written to obj->f (obj->ww precomputed).
+void csr_forward(const CsrView& X, int group, int loss, const double* w, const double* y, double C,
+                 double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
+                 Scratch sc, cudaStream_t s);
+// a_i = (x_i . p) * dvec_i  (or mask_i ? x_i . p : 0 when mask given)
+void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
+            double* a, cudaStream_t s);
+// Transposed product over the CSC copy (merge-path, atomic-free).
+void csc_spmv(const CsrView& At, const MergeView& plan, const UView& u, bool squared,
+              const EpiView& epi, double* out, cudaStream_t s);
+// Build the merge-path plan for a compressed matrix (one-time setup).
+void merge_plan_build(const CsrView& A, int32_t* tile_row, int32_t* tile_nz, int32_t* fix_chain,
+                      int32_t num_tiles, cudaStream_t s);
+int32_t merge_num_tiles(int64_t rows, int64_t nnz);
+// Device CSC construction from device CSR (stable in row order).
+// Returns 0 on success; temp storage allocated internally.
+int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s);
+// Row-offset narrowing int64 -> int32 (device).
+void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s);
+
+// ---- vector kernels (vec_kernels.cu) -----------------------------------------
+// wc = w + d (d may be null: wc = w); obj->ww = wc.wc
+void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjScalars* obj,
+                  Scratch sc, cudaStream_t s);
+// obj->gnorm = ||g||, obj->grad_nonfinite
+void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s);
+// out = base + scale*raw  (after an allreduce of raw partials)
+void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
+
+// Large-n CG engine (one kernel per phase; conditional handle optional).
+struct CgVectors {
+  int64_t n;
+  const double* g;
+  const double* M;  // nullable
+  double* d;
+  double* r0;
+  double* r1;
+  double* p;
+  double* hp;
+};
+void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
+                   cudaStream_t s);
+void cg_large_php(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
+                  cudaStream_t s);
+void cg_large_update(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
+                     cudaStream_t s);
+void cg_large_direction(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
+                        cudaStream_t s);
+void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s);
+
+// Small-n CG engine (n <= kSmallCgMaxN): one single-block kernel per
+// iteration.  When `partials` is non-null, hp_j = p_j + scale*sum_b
+// partials[b*n+j] is formed first (dense tall-skinny Hv second stage).
+constexpr int64_t kSmallCgMaxN = 4096;
+void cg_small_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
+void cg_small_step(const CgVectors& v, const double* partials, int nparts, double scale,
+                   CgState* st, Cond cond, cudaStream_t s);
+
+// ---- dense column-major kernels (dense_kernels.cu), n <= 64 -----------------
+constexpr int kDenseMaxN = 64;
+int dense_grid(int64_t l);
+void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, int loss, const double* w,
+                   const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
+                   ObjScalars* obj, Scratch sc, cudaStream_t s);
+// partial sums per block (grid = dense_grid(l)) of:
+//  GRAD:    sum_i c_i x_i   with c = zhat (LR) or mask?(z-y):0 (SVM)
+//  HV:      sum_i c_i x_i   with c = (x_i.v)*dvec_i (LR) or mask?(x_i.v):0 (SVM;
+//           mask == nullptr => every row active, used on the gathered panel)
+//  PRECOND: sum_i (c_i x_ij) x_ij with c = dvec (LR) or mask (SVM)
+enum DenseAccum : int { DA_GRAD = 0, DA_HV = 1, DA_PRECOND = 2 };
+void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X, int loss,
+                 const double* v, const double* zhat, const double* dvec, const uint8_t* mask,
+                 const double* z, const double* y, double* partials, cudaStream_t s);
+// out_j = base_j (or cbase) + scale * sum_b partials[b*n + j]
+void dense_finalize(int64_t n, const double* partials, int nparts, const EpiView& epi, double* out,
+                    cudaStream_t s);
+// Row-major host chunk (rows x n, already on device) -> column-major X.
+void dense_transpose_chunk(const double* rm, int64_t rows, int64_t n, double* X, int64_t ld,
+                           int64_t row0, cudaStream_t s);
+// Active-set compaction: ascending int32 row indices of mask (ballot+scan).
+// count_out (device) receives |I|. tmp needs >= ceil(l/1024)+1 ints.
+void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, long long* count_out,
+                  cudaStream_t s);
+// Gathered strategy: Xg (ld_g rows) <- rows idx of X (column-major both).
+void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int32_t* idx,
+                  double* Xg, int64_t ldg, cudaStream_t s);
+
+}  // namespace tb

@@ -1,0 +1,516 @@
+// Device-resident truncated CG (tron.cpp:37-108) and the n-vector helpers
+// of the outer loop (tron.cpp:127-217).  Only scalars ever need to leave
+// the device: every dot/norm of the reference's serial vector ops
+// (linalg.cpp:267-286) becomes a two-stage block reduction whose second
+// stage runs in the last block to finish (fixed order => deterministic).
+//
+// Two engines:
+//  * large-n: one grid-stride kernel per CG phase (php, update, direction),
+//    used for the high-dimensional sparse problems (n up to 2e7);
+//  * small-n: the whole iteration in one single-block kernel (n <= 4096),
+//    used for the tall-skinny dense problems (n = 40) where launch count,
+//    not bandwidth, is the cost.
+// Both can run under a CUDA-graph while node: the kernel that decides
+// whether CG continues sets the conditional handle.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tb {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+int vec_grid(int64_t n) {
+  int64_t g = (n + kBlock * 4 - 1) / (kBlock * 4);
+  int64_t cap = (int64_t)device_sm_count() * 4;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+__device__ __forceinline__ void set_cond(Cond c, int v) {
+  if (c.on) cudaGraphSetConditional((cudaGraphConditionalHandle)c.h, v ? 1u : 0u);
+}
+
+#define GRID_STRIDE(j, n)                                                       \
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < (n); \
+       j += (long long)gridDim.x * blockDim.x)
+
+__global__ void __launch_bounds__(kBlock) axpy_dot_kernel(long long n, const double* w,
+                                                         const double* d, double* wc,
+                                                         ObjScalars* obj, Scratch sc) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  double acc = 0.0;
+  GRID_STRIDE(j, n) {
+    const double v = d ? w[j] + d[j] : w[j];  // axpy_inplace(1.0, d, w_cand), tron.cpp:176-177
+    wc[j] = v;
+    acc += v * v;
+  }
+  const double b = block_sum<kBlock>(acc, sh, true);
+  if (threadIdx.x == 0) sc.partials[blockIdx.x] = b;
+  if (last_block_arrive(sc.tickets + T_AXPY)) {
+    const double tot = reduce_partials<kBlock>(sc.partials, gridDim.x, 1, 0, sh);
+    if (threadIdx.x == 0) obj->ww = tot;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const double* g,
+                                                           ObjScalars* obj, Scratch sc) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  double acc = 0.0, bad = 0.0;
+  GRID_STRIDE(j, n) {
+    const double v = g[j];
+    acc += v * v;
+    if (!isfinite(v)) bad = 1.0;
+  }
+  const double b = block_sum<kBlock>(acc, sh, true);
+  const double bb = block_sum<kBlock>(bad, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[2 * blockIdx.x] = b;
+    sc.partials[2 * blockIdx.x + 1] = bb;
+  }
+  if (last_block_arrive(sc.tickets + T_NORM)) {
+    const double tot = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 0, sh);
+    const double nb = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      obj->gnorm = sqrt(tot);
+      obj->grad_nonfinite = nb > 0.0;
+    }
+  }
+}
+
+__global__ void epilogue_kernel(long long n, const double* raw, EpiView E, double* out) {
+  GRID_STRIDE(j, n) {
+    const double s = raw[j];
+    out[j] = E.kind == EPI_VEC ? E.base[j] + E.scale * s
+                               : (E.kind == EPI_CONST ? E.cbase + E.scale * s : s);
+  }
+}
+
+// ---------------- large-n CG ----------------
+
+__device__ __forceinline__ double zval(const double* r, const double* M, long long j) {
+  return M ? r[j] / M[j] : r[j];  // apply_precond, tron.cpp:46-53
+}
+
+__global__ void __launch_bounds__(kBlock) cg_init_kernel(CgVectors v, CgState* st, Scratch sc,
+                                                        Cond cond) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  double rz = 0.0, rr = 0.0;
+  GRID_STRIDE(j, v.n) {
+    v.d[j] = 0.0;
+    const double r = -v.g[j];
+    v.r0[j] = r;
+    const double z = v.M ? r / v.M[j] : r;
+    v.p[j] = z;
+    rz += r * z;
+    rr += r * r;
+  }
+  const double a = block_sum<kBlock>(rz, sh, true);
+  const double b = block_sum<kBlock>(rr, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[2 * blockIdx.x] = a;
+    sc.partials[2 * blockIdx.x + 1] = b;
+  }
+  if (last_block_arrive(sc.tickets + T_CG_INIT)) {
+    const double trz = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 0, sh);
+    const double trr = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      st->rz = trz;
+      st->rnorm = sqrt(trr);
+      st->rpar = 0;
+      st->iters = 0;
+      st->boundary = 0;
+      st->fail = 0;
+      st->exit_kind = 0;
+      const int cont = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
+      st->cont = cont;
+      set_cond(cond, cont);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) cg_php_kernel(CgVectors v, CgState* st, Scratch sc,
+                                                       Cond cond) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  double acc = 0.0;
+  GRID_STRIDE(j, v.n) acc += v.p[j] * v.hp[j];
+  const double b = block_sum<kBlock>(acc, sh, true);
+  if (threadIdx.x == 0) sc.partials[blockIdx.x] = b;
+  if (last_block_arrive(sc.tickets + T_CG_PHP)) {
+    const double php = reduce_partials<kBlock>(sc.partials, gridDim.x, 1, 0, sh);
+    if (threadIdx.x == 0) {
+      st->iters += 1;
+      st->php = php;
+      if (!(php > 0.0)) {  // tron.cpp:72-75 non-positive curvature
+        st->fail = 1;
+        st->cont = 0;
+        set_cond(cond, 0);
+      } else {
+        st->alpha = st->rz / php;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) cg_update_kernel(CgVectors v, CgState* st, Scratch sc,
+                                                          Cond cond) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  if (st->fail) return;  // uniform across the grid
+  const double alpha = st->alpha;
+  const double* rc = st->rpar ? v.r1 : v.r0;
+  double* rn = st->rpar ? v.r0 : v.r1;
+  double dd = 0.0, rz = 0.0, rr = 0.0;
+  GRID_STRIDE(j, v.n) {
+    const double dj = v.d[j] + alpha * v.p[j];  // tron.cpp:77
+    v.d[j] = dj;
+    dd += dj * dj;
+    const double r = rc[j] + (-alpha) * v.hp[j];  // tron.cpp:91 (speculative)
+    rn[j] = r;
+    const double z = v.M ? r / v.M[j] : r;
+    rz += r * z;
+    rr += r * r;
+  }
+  const double a = block_sum<kBlock>(dd, sh, true);
+  const double b = block_sum<kBlock>(rz, sh, true);
+  const double c = block_sum<kBlock>(rr, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[3 * blockIdx.x] = a;
+    sc.partials[3 * blockIdx.x + 1] = b;
+    sc.partials[3 * blockIdx.x + 2] = c;
+  }
+  if (last_block_arrive(sc.tickets + T_CG_UPD)) {
+    const double tdd = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 0, sh);
+    const double trz = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 1, sh);
+    const double trr = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 2, sh);
+    if (threadIdx.x == 0) {
+      if (sqrt(tdd) > st->delta) {  // tron.cpp:78
+        st->boundary = 1;
+        st->cont = 0;
+        set_cond(cond, 0);
+      } else {
+        st->beta = trz / st->rz;  // tron.cpp:93-95
+        st->rz = trz;
+        st->rpar ^= 1;
+        st->rnorm = sqrt(trr);
+        st->exit_kind = kCgMaxIters;
+        const int cont = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
+        st->cont = cont;
+        set_cond(cond, cont);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) cg_direction_kernel(CgVectors v, CgState* st,
+                                                             Scratch sc, Cond cond) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  if (st->fail) return;
+  if (!st->boundary) {
+    const double beta = st->beta;
+    const double* r = st->rpar ? v.r1 : v.r0;
+    GRID_STRIDE(j, v.n) v.p[j] = zval(r, v.M, j) + beta * v.p[j];  // tron.cpp:96
+    return;
+  }
+  // Boundary: retreat, then solve for tau on ||d + tau p|| = delta (tron.cpp:78-90).
+  const double alpha = st->alpha;
+  double dp = 0.0, dd = 0.0, pp = 0.0;
+  GRID_STRIDE(j, v.n) {
+    const double pj = v.p[j];
+    const double dj = v.d[j] + (-alpha) * pj;
+    v.d[j] = dj;
+    dp += dj * pj;
+    dd += dj * dj;
+    pp += pj * pj;
+  }
+  const double a = block_sum<kBlock>(dp, sh, true);
+  const double b = block_sum<kBlock>(dd, sh, true);
+  const double c = block_sum<kBlock>(pp, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[3 * blockIdx.x] = a;
+    sc.partials[3 * blockIdx.x + 1] = b;
+    sc.partials[3 * blockIdx.x + 2] = c;
+  }
+  if (last_block_arrive(sc.tickets + T_CG_P)) {
+    const double tdp = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 0, sh);
+    const double tdd = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 1, sh);
+    const double tpp = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 2, sh);
+    if (threadIdx.x == 0) {
+      const double delta = st->delta;
+      const double rad = sqrt(tdp * tdp + tpp * (delta * delta - tdd));
+      st->tau = tdp >= 0.0 ? (delta * delta - tdd) / (tdp + rad) : (rad - tdp) / tpp;
+      st->exit_kind = kCgBoundary;
+      st->cont = 0;
+      set_cond(cond, 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) cg_post_kernel(CgVectors v, CgState* st, Scratch sc) {
+  __shared__ double sh[kBlock / kWarp + 1];
+  const bool boundary = st->boundary && !st->fail;
+  const double tau = st->tau;
+  double* r = st->rpar ? v.r1 : v.r0;
+  double dg = 0.0, dr = 0.0, dd = 0.0;
+  GRID_STRIDE(j, v.n) {
+    double dj = v.d[j];
+    double rj = r[j];
+    if (boundary) {
+      dj = dj + tau * v.p[j];          // tron.cpp:86
+      rj = rj + (-tau) * v.hp[j];      // tron.cpp:87
+      v.d[j] = dj;
+      r[j] = rj;
+    }
+    dg += dj * v.g[j];
+    dr += dj * rj;
+    dd += dj * dj;
+  }
+  const double a = block_sum<kBlock>(dg, sh, true);
+  const double b = block_sum<kBlock>(dr, sh, true);
+  const double c = block_sum<kBlock>(dd, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[3 * blockIdx.x] = a;
+    sc.partials[3 * blockIdx.x + 1] = b;
+    sc.partials[3 * blockIdx.x + 2] = c;
+  }
+  if (last_block_arrive(sc.tickets + T_CG_POST)) {
+    const double tdg = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 0, sh);
+    const double tdr = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 1, sh);
+    const double tdd = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 2, sh);
+    if (threadIdx.x == 0) {
+      // tron.cpp:99-103 exit classification
+      if (st->iters >= st->max_iters && st->exit_kind != kCgBoundary &&
+          st->rnorm > st->stop)
+        st->exit_kind = kCgMaxIters;
+      else if (st->exit_kind != kCgBoundary)
+        st->exit_kind = kCgConverged;
+      st->q = 0.5 * (tdg - tdr);  // tron.cpp:106
+      st->dnorm = sqrt(tdd);
+    }
+  }
+}
+
+// ---------------- small-n CG (single block) ----------------
+
+constexpr int kSmallBlock = 512;
+
+__device__ __forceinline__ double sblock_sum(double v, double* sh) {
+  return block_sum<kSmallBlock>(v, sh, true);
+}
+
+__device__ void small_finish(const CgVectors& v, CgState* st, double* sh) {
+  // exit classification + q(d) + ||d|| (tron.cpp:99-106)
+  const double* r = st->rpar ? v.r1 : v.r0;
+  double dg = 0.0, dr = 0.0, dd = 0.0;
+  for (long long j = threadIdx.x; j < v.n; j += kSmallBlock) {
+    dg += v.d[j] * v.g[j];
+    dr += v.d[j] * r[j];
+    dd += v.d[j] * v.d[j];
+  }
+  dg = sblock_sum(dg, sh);
+  dr = sblock_sum(dr, sh);
+  dd = sblock_sum(dd, sh);
+  if (threadIdx.x == 0) {
+    if (st->iters >= st->max_iters && st->exit_kind != kCgBoundary && st->rnorm > st->stop)
+      st->exit_kind = kCgMaxIters;
+    else if (st->exit_kind != kCgBoundary)
+      st->exit_kind = kCgConverged;
+    st->q = 0.5 * (dg - dr);
+    st->dnorm = sqrt(dd);
+  }
+}
+
+__global__ void __launch_bounds__(kSmallBlock) cg_small_init_kernel(CgVectors v, CgState* st,
+                                                                    Cond cond) {
+  __shared__ double sh[kSmallBlock / kWarp + 1];
+  double rz = 0.0, rr = 0.0;
+  for (long long j = threadIdx.x; j < v.n; j += kSmallBlock) {
+    v.d[j] = 0.0;
+    const double r = -v.g[j];
+    v.r0[j] = r;
+    const double z = v.M ? r / v.M[j] : r;
+    v.p[j] = z;
+    rz += r * z;
+    rr += r * r;
+  }
+  rz = sblock_sum(rz, sh);
+  rr = sblock_sum(rr, sh);
+  __shared__ int s_cont;
+  if (threadIdx.x == 0) {
+    st->rz = rz;
+    st->rnorm = sqrt(rr);
+    st->rpar = 0;
+    st->iters = 0;
+    st->boundary = 0;
+    st->fail = 0;
+    st->exit_kind = kCgConverged;
+    s_cont = (0 < st->max_iters) && !(st->rnorm <= st->stop);
+    st->cont = s_cont;
+    set_cond(cond, s_cont);
+  }
+  __syncthreads();
+  if (!s_cont) small_finish(v, st, sh);
+}
+
+template <int SPLIT>
+__global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
+                                                                    const double* partials,
+                                                                    int nparts, double scale,
+                                                                    CgState* st, Cond cond) {
+  __shared__ double sh[kSmallBlock / kWarp + 1];
+  __shared__ double s_part[kSmallBlock];
+  __shared__ int s_flag;
+  const long long n = v.n;
+  if (partials) {
+    // hp_j = p_j + scale * sum_b partials[b*n + j], fixed order (SPLIT lanes per j)
+    const int per = kSmallBlock / SPLIT;  // coordinates handled per pass
+    for (long long j0 = 0; j0 < n; j0 += per) {
+      const int jj = threadIdx.x % per, grp = threadIdx.x / per;
+      const long long j = j0 + jj;
+      double acc = 0.0;
+      if (j < n)
+        for (int b = grp; b < nparts; b += SPLIT) acc += __ldcg(partials + (long long)b * n + j);
+      s_part[threadIdx.x] = acc;
+      __syncthreads();
+      if (grp == 0 && j < n) {
+        double t = 0.0;
+        for (int g2 = 0; g2 < SPLIT; ++g2) t += s_part[g2 * per + jj];
+        v.hp[j] = v.p[j] + scale * t;
+      }
+      __syncthreads();
+    }
+  }
+  // php (tron.cpp:70-76)
+  double php = 0.0;
+  for (long long j = threadIdx.x; j < n; j += kSmallBlock) php += v.p[j] * v.hp[j];
+  php = sblock_sum(php, sh);
+  if (threadIdx.x == 0) {
+    st->iters += 1;
+    st->php = php;
+    s_flag = !(php > 0.0);
+    if (s_flag) {
+      st->fail = 1;
+      st->cont = 0;
+      set_cond(cond, 0);
+    } else {
+      st->alpha = st->rz / php;
+    }
+  }
+  __syncthreads();
+  if (s_flag) return;
+  const double alpha = st->alpha;
+  double dd = 0.0;
+  for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
+    const double dj = v.d[j] + alpha * v.p[j];
+    v.d[j] = dj;
+    dd += dj * dj;
+  }
+  dd = sblock_sum(dd, sh);
+  const bool boundary = sqrt(dd) > st->delta;  // uniform
+  double* r = st->rpar ? v.r1 : v.r0;
+  if (boundary) {
+    double dp = 0.0, d2 = 0.0, pp = 0.0;
+    for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
+      const double pj = v.p[j];
+      const double dj = v.d[j] + (-alpha) * pj;
+      v.d[j] = dj;
+      dp += dj * pj;
+      d2 += dj * dj;
+      pp += pj * pj;
+    }
+    dp = sblock_sum(dp, sh);
+    d2 = sblock_sum(d2, sh);
+    pp = sblock_sum(pp, sh);
+    const double delta = st->delta;
+    const double rad = sqrt(dp * dp + pp * (delta * delta - d2));
+    const double tau = dp >= 0.0 ? (delta * delta - d2) / (dp + rad) : (rad - dp) / pp;
+    for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
+      v.d[j] = v.d[j] + tau * v.p[j];
+      r[j] = r[j] + (-tau) * v.hp[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      st->tau = tau;
+      st->boundary = 1;
+      st->exit_kind = kCgBoundary;
+      st->cont = 0;
+      set_cond(cond, 0);
+    }
+    __syncthreads();
+    small_finish(v, st, sh);
+    return;
+  }
+  double rz = 0.0, rr = 0.0;
+  for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
+    const double rj = r[j] + (-alpha) * v.hp[j];
+    r[j] = rj;
+    const double z = v.M ? rj / v.M[j] : rj;
+    rz += rj * z;
+    rr += rj * rj;
+  }
+  rz = sblock_sum(rz, sh);
+  rr = sblock_sum(rr, sh);
+  const double beta = rz / st->rz;
+  for (long long j = threadIdx.x; j < n; j += kSmallBlock)
+    v.p[j] = zval(r, v.M, j) + beta * v.p[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->beta = beta;
+    st->rz = rz;
+    st->rnorm = sqrt(rr);
+    st->exit_kind = kCgMaxIters;
+    s_flag = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
+    st->cont = s_flag;
+    set_cond(cond, s_flag);
+  }
+  __syncthreads();
+  if (!s_flag) small_finish(v, st, sh);
+}
+
+}  // namespace
+
+void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjScalars* obj,
+                  Scratch sc, cudaStream_t s) {
+  axpy_dot_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, w, d, wc, obj, sc);
+}
+
+void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s) {
+  norm_check_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, g, obj, sc);
+}
+
+void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {
+  epilogue_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, raw, epi, out);
+}
+
+void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
+  cg_init_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+}
+void cg_large_php(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
+  cg_php_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+}
+void cg_large_update(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
+  cg_update_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+}
+void cg_large_direction(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
+  cg_direction_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+}
+void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s) {
+  cg_post_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc);
+}
+
+void cg_small_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s) {
+  cg_small_init_kernel<<<1, kSmallBlock, 0, s>>>(v, st, cond);
+}
+
+void cg_small_step(const CgVectors& v, const double* partials, int nparts, double scale,
+                   CgState* st, Cond cond, cudaStream_t s) {
+  if (v.n <= 32)
+    cg_small_step_kernel<16><<<1, kSmallBlock, 0, s>>>(v, partials, nparts, scale, st, cond);
+  else if (v.n <= 64)
+    cg_small_step_kernel<8><<<1, kSmallBlock, 0, s>>>(v, partials, nparts, scale, st, cond);
+  else
+    cg_small_step_kernel<1><<<1, kSmallBlock, 0, s>>>(v, partials, nparts, scale, st, cond);
+}
+
+}  // namespace tb
