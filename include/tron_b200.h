@@ -71,7 +71,9 @@ typedef struct {
   uint64_t n_iterations;
   int32_t converged;
   int32_t status;
-  uint64_t hessian_products; /* device Hv launches during the solve */
+  uint64_t hessian_products; /* device Hv products during the solve */
+  double device_ms;          /* CUDA-event time of the solve on the context's stream
+                                (inputs resident; excludes the final copy of w to the host) */
 } tron_solve_info;
 
 /* TransferLedger (backend.hpp:32-43): the GPU is the staging domain the

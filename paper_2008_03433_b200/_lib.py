@@ -39,7 +39,7 @@ class tron_solve_info(ctypes.Structure):
                 ("objective", c_double), ("accepted_steps", c_uint64),
                 ("gradient_materializations", c_uint64), ("objective_evaluations", c_uint64),
                 ("n_iterations", c_uint64), ("converged", c_int32), ("status", c_int32),
-                ("hessian_products", c_uint64)]
+                ("hessian_products", c_uint64), ("device_ms", c_double)]
 
 
 class tron_ledger(ctypes.Structure):

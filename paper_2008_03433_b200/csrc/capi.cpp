@@ -1,6 +1,7 @@
 // extern "C" entry points of libtron_b200.so (declared in include/tron_b200.h).
 // C++ exceptions never cross this boundary: each call maps them to a
 // tron_status and records the message for tron_gpu_last_error().
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -268,6 +269,7 @@ int tron_gpu_solve(tron_gpu_ctx* ctx, const tron_config* cfg, const double* w0, 
   if (cfg) c = *cfg;
   std::memset(info, 0, sizeof(*info));
   if (c.solve_mode == TRON_SOLVE_HOST_CG) {
+    const auto t0 = std::chrono::steady_clock::now();
     int st = TRON_OK;
     tron_b200::SolverTrace partial;
     bool have_partial = false;
@@ -291,6 +293,8 @@ int tron_gpu_solve(tron_gpu_ctx* ctx, const tron_config* cfg, const double* w0, 
     });
     if (have_partial) fill_trace(partial, info, trace, trace_cap);
     info->status = st;
+    info->device_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return st;
   }
   const int st = guarded([&] { ctx->engine->solve_device(c, w0, w_out, info, trace, trace_cap); });

@@ -32,8 +32,46 @@ __device__ __forceinline__ double log1p_exp_neg(double t) {  // loss.hpp:99-102
   return -t + log1p(exp(t));
 }
 
+// Streaming loads of matrix entries: read once per pass, keep them out of L1
+// so the gathered vector (u or p) keeps the cache.
+__device__ __forceinline__ int ldg_stream(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // CSR forward pass: groups of G lanes per row.
+// Lane `sub` of the group sums entries sub, sub+G, ... of the row; four
+// entries are loaded before any gathered v_j is consumed (latency hiding).
+template <int G>
+__device__ __forceinline__ double row_dot_sub(const CsrView& X, long long row, int sub,
+                                              const double* __restrict__ v) {
+  const int beg = X.ptr[row], end = X.ptr[row + 1];
+  double s = 0.0;
+  int k = beg + sub;
+  for (; k + 3 * G < end; k += 4 * G) {
+    int c[4];
+    double a[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      c[m] = ldg_stream(X.idx + k + m * G);
+      a[m] = ldg_stream(X.val + k + m * G);
+    }
+    double b[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) b[m] = __ldg(v + c[m]);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) s += a[m] * b[m];
+  }
+  for (; k < end; k += G) s += ldg_stream(X.val + k) * __ldg(v + ldg_stream(X.idx + k));
+  return s;
+}
 // ---------------------------------------------------------------------------
 template <int G, int LOSS>
 __global__ void __launch_bounds__(kBlock) csr_forward_kernel(CsrView X, const double* __restrict__ w,
@@ -54,8 +92,7 @@ __global__ void __launch_bounds__(kBlock) csr_forward_kernel(CsrView X, const do
     const long long row = r0 + lane / G;
     double s = 0.0;
     if (row < X.rows) {
-      const int beg = X.ptr[row], end = X.ptr[row + 1];
-      for (int k = beg + sub; k < end; k += G) s += X.val[k] * __ldg(w + X.idx[k]);
+      s = row_dot_sub<G>(X, row, sub, w);
     }
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
@@ -113,8 +150,7 @@ __global__ void __launch_bounds__(kBlock) csr_dv_kernel(CsrView X, const double*
     if (active && mask) active = mask[row] != 0;
     double s = 0.0;
     if (active) {
-      const int beg = X.ptr[row], end = X.ptr[row + 1];
-      for (int k = beg + sub; k < end; k += G) s += X.val[k] * __ldg(p + X.idx[k]);
+      s = row_dot_sub<G>(X, row, sub, p);
     }
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
@@ -176,10 +212,31 @@ __global__ void __launch_bounds__(kBlock) merge_spmv_kernel(CsrView A, MergeView
   const int nz = P.tile_nz[t + 1] - y0;
   const int tid = threadIdx.x;
 
-  for (int i = tid; i < nr; i += kBlock) s_end[i] = A.ptr[x0 + 1 + i];
-  for (int i = tid; i < nz; i += kBlock) {
-    const int k = y0 + i;
-    s_val[i] = weight<UK, SQ>(U, A.idx[k], A.val[k]);
+  // Stage the tile: all loads of a thread are issued before any is consumed
+  // (kIpt coalesced idx/val loads in flight, then kIpt independent gathers).
+  {
+    int ridx[kIpt];
+    double rval[kIpt];
+#pragma unroll
+    for (int m = 0; m < kIpt; ++m) {
+      const int i = tid + m * kBlock;
+      const bool ok = i < nz;
+      ridx[m] = ok ? ldg_stream(A.idx + y0 + i) : 0;
+      rval[m] = ok ? ldg_stream(A.val + y0 + i) : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < kIpt; ++m) {
+      const int i = tid + m * kBlock;
+      if (i < nr) s_end[i] = __ldg(A.ptr + x0 + 1 + i);
+    }
+    double w[kIpt];
+#pragma unroll
+    for (int m = 0; m < kIpt; ++m) w[m] = (tid + m * kBlock < nz) ? weight<UK, SQ>(U, ridx[m], rval[m]) : 0.0;
+#pragma unroll
+    for (int m = 0; m < kIpt; ++m) {
+      const int i = tid + m * kBlock;
+      if (i < nz) s_val[i] = w[m];
+    }
   }
   __syncthreads();
 

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -170,7 +171,10 @@ void Engine::common_alloc() {
   if (!dense_) a_.alloc(ll);
   if (dense_) parts_.alloc((size_t)dense_grid(l_) * nn);
   small_engine_ = dense_ || n_ <= kSmallCgMaxN;
-  use_graphs_ = !comm_.active();
+  // TRON_B200_NO_GRAPH=1 runs the CG loop host-driven (per-kernel profiling:
+  // ncu cannot profile kernel nodes of graphs with conditional nodes).
+  const char* ng = std::getenv("TRON_B200_NO_GRAPH");
+  use_graphs_ = !comm_.active() && !(ng && ng[0] == '1');
 }
 
 std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, const int64_t* ro,
@@ -808,7 +812,18 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   std::memset(info, 0, sizeof(*info));
   const uint64_t launches0 = launches;
   uint64_t hv_count = 0;
+  cudaEvent_t ev0, ev1;
+  cuda_check(cudaEventCreate(&ev0), "event");
+  cuda_check(cudaEventCreate(&ev1), "event");
+  cuda_check(cudaEventRecord(ev0, s_), "event record");
   auto finish = [&](int status) {
+    cudaEventRecord(ev1, s_);
+    cudaEventSynchronize(ev1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    info->device_ms = ms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (w_out && n_ > 0) {
       cuda_check(cudaMemcpyAsync(w_out, slot_[cand_ ^ 1].w.p, n_ * 8, cudaMemcpyDeviceToHost, s_),
                  "D2H");
@@ -829,10 +844,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   info->objective_evaluations = 1;
   if (!std::isfinite(f)) {
     // w_out must reflect the starting point like the reference's result.w
-    if (w_out && n_ > 0) {
-      if (w0) std::memcpy(w_out, w0, n_ * 8); else std::memset(w_out, 0, n_ * 8);
-    }
-    info->status = TRON_ERR_NUMERICAL;
+    finish(TRON_ERR_NUMERICAL);
     raise(TRON_ERR_NUMERICAL, "objective is not finite at the starting point");
   }
   commit(nullptr);

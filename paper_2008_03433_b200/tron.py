@@ -166,6 +166,7 @@ class SolveResult:
     objective: float = 0.0
     converged: bool = False
     hessian_products: int = 0
+    device_ms: float = 0.0
 
 
 @dataclass
@@ -447,7 +448,8 @@ class GpuEvaluator:
                                                     bool(r.accepted), int(r.cg_iters), CgExit(r.cg_exit)))
         self._sync_ledger()
         _raise(st, trace)
-        return SolveResult(w, trace, info.objective, bool(info.converged), int(info.hessian_products))
+        return SolveResult(w, trace, info.objective, bool(info.converged), int(info.hessian_products),
+                           float(info.device_ms))
 
     # -- plumbing
     def ledger(self) -> TransferLedger:

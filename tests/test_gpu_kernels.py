@@ -1,0 +1,323 @@
+"""GPU parity of the hot-path kernels (fun / grad / Hv / preconditioner / CG)
+against the oracle, through the C ABI.  GPU twins of the reference KATs in
+proj/tests/test_loss.cpp and test_linalg.cpp, plus random-fixture parity.
+
+Tolerances: bit-exact where the reference's arithmetic order is reproduced
+(dense margins z, hence the L2-SVM active set); otherwise FP64 rounding
+level (<= 1e-12 relative, oracles::rel_err), since device reductions sum in
+a different (fixed) order than the reference's 64-block tree.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from paper_2008_03433_b200 import (BoundsError, BudgetExceededError, DimensionError, ExecutionPlan,
+                                   FeatureMatrix, LogicError, LossKind, Problem,
+                                   StrategyPreconditionError, SvmStrategy, TrustRegionConfig,
+                                   make_evaluator, synth)
+from paper_2008_03433_b200.tron import CgExit
+
+pytestmark = pytest.mark.gpu
+
+LR, SVM = LossKind.Logistic, LossKind.L2Svm
+
+
+def gpu(problem, loss, **kw):
+    return make_evaluator(problem, loss, ExecutionPlan.gpu(**kw))
+
+
+def dense(rows, cols, vals, y, C=1.0):
+    return Problem(FeatureMatrix.dense(rows, cols, vals), np.array(y, dtype=float), C)
+
+
+# ---------------------------------------------------------------- KATs (test_loss.cpp)
+
+def test_logistic_fused_pass_at_zero():  # test_loss.cpp:45-55
+    p = synth.testgen_dense_problem(5, 4, 3, 1.0)
+    with gpu(p, LR) as ev:
+        f = ev.eval_candidate(np.zeros(3))
+        assert rel_err(f, 4 * math.log(2.0)) <= 1e-14
+        s = ev.candidate_state()
+        assert np.all(s.z == 0.0)
+        assert np.all(s.dvec == 0.25)
+        assert np.array_equal(s.zhat, -p.y / 2.0)
+
+
+def test_logistic_saturates_cleanly():  # test_loss.cpp:57-78
+    p = dense(2, 1, [1000.0, 1000.0], [1.0, -1.0])
+    with gpu(p, LR) as ev:
+        f = ev.eval_candidate([2.0])
+        s = ev.candidate_state()
+        assert s.zhat[0] == 0.0 and s.dvec[0] == 0.0
+        assert s.zhat[1] == 1.0 and s.dvec[1] == 0.0
+        assert math.isfinite(f)
+    q = dense(2, 1, [1000.0, 500.0], [1.0, 1.0])
+    with gpu(q, LR) as ev:
+        assert ev.eval_candidate([2.0]) == 0.5 * 4.0
+
+
+def test_logistic_one_by_one():  # test_loss.cpp:80-91
+    p = dense(1, 1, [1.0], [1.0], C=2.0)
+    with gpu(p, LR) as ev:
+        f = ev.eval_candidate([1.0])
+        assert rel_err(f, 0.5 + 2.0 * math.log1p(math.exp(-1.0))) <= 1e-12
+        ev.commit()
+        g = ev.gradient()
+        assert rel_err(g[0], 1.0 - 2.0 / (1.0 + math.exp(1.0))) <= 1e-12
+
+
+def test_logistic_hessian_basics():  # test_loss.cpp:139-165
+    p = synth.testgen_dense_problem(41, 6, 4, 2.0)
+    w = synth.testgen_random_vector(42, 4)
+    with gpu(p, LR) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        assert np.array_equal(ev.hessian_vec(np.zeros(4)), np.zeros(4))
+    zero = dense(3, 2, [0.0] * 6, [1.0, -1.0, 1.0], C=5.0)
+    with gpu(zero, LR) as ev:
+        ev.eval_candidate([1.0, 2.0])
+        ev.commit()
+        assert np.array_equal(ev.hessian_vec([0.5, -0.25]), [0.5, -0.25])
+    eye = dense(2, 2, [1.0, 0.0, 0.0, 1.0], [1.0, -1.0])
+    with gpu(eye, LR) as ev:
+        ev.eval_candidate([0.0, 0.0])
+        ev.commit()
+        out = ev.hessian_vec([1.0, 1.0])
+        assert rel_err(out[0], 1.25) <= 1e-15 and rel_err(out[1], 1.25) <= 1e-15
+
+
+def test_svm_active_set_kats():  # test_loss.cpp:167-209
+    p = synth.testgen_dense_problem(51, 5, 3, 1.0)
+    with gpu(p, SVM) as ev:
+        assert ev.eval_candidate(np.zeros(3)) == 5.0
+        assert ev.candidate_state().active.size == 5
+    q = dense(3, 1, [1.0, 2.0, 1.0], [1.0, 1.0, -1.0], C=7.0)
+    with gpu(q, SVM) as ev:
+        ev.eval_candidate([1.0])
+        assert list(ev.candidate_state().active) == [2]
+    r = dense(3, 1, [1.0, 2.0, 1.0], [1.0, 1.0, 1.0], C=7.0)
+    with gpu(r, SVM) as ev:
+        assert ev.eval_candidate([1.0]) == 0.5
+        assert ev.candidate_state().active.size == 0
+    one = dense(1, 1, [1.0], [1.0])
+    with gpu(one, SVM) as ev:
+        ev.eval_candidate([1.0 - 1e-9])
+        assert ev.candidate_state().active.size == 1
+        ev.eval_candidate([1.0])
+        assert ev.candidate_state().active.size == 0
+        ev.eval_candidate([1.0 + 1e-9])
+        assert ev.candidate_state().active.size == 0
+
+
+def test_svm_gradient_and_hessian_kats():  # test_loss.cpp:211-259
+    q = dense(1, 1, [1.0], [1.0], C=3.0)
+    with gpu(q, SVM) as ev:
+        ev.eval_candidate([2.0])
+        ev.commit()
+        assert np.array_equal(ev.gradient(), [2.0])  # empty active set
+    r = dense(1, 1, [1.0], [1.0])
+    with gpu(r, SVM) as ev:
+        ev.eval_candidate([0.5])
+        ev.commit()
+        assert np.array_equal(ev.gradient(), [-0.5])
+    # active = {0, 2} of a 3x2 problem, v = (1, 0) -> (5, 2)
+    p = dense(3, 2, [1.0, 0.0, 0.0, 1.0, 1.0, 1.0], [1.0, 1.0, -1.0])
+    with gpu(p, SVM) as ev:
+        ev.eval_candidate([0.0, 0.0])  # all margins 1 -> I = {0,1,2}
+        ev.commit()
+        out = ev.hessian_vec([1.0, 0.0])
+        assert np.array_equal(out, [1.0 + 2.0 * 2.0, 2.0 * 1.0])
+
+
+def test_preconditioner_kats():  # test_loss.cpp:278-298
+    zero = dense(2, 3, [0.0] * 6, [1.0, -1.0], C=4.0)
+    with gpu(zero, LR) as ev:
+        ev.eval_candidate(np.zeros(3))
+        ev.commit()
+        assert np.array_equal(ev.precond_diagonal(), np.ones(3))
+    p = dense(1, 1, [2.0], [1.0])
+    with gpu(p, LR) as ev:
+        ev.eval_candidate([0.0])
+        ev.commit()
+        assert np.array_equal(ev.precond_diagonal(), [2.0])
+    with gpu(p, SVM) as ev:
+        ev.eval_candidate([0.0])
+        ev.commit()
+        assert np.array_equal(ev.precond_diagonal(), [1.0 + 2.0 * 4.0])
+
+
+# ---------------------------------------------------------------- random-fixture parity
+
+def _fixtures():
+    out = []
+    for seed in range(3):
+        out.append(("dense", synth.testgen_dense_problem(300 + seed, 257, 13, 0.5 + seed)))
+        out.append(("sparse", synth.testgen_sparse_problem(400 + seed, 611, 97, 1.5, 0.08)))
+    out.append(("dense40", synth.synth_dense(7, 3001, 40)))
+    out.append(("synth", synth.synth_sparse(9, 2000, 5000, 37)))
+    out.append(("wide", synth.testgen_dense_problem(77, 50, 70, 1.0)))  # n > 64: CSR path
+    return out
+
+
+@pytest.mark.parametrize("case", range(9))
+@pytest.mark.parametrize("loss", [LR, SVM])
+def test_fun_grad_hv_precond_parity(port, case, loss):
+    name, p = _fixtures()[case]
+    n = p.X.cols
+    w = synth.testgen_random_vector(1000 + case, n, 0.3)
+    v = synth.testgen_random_vector(2000 + case, n, 1.0)
+    want = port.logistic(p, w, v) if loss == LR else port.svm(p, w, v)
+    with gpu(p, loss) as ev:
+        f = ev.eval_candidate(w)
+        assert rel_err(f, want["f"]) <= 1e-13, name
+        s = ev.candidate_state()
+        if p.X.layout == "dense" and n <= 64:
+            assert np.array_equal(s.z, want["z"]), "dense margins must be bit-exact"
+        else:
+            assert rel_err(s.z, want["z"]) <= 1e-14
+        if loss == SVM:
+            assert np.array_equal(s.active, want["active"]), "active set must be identical"
+        else:
+            assert rel_err(s.zhat, want["zhat"]) <= 1e-13
+            assert rel_err(s.dvec, want["dvec"]) <= 1e-13
+        gn = ev.commit()
+        g = ev.gradient()
+        assert rel_err(g, want["g"]) <= 1e-12, name
+        assert rel_err(gn, np.linalg.norm(want["g"])) <= 1e-12
+        assert rel_err(ev.hessian_vec(v), want["hv"]) <= 1e-12, name
+        assert rel_err(ev.precond_diagonal(), want["M"]) <= 1e-12, name
+        # committed state is the candidate we evaluated
+        cs = ev.committed_state()
+        assert rel_err(cs.z, want["z"]) <= 1e-14
+
+
+def test_csc_transposed_product_zipf_columns(port):
+    # Zipf-hot columns span many merge-path tiles; empty columns must emit w_j.
+    p = synth.synth_sparse(3, 6000, 20000, 12)
+    w = np.zeros(p.X.cols)
+    want = port.logistic(p, w)
+    with gpu(p, LR) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        g = ev.gradient()
+    assert rel_err(g, want["g"]) <= 1e-12
+    cols_used = np.zeros(p.X.cols, bool)
+    cols_used[p.X.col_indices] = True
+    assert np.all(g[~cols_used] == 0.0)
+
+
+def test_gradient_deterministic_across_runs():
+    p = synth.synth_sparse(5, 3000, 8000, 20)
+    w = synth.testgen_random_vector(6, p.X.cols, 0.1)
+    outs = []
+    for _ in range(2):
+        with gpu(p, LR) as ev:
+            ev.eval_candidate(w)
+            ev.commit()
+            outs.append((ev.gradient(), ev.hessian_vec(w), ev.precond_diagonal()))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- device CG
+
+@pytest.mark.parametrize("case", [0, 1, 6, 7])
+@pytest.mark.parametrize("precond", [False, True])
+def test_device_cg_matches_host_cg(port, case, precond):
+    name, p = _fixtures()[case]
+    n = p.X.cols
+    w = synth.testgen_random_vector(3000 + case, n, 0.3)
+    with gpu(p, LR) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        g = ev.gradient()
+        M = ev.precond_diagonal() if precond else None
+        # SYNTH dense (2-decade column scales) is ill-conditioned: beyond ~12 CG
+        # iterations rounding differences grow ~10x per iteration in any two
+        # FP64 implementations, so that case runs at TRON's own cg_tol (0.1).
+        cg_tol = 0.1 if name == "dense40" else 1e-6
+        for delta, tol in ((1e6, 1e-10), (0.5 * np.linalg.norm(g), 1e-10), (1e-3, 1e-10)):
+            cfg = TrustRegionConfig(cg_tol=cg_tol, use_preconditioner=precond)
+            dev = ev.truncated_cg(delta, cfg)
+            host = port.truncated_cg(g, ev.hessian_vec, delta, M, cg_tol=cg_tol)
+            assert dev.iters == host["iters"], name
+            assert int(dev.exit) == host["exit"], name
+            assert rel_err(dev.d, host["d"]) <= tol, name
+            assert rel_err(dev.model_value, host["model_value"]) <= 1e-9, name
+            assert np.linalg.norm(dev.d) <= delta * (1 + 1e-12)
+
+
+def test_device_cg_iteration_cap():  # test_tron.cpp:75-90
+    p = synth.testgen_dense_problem(1100, 30, 6, 1.0)
+    w = synth.testgen_random_vector(1101, 6)
+    with gpu(p, LR) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        res = ev.truncated_cg(1e6, TrustRegionConfig(max_cg_iters=1, cg_tol=1e-10))
+        assert res.iters == 1 and res.exit == CgExit.MaxIters and res.model_value < 0.0
+
+
+# ---------------------------------------------------------------- errors (error.hpp)
+
+def test_validation_errors():
+    with pytest.raises(DimensionError):
+        gpu(dense(2, 1, [1.0, 2.0], [1.0, 3.0]), LR)
+    with pytest.raises(DimensionError):
+        gpu(dense(2, 1, [1.0, 2.0], [1.0, -1.0], C=0.0), LR)
+    bad_col = Problem(FeatureMatrix("csr", 1, 2, np.array([1.0]), np.array([0, 1], np.int64),
+                                    np.array([5], np.int32)), np.array([1.0]))
+    with pytest.raises(BoundsError):
+        gpu(bad_col, LR)
+    unsorted = Problem(FeatureMatrix("csr", 1, 2, np.array([1.0, 2.0]), np.array([0, 2], np.int64),
+                                     np.array([1, 0], np.int32)), np.array([1.0]))
+    with pytest.raises(DimensionError):
+        gpu(unsorted, LR)
+
+
+def test_evaluator_misuse():  # test_backend.cpp:95-102
+    p = synth.testgen_dense_problem(2030, 10, 3, 1.0)
+    with gpu(p, LR) as ev:
+        with pytest.raises(LogicError):
+            ev.commit()
+        with pytest.raises(LogicError):
+            ev.hessian_vec([1.0, 2.0, 3.0])
+
+
+def test_gathered_budget_names_mix():  # test_backend.cpp:104-139
+    n = 18
+    p = synth.testgen_dense_problem(3100, 10000, n, 1.0)
+    with gpu(p, SVM, svm_strategy=SvmStrategy.Gathered, gathered_budget_bytes=1 << 20) as ev:
+        ev.eval_candidate(np.zeros(n))
+        with pytest.raises(BudgetExceededError) as e:
+            ev.commit()
+        assert "MixedActiveSet" in str(e.value)
+    for l in (100, 1000, 10000):
+        p = synth.testgen_dense_problem(3000 + l, l, n, 1.0)
+        plan = ExecutionPlan.gpu(svm_strategy=SvmStrategy.Gathered)
+        with make_evaluator(p, SVM, plan) as ev:
+            ev.eval_candidate(np.zeros(n))
+            ev.commit()
+            lg = ev.ledger()
+            assert lg.gathered_submatrix_bytes == l * n * 8
+            assert lg.index_set_bytes == l * 8
+
+
+def test_gathered_equals_indirect(port):
+    p = synth.testgen_dense_problem(71, 4000, 6, 1.5)
+    w = synth.testgen_random_vector(72, 6, 0.5)
+    outs = []
+    for strat in (SvmStrategy.Gathered, SvmStrategy.Indirect):
+        with gpu(p, SVM, svm_strategy=strat) as ev:
+            ev.eval_candidate(w)
+            ev.commit()
+            outs.append([ev.hessian_vec(synth.testgen_random_vector(90 + k, 6)) for k in range(5)])
+    for a, b in zip(*outs):
+        assert rel_err(a, b) <= 1e-12
+
+
+def test_gathered_csr_rejected():
+    p = synth.testgen_sparse_problem(1, 20, 10, 1.0, 0.3)
+    with pytest.raises(StrategyPreconditionError):
+        gpu(p, SVM, svm_strategy=SvmStrategy.Gathered)

@@ -1,0 +1,214 @@
+"""End-to-end TRON solves on the GPU vs the reference CPU solver on the same
+inputs (BASELINE.json parity gate): objective and w within 1e-6 relative,
+outer/accepted/CG iteration counts identical or within +-1, L2-SVM active
+set and test predictions identical.  Also the reference's solver-level
+properties (proj/tests/test_tron.cpp, test_backend.cpp) on the GPU backend.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from paper_2008_03433_b200 import (ExecutionPlan, FeatureMatrix, LossKind, NumericalFailureError,
+                                   Problem, SvmStrategy, TrustRegionConfig, make_evaluator, solve,
+                                   synth)
+
+pytestmark = pytest.mark.gpu
+
+LR, SVM = LossKind.Logistic, LossKind.L2Svm
+GOLDEN = {  # proj/tests/support/golden.hpp:10-17
+    "lr50x5": 23.2600071465565482846,
+    "lr200x20": 84.0054573043513978445,
+    "svm200x20": 88.1453447856914700312,
+}
+
+
+def plan(**kw):
+    return ExecutionPlan.gpu(**kw)
+
+
+def counts(trace):
+    its = trace.iterations if hasattr(trace, "iterations") else trace["iterations"]
+    if its and isinstance(its[0], dict):
+        return len(its), sum(r["accepted"] for r in its), sum(r["cg_iters"] for r in its)
+    return len(its), sum(r.accepted for r in its), sum(r.cg_iters for r in its)
+
+
+def predict(X, w):  # model.cpp:88-117: sign(x.w), ties -> +1
+    scores = X.to_dense() @ w if X.layout == "csr" else X.values.reshape(X.rows, X.cols) @ w
+    return np.where(scores < 0.0, -1.0, 1.0)
+
+
+def assert_parity(res, w_ref, t_ref, X=None, tol=1e-6):
+    assert rel_err(res.objective, t_ref["objective"]) <= tol
+    assert rel_err(res.w, w_ref) <= tol
+    o, a, c = counts(res.trace)
+    o2, a2, c2 = counts(t_ref)
+    assert abs(o - o2) <= 1 and abs(a - a2) <= 1 and abs(c - c2) <= 1, ((o, a, c), (o2, a2, c2))
+    assert res.converged == t_ref["converged"]
+    if X is not None:
+        assert np.array_equal(predict(X, res.w), predict(X, w_ref))
+
+
+@pytest.mark.parametrize("mode", ["device", "host_cg"])
+def test_golden_objectives(mode):  # test_tron.cpp:199-207, acceptance criterion 3
+    p = synth.testgen_dense_problem(1001, 50, 5, 1.0)
+    r = solve(p, LR, TrustRegionConfig(eps=1e-8), plan(solve_mode=mode))
+    assert r.converged and rel_err(r.objective, GOLDEN["lr50x5"]) <= 1e-6
+    for loss, seed, key in ((LR, 2001, "lr200x20"), (SVM, 3001, "svm200x20")):
+        p = synth.testgen_dense_problem(seed, 200, 20, 1.0)
+        r = solve(p, loss, TrustRegionConfig(eps=1e-8, max_outer_iters=100), plan(solve_mode=mode))
+        assert r.converged and rel_err(r.objective, GOLDEN[key]) <= 1e-6
+
+
+CASES = [
+    ("dense-lr", lambda: synth.testgen_dense_problem(1300, 60, 8, 4.0), LR, 1e-6),
+    ("dense-svm", lambda: synth.testgen_dense_problem(1300, 60, 8, 4.0), SVM, 1e-6),
+    ("sparse-lr", lambda: synth.testgen_sparse_problem(3400, 400, 60, 2.0, 0.15), LR, 1e-7),
+    ("sparse-svm", lambda: synth.testgen_sparse_problem(3400, 400, 60, 2.0, 0.15), SVM, 1e-7),
+    ("crit4-lr", lambda: synth.testgen_sparse_problem(6000, 10000, 500, 1.0, 0.02), LR, 1e-4),
+    ("crit4-svm", lambda: synth.testgen_dense_problem(6001, 10000, 18, 1.0), SVM, 1e-4),
+    ("scaled-lr", lambda: synth.testgen_dense_problem_scaled(117, 80, 8, 1000.0, 20.0), LR, 1e-6),
+    ("scaled-svm", lambda: synth.testgen_dense_problem_scaled(117, 80, 8, 1000.0, 20.0), SVM, 1e-6),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+@pytest.mark.parametrize("precond", [False, True])
+@pytest.mark.parametrize("mode", ["device", "host_cg"])
+def test_solve_parity_vs_reference(ref, case, precond, mode):
+    name, mk, loss, eps = CASES[case]
+    p = mk()
+    cfg = TrustRegionConfig(eps=eps, use_preconditioner=precond)
+    w_ref, t_ref = ref.solve(p, 0 if loss == LR else 1, cfg)
+    r = solve(p, loss, cfg, plan(solve_mode=mode))
+    assert_parity(r, w_ref, t_ref, X=p.X)
+    # lazy-gradient contract (acceptance criterion 6)
+    assert r.trace.gradient_materializations == r.trace.accepted_steps + 1
+    assert r.trace.objective_evaluations == len(r.trace.iterations) + 1
+    if loss == SVM:
+        with make_evaluator(p, SVM, plan()) as ev:
+            ev.eval_candidate(r.w)
+            got = ev.candidate_state().active
+        want = ref.svm(p, w_ref, np.zeros(p.X.cols))["active"]
+        assert np.array_equal(got, want)
+
+
+def test_synth_r1_full_size(ref):
+    """rcv1-shaped SYNTH-v1 (BASELINE.json configs[0]) at full size."""
+    p = synth.make_shape("R1")
+    cfg = TrustRegionConfig(eps=0.01)
+    w_ref, t_ref = ref.solve(p, 0, cfg, backend=1, workers=8)
+    assert rel_err(t_ref["objective"], 1.097269983508039e04) <= 1e-15
+    r = solve(p, LR, cfg, plan())
+    assert_parity(r, w_ref, t_ref)
+    assert counts(r.trace) == counts(t_ref)
+
+
+def test_synth_p1_reduced_rows_active_set(ref):
+    """proteomics-shaped dense L2-SVM (configs[2]) at 2e5 rows: active set + predictions."""
+    p = synth.synth_dense(1, 200_000, 40)
+    cfg = TrustRegionConfig(eps=0.01)
+    w_ref, t_ref = ref.solve(p, 1, cfg, backend=1, workers=8)
+    r = solve(p, SVM, cfg, plan())
+    assert_parity(r, w_ref, t_ref, X=p.X)
+    with make_evaluator(p, SVM, plan()) as ev:
+        ev.eval_candidate(w_ref)  # same w: the active set must be bit-identical
+        got = ev.candidate_state().active
+    want = ref.svm(p, w_ref, np.zeros(40))["active"]
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- solver properties
+
+def test_stationary_start_and_quadratic():  # test_tron.cpp:159-197
+    l, n = 4, 3
+    y = np.ones(l)
+    y[0::2] = -1.0
+    p = Problem(FeatureMatrix.dense(l, n, np.zeros(l * n)), y, 1.0)
+    r = solve(p, LR, TrustRegionConfig(), plan())
+    assert r.converged and not r.trace.iterations
+    assert rel_err(r.objective, 4 * math.log(2.0)) <= 1e-14
+    q = Problem(FeatureMatrix.dense(3, 4, np.zeros(12)), np.array([-1.0, 1.0, -1.0]), 2.0)
+    r = solve(q, LR, TrustRegionConfig(eps=1e-12), plan(), warm_start=[1.0, -2.0, 0.5, 3.0])
+    assert r.converged and len(r.trace.iterations) == 1
+    assert r.trace.iterations[0].accepted
+    assert abs(r.trace.iterations[0].sigma - 1.0) <= 1e-12
+    assert np.linalg.norm(r.w) <= 1e-12
+
+
+def test_symmetric_two_point():  # test_tron.cpp:171-182
+    p = Problem(FeatureMatrix.dense(2, 1, [1.0, 1.0]), np.array([1.0, -1.0]), 1.0)
+    r = solve(p, LR, TrustRegionConfig(eps=1e-10), plan())
+    assert r.converged and abs(r.w[0]) <= 1e-10
+
+
+def test_descent_and_stopping_rule():  # test_tron.cpp:209-236
+    for loss in (LR, SVM):
+        p = synth.testgen_dense_problem(1300, 60, 8, 4.0)
+        cfg = TrustRegionConfig(eps=1e-6)
+        pl = plan()
+        r = solve(p, loss, cfg, pl)
+        assert r.converged
+        last = r.trace.f_initial
+        for rec in r.trace.iterations:
+            if rec.accepted:
+                assert rec.f_candidate < last
+                last = rec.f_candidate
+        assert pl.ledger.gradient_materializations == r.trace.accepted_steps + 1
+        with make_evaluator(p, loss, plan()) as ev:
+            ev.eval_candidate(r.w)
+            ev.commit()
+            assert np.linalg.norm(ev.gradient()) <= cfg.eps * r.trace.gradient_norm_initial * (1 + 1e-12)
+
+
+def test_determinism():  # test_tron.cpp:264-274
+    p = synth.testgen_sparse_problem(1500, 120, 30, 2.0, 0.2)
+    cfg = TrustRegionConfig(eps=1e-7)
+    a = solve(p, SVM, cfg, plan())
+    b = solve(p, SVM, cfg, plan())
+    assert a.trace == b.trace and np.array_equal(a.w, b.w)
+
+
+def test_preconditioning_neutrality():  # test_tron.cpp:276-290
+    for loss in (LR, SVM):
+        p = synth.testgen_dense_problem(1600, 80, 10, 2.0)
+        off = solve(p, loss, TrustRegionConfig(eps=1e-8), plan())
+        on = solve(p, loss, TrustRegionConfig(eps=1e-8, use_preconditioner=True), plan())
+        assert off.converged and on.converged
+        assert rel_err(on.objective, off.objective) <= 1e-8
+
+
+@pytest.mark.parametrize("mode", ["device", "host_cg"])
+def test_nonfinite_objective_aborts(mode):  # test_tron.cpp:292-304
+    p = synth.testgen_dense_problem(1700, 10, 3, 1.0)
+    with pytest.raises(NumericalFailureError) as e:
+        solve(p, LR, TrustRegionConfig(), plan(solve_mode=mode), warm_start=[1e200] * 3)
+    assert e.value.trace.objective_evaluations == 1
+
+
+def test_outer_cap():  # test_tron.cpp:306-315
+    p = synth.testgen_dense_problem(1800, 60, 8, 50.0)
+    r = solve(p, LR, TrustRegionConfig(eps=1e-14, max_outer_iters=2), plan())
+    assert not r.converged and len(r.trace.iterations) == 2
+
+
+def test_gathered_vs_indirect_solve():  # test_backend.cpp:245-257
+    p = synth.testgen_dense_problem(3500, 200, 18, 1.0)
+    cfg = TrustRegionConfig(eps=1e-8)
+    pg = plan(svm_strategy=SvmStrategy.Gathered)
+    a = solve(p, SVM, cfg, pg)
+    b = solve(p, SVM, cfg, plan(svm_strategy=SvmStrategy.Indirect))
+    assert rel_err(a.w, b.w) <= 1e-10 and rel_err(a.objective, b.objective) <= 1e-10
+    assert pg.ledger.gathered_submatrix_bytes > 0
+
+
+def test_host_cg_ledger_schedule():  # test_backend.cpp:152-184 (staged semantics)
+    p = synth.testgen_dense_problem_scaled(117, 80, 8, 1000.0, 20.0)
+    pl = plan(solve_mode="host_cg")
+    r = solve(p, LR, TrustRegionConfig(eps=1e-6), pl)
+    assert pl.ledger.scalar_returns == r.trace.objective_evaluations
+    assert pl.ledger.margin_passes == r.trace.objective_evaluations
+    assert pl.ledger.bulk_handoffs == r.trace.accepted_steps + 1
+    assert any(not it.accepted for it in r.trace.iterations)
