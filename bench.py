@@ -330,7 +330,7 @@ def main():
         "outer_iterations": len(res.trace.iterations), "hessian_products": res.hessian_products,
         "hv_per_s": res.hessian_products / t_step if t_step > 0 else None,
         "wall_ms_per_step": float(np.mean(wall)) * 1e3,
-        "roofline": {"bound": "hbm", "kernel": "Hessian-vector product (CSR D*Xv + CSC merge-path X^T)",
+        "roofline": {"bound": "hbm", "kernel": "Hessian-vector product (CSR D*Xv + CSC segmented X^T u)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_kind, "traffic": read_traffic(args.workload),
                      "algorithmic_bytes_per_launch": ab["hv"], "avg_launch_ms": kt["hv_ms"],

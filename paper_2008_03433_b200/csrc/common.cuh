@@ -83,6 +83,46 @@ __device__ __forceinline__ double reduce_partials(const double* partials, int co
   return block_sum<BLOCK>(acc, sh, true);
 }
 
+// Copies `count` doubles global -> shared with TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx), issued by one thread; every
+// thread of the block returns once the bytes have landed.  `src` must be
+// 16-byte aligned (cudaMalloc'd vectors are).
+__device__ __forceinline__ void bulk_stage_f64(double* dst, const double* src, long long count) {
+  __shared__ __align__(8) unsigned long long mbar;
+  const long long full = count & ~1LL;  // 16-byte multiple handled by TMA
+  const unsigned bytes = (unsigned)(full * 8);
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                 : "memory");
+    const unsigned d0 = (unsigned)__cvta_generic_to_shared(dst);
+    constexpr unsigned kPiece = 32768;
+    for (unsigned off = 0; off < bytes; off += kPiece) {
+      const unsigned sz = bytes - off < kPiece ? bytes - off : kPiece;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              d0 + off),
+          "l"((const char*)src + off), "r"(sz), "r"(mb)
+          : "memory");
+    }
+    if (full < count) dst[full] = src[full];
+  }
+  __syncthreads();
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb)
+        : "memory");
+  }
+  __syncthreads();
+}
+
 #define TB_LAUNCH_CHECK() \
   do {                    \
   } while (0)

@@ -4,15 +4,11 @@
 //    (matvec, linalg.cpp:154-162) fused with the per-instance epilogues of
 //    logistic_fused_pass (loss.cpp:35-58), svm_fused_pass (loss.cpp:94-122)
 //    and the D-scaling of logistic_hessian_vec (loss.cpp:82-92).
-//  * csc_spmv: X^T u as a row product over the device-built CSC copy, i.e.
-//    the reference's matvec_transpose / masked_matvec_transpose /
-//    weighted_sq_col_sums (linalg.cpp:175-265) without its 64 private
-//    n-length buffers and serial merge.  Work is split by merge path
-//    (columns + nonzeros per 256-thread tile are constant), so Zipf-hot
-//    columns do not unbalance the grid; split columns are combined by a
-//    block-wide segmented scan and a fixed-order fix-up pass.  No atomics:
-//    results are bit-reproducible run to run.
+//  * build_csc: the device-built CSC copy (stable in row order) that
+//    csc_seg.cu streams for every X^T u.
 #include <cub/device/device_radix_sort.cuh>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -22,8 +18,9 @@ namespace tb {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kIpt = 8;                 // merge items per thread
-constexpr int kTile = kBlock * kIpt;    // merge items per tile
+constexpr int kStagedBlock = 512;                  // one 16-warp block per SM
+constexpr int kHotMax = 200 * 1024 / 8;            // staged prefix entries (200 KB)
+constexpr long long kStageMinNnz = 1 << 20;        // stage only for big passes
 
 int g_sm_count = 0;
 
@@ -47,52 +44,72 @@ __device__ __forceinline__ double ldg_stream(const double* p) {
 
 // ---------------------------------------------------------------------------
 // CSR forward pass: groups of G lanes per row.
-// Lane `sub` of the group sums entries sub, sub+G, ... of the row; four
+// Lane `sub` of the group sums entries sub, sub+G, ... of the row; eight
 // entries are loaded before any gathered v_j is consumed (latency hiding).
-template <int G>
+template <int G, bool STAGED>
 __device__ __forceinline__ double row_dot_sub(const CsrView& X, long long row, int sub,
-                                              const double* __restrict__ v) {
+                                              const double* __restrict__ v, const double* sv,
+                                              int hot) {
+  constexpr int U = 8;  // entries in flight per lane
   const int beg = X.ptr[row], end = X.ptr[row + 1];
   double s = 0.0;
-  int k = beg + sub;
-  for (; k + 3 * G < end; k += 4 * G) {
-    int c[4];
-    double a[4];
+  for (int k0 = beg + sub; k0 < end; k0 += U * G) {
+    int c[U];
+    double a[U];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      c[m] = ldg_stream(X.idx + k + m * G);
-      a[m] = ldg_stream(X.val + k + m * G);
+    for (int m = 0; m < U; ++m) {
+      const int k = k0 + m * G;
+      c[m] = k < end ? ldg_stream(X.idx + k) : 0;
+      a[m] = k < end ? ldg_stream(X.val + k) : 0.0;
     }
-    double b[4];
+    double b[U];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) b[m] = __ldg(v + c[m]);
+    for (int m = 0; m < U; ++m) {
+      if (STAGED)
+        b[m] = (k0 + m * G < end) ? (c[m] < hot ? sv[c[m]] : __ldg(v + c[m])) : 0.0;
+      else
+        b[m] = (k0 + m * G < end) ? __ldg(v + c[m]) : 0.0;
+    }
 #pragma unroll
-    for (int m = 0; m < 4; ++m) s += a[m] * b[m];
+    for (int m = 0; m < U; ++m)
+      if (k0 + m * G < end) s += a[m] * b[m];
   }
-  for (; k < end; k += G) s += ldg_stream(X.val + k) * __ldg(v + ldg_stream(X.idx + k));
   return s;
 }
-// ---------------------------------------------------------------------------
-template <int G, int LOSS>
-__global__ void __launch_bounds__(kBlock) csr_forward_kernel(CsrView X, const double* __restrict__ w,
+
+// Hot-prefix staging: v[0, hot) is copied to shared memory once per block so
+// that gathers of popular features are LDS, not L1 wavefronts (the limit of
+// a gather-bound SpMV).  SYNTH-v1 draws columns Zipf(1) by index, so the
+// first 25.6k columns carry ~70% of news20-shaped nonzeros.
+template <bool STAGED, int BLK>
+__device__ __forceinline__ void stage_prefix(const double* __restrict__ v, double* sv, int hot) {
+  if (STAGED) bulk_stage_f64(sv, v, hot);
+}
+
+template <int G, int LOSS, bool STAGED>
+__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
+    csr_forward_kernel(CsrView X, int hot, const double* __restrict__ w,
                                                             const double* __restrict__ y, double C,
                                                             double* __restrict__ z,
                                                             double* __restrict__ zhat,
                                                             double* __restrict__ dvec,
                                                             uint8_t* __restrict__ mask,
                                                             ObjScalars* obj, Scratch sc) {
+  constexpr int BLK = STAGED ? kStagedBlock : kBlock;
   constexpr int RPW = kWarp / G;  // rows per warp
-  __shared__ double sh[kBlock / kWarp + 1];
+  __shared__ double sh[BLK / kWarp + 1];
+  extern __shared__ double sv[];
+  stage_prefix<STAGED, BLK>(w, sv, hot);
   const int lane = threadIdx.x & 31;
   const int sub = lane % G;
-  const long long gwarp = (blockIdx.x * (long long)kBlock + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * kBlock) >> 5;
+  const long long gwarp = (blockIdx.x * (long long)BLK + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * BLK) >> 5;
   double term_acc = 0.0, cnt_acc = 0.0;
   for (long long r0 = gwarp * RPW; r0 < X.rows; r0 += nwarps * RPW) {
     const long long row = r0 + lane / G;
     double s = 0.0;
     if (row < X.rows) {
-      s = row_dot_sub<G>(X, row, sub, w);
+      s = row_dot_sub<G, STAGED>(X, row, sub, w, sv, hot);
     }
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
@@ -116,15 +133,15 @@ __global__ void __launch_bounds__(kBlock) csr_forward_kernel(CsrView X, const do
       }
     }
   }
-  const double bt = block_sum<kBlock>(term_acc, sh, true);
-  const double bc = block_sum<kBlock>(cnt_acc, sh, true);
+  const double bt = block_sum<BLK>(term_acc, sh, true);
+  const double bc = block_sum<BLK>(cnt_acc, sh, true);
   if (threadIdx.x == 0) {
     sc.partials[2 * blockIdx.x] = bt;
     sc.partials[2 * blockIdx.x + 1] = bc;
   }
   if (last_block_arrive(sc.tickets + T_FUN)) {
-    const double tot = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 0, sh);
-    const double cnt = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 1, sh);
+    const double tot = reduce_partials<BLK>(sc.partials, gridDim.x, 2, 0, sh);
+    const double cnt = reduce_partials<BLK>(sc.partials, gridDim.x, 2, 1, sh);
     if (threadIdx.x == 0) {
       obj->f = 0.5 * obj->ww + C * tot;  // loss.cpp:57 / :121
       obj->nact = (long long)cnt;
@@ -134,23 +151,27 @@ __global__ void __launch_bounds__(kBlock) csr_forward_kernel(CsrView X, const do
   }
 }
 
-template <int G>
-__global__ void __launch_bounds__(kBlock) csr_dv_kernel(CsrView X, const double* __restrict__ p,
+template <int G, bool STAGED>
+__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
+    csr_dv_kernel(CsrView X, int hot, const double* __restrict__ p,
                                                        const double* __restrict__ dvec,
                                                        const uint8_t* __restrict__ mask,
                                                        double* __restrict__ a) {
+  constexpr int BLK = STAGED ? kStagedBlock : kBlock;
   constexpr int RPW = kWarp / G;
+  extern __shared__ double sv[];
+  stage_prefix<STAGED, BLK>(p, sv, hot);
   const int lane = threadIdx.x & 31;
   const int sub = lane % G;
-  const long long gwarp = (blockIdx.x * (long long)kBlock + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * kBlock) >> 5;
+  const long long gwarp = (blockIdx.x * (long long)BLK + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * BLK) >> 5;
   for (long long r0 = gwarp * RPW; r0 < X.rows; r0 += nwarps * RPW) {
     const long long row = r0 + lane / G;
     bool active = row < X.rows;
     if (active && mask) active = mask[row] != 0;
     double s = 0.0;
     if (active) {
-      s = row_dot_sub<G>(X, row, sub, p);
+      s = row_dot_sub<G, STAGED>(X, row, sub, p, sv, hot);
     }
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
@@ -167,208 +188,6 @@ int forward_grid(int64_t rows, int group) {
   if (want > cap) want = cap;
   if (want < 1) want = 1;
   return (int)want;
-}
-
-// ---------------------------------------------------------------------------
-// Merge-path transposed product.
-// ---------------------------------------------------------------------------
-template <int UK, bool SQ>
-__device__ __forceinline__ double weight(const UView& U, int r, double v) {
-  double u;
-  if (UK == U_VEC) {
-    u = __ldg(U.u + r);
-  } else if (UK == U_SVM_RESID) {
-    u = U.mask[r] ? (U.z[r] - U.y[r]) : 0.0;
-  } else {
-    u = U.mask[r] ? 1.0 : 0.0;
-  }
-  // row_axpy: out += a*v ; row_axpy_squared: out += a*v*v  (linalg.cpp:88-109)
-  return SQ ? (u * v) * v : u * v;
-}
-
-template <int EPI>
-__device__ __forceinline__ void emit(const EpiView& E, double* out, long long j, double sum) {
-  if (EPI == EPI_VEC)
-    out[j] = E.base[j] + E.scale * sum;
-  else if (EPI == EPI_CONST)
-    out[j] = E.cbase + E.scale * sum;
-  else
-    out[j] = sum;
-}
-
-template <int UK, bool SQ, int EPI>
-__global__ void __launch_bounds__(kBlock) merge_spmv_kernel(CsrView A, MergeView P, UView U,
-                                                           EpiView E, double* __restrict__ out) {
-  __shared__ double s_val[kTile];
-  __shared__ int s_end[kTile];
-  __shared__ double s_scan[kBlock];
-  __shared__ int s_key[kBlock];
-  __shared__ double s_wval[kBlock / kWarp];
-  __shared__ int s_wkey[kBlock / kWarp];
-
-  const int t = blockIdx.x;
-  const int x0 = P.tile_row[t], y0 = P.tile_nz[t];
-  const int nr = P.tile_row[t + 1] - x0;
-  const int nz = P.tile_nz[t + 1] - y0;
-  const int tid = threadIdx.x;
-
-  // Stage the tile: all loads of a thread are issued before any is consumed
-  // (kIpt coalesced idx/val loads in flight, then kIpt independent gathers).
-  {
-    int ridx[kIpt];
-    double rval[kIpt];
-#pragma unroll
-    for (int m = 0; m < kIpt; ++m) {
-      const int i = tid + m * kBlock;
-      const bool ok = i < nz;
-      ridx[m] = ok ? ldg_stream(A.idx + y0 + i) : 0;
-      rval[m] = ok ? ldg_stream(A.val + y0 + i) : 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < kIpt; ++m) {
-      const int i = tid + m * kBlock;
-      if (i < nr) s_end[i] = __ldg(A.ptr + x0 + 1 + i);
-    }
-    double w[kIpt];
-#pragma unroll
-    for (int m = 0; m < kIpt; ++m) w[m] = (tid + m * kBlock < nz) ? weight<UK, SQ>(U, ridx[m], rval[m]) : 0.0;
-#pragma unroll
-    for (int m = 0; m < kIpt; ++m) {
-      const int i = tid + m * kBlock;
-      if (i < nz) s_val[i] = w[m];
-    }
-  }
-  __syncthreads();
-
-  // Merge-path coordinate of this thread inside the tile.
-  const int total = nr + nz;
-  const int d = min(tid * kIpt, total);
-  const int d_end = min(d + kIpt, total);
-  int lo = max(d - nz, 0), hi = min(d, nr);
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (s_end[mid] <= y0 + d - mid - 1)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  int tx = lo, ty = d - lo;
-  double acc = 0.0, first_val = 0.0;
-  int first_col = -1;
-  for (int step = d; step < d_end; ++step) {
-    if (tx < nr && (ty >= nz || s_end[tx] <= y0 + ty)) {  // row (column of X) ends
-      if (first_col < 0) {
-        first_col = tx;
-        first_val = acc;
-      } else {
-        emit<EPI>(E, out, (long long)x0 + tx, acc);  // wholly inside this thread
-      }
-      acc = 0.0;
-      ++tx;
-    } else {
-      acc += s_val[ty];
-      ++ty;
-    }
-  }
-
-  // Block-wide inclusive segmented scan of the carries (keys are monotone).
-  const int lane = tid & 31, wid = tid >> 5;
-  int key = tx;
-  double val = acc;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int k2 = __shfl_up_sync(0xffffffffu, key, off);
-    const double v2 = __shfl_up_sync(0xffffffffu, val, off);
-    if (lane >= off && k2 == key) val = v2 + val;
-  }
-  if (lane == 31) {
-    s_wkey[wid] = key;
-    s_wval[wid] = val;
-  }
-  __syncthreads();
-  if (wid == 0) {
-    constexpr int NW = kBlock / kWarp;
-    int wk = lane < NW ? s_wkey[lane] : 0x7fffffff;
-    double wv = lane < NW ? s_wval[lane] : 0.0;
-#pragma unroll
-    for (int off = 1; off < NW; off <<= 1) {
-      const int k2 = __shfl_up_sync(0xffffffffu, wk, off);
-      const double v2 = __shfl_up_sync(0xffffffffu, wv, off);
-      if (lane >= off && k2 == wk) wv = v2 + wv;
-    }
-    if (lane < NW) {
-      s_wkey[lane] = wk;
-      s_wval[lane] = wv;
-    }
-  }
-  __syncthreads();
-  if (wid > 0 && s_wkey[wid - 1] == key) val = s_wval[wid - 1] + val;
-  s_scan[tid] = val;
-  s_key[tid] = key;
-  __syncthreads();
-
-  if (first_col >= 0) {
-    double tot = first_val;
-    if (tid > 0 && s_key[tid - 1] == first_col) tot = s_scan[tid - 1] + first_val;
-    const long long col = (long long)x0 + first_col;
-    if (first_col == 0 && A.ptr[x0] < y0)
-      P.head[t] = tot;  // started in an earlier tile: finished by the fix-up pass
-    else
-      emit<EPI>(E, out, col, tot);
-  }
-  if (tid == kBlock - 1) P.carry[t] = s_scan[tid];
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(kBlock) merge_fixup_kernel(MergeView P, EpiView E,
-                                                            double* __restrict__ out) {
-  const int t = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= P.num_tiles) return;
-  const int ts = P.fix_chain[t];
-  if (ts < 0) return;
-  double s = 0.0;
-  for (int k = ts + lane; k < t; k += 32) s += P.carry[k];
-  s = warp_sum(s);
-  if (lane == 0) emit<EPI>(E, out, P.tile_row[t], s + P.head[t]);
-}
-
-__global__ void merge_plan_kernel(CsrView A, int32_t* tile_row, int32_t* tile_nz, int num_tiles) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > num_tiles) return;
-  const long long total = (long long)A.rows + (long long)A.nnz;
-  const long long diag = min((long long)t * kTile, total);
-  long long lo = max(diag - (long long)A.nnz, 0LL), hi = min(diag, (long long)A.rows);
-  while (lo < hi) {
-    const long long mid = (lo + hi) >> 1;
-    if ((long long)A.ptr[mid + 1] <= diag - mid - 1)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  tile_row[t] = (int32_t)lo;
-  tile_nz[t] = (int32_t)(diag - lo);
-}
-
-__global__ void merge_chain_kernel(CsrView A, const int32_t* tile_row, const int32_t* tile_nz,
-                                   int32_t* fix_chain, int num_tiles) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= num_tiles) return;
-  const int x0 = tile_row[t], y0 = tile_nz[t];
-  if (tile_row[t + 1] > x0 && A.ptr[x0] < y0) {
-    // first tile ts whose end coordinate tile_row[ts+1] reaches x0
-    int lo = 0, hi = t;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (tile_row[mid + 1] < x0)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    fix_chain[t] = lo;
-  } else {
-    fix_chain[t] = -1;
-  }
 }
 
 // CSC construction helpers
@@ -458,70 +277,72 @@ int choose_group(int64_t rows, int64_t nnz) {
     default: { constexpr int GG = 2; __VA_ARGS__; } break;  \
   }
 
+template <class K>
+static void set_smem(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotMax * 8);
+}
+
+// Opt-in (TRON_B200_STAGE=1): measured slower on N1 (occupancy drops to one
+// 16-warp block per SM while the kernel is bound by streaming-load latency).
+static bool stage_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("TRON_B200_STAGE");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return on != 0;
+}
+static bool stage_rows(const CsrView& X) {
+  return stage_enabled() && X.nnz >= kStageMinNnz && X.cols > 4096;
+}
+
 void csr_forward(const CsrView& X, int group, int loss, const double* w, const double* y, double C,
                  double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
                  Scratch sc, cudaStream_t s) {
+  if (stage_rows(X)) {
+    const int hot = (int)(X.cols < kHotMax ? X.cols : kHotMax);
+    const int grid = device_sm_count();
+    const size_t smem = (size_t)hot * 8;
+    if (loss == kLossLogistic) {
+      TB_GROUP_DISPATCH(group, {
+        auto k = csr_forward_kernel<GG, kLossLogistic, true>;
+        static bool once = (set_smem(k), true);
+        (void)once;
+        k<<<grid, kStagedBlock, smem, s>>>(X, hot, w, y, C, z, zhat, dvec, mask, obj, sc);
+      });
+    } else {
+      TB_GROUP_DISPATCH(group, {
+        auto k = csr_forward_kernel<GG, kLossSvm, true>;
+        static bool once = (set_smem(k), true);
+        (void)once;
+        k<<<grid, kStagedBlock, smem, s>>>(X, hot, w, y, C, z, zhat, dvec, mask, obj, sc);
+      });
+    }
+    return;
+  }
   const int grid = forward_grid(X.rows, group);
   if (loss == kLossLogistic) {
-    TB_GROUP_DISPATCH(group, (csr_forward_kernel<GG, kLossLogistic><<<grid, kBlock, 0, s>>>(
-                                 X, w, y, C, z, zhat, dvec, mask, obj, sc)));
+    TB_GROUP_DISPATCH(group, (csr_forward_kernel<GG, kLossLogistic, false><<<grid, kBlock, 0, s>>>(
+                                 X, 0, w, y, C, z, zhat, dvec, mask, obj, sc)));
   } else {
-    TB_GROUP_DISPATCH(group, (csr_forward_kernel<GG, kLossSvm><<<grid, kBlock, 0, s>>>(
-                                 X, w, y, C, z, zhat, dvec, mask, obj, sc)));
+    TB_GROUP_DISPATCH(group, (csr_forward_kernel<GG, kLossSvm, false><<<grid, kBlock, 0, s>>>(
+                                 X, 0, w, y, C, z, zhat, dvec, mask, obj, sc)));
   }
 }
 
 void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
             double* a, cudaStream_t s) {
+  if (stage_rows(X)) {
+    const int hot = (int)(X.cols < kHotMax ? X.cols : kHotMax);
+    TB_GROUP_DISPATCH(group, {
+      auto k = csr_dv_kernel<GG, true>;
+      static bool once = (set_smem(k), true);
+      (void)once;
+      k<<<device_sm_count(), kStagedBlock, (size_t)hot * 8, s>>>(X, hot, p, dvec, mask, a);
+    });
+    return;
+  }
   const int grid = forward_grid(X.rows, group);
-  TB_GROUP_DISPATCH(group, (csr_dv_kernel<GG><<<grid, kBlock, 0, s>>>(X, p, dvec, mask, a)));
-}
-
-int32_t merge_num_tiles(int64_t rows, int64_t nnz) {
-  return (int32_t)((rows + nnz + kTile - 1) / kTile);
-}
-
-void merge_plan_build(const CsrView& A, int32_t* tile_row, int32_t* tile_nz, int32_t* fix_chain,
-                      int32_t num_tiles, cudaStream_t s) {
-  merge_plan_kernel<<<(num_tiles + 1 + 255) / 256, 256, 0, s>>>(A, tile_row, tile_nz, num_tiles);
-  if (num_tiles > 0)
-    merge_chain_kernel<<<(num_tiles + 255) / 256, 256, 0, s>>>(A, tile_row, tile_nz, fix_chain,
-                                                               num_tiles);
-}
-
-template <int UK, bool SQ>
-static void launch_merge(const CsrView& A, const MergeView& P, const UView& U, const EpiView& E,
-                         double* out, cudaStream_t s) {
-  const int fix_grid = (P.num_tiles * 32 + kBlock - 1) / kBlock;
-  switch (E.kind) {
-    case EPI_VEC:
-      merge_spmv_kernel<UK, SQ, EPI_VEC><<<P.num_tiles, kBlock, 0, s>>>(A, P, U, E, out);
-      merge_fixup_kernel<EPI_VEC><<<fix_grid, kBlock, 0, s>>>(P, E, out);
-      break;
-    case EPI_CONST:
-      merge_spmv_kernel<UK, SQ, EPI_CONST><<<P.num_tiles, kBlock, 0, s>>>(A, P, U, E, out);
-      merge_fixup_kernel<EPI_CONST><<<fix_grid, kBlock, 0, s>>>(P, E, out);
-      break;
-    default:
-      merge_spmv_kernel<UK, SQ, EPI_RAW><<<P.num_tiles, kBlock, 0, s>>>(A, P, U, E, out);
-      merge_fixup_kernel<EPI_RAW><<<fix_grid, kBlock, 0, s>>>(P, E, out);
-      break;
-  }
-}
-
-void csc_spmv(const CsrView& At, const MergeView& P, const UView& U, bool squared,
-              const EpiView& E, double* out, cudaStream_t s) {
-  if (P.num_tiles <= 0) return;
-  if (U.kind == U_VEC) {
-    if (squared)
-      launch_merge<U_VEC, true>(At, P, U, E, out, s);
-    else
-      launch_merge<U_VEC, false>(At, P, U, E, out, s);
-  } else if (U.kind == U_SVM_RESID) {
-    launch_merge<U_SVM_RESID, false>(At, P, U, E, out, s);
-  } else {
-    launch_merge<U_MASK, true>(At, P, U, E, out, s);
-  }
+  TB_GROUP_DISPATCH(group, (csr_dv_kernel<GG, false><<<grid, kBlock, 0, s>>>(X, 0, p, dvec, mask, a)));
 }
 
 int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s) {

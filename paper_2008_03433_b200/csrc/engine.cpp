@@ -143,14 +143,15 @@ void Engine::common_alloc() {
   cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "cudaStreamCreate");
   sc_partials_.alloc(kMaxPartialBlocks * 4);
   sc_tickets_.alloc(kNumTickets);
-  cuda_check(cudaMemset(sc_tickets_.p, 0, sc_tickets_.bytes()), "memset");
+  cuda_check(cudaMemsetAsync(sc_tickets_.p, 0, sc_tickets_.bytes(), s_), "memset");
   sc_.partials = sc_partials_.p;
   sc_.tickets = sc_tickets_.p;
   cuda_check(cudaMalloc(&obj_d_, sizeof(ObjScalars)), "cudaMalloc");
-  cuda_check(cudaMemset(obj_d_, 0, sizeof(ObjScalars)), "memset");
+  cuda_check(cudaMemsetAsync(obj_d_, 0, sizeof(ObjScalars), s_), "memset");
   cuda_check(cudaMallocHost(&obj_h_, sizeof(ObjScalars)), "cudaMallocHost");
   cuda_check(cudaMalloc(&st_d_, sizeof(CgState)), "cudaMalloc");
-  cuda_check(cudaMemset(st_d_, 0, sizeof(CgState)), "memset");
+  cuda_check(cudaMemsetAsync(st_d_, 0, sizeof(CgState), s_), "memset");
+  cuda_check(cudaStreamSynchronize(s_), "init");
   cuda_check(cudaMallocHost(&st_h_, sizeof(CgState)), "cudaMallocHost");
   std::memset(obj_h_, 0, sizeof(ObjScalars));
   std::memset(st_h_, 0, sizeof(CgState));
@@ -218,7 +219,8 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
   {
     DevBuf<int64_t> ro64;
     ro64.alloc(l + 1);
-    cuda_check(cudaMemcpy(ro64.p, ro, (l + 1) * sizeof(int64_t), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpyAsync(ro64.p, ro, (l + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s),
+               "H2D");
     narrow_offsets(ro64.p, e->rptr_.p, (int64_t)(l + 1), s);
     if (nnz > 0) {
       cuda_check(cudaMemcpyAsync(e->cidx_.p, ci, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s),
@@ -234,15 +236,44 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
   const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
   if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
   e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
-  const int32_t tiles = merge_num_tiles(n, nnz);
-  e->tile_row_.alloc(tiles + 1);
-  e->tile_nz_.alloc(tiles + 1);
-  e->fix_chain_.alloc(tiles > 0 ? tiles : 1);
-  e->head_.alloc(tiles > 0 ? tiles : 1);
-  e->carry_.alloc(tiles > 0 ? tiles : 1);
-  merge_plan_build(e->Xt_, e->tile_row_.p, e->tile_nz_.p, e->fix_chain_.p, tiles, s);
-  e->plan_ = MergeView{tiles, e->tile_row_.p, e->tile_nz_.p, e->fix_chain_.p, e->head_.p,
-                       e->carry_.p};
+  {
+    // one-time structure analysis of the CSC copy on the host (csc_seg.cu)
+    std::vector<int32_t> cptr_h(n + 1);
+    cuda_check(cudaMemcpyAsync(cptr_h.data(), e->cptr_.p, (n + 1) * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, s),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(s), "cptr download");
+    SegPlanHost P;
+    seg_plan_host(cptr_h.data(), (int64_t)n, nnz, &P);
+    const size_t nch = P.chunk_rank.size();
+    auto up = [&](auto& buf, const auto& vec) {
+      using T = typename std::decay_t<decltype(vec)>::value_type;
+      buf.alloc(std::max<size_t>(vec.size(), 1));
+      if (!vec.empty())
+        cuda_check(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T),
+                                   cudaMemcpyHostToDevice, s),
+                   "H2D");
+    };
+    up(e->chunk_start_, P.chunk_start);
+    up(e->chunk_rank_, P.chunk_rank);
+    up(e->lastbits_, P.lastbits);
+    up(e->nz_col_, P.nz_col);
+    up(e->fix_chunk_, P.fix_chunk);
+    up(e->fix_first_, P.fix_first);
+    e->head_.alloc(std::max<size_t>(nch, 1));
+    e->carry_.alloc(std::max<size_t>(nch, 1));
+    e->plan_.nchunks = (int64_t)nch;
+    e->plan_.nfix = (int64_t)P.fix_chunk.size();
+    e->plan_.chunk_start = e->chunk_start_.p;
+    e->plan_.chunk_rank = e->chunk_rank_.p;
+    e->plan_.lastbits = e->lastbits_.p;
+    e->plan_.nz_col = e->nz_col_.p;
+    e->plan_.fix_chunk = e->fix_chunk_.p;
+    e->plan_.fix_first = e->fix_first_.p;
+    e->plan_.head = e->head_.p;
+    e->plan_.carry = e->carry_.p;
+    cuda_check(cudaStreamSynchronize(s), "seg plan upload");
+  }
   e->group_ = choose_group((int64_t)l, nnz);
   cuda_check(cudaStreamSynchronize(s), "csc build");
   cuda_check(cudaGetLastError(), "csc build");
@@ -335,7 +366,9 @@ Engine::~Engine() {
 
 uint64_t Engine::memory_bytes() const {
   uint64_t b = rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
-               cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes();
+               cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes() + lastbits_.bytes() +
+               chunk_rank_.bytes() + chunk_start_.bytes() + fix_chunk_.bytes() +
+               fix_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
   for (const auto& S : slot_)
     b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes();
   b += g_.bytes() * 9 + a_.bytes() + parts_.bytes();
@@ -634,7 +667,9 @@ void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint
   if (n_active) *n_active = (uint64_t)cnt;
   if (active && cnt > 0) {
     std::vector<int32_t> h(cnt);
-    cuda_check(cudaMemcpy(h.data(), idx.p, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpyAsync(h.data(), idx.p, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, s_),
+               "D2H");
+    synchronize();
     const uint64_t m = std::min<uint64_t>(cap, (uint64_t)cnt);
     for (uint64_t k = 0; k < m; ++k) active[k] = (int64_t)h[k] + (int64_t)row_begin_;
   }

@@ -137,10 +137,11 @@ class Engine {
   // CSR + CSC (sparse layout)
   DevBuf<int32_t> rptr_, cidx_, cptr_, ridx_;
   DevBuf<double> rval_, cval_;
-  DevBuf<int32_t> tile_row_, tile_nz_, fix_chain_;
+  DevBuf<uint32_t> lastbits_, chunk_rank_;
+  DevBuf<int32_t> chunk_start_, fix_chunk_, fix_first_, nz_col_;
   DevBuf<double> head_, carry_;
   CsrView X_{}, Xt_{};
-  MergeView plan_{};
+  SegView plan_{};
   int group_ = 4;
   // dense column-major
   DevBuf<double> Xc_;

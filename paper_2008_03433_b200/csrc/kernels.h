@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace tb {
 
@@ -21,15 +22,31 @@ struct CsrView {
   const double* val = nullptr;
 };
 
-// Merge-path tiling of a compressed matrix (fixed per matrix structure).
-struct MergeView {
-  int32_t num_tiles = 0;
-  const int32_t* tile_row = nullptr;   // [num_tiles+1] rows ended before tile start
-  const int32_t* tile_nz = nullptr;    // [num_tiles+1] nonzeros consumed before tile start
-  const int32_t* fix_chain = nullptr;  // [num_tiles] first carry tile of the head row, or -1
-  double* head = nullptr;              // [num_tiles] partial of a tile's first (split) row
-  double* carry = nullptr;             // [num_tiles] carry-out toward the next tile
+// Segmented-chunk plan of a compressed matrix (fixed per structure): the
+// nonzeros are cut into chunks of at most 32*kSegLaneItems (one warp each)
+// whose boundaries follow row boundaries, so only rows longer than a chunk
+// are split (and finished by the fix-up pass).
+constexpr int kSegLaneItems = 8;
+constexpr int kSegChunk = 32 * kSegLaneItems;
+struct SegView {
+  int64_t nchunks = 0;
+  int64_t nfix = 0;
+  const int32_t* chunk_start = nullptr;  // [nchunks+1] first entry of each chunk; [nchunks] = nnz
+  const uint32_t* chunk_rank = nullptr;  // rank of the row holding the chunk's first entry
+                                         // | 0x80000000 when that row began in an earlier chunk
+  const uint32_t* lastbits = nullptr;    // bit k: entry k is the last of its row
+  const int32_t* nz_col = nullptr;       // [nnzc+1] index of the r-th non-empty row; [nnzc] = rows
+  const int32_t* fix_chunk = nullptr;    // [nfix] chunk finishing a split row
+  const int32_t* fix_first = nullptr;    // [nfix] first chunk of that row
+  double* head = nullptr;                // [nchunks] partial of a chunk's split head row
+  double* carry = nullptr;               // [nchunks] carry-out toward the next chunk
 };
+// Host-side plan construction from the compressed-row offsets (ptr, rows+1).
+struct SegPlanHost {
+  std::vector<int32_t> chunk_start, nz_col, fix_chunk, fix_first;
+  std::vector<uint32_t> chunk_rank, lastbits;
+};
+void seg_plan_host(const int32_t* ptr, int64_t rows, int64_t nnz, SegPlanHost* out);
 
 // Per-source-row weight u_i used by the transposed product sum_i u_i x_ij.
 enum UKind : int {
@@ -103,13 +120,10 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
 // a_i = (x_i . p) * dvec_i  (or mask_i ? x_i . p : 0 when mask given)
 void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
             double* a, cudaStream_t s);
-// Transposed product over the CSC copy (merge-path, atomic-free).
-void csc_spmv(const CsrView& At, const MergeView& plan, const UView& u, bool squared,
+// Transposed product over the CSC copy (csc_seg.cu; segmented chunks, atomic-free).
+void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squared,
               const EpiView& epi, double* out, cudaStream_t s);
-// Build the merge-path plan for a compressed matrix (one-time setup).
-void merge_plan_build(const CsrView& A, int32_t* tile_row, int32_t* tile_nz, int32_t* fix_chain,
-                      int32_t num_tiles, cudaStream_t s);
-int32_t merge_num_tiles(int64_t rows, int64_t nnz);
+
 // Device CSC construction from device CSR (stable in row order).
 // Returns 0 on success; temp storage allocated internally.
 int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s);
@@ -122,7 +136,7 @@ void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjSc
                   Scratch sc, cudaStream_t s);
 // obj->gnorm = ||g||, obj->grad_nonfinite
 void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s);
-// out = base + scale*raw  (after an allreduce of raw partials)
+// out = base + scale*raw  (after an allreduce of raw partials; raw == nullptr => 0)
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
 
 // Large-n CG engine (one kernel per phase; conditional handle optional).

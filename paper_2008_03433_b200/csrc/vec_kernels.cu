@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const d
 
 __global__ void epilogue_kernel(long long n, const double* raw, EpiView E, double* out) {
   GRID_STRIDE(j, n) {
-    const double s = raw[j];
+    const double s = raw ? raw[j] : 0.0;
     out[j] = E.kind == EPI_VEC ? E.base[j] + E.scale * s
                                : (E.kind == EPI_CONST ? E.cbase + E.scale * s : s);
   }
