@@ -1,157 +1,309 @@
 // Tall-skinny dense kernels (l >> n, n <= 64) on sm_100a, FP64.
 //
-// X lives column-major on the device (X[j*ld + i]) so that one thread per
-// instance reads its row with fully coalesced warp loads (32 consecutive
-// instances of a column = 256 contiguous bytes per load instruction).
-// Each thread accumulates n partial sums in registers over its grid-stride
-// rows; a fixed-shape warp/block tree produces one n-vector per block and a
-// fixed-order second stage finishes it.  The per-row dot x_i.v is the
-// sequential j = 0..n-1 loop of FeatureMatrix::row_dot (linalg.cpp:75-86)
-// compiled without FMA contraction, so margins z -- and therefore the
-// L2-SVM active set I (loss.cpp:94-122) -- are bit-identical to the
-// reference's.
+// X lives column-major on the device (X[j*ld + i], ld = l rounded up to a
+// multiple of 256 rows, padding zeroed).  Every pass is one stream over X
+// through a TMA bulk-copy pipeline:
+//
+//  * a persistent CTA (one per SM) walks 256-row tiles t = blockIdx.x,
+//    blockIdx.x + gridDim.x, ...;
+//  * warp 0 issues one `cp.async.bulk` per column (2 KB contiguous each)
+//    plus the per-row side arrays the pass needs (y, D, mask, ...) into a
+//    shared-memory stage, completing on that stage's mbarrier;
+//  * 2-4 stages are in flight, so the bytes outstanding per SM are set by
+//    shared memory (80-160 KB), not by registers -- the limiter of the
+//    register-blocked thread-per-row kernel this replaces (255 regs, 12%
+//    warps active, 45% of HBM peak: profiles/round1_P1_kernels.md);
+//  * one thread per row reads its row from shared memory (conflict-free:
+//    consecutive rows are consecutive doubles), forms the row dot
+//    sequentially over j = 0..n-1 exactly like FeatureMatrix::row_dot
+//    (linalg.cpp:75-86; no FMA contraction, so margins -- and with them the
+//    L2-SVM active set I (loss.cpp:94-122) -- are bit-identical to the
+//    reference), and accumulates c_i * x_i into n register accumulators;
+//  * a fixed-shape block tree emits one n-vector per CTA; a fixed-order
+//    second stage (dense_finalize / cg_small_step) finishes it.
+//
+// The margin pass also accumulates the gradient partials of the candidate
+// (loss.cpp:74-80 / :129-137) -- free under the HBM bound -- so commit()
+// never re-reads X.
 #include "common.cuh"
 #include "kernels.h"
+
+#include <cstdlib>
 
 namespace tb {
 
 namespace {
 
-constexpr int kBlock = 256;
+constexpr int kSmemBudget = 200 * 1024;
+
+// Per-row side arrays staged with each tile (slot offsets inside a stage).
+struct StageLayout {
+  int n, T;
+  int nd;            // number of staged double side arrays (<= 3)
+  bool has_mask;     // staged uint8 mask
+  __host__ __device__ int bytes() const { return (n + nd) * T * 8 + (has_mask ? T : 0); }
+};
 
 __device__ __forceinline__ double log1p_exp_neg(double t) {  // loss.hpp:99-102
   if (t >= 0.0) return log1p(exp(-t));
   return -t + log1p(exp(t));
 }
 
-template <int NMAX, int LOSS>
-__global__ void __launch_bounds__(kBlock) dense_forward_kernel(
-    long long l, int n, long long ld, const double* __restrict__ X, const double* __restrict__ w,
-    const double* __restrict__ y, double C, double* __restrict__ z, double* __restrict__ zhat,
-    double* __restrict__ dvec, uint8_t* __restrict__ mask, ObjScalars* obj, Scratch sc) {
-  __shared__ double s_w[NMAX];
-  __shared__ double sh[kBlock / kWarp + 1];
-  for (int j = threadIdx.x; j < NMAX; j += kBlock) s_w[j] = j < n ? w[j] : 0.0;
-  __syncthreads();
-  double term_acc = 0.0, cnt_acc = 0.0;
-  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < l;
-       i += (long long)gridDim.x * kBlock) {
-    double x[NMAX];
-#pragma unroll
-    for (int j = 0; j < NMAX; ++j) x[j] = j < n ? X[(long long)j * ld + i] : 0.0;
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < NMAX; ++j)
-      if (j < n) s += x[j] * s_w[j];
-    const double yi = y[i];
-    z[i] = s;
-    if (LOSS == kLossLogistic) {
-      const double t = yi * s;
-      const double sig = 1.0 / (1.0 + exp(t));
-      zhat[i] = -yi * sig;
-      dvec[i] = (1.0 - sig) * sig;
-      term_acc += log1p_exp_neg(t);
-    } else {
-      const double margin = 1.0 - yi * s;
-      if (margin > 0.0) {
-        mask[i] = 1;
-        term_acc += margin * margin;
-        cnt_acc += 1.0;
-      } else {
-        mask[i] = 0;
-      }
-    }
-  }
-  const double bt = block_sum<kBlock>(term_acc, sh, true);
-  const double bc = block_sum<kBlock>(cnt_acc, sh, true);
-  if (threadIdx.x == 0) {
-    sc.partials[2 * blockIdx.x] = bt;
-    sc.partials[2 * blockIdx.x + 1] = bc;
-  }
-  if (last_block_arrive(sc.tickets + T_FUN)) {
-    const double tot = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 0, sh);
-    const double cnt = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 1, sh);
-    // ww of a short vector is done here, serially, like dot() (linalg.cpp:267-272)
-    if (threadIdx.x == 0) {
-      double ww = 0.0;
-      for (int j = 0; j < n; ++j) ww += w[j] * w[j];
-      obj->ww = ww;
-      obj->f = 0.5 * ww + C * tot;
-      obj->nact = (long long)cnt;
-      obj->red[0] = tot;
-      obj->red[1] = cnt;
-    }
-  }
-}
+struct PassArgs {
+  long long l, ld;
+  int n;
+  const double* X;
+  const double* v;       // w (FWD) or v (HV)
+  const double* y;
+  const double* dvec;    // LR: D (HV, PRECOND)
+  const uint8_t* mask;   // SVM: active mask (HV, PRECOND); nullptr = all rows active
+  double C;
+  // FWD outputs
+  double* z;
+  double* zhat;
+  double* dvec_out;
+  uint8_t* mask_out;
+  ObjScalars* obj;
+  Scratch sc;
+  double* partials;      // [gridDim.x][n]
+};
 
-// Per-block n-vector partials; block tree over warps then a fixed warp order.
-template <int NMAX>
-__device__ __forceinline__ void store_block_vector(const double (&acc)[NMAX], int n,
-                                                   double* out_block) {
-  __shared__ double s_red[kBlock / kWarp][NMAX];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j < NMAX; ++j) {
-    if (j < n) {
-      const double v = warp_sum(acc[j]);
-      if (lane == 0) s_red[wid][j] = v;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < n) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kBlock / kWarp; ++w) t += s_red[w][threadIdx.x];
-    out_block[threadIdx.x] = t;
-  }
-}
+enum PassMode : int { PM_FWD = 0, PM_HV = 1, PM_PRECOND = 2 };
 
-template <int NMAX, int KIND, int LOSS>
-__global__ void __launch_bounds__(kBlock) dense_accum_kernel(
-    long long l, int n, long long ld, const double* __restrict__ X, const double* __restrict__ v,
-    const double* __restrict__ zhat, const double* __restrict__ dvec,
-    const uint8_t* __restrict__ mask, const double* __restrict__ z, const double* __restrict__ y,
-    double* __restrict__ partials) {
+// Side arrays of a mode: d-arrays in order, then the mask.
+template <int MODE, int LOSS>
+struct Side {
+  static constexpr int nd = (MODE == PM_FWD) ? 1 : (LOSS == kLossLogistic ? 1 : 0);
+  static constexpr bool mask = (MODE != PM_FWD) && LOSS == kLossSvm;
+};
+
+// T compute threads (one row of the tile each) + one producer warp.
+template <int NMAX, int T, int MODE, int LOSS>
+__global__ void __launch_bounds__(T + kWarp, 1)
+    dense_pass_kernel(const __grid_constant__ CUtensorMap xmap, PassArgs a, int nstages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long full[4], empty[4];
   __shared__ double s_v[NMAX];
-  if (KIND == DA_HV) {
-    for (int j = threadIdx.x; j < NMAX; j += kBlock) s_v[j] = j < n ? v[j] : 0.0;
-    __syncthreads();
+  constexpr int BLK = T + kWarp;
+  constexpr int NCW = T / kWarp;  // compute warps
+  __shared__ double sh[BLK / kWarp + 1];
+  using SD = Side<MODE, LOSS>;
+  const int n = a.n;
+  const bool use_mask = SD::mask && a.mask != nullptr;
+  StageLayout L{n, T, SD::nd, use_mask};
+  const int sbytes = (L.bytes() + 127) & ~127;
+  const long long ntiles = (a.l + T - 1) / T;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  if (tid == 0) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    mbar_fence_init();
   }
+  for (int j = tid; j < NMAX; j += BLK) s_v[j] = (j < n && MODE != PM_PRECOND) ? a.v[j] : 0.0;
+  __syncthreads();
+
   double acc[NMAX];
 #pragma unroll
   for (int j = 0; j < NMAX; ++j) acc[j] = 0.0;
-  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < l;
-       i += (long long)gridDim.x * kBlock) {
-    if (LOSS == kLossSvm && mask != nullptr && !mask[i]) continue;  // i not in I
-    if (KIND == DA_HV) {
-      double x[NMAX];
-#pragma unroll
-      for (int j = 0; j < NMAX; ++j) x[j] = j < n ? X[(long long)j * ld + i] : 0.0;
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < NMAX; ++j)
-        if (j < n) s += x[j] * s_v[j];
-      // LR: a0_i = (x_i.v) * dvec_i (loss.cpp:85-89); SVM: row_axpy(i, row_dot(i,v)) (:455)
-      const double c = LOSS == kLossLogistic ? s * dvec[i] : s;
-#pragma unroll
-      for (int j = 0; j < NMAX; ++j) acc[j] += c * x[j];
-    } else if (KIND == DA_GRAD) {
-      const double c = LOSS == kLossLogistic ? zhat[i] : z[i] - y[i];
-#pragma unroll
-      for (int j = 0; j < NMAX; ++j)
-        if (j < n) acc[j] += c * X[(long long)j * ld + i];
-    } else {  // DA_PRECOND: row_axpy_squared, out += a*v*v
-      const double c = LOSS == kLossLogistic ? dvec[i] : 1.0;
-#pragma unroll
-      for (int j = 0; j < NMAX; ++j) {
-        if (j < n) {
-          const double xv = X[(long long)j * ld + i];
-          acc[j] += (c * xv) * xv;
+  double term_acc = 0.0, cnt_acc = 0.0;
+
+  if (wid == NCW) {
+    // ---- producer warp: one 2-D TMA box {T rows x n columns} of X per
+    // tile plus the per-row side arrays, into stage k % nstages
+    if (lane == 0) {
+      for (long long k = 0;; ++k) {
+        const long long t = blockIdx.x + k * gridDim.x;
+        if (t >= ntiles) break;
+        const int s = (int)(k % nstages);
+        if (k >= nstages) mbar_wait_parity(&empty[s], (unsigned)(((k / nstages) - 1) & 1));
+        unsigned char* base = smem + (size_t)s * sbytes;
+        const long long row0 = t * T;
+        mbar_arrive_expect_tx(&full[s], (unsigned)L.bytes());
+        tma_load_2d(base, &xmap, (int)row0, 0, &full[s]);
+        if (SD::nd >= 1) {
+          const double* src = MODE == PM_FWD ? a.y : a.dvec;
+          bulk_g2s(base + (size_t)n * T * 8, src + row0, T * 8, &full[s]);
         }
+        if (use_mask) bulk_g2s(base + (size_t)(n + SD::nd) * T * 8, a.mask + row0, T, &full[s]);
+      }
+    }
+  } else {
+  for (long long k = 0;; ++k) {
+    const long long t = blockIdx.x + k * gridDim.x;
+    if (t >= ntiles) break;
+    const int s = (int)(k % nstages);
+    mbar_wait_parity(&full[s], (unsigned)((k / nstages) & 1));
+    const double* xs = reinterpret_cast<const double*>(smem + (size_t)s * sbytes);
+    const double* side = xs + (size_t)n * T;
+    const uint8_t* ms = reinterpret_cast<const uint8_t*>(side + (size_t)SD::nd * T);
+    const long long i = t * T + tid;
+    const bool in = i < a.l;
+
+    // the whole row into registers first: all LDS issued back to back
+    double x[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) x[j] = j < n ? xs[j * T + tid] : 0.0;
+    if (MODE == PM_PRECOND) {
+      // row_axpy_squared: out += c*x*x with c = D_i (LR) or [i in I] (SVM)
+      double c = LOSS == kLossLogistic ? side[tid] : (use_mask ? (ms[tid] ? 1.0 : 0.0) : 1.0);
+      if (!in) c = 0.0;
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j) acc[j] += (c * x[j]) * x[j];
+    } else {
+      // sequential row dot (row_dot, linalg.cpp:75-86)
+      double sdot = 0.0;
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j)
+        if (j < n) sdot += x[j] * s_v[j];
+      double c;
+      if (MODE == PM_FWD) {
+        const double yi = side[tid];
+        c = 0.0;
+        if (in) {
+          a.z[i] = sdot;
+          if (LOSS == kLossLogistic) {  // logistic_fused_pass, loss.cpp:35-58
+            const double tt = yi * sdot;
+            const double sig = 1.0 / (1.0 + exp(tt));  // exp overflow -> inf -> 0
+            const double zh = -yi * sig;
+            a.zhat[i] = zh;
+            a.dvec_out[i] = (1.0 - sig) * sig;
+            term_acc += log1p_exp_neg(tt);
+            c = zh;  // gradient coefficient (loss.cpp:74-80)
+          } else {  // svm_fused_pass, loss.cpp:94-122 (strict margin > 0)
+            const double margin = 1.0 - yi * sdot;
+            if (margin > 0.0) {
+              a.mask_out[i] = 1;
+              term_acc += margin * margin;
+              cnt_acc += 1.0;
+              c = sdot - yi;  // svm_gradient coefficient (loss.cpp:129-137)
+            } else {
+              a.mask_out[i] = 0;
+            }
+          }
+        }
+      } else {  // PM_HV: LR a0_i = (x_i.v) D_i (loss.cpp:85-89); SVM row_axpy(i, x_i.v) over I
+        if (LOSS == kLossLogistic)
+          c = sdot * side[tid];
+        else
+          c = use_mask ? (ms[tid] ? sdot : 0.0) : sdot;
+        if (!in) c = 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j) acc[j] += c * x[j];  // x[j] = 0 beyond n
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+  }
+  }
+  __syncthreads();  // all stages consumed; the producer has no copy in flight
+
+  // block tree: warp sums, then a fixed warp order (producer warp adds zeros)
+  double* s_red = reinterpret_cast<double*>(smem);
+  constexpr int NW = NCW;
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+    if (j < n) {
+      const double r = warp_sum(acc[j]);
+      if (lane == 0 && wid < NCW) s_red[wid * NMAX + j] = r;
+    }
+  }
+  __syncthreads();
+  if (tid < n) {
+    double tsum = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) tsum += s_red[w * NMAX + tid];
+    a.partials[(long long)blockIdx.x * n + tid] = tsum;
+  }
+
+  if (MODE == PM_FWD) {
+    const double bt = block_sum<BLK>(term_acc, sh, true);
+    const double bc = block_sum<BLK>(cnt_acc, sh, true);
+    if (tid == 0) {
+      a.sc.partials[2 * blockIdx.x] = bt;
+      a.sc.partials[2 * blockIdx.x + 1] = bc;
+    }
+    if (last_block_arrive(a.sc.tickets + T_FUN)) {
+      const double tot = reduce_partials<BLK>(a.sc.partials, gridDim.x, 2, 0, sh);
+      const double cnt = reduce_partials<BLK>(a.sc.partials, gridDim.x, 2, 1, sh);
+      // ww of a short vector, serially like dot() (linalg.cpp:267-272)
+      if (tid == 0) {
+        double ww = 0.0;
+        for (int j = 0; j < n; ++j) ww += a.v[j] * a.v[j];
+        a.obj->ww = ww;
+        a.obj->f = 0.5 * ww + a.C * tot;
+        a.obj->nact = (long long)cnt;
+        a.obj->red[0] = tot;
+        a.obj->red[1] = cnt;
       }
     }
   }
-  store_block_vector<NMAX>(acc, n, partials + (long long)blockIdx.x * n);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
+template <int NMAX, int T, int MODE, int LOSS>
+void launch_pass(const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
+  using SD = Side<MODE, LOSS>;
+  StageLayout L{a.n, T, SD::nd, SD::mask && a.mask != nullptr};
+  const int sbytes = (L.bytes() + 127) & ~127;
+  static const int max_stages = env_int("TRON_B200_DENSE_STAGES", 4);
+  int ns = kSmemBudget / sbytes;
+  if (ns > max_stages) ns = max_stages;
+  if (ns > 4) ns = 4;
+  if (ns < 2) ns = 2;
+  size_t smem = (size_t)ns * sbytes;
+  const size_t red = (size_t)(T / kWarp) * NMAX * 8;
+  if (smem < red) smem = red;
+  auto k = dense_pass_kernel<NMAX, T, MODE, LOSS>;
+  static size_t configured = 0;  // per instantiation; the attribute must not exceed
+  if (smem > configured) {       // opt-in max minus the kernel's static shared memory
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  const int grid = dense_grid(a.l, a.n);
+  k<<<grid, T + kWarp, smem, s>>>(m, a, ns);
+}
+
+template <int NMAX, int T>
+void launch_mode_t(int mode, int loss, const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
+  if (loss == kLossLogistic) {
+    if (mode == PM_FWD) launch_pass<NMAX, T, PM_FWD, kLossLogistic>(m, a, s);
+    else if (mode == PM_HV) launch_pass<NMAX, T, PM_HV, kLossLogistic>(m, a, s);
+    else launch_pass<NMAX, T, PM_PRECOND, kLossLogistic>(m, a, s);
+  } else {
+    if (mode == PM_FWD) launch_pass<NMAX, T, PM_FWD, kLossSvm>(m, a, s);
+    else if (mode == PM_HV) launch_pass<NMAX, T, PM_HV, kLossSvm>(m, a, s);
+    else launch_pass<NMAX, T, PM_PRECOND, kLossSvm>(m, a, s);
+  }
+}
+
+template <int NMAX>
+void launch_mode(int mode, int loss, const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
+  if (dense_tile_rows(a.n) == 128)
+    launch_mode_t<NMAX, 128>(mode, loss, m, a, s);
+  else if (NMAX <= 48)
+    launch_mode_t<NMAX, 256>(mode, loss, m, a, s);
+}
+
+#define TB_NMAX_DISPATCH(n, CALL)                      \
+  if ((n) <= 8) { CALL(8); }                           \
+  else if ((n) <= 16) { CALL(16); }                    \
+  else if ((n) <= 24) { CALL(24); }                    \
+  else if ((n) <= 32) { CALL(32); }                    \
+  else if ((n) <= 40) { CALL(40); }                    \
+  else if ((n) <= 48) { CALL(48); }                    \
+  else { CALL(64); }
+
+void launch(int mode, int loss, const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
+#define TB_CALL(NM) launch_mode<NM>(mode, loss, m, a, s)
+  TB_NMAX_DISPATCH(a.n, TB_CALL)
+#undef TB_CALL
 }
 
 __global__ void __launch_bounds__(1024) dense_finalize_kernel(int n, const double* partials,
@@ -191,6 +343,7 @@ __global__ void transpose_kernel(const double* __restrict__ rm, long long rows, 
 }
 
 // Active-set compaction, ascending (the IndexSet invariant, linalg.hpp:65-86).
+constexpr int kBlock = 256;
 constexpr int kChunk = 1024;  // mask entries per block (256 threads x 4)
 
 __global__ void count_kernel(long long l, const uint8_t* mask, int32_t* counts) {
@@ -244,7 +397,7 @@ __global__ void scatter_kernel(long long l, const uint8_t* mask, const int32_t* 
     flags[k] = (base + k < l) ? mask[base + k] != 0 : 0;
     c += flags[k];
   }
-  // exclusive block scan of c (ballot-free warp scan on small ints)
+  // exclusive block scan of c
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int incl = c;
 #pragma unroll
@@ -262,87 +415,104 @@ __global__ void scatter_kernel(long long l, const uint8_t* mask, const int32_t* 
     if (flags[k]) idx[pos++] = (int32_t)(base + k);
 }
 
+// Gathered panel: rows idx of X, column-major with ldg rows; rows
+// [nI, ldg) are zero so the tiled passes can stream whole tiles.
 __global__ void gather_kernel(long long nI, int n, const double* __restrict__ X, long long ld,
                               const int32_t* __restrict__ idx, double* __restrict__ Xg,
                               long long ldg) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nI;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < ldg;
        k += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx[k];
-    for (int j = 0; j < n; ++j) Xg[(long long)j * ldg + k] = X[(long long)j * ld + i];
+    if (k < nI) {
+      const long long i = idx[k];
+      for (int j = 0; j < n; ++j) Xg[(long long)j * ldg + k] = X[(long long)j * ld + i];
+    } else {
+      for (int j = 0; j < n; ++j) Xg[(long long)j * ldg + k] = 0.0;
+    }
   }
-}
-
-template <int NMAX>
-void launch_forward(long long l, int n, long long ld, const double* X, int loss, const double* w,
-                    const double* y, double C, double* z, double* zhat, double* dvec,
-                    uint8_t* mask, ObjScalars* obj, Scratch sc, cudaStream_t s) {
-  const int grid = dense_grid(l);
-  if (loss == kLossLogistic)
-    dense_forward_kernel<NMAX, kLossLogistic><<<grid, kBlock, 0, s>>>(l, n, ld, X, w, y, C, z, zhat,
-                                                                      dvec, mask, obj, sc);
-  else
-    dense_forward_kernel<NMAX, kLossSvm><<<grid, kBlock, 0, s>>>(l, n, ld, X, w, y, C, z, zhat,
-                                                                 dvec, mask, obj, sc);
-}
-
-template <int NMAX, int KIND>
-void launch_accum_kind(long long l, int n, long long ld, const double* X, int loss, const double* v,
-                       const double* zhat, const double* dvec, const uint8_t* mask,
-                       const double* z, const double* y, double* partials, cudaStream_t s) {
-  const int grid = dense_grid(l);
-  if (loss == kLossLogistic)
-    dense_accum_kernel<NMAX, KIND, kLossLogistic><<<grid, kBlock, 0, s>>>(l, n, ld, X, v, zhat,
-                                                                          dvec, mask, z, y, partials);
-  else
-    dense_accum_kernel<NMAX, KIND, kLossSvm><<<grid, kBlock, 0, s>>>(l, n, ld, X, v, zhat, dvec,
-                                                                     mask, z, y, partials);
-}
-
-template <int NMAX>
-void launch_accum(int kind, long long l, int n, long long ld, const double* X, int loss,
-                  const double* v, const double* zhat, const double* dvec, const uint8_t* mask,
-                  const double* z, const double* y, double* partials, cudaStream_t s) {
-  if (kind == DA_HV)
-    launch_accum_kind<NMAX, DA_HV>(l, n, ld, X, loss, v, zhat, dvec, mask, z, y, partials, s);
-  else if (kind == DA_GRAD)
-    launch_accum_kind<NMAX, DA_GRAD>(l, n, ld, X, loss, v, zhat, dvec, mask, z, y, partials, s);
-  else
-    launch_accum_kind<NMAX, DA_PRECOND>(l, n, ld, X, loss, v, zhat, dvec, mask, z, y, partials, s);
 }
 
 }  // namespace
 
-int dense_grid(int64_t l) {
-  int64_t g = (l + kBlock - 1) / kBlock;
-  int64_t cap = (int64_t)device_sm_count() * 4;
+int64_t dense_ld(int64_t l) { return (l + kDenseTile - 1) / kDenseTile * kDenseTile; }
+
+int dense_make_map(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, int64_t n) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  if (!encode) return -1;
+  if (rows < 1) rows = 1;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)(n > 0 ? n : 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)dense_tile_rows(n), (cuuint32_t)(n > 0 ? n : 1)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+int dense_tile_rows(int64_t n) {
+  static const int forced = env_int("TRON_B200_DENSE_TILE", 0);  // A/B experiments
+  if (n > 48) return 128;
+  return forced == 128 ? 128 : 256;
+}
+
+int dense_grid(int64_t l, int64_t n) {
+  const int64_t T = dense_tile_rows(n);
+  int64_t g = (l + T - 1) / T;
+  const int64_t cap = (int64_t)device_sm_count();
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
 }
 
-#define TB_NMAX_DISPATCH(n, CALL)                      \
-  if ((n) <= 8) { CALL(8); }                           \
-  else if ((n) <= 16) { CALL(16); }                    \
-  else if ((n) <= 24) { CALL(24); }                    \
-  else if ((n) <= 32) { CALL(32); }                    \
-  else if ((n) <= 40) { CALL(40); }                    \
-  else if ((n) <= 48) { CALL(48); }                    \
-  else { CALL(64); }
-
-void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, int loss, const double* w,
+void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUtensorMap& xmap,
+                   int loss, const double* w,
                    const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
-                   ObjScalars* obj, Scratch sc, cudaStream_t s) {
-#define TB_CALL(NM) launch_forward<NM>(l, (int)n, ld, X, loss, w, y, C, z, zhat, dvec, mask, obj, sc, s)
-  TB_NMAX_DISPATCH(n, TB_CALL)
-#undef TB_CALL
+                   double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s) {
+  PassArgs a{};
+  a.l = l;
+  a.ld = ld;
+  a.n = (int)n;
+  a.X = X;
+  a.v = w;
+  a.y = y;
+  a.C = C;
+  a.z = z;
+  a.zhat = zhat;
+  a.dvec_out = dvec;
+  a.mask_out = mask;
+  a.obj = obj;
+  a.sc = sc;
+  a.partials = gparts;
+  launch(PM_FWD, loss, xmap, a, s);
 }
 
-void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X, int loss,
-                 const double* v, const double* zhat, const double* dvec, const uint8_t* mask,
-                 const double* z, const double* y, double* partials, cudaStream_t s) {
-#define TB_CALL(NM) launch_accum<NM>(kind, l, (int)n, ld, X, loss, v, zhat, dvec, mask, z, y, partials, s)
-  TB_NMAX_DISPATCH(n, TB_CALL)
-#undef TB_CALL
+void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X,
+                 const CUtensorMap& xmap, int loss,
+                 const double* v, const double* dvec, const uint8_t* mask, double* partials,
+                 cudaStream_t s) {
+  PassArgs a{};
+  a.l = l;
+  a.ld = ld;
+  a.n = (int)n;
+  a.X = X;
+  a.v = v;
+  a.dvec = dvec;
+  a.mask = mask;
+  a.partials = partials;
+  launch(kind == DA_HV ? PM_HV : PM_PRECOND, loss, xmap, a, s);
 }
 
 void dense_finalize(int64_t n, const double* partials, int nparts, const EpiView& epi, double* out,
@@ -370,7 +540,7 @@ void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, lo
 
 void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int32_t* idx,
                   double* Xg, int64_t ldg, cudaStream_t s) {
-  long long g = (nI + 255) / 256;
+  long long g = (ldg + 255) / 256;
   if (g > (long long)device_sm_count() * 16) g = (long long)device_sm_count() * 16;
   if (g < 1) g = 1;
   gather_kernel<<<(int)g, 256, 0, s>>>(nI, (int)n, X, ld, idx, Xg, ldg);

@@ -156,21 +156,27 @@ void Engine::common_alloc() {
   std::memset(obj_h_, 0, sizeof(ObjScalars));
   std::memset(st_h_, 0, sizeof(CgState));
 
-  const size_t nn = n_ > 0 ? n_ : 1, ll = l_ > 0 ? l_ : 1;
+  const size_t nn = n_ > 0 ? n_ : 1;
+  // dense passes stream whole 256-row tiles of every per-row array they
+  // stage: pad to ld and zero the padding once
+  const size_t ll = dense_ ? (size_t)std::max<int64_t>(ld_, 1) : (size_t)(l_ > 0 ? l_ : 1);
   for (auto& S : slot_) {
     S.w.alloc(nn);
     S.z.alloc(ll);
     if (loss_ == TRON_LOSS_LOGISTIC) {
       S.zhat.alloc(ll);
       S.dvec.alloc(ll);
+      if (dense_) cuda_check(cudaMemsetAsync(S.dvec.p, 0, S.dvec.bytes(), s_), "memset");
     } else {
       S.mask.alloc(ll);
+      if (dense_) cuda_check(cudaMemsetAsync(S.mask.p, 0, S.mask.bytes(), s_), "memset");
     }
+    if (dense_) S.gparts.alloc((size_t)dense_grid(l_, n_) * nn);
   }
   for (DevBuf<double>* b : {&g_, &M_, &d_, &r0_, &r1_, &p_, &hp_, &vtmp_, &otmp_}) b->alloc(nn);
   if (comm_.active()) raw_.alloc(nn);
   if (!dense_) a_.alloc(ll);
-  if (dense_) parts_.alloc((size_t)dense_grid(l_) * nn);
+  if (dense_) parts_.alloc((size_t)dense_grid(l_, n_) * nn);
   small_engine_ = dense_ || n_ <= kSmallCgMaxN;
   // TRON_B200_NO_GRAPH=1 runs the CG loop host-driven (per-kernel profiling:
   // ncu cannot profile kernel nodes of graphs with conditional nodes).
@@ -309,11 +315,16 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->budget_ = opt.gathered_budget_bytes;
   e->row_begin_ = opt.row_begin;
   e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
+  e->ld_ = dense_ld((int64_t)l);
   e->common_alloc();
   cudaStream_t s = e->s_;
-  e->ld_ = (int64_t)((l + 3) / 4 * 4);
-  e->Xc_.alloc((size_t)e->ld_ * (n > 0 ? n : 1));
-  e->y_.alloc(l > 0 ? l : 1);
+  e->Xc_.alloc((size_t)std::max<int64_t>(e->ld_, 1) * (n > 0 ? n : 1));
+  e->y_.alloc((size_t)std::max<int64_t>(e->ld_, 1));
+  cuda_check(cudaMemsetAsync(e->y_.p, 0, e->y_.bytes(), s), "memset");
+  if (n > 0 && e->ld_ > (int64_t)l)
+    cuda_check(cudaMemset2DAsync(e->Xc_.p + l, e->ld_ * sizeof(double), 0,
+                                 (e->ld_ - (int64_t)l) * sizeof(double), n, s),
+               "memset pad");
   if (l > 0) {
     cuda_check(cudaMemcpyAsync(e->y_.p, y, l * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
     // chunked row-major upload + on-device transpose to column-major
@@ -341,6 +352,8 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
   }
+  if (dense_make_map(&e->xmap_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n) != 0)
+    raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the dense matrix");
   if (loss == TRON_LOSS_L2SVM) {
     e->idx_.alloc(l > 0 ? l : 1);
     e->idx_tmp_.alloc((l + 1023) / 1024 + 2);
@@ -370,7 +383,8 @@ uint64_t Engine::memory_bytes() const {
                chunk_rank_.bytes() + chunk_start_.bytes() + fix_chunk_.bytes() +
                fix_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
   for (const auto& S : slot_)
-    b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes();
+    b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes() +
+         S.gparts.bytes();
   b += g_.bytes() * 9 + a_.bytes() + parts_.bytes();
   return b;
 }
@@ -395,8 +409,8 @@ void Engine::read_cg(CgState* out) {
 void Engine::forward(Slot& S) {
   const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
   if (dense_) {
-    dense_forward(l_, n_, ld_, Xc_.p, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
-                  obj_d_, sc_, s_);
+    dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
+                  S.gparts.p, obj_d_, sc_, s_);
   } else {
     csr_forward(X_, group_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_,
                 s_);
@@ -457,29 +471,35 @@ void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& 
   count_launch(3);
 }
 
+// kind = DA_HV / DA_PRECOND (one tiled pass) or -1: finish the gradient
+// partials the committed slot's margin pass already accumulated.
 void Engine::dense_vector(int kind, const double* v, const EpiView& epi, double* out) {
   const Slot& S = slot_[cand_ ^ 1];
   const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
   const bool gathered = kind == DA_HV && gathered_valid_;
-  if (gathered) {
-    dense_accum(DA_HV, nI_, n_, ldg_, Xg_.p, kLossSvm, v, nullptr, nullptr, nullptr, nullptr,
-                nullptr, parts_.p, s_);
+  const double* parts = parts_.p;
+  int nparts = dense_grid(gathered ? nI_ : l_, n_);
+  if (kind < 0) {
+    parts = S.gparts.p;
+    nparts = dense_grid(l_, n_);
+  } else if (gathered) {
+    dense_accum(DA_HV, nI_, n_, ldg_, Xg_.p, gmap_, kLossSvm, v, nullptr, nullptr, parts_.p, s_);
+    count_launch(1);
   } else {
-    dense_accum(kind, l_, n_, ld_, Xc_.p, loss, v, S.zhat.p, S.dvec.p, S.mask.p, S.z.p, y_.p,
-                parts_.p, s_);
+    dense_accum(kind, l_, n_, ld_, Xc_.p, xmap_, loss, v, S.dvec.p, S.mask.p, parts_.p, s_);
+    count_launch(1);
   }
-  const int nparts = dense_grid(gathered ? nI_ : l_);
   if (!comm_.active()) {
-    dense_finalize(n_, parts_.p, nparts, epi, out, s_);
-    count_launch(2);
+    dense_finalize(n_, parts, nparts, epi, out, s_);
+    count_launch(1);
     return;
   }
   EpiView raw;
   raw.kind = EPI_RAW;
-  dense_finalize(n_, parts_.p, nparts, raw, raw_.p, s_);
+  dense_finalize(n_, parts, nparts, raw, raw_.p, s_);
   comm_.allreduce_sum(raw_.p, n_, s_);
   vec_epilogue(n_, raw_.p, epi, out, s_);
-  count_launch(3);
+  count_launch(2);
 }
 
 // ----------------------------------------------------------------------------
@@ -492,7 +512,7 @@ void Engine::gradient_dev() {
   epi.base = S.w.p;
   epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
   if (dense_) {
-    dense_vector(DA_GRAD, nullptr, epi, g_.p);
+    dense_vector(-1, nullptr, epi, g_.p);  // partials from the fused margin pass
   } else {
     UView u;
     if (loss_ == TRON_LOSS_LOGISTIC) {
@@ -529,12 +549,14 @@ void Engine::gather_active() {
                                "answers Hessian products by index-indirect traversal instead");
   }
   const int nI = compact(S, idx_);
-  const int64_t ldg = (int64_t)((nI + 3) / 4 * 4);
-  if ((size_t)ldg * n_ > Xg_.n) Xg_.alloc((size_t)std::max<int64_t>(ldg, 4) * n_);
+  const int64_t ldg = dense_ld(nI);
+  if ((size_t)ldg * n_ > Xg_.n) Xg_.alloc((size_t)std::max<int64_t>(ldg, kDenseTile) * n_);
   if (nI > 0) {
     dense_gather(nI, n_, Xc_.p, ld_, idx_.p, Xg_.p, ldg, s_);
     count_launch(1);
   }
+  if (dense_make_map(&gmap_, Xg_.p, ldg, nI, n_) != 0)
+    raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gathered panel");
   nI_ = nI;
   ldg_ = ldg;
   gathered_valid_ = true;
@@ -728,9 +750,8 @@ void Engine::build_graph(int k, bool use_m) {
     if (dense_) {
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
-      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, loss, p_.p, S.zhat.p, S.dvec.p, S.mask.p, S.z.p, y_.p,
-                  parts_.p, s_);
-      cg_small_step(v, parts_.p, dense_grid(l_), loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_,
+      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, xmap_, loss, p_.p, S.dvec.p, S.mask.p, parts_.p, s_);
+      cg_small_step(v, parts_.p, dense_grid(l_, n_), loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_,
                     st_d_, cond, s_);
       count_launch(2);
     } else {
@@ -1004,12 +1025,12 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
   } else {
     const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
     out->transposed_ms = time_it([&] {
-      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, loss, vtmp_.p, S.zhat.p, S.dvec.p, S.mask.p, S.z.p,
-                  y_.p, parts_.p, s_);
+      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, xmap_, loss, vtmp_.p, S.dvec.p, S.mask.p, parts_.p, s_);
     });
     out->forward_ms = time_it([&] {
-      dense_forward(l_, n_, ld_, Xc_.p, loss, S.w.p, y_.p, C_, slot_[cand_].z.p,
-                    slot_[cand_].zhat.p, slot_[cand_].dvec.p, slot_[cand_].mask.p, obj_d_, sc_, s_);
+      dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, slot_[cand_].z.p,
+                    slot_[cand_].zhat.p, slot_[cand_].dvec.p, slot_[cand_].mask.p,
+                    slot_[cand_].gparts.p, obj_d_, sc_, s_);
     });
   }
   out->grad_ms = time_it([&] { gradient_dev(); });

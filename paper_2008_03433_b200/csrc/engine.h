@@ -106,6 +106,7 @@ class Engine {
   struct Slot {
     DevBuf<double> w, z, zhat, dvec;
     DevBuf<uint8_t> mask;
+    DevBuf<double> gparts;  // dense: gradient partials from this slot's margin pass
     double f = 0.0;
     long long nact = 0;
     bool valid = false;
@@ -146,6 +147,8 @@ class Engine {
   // dense column-major
   DevBuf<double> Xc_;
   int64_t ld_ = 0;
+  alignas(64) CUtensorMap xmap_{};  // 2-D TMA descriptor of Xc_
+  alignas(64) CUtensorMap gmap_{};  // ... of the gathered panel Xg_
   DevBuf<double> Xg_;  // gathered panel X_{I,:} (Gathered strategy)
   int64_t ldg_ = 0, nI_ = 0;
   bool gathered_valid_ = false;

@@ -3,6 +3,7 @@
 // nnz and n below 2^31 per shard).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -169,20 +170,35 @@ void cg_small_step(const CgVectors& v, const double* partials, int nparts, doubl
                    CgState* st, Cond cond, cudaStream_t s);
 
 // ---- dense column-major kernels (dense_kernels.cu), n <= 64 -----------------
+// X is column-major with ld = dense_ld(l) rows (a multiple of kDenseTile,
+// padding zeroed); every per-row side array a pass stages (y, D, mask) must
+// also be allocated and zero-padded to ld entries.
 constexpr int kDenseMaxN = 64;
-int dense_grid(int64_t l);
-void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, int loss, const double* w,
+constexpr int64_t kDenseTile = 256;
+int64_t dense_ld(int64_t l);
+// Rows per tile (= threads per CTA) of the tiled passes for n features.
+int dense_tile_rows(int64_t n);
+// Number of CTAs (= per-block partial vectors) of every tiled pass.
+int dense_grid(int64_t l, int64_t n);
+// Fused margin pass: z, LR zhat/dvec or SVM mask, f into obj, and the
+// candidate's gradient partials gparts[grid][n] (sum_i c_i x_i with
+// c = zhat (LR) or [i in I](z_i - y_i) (SVM)).
+// 2-D TMA descriptor of a column-major X (rows x n, leading dimension ld):
+// box = {dense_tile_rows(n) rows, n columns}.  Returns 0 on success.
+int dense_make_map(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, int64_t n);
+void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUtensorMap& xmap,
+                   int loss, const double* w,
                    const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
-                   ObjScalars* obj, Scratch sc, cudaStream_t s);
-// partial sums per block (grid = dense_grid(l)) of:
-//  GRAD:    sum_i c_i x_i   with c = zhat (LR) or mask?(z-y):0 (SVM)
+                   double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s);
+// partial sums per block (grid = dense_grid(l, n)) of:
 //  HV:      sum_i c_i x_i   with c = (x_i.v)*dvec_i (LR) or mask?(x_i.v):0 (SVM;
 //           mask == nullptr => every row active, used on the gathered panel)
 //  PRECOND: sum_i (c_i x_ij) x_ij with c = dvec (LR) or mask (SVM)
-enum DenseAccum : int { DA_GRAD = 0, DA_HV = 1, DA_PRECOND = 2 };
-void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X, int loss,
-                 const double* v, const double* zhat, const double* dvec, const uint8_t* mask,
-                 const double* z, const double* y, double* partials, cudaStream_t s);
+enum DenseAccum : int { DA_HV = 1, DA_PRECOND = 2 };
+void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X,
+                 const CUtensorMap& xmap, int loss,
+                 const double* v, const double* dvec, const uint8_t* mask, double* partials,
+                 cudaStream_t s);
 // out_j = base_j (or cbase) + scale * sum_b partials[b*n + j]
 void dense_finalize(int64_t n, const double* partials, int nparts, const EpiView& epi, double* out,
                     cudaStream_t s);
@@ -193,7 +209,7 @@ void dense_transpose_chunk(const double* rm, int64_t rows, int64_t n, double* X,
 // count_out (device) receives |I|. tmp needs >= ceil(l/1024)+1 ints.
 void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, long long* count_out,
                   cudaStream_t s);
-// Gathered strategy: Xg (ld_g rows) <- rows idx of X (column-major both).
+// Gathered strategy: Xg (ldg = dense_ld(nI) rows, tail zeroed) <- rows idx of X.
 void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int32_t* idx,
                   double* Xg, int64_t ldg, cudaStream_t s);
 
