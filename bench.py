@@ -117,6 +117,25 @@ def h2d_bytes(p):
     return int(b)
 
 
+def pin_problem(p, torch):
+    """Copy of a Problem whose arrays live in page-locked host memory."""
+    from paper_2008_03433_b200.tron import FeatureMatrix, Problem
+
+    def pinned(a):
+        t = torch.empty(a.size, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+        out = t.numpy()
+        out[...] = a.reshape(-1)
+        return out
+
+    X = p.X
+    if X.layout == "csr":
+        Xp = FeatureMatrix("csr", X.rows, X.cols, pinned(X.values), pinned(X.row_offsets),
+                           pinned(X.col_indices))
+    else:
+        Xp = FeatureMatrix("dense", X.rows, X.cols, pinned(X.values))
+    return Problem(Xp, pinned(p.y), p.C)
+
+
 def read_traffic(workload):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -270,14 +289,17 @@ def main():
     achieved = ab["hv"] / hv_s / 1e9
     trans_gbs = ab["transposed"] / (kt["transposed_ms"] / 1e3) / 1e9
 
-    # ---- e2e: host buffers through the C ABI (create = H2D + CSC build, solve, w D2H)
+    # ---- e2e: the public API from pinned host buffers (create = H2D + on-device
+    # CSC build, solve, w D2H), every step; the pinned copies are made untimed
+    p_pin = pin_problem(p, torch)
     e2e = []
     for k in range(max(2, min(args.steps, 5))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        with make_evaluator(p, loss, plan) as ev2:
+        with make_evaluator(p_pin, loss, plan) as ev2:
             r2 = ev2.solve(cfg)
         e2e.append(time.perf_counter() - t0)
+    del p_pin
     e2e_v = float(np.median(e2e))
     if dist is not None:
         t = torch.tensor([e2e_v], dtype=torch.float64)
@@ -338,7 +360,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes(p),
                 "d2h_bytes_per_step": int(8 * p.X.cols + 64),
-                "what": "create (H2D + device CSC build) + solve + w to host, via the C ABI"},
+                "what": "make_evaluator from pinned host arrays (H2D + device CSC build / transpose) + solve + w to host + destroy, via the C ABI"},
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
         "device_memory_bytes": ev.memory_bytes(),

@@ -9,6 +9,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -99,33 +102,87 @@ void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
 // ----------------------------------------------------------------------------
 namespace {
 
+// Input validation runs on the worker pool; the first offending row found
+// is re-checked sequentially so the error (class + message) is exactly the
+// one a front-to-back scan reports.
+template <class Bad>
+uint64_t first_bad(uint64_t count, Bad bad) {
+  std::atomic<uint64_t> first{UINT64_MAX};
+  parallel_for(count, 1u << 16, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e && i < first.load(std::memory_order_relaxed); ++i)
+      if (bad(i)) {
+        uint64_t cur = first.load();
+        while (i < cur && !first.compare_exchange_weak(cur, i)) {
+        }
+        return;
+      }
+  });
+  return first.load();
+}
+
 void validate_labels_C(uint64_t l, const double* y, double C) {
-  for (uint64_t i = 0; i < l; ++i) {
-    const double v = y[i];
-    if (v != 1.0 && v != -1.0)
-      raise(TRON_ERR_DIMENSION, "problem: label " + std::to_string(v) + " not in {-1,+1}");
-  }
+  const uint64_t i = first_bad(l, [&](uint64_t k) { return y[k] != 1.0 && y[k] != -1.0; });
+  if (i != UINT64_MAX)
+    raise(TRON_ERR_DIMENSION, "problem: label " + std::to_string(y[i]) + " not in {-1,+1}");
   if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");
 }
 
 void validate_csr(uint64_t l, uint64_t n, const int64_t* ro, const int32_t* ci) {
   if (ro[0] != 0) raise(TRON_ERR_DIMENSION, "csr matrix: offsets/indices/values disagree");
-  for (uint64_t i = 0; i < l; ++i) {
-    if (ro[i] > ro[i + 1])
-      raise(TRON_ERR_DIMENSION, "csr matrix: decreasing row offset at row " + std::to_string(i));
+  auto check_row = [&](uint64_t i, bool throw_it) {
+    if (ro[i] > ro[i + 1]) {
+      if (throw_it)
+        raise(TRON_ERR_DIMENSION, "csr matrix: decreasing row offset at row " + std::to_string(i));
+      return true;
+    }
     int32_t prev = -1;
     for (int64_t k = ro[i]; k < ro[i + 1]; ++k) {
       const int32_t c = ci[k];
-      if (c < 0 || static_cast<uint64_t>(c) >= n)
-        raise(TRON_ERR_BOUNDS, "csr matrix: column " + std::to_string(c) + " out of range in row " +
-                                   std::to_string(i));
-      if (c <= prev)
-        raise(TRON_ERR_DIMENSION,
-              "csr matrix: column indices not strictly ascending in row " + std::to_string(i));
+      if (c < 0 || static_cast<uint64_t>(c) >= n) {
+        if (throw_it)
+          raise(TRON_ERR_BOUNDS, "csr matrix: column " + std::to_string(c) +
+                                     " out of range in row " + std::to_string(i));
+        return true;
+      }
+      if (c <= prev) {
+        if (throw_it)
+          raise(TRON_ERR_DIMENSION,
+                "csr matrix: column indices not strictly ascending in row " + std::to_string(i));
+        return true;
+      }
       prev = c;
     }
-  }
+    return false;
+  };
+  // offsets first (a decreasing offset makes later rows' ranges meaningless)
+  const uint64_t dec = first_bad(l, [&](uint64_t i) { return ro[i] > ro[i + 1]; });
+  const uint64_t lim = dec == UINT64_MAX ? l : dec;
+  const uint64_t bad = first_bad(lim, [&](uint64_t i) { return check_row(i, false); });
+  if (bad != UINT64_MAX) check_row(bad, true);
+  if (dec != UINT64_MAX) check_row(dec, true);
 }
+
+// TRON_B200_TRACE=1: phase times of context creation on stderr.
+struct PhaseTrace {
+  bool on;
+  cudaStream_t s = nullptr;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit PhaseTrace(const char* what) {
+    const char* e = std::getenv("TRON_B200_TRACE");
+    on = e && e[0] == '1';
+    t0 = last = std::chrono::steady_clock::now();
+    if (on) std::fprintf(stderr, "[tron_b200] %s\n", what);
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    if (s) cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tron_b200]   %-28s %8.3f ms (total %8.3f)\n", phase,
+                 std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 
 void check_options(int loss, const tron_gpu_options& opt) {
   if (loss != TRON_LOSS_LOGISTIC && loss != TRON_LOSS_L2SVM)
@@ -140,21 +197,24 @@ void check_options(int loss, const tron_gpu_options& opt) {
 
 void Engine::common_alloc() {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  prepare_device_pool(device_);
   cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "cudaStreamCreate");
+  stream_owner_.s = s_;
+  alloc_stream() = s_;  // the creating entry holds an AllocScope
   sc_partials_.alloc(kMaxPartialBlocks * 4);
   sc_tickets_.alloc(kNumTickets);
   cuda_check(cudaMemsetAsync(sc_tickets_.p, 0, sc_tickets_.bytes(), s_), "memset");
   sc_.partials = sc_partials_.p;
   sc_.tickets = sc_tickets_.p;
-  cuda_check(cudaMalloc(&obj_d_, sizeof(ObjScalars)), "cudaMalloc");
+  obj_buf_.alloc(1);
+  st_buf_.alloc(1);
+  obj_d_ = obj_buf_.p;
+  st_d_ = st_buf_.p;
   cuda_check(cudaMemsetAsync(obj_d_, 0, sizeof(ObjScalars), s_), "memset");
-  cuda_check(cudaMallocHost(&obj_h_, sizeof(ObjScalars)), "cudaMallocHost");
-  cuda_check(cudaMalloc(&st_d_, sizeof(CgState)), "cudaMalloc");
   cuda_check(cudaMemsetAsync(st_d_, 0, sizeof(CgState), s_), "memset");
-  cuda_check(cudaStreamSynchronize(s_), "init");
-  cuda_check(cudaMallocHost(&st_h_, sizeof(CgState)), "cudaMallocHost");
-  std::memset(obj_h_, 0, sizeof(ObjScalars));
-  std::memset(st_h_, 0, sizeof(CgState));
+  static_assert(sizeof(ObjScalars) <= 256 && sizeof(CgState) <= 256, "pinned block size");
+  obj_h_ = static_cast<ObjScalars*>(pinned_block_get());
+  st_h_ = static_cast<CgState*>(pinned_block_get());
 
   const size_t nn = n_ > 0 ? n_ : 1;
   // dense passes stream whole 256-row tiles of every per-row array they
@@ -187,11 +247,14 @@ void Engine::common_alloc() {
 std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, const int64_t* ro,
                                            const int32_t* ci, const double* vals, const double* y,
                                            double C, const tron_gpu_options& opt) {
+  AllocScope scope(nullptr);
+  PhaseTrace tr("create_csr");
   check_options(loss, opt);
   if (!ro || !y || (l > 0 && ro[l] > 0 && (!ci || !vals)))
     raise(TRON_ERR_ARGUMENT, "null problem array");
   validate_csr(l, n, ro, ci);
   validate_labels_C(l, y, C);
+  tr.mark("host validation");
   const int64_t nnz = ro[l];
   if (nnz >= (int64_t{1} << 31) || n >= (uint64_t{1} << 31) || l >= (uint64_t{1} << 31))
     raise(TRON_ERR_DIMENSION,
@@ -214,6 +277,8 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
   e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
   e->common_alloc();
   cudaStream_t s = e->s_;
+  tr.s = s;
+  tr.mark("context + state alloc");
 
   e->rptr_.alloc(l + 1);
   e->cidx_.alloc(nnz);
@@ -225,23 +290,20 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
   {
     DevBuf<int64_t> ro64;
     ro64.alloc(l + 1);
-    cuda_check(cudaMemcpyAsync(ro64.p, ro, (l + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s),
-               "H2D");
+    upload(ro64.p, ro, (l + 1) * sizeof(int64_t), s);
     narrow_offsets(ro64.p, e->rptr_.p, (int64_t)(l + 1), s);
     if (nnz > 0) {
-      cuda_check(cudaMemcpyAsync(e->cidx_.p, ci, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s),
-                 "H2D");
-      cuda_check(cudaMemcpyAsync(e->rval_.p, vals, nnz * sizeof(double), cudaMemcpyHostToDevice, s),
-                 "H2D");
+      upload(e->cidx_.p, ci, nnz * sizeof(int32_t), s);
+      upload(e->rval_.p, vals, nnz * sizeof(double), s);
     }
-    if (l > 0)
-      cuda_check(cudaMemcpyAsync(e->y_.p, y, l * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
-    cuda_check(cudaStreamSynchronize(s), "upload");
+    if (l > 0) upload(e->y_.p, y, l * sizeof(double), s);
   }
+  tr.mark("matrix alloc + H2D");
   e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
   const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
   if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
   e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
+  tr.mark("device CSC build");
   {
     // one-time structure analysis of the CSC copy on the host (csc_seg.cu)
     std::vector<int32_t> cptr_h(n + 1);
@@ -280,6 +342,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     e->plan_.carry = e->carry_.p;
     cuda_check(cudaStreamSynchronize(s), "seg plan upload");
   }
+  tr.mark("segmented plan");
   e->group_ = choose_group((int64_t)l, nnz);
   cuda_check(cudaStreamSynchronize(s), "csc build");
   cuda_check(cudaGetLastError(), "csc build");
@@ -289,9 +352,12 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
 std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
                                              const double* row_major, const double* y, double C,
                                              const tron_gpu_options& opt) {
+  AllocScope scope(nullptr);
+  PhaseTrace tr("create_dense");
   check_options(loss, opt);
   if (!y || (l * n > 0 && !row_major)) raise(TRON_ERR_ARGUMENT, "null problem array");
   validate_labels_C(l, y, C);
+  tr.mark("host validation");
   if (n > (uint64_t)kDenseMaxN) {
     // Wide dense problems run through the sparse kernels (explicit entries).
     if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
@@ -318,6 +384,8 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->ld_ = dense_ld((int64_t)l);
   e->common_alloc();
   cudaStream_t s = e->s_;
+  tr.s = s;
+  tr.mark("context + state alloc");
   e->Xc_.alloc((size_t)std::max<int64_t>(e->ld_, 1) * (n > 0 ? n : 1));
   e->y_.alloc((size_t)std::max<int64_t>(e->ld_, 1));
   cuda_check(cudaMemsetAsync(e->y_.p, 0, e->y_.bytes(), s), "memset");
@@ -326,7 +394,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
                                  (e->ld_ - (int64_t)l) * sizeof(double), n, s),
                "memset pad");
   if (l > 0) {
-    cuda_check(cudaMemcpyAsync(e->y_.p, y, l * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    upload(e->y_.p, y, l * sizeof(double), s);
     // chunked row-major upload + on-device transpose to column-major
     const int64_t chunk_rows =
         std::max<int64_t>(1, (int64_t{64} << 20) / (int64_t)(sizeof(double) * std::max<uint64_t>(n, 1)));
@@ -341,9 +409,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     for (int64_t r0 = 0; r0 < (int64_t)l; r0 += chunk_rows, k ^= 1) {
       const int64_t rows = std::min<int64_t>(chunk_rows, (int64_t)l - r0);
       if (used[k]) cudaEventSynchronize(ev[k]);
-      cuda_check(cudaMemcpyAsync(stage[k].p, row_major + (size_t)r0 * n, rows * n * sizeof(double),
-                                 cudaMemcpyHostToDevice, s),
-                 "H2D");
+      upload(stage[k].p, row_major + (size_t)r0 * n, rows * n * sizeof(double), s);
       dense_transpose_chunk(stage[k].p, rows, n, e->Xc_.p, e->ld_, r0, s);
       cudaEventRecord(ev[k], s);
       used[k] = true;
@@ -352,6 +418,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
   }
+  tr.mark("matrix alloc + H2D + transpose");
   if (dense_make_map(&e->xmap_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n) != 0)
     raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the dense matrix");
   if (loss == TRON_LOSS_L2SVM) {
@@ -370,11 +437,9 @@ Engine::~Engine() {
       if (graph_exec_[a][b]) cudaGraphExecDestroy(graph_exec_[a][b]);
       if (graph_[a][b]) cudaGraphDestroy(graph_[a][b]);
     }
-  if (obj_d_) cudaFree(obj_d_);
-  if (obj_h_) cudaFreeHost(obj_h_);
-  if (st_d_) cudaFree(st_d_);
-  if (st_h_) cudaFreeHost(st_h_);
-  if (s_) cudaStreamDestroy(s_);
+  pinned_block_put(obj_h_);
+  pinned_block_put(st_h_);
+  // DevBuf members queue their frees on s_; stream_owner_ then syncs + destroys it
 }
 
 uint64_t Engine::memory_bytes() const {
@@ -540,6 +605,7 @@ int Engine::compact(const Slot& S, DevBuf<int32_t>& idx) {
 }
 
 void Engine::gather_active() {
+  AllocScope scope(s_);
   const Slot& S = slot_[cand_ ^ 1];
   const uint64_t projected = (uint64_t)S.nact * (uint64_t)n_ * sizeof(double);
   if (projected > budget_) {
@@ -674,6 +740,7 @@ void Engine::state_lr(int which, double* z, double* zhat, double* dvec) {
 }
 
 void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint64_t* n_active) {
+  AllocScope scope(s_);
   if (loss_ != TRON_LOSS_L2SVM) raise(TRON_ERR_LOGIC, "not an L2-SVM evaluator");
   const Slot& S = which == 0 ? slot_[cand_] : slot_[cand_ ^ 1];
   if (!(which == 0 ? S.valid : committed_valid_)) raise(TRON_ERR_LOGIC, "state slot is empty");
@@ -986,6 +1053,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
 // per-kernel timing for the roofline figures of bench.py
 // ----------------------------------------------------------------------------
 void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
+  AllocScope scope(s_);
   if (!committed_valid_) raise(TRON_ERR_LOGIC, "bench_kernels() needs a committed state");
   if (flush_l2 && flush_.n == 0) flush_.alloc((size_t)(256u << 20) / 8);  // 256 MiB > L2
   cudaEvent_t a, b;

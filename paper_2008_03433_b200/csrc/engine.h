@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "hostio.h"
 #include "kernels.h"
 #include "tron_b200.h"
 
@@ -23,10 +24,13 @@ struct StatusError : std::runtime_error {
 [[noreturn]] void raise(int status, const std::string& msg);
 void cuda_check(cudaError_t e, const char* what);
 
+// Device buffer from the stream-ordered pool (hostio.h): allocated and
+// freed in the order of the stream current at alloc() (AllocScope).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -34,14 +38,32 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    s = alloc_stream();
+    if (count)
+      cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s),
+                 "cudaMallocAsync");
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
   }
   size_t bytes() const { return n * sizeof(T); }
+};
+
+// Owns the context stream; declared first in Engine so it is destroyed after
+// every DevBuf member has queued its free on it.
+struct StreamOwner {
+  cudaStream_t s = nullptr;
+  StreamOwner() = default;
+  StreamOwner(const StreamOwner&) = delete;
+  StreamOwner& operator=(const StreamOwner&) = delete;
+  ~StreamOwner() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
 };
 
 // Lazily-loaded NCCL (libnccl.so.2) for the row-sharded multi-GPU layout.
@@ -103,6 +125,7 @@ class Engine {
 
  private:
   Engine() = default;
+  StreamOwner stream_owner_;  // first member: destroyed last
   struct Slot {
     DevBuf<double> w, z, zhat, dvec;
     DevBuf<uint8_t> mask;
@@ -166,6 +189,8 @@ class Engine {
   DevBuf<double> sc_partials_;
   DevBuf<unsigned int> sc_tickets_;
   Scratch sc_{};
+  DevBuf<ObjScalars> obj_buf_;
+  DevBuf<CgState> st_buf_;
   ObjScalars* obj_d_ = nullptr;
   ObjScalars* obj_h_ = nullptr;  // pinned
   CgState* st_d_ = nullptr;
