@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <future>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -125,6 +126,13 @@ void validate_labels_C(uint64_t l, const double* y, double C) {
   if (i != UINT64_MAX)
     raise(TRON_ERR_DIMENSION, "problem: label " + std::to_string(y[i]) + " not in {-1,+1}");
   if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");
+}
+
+void validate_offsets(uint64_t l, const int64_t* ro) {
+  if (ro[0] != 0) raise(TRON_ERR_DIMENSION, "csr matrix: offsets/indices/values disagree");
+  const uint64_t dec = first_bad(l, [&](uint64_t i) { return ro[i] > ro[i + 1]; });
+  if (dec != UINT64_MAX)
+    raise(TRON_ERR_DIMENSION, "csr matrix: decreasing row offset at row " + std::to_string(dec));
 }
 
 void validate_csr(uint64_t l, uint64_t n, const int64_t* ro, const int32_t* ci) {
@@ -252,9 +260,9 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
   check_options(loss, opt);
   if (!ro || !y || (l > 0 && ro[l] > 0 && (!ci || !vals)))
     raise(TRON_ERR_ARGUMENT, "null problem array");
-  validate_csr(l, n, ro, ci);
-  validate_labels_C(l, y, C);
-  tr.mark("host validation");
+  // offsets first (they size the device arrays); the O(nnz) column checks and
+  // the labels run on the worker pool while the uploads are in flight
+  validate_offsets(l, ro);
   const int64_t nnz = ro[l];
   if (nnz >= (int64_t{1} << 31) || n >= (uint64_t{1} << 31) || l >= (uint64_t{1} << 31))
     raise(TRON_ERR_DIMENSION,
@@ -264,89 +272,102 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     raise(TRON_ERR_STRATEGY,
           "gathered L2-SVM strategy needs dense features on the GPU backend; use Indirect "
           "(masked CSR/CSC traversal)");
-  std::unique_ptr<Engine> e(new Engine());
-  e->loss_ = loss;
-  e->dense_ = false;
-  e->l_ = (int64_t)l;
-  e->n_ = (int64_t)n;
-  e->C_ = C;
-  e->device_ = opt.device;
-  e->svm_strategy_ = opt.svm_strategy;
-  e->budget_ = opt.gathered_budget_bytes;
-  e->row_begin_ = opt.row_begin;
-  e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
-  e->common_alloc();
-  cudaStream_t s = e->s_;
-  tr.s = s;
-  tr.mark("context + state alloc");
+  // column + label checks run on the worker pool while the uploads are in flight
+  auto valid = std::async(std::launch::async, [&] {
+    validate_csr(l, n, ro, ci);
+    validate_labels_C(l, y, C);
+  });
+  try {
+    std::unique_ptr<Engine> e(new Engine());
+    e->loss_ = loss;
+    e->dense_ = false;
+    e->l_ = (int64_t)l;
+    e->n_ = (int64_t)n;
+    e->C_ = C;
+    e->device_ = opt.device;
+    e->svm_strategy_ = opt.svm_strategy;
+    e->budget_ = opt.gathered_budget_bytes;
+    e->row_begin_ = opt.row_begin;
+    e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
+    e->common_alloc();
+    cudaStream_t s = e->s_;
+    tr.s = s;
+    tr.mark("context + state alloc");
 
-  e->rptr_.alloc(l + 1);
-  e->cidx_.alloc(nnz);
-  e->rval_.alloc(nnz);
-  e->cptr_.alloc(n + 1);
-  e->ridx_.alloc(nnz);
-  e->cval_.alloc(nnz);
-  e->y_.alloc(l > 0 ? l : 1);
-  {
-    DevBuf<int64_t> ro64;
-    ro64.alloc(l + 1);
-    upload(ro64.p, ro, (l + 1) * sizeof(int64_t), s);
-    narrow_offsets(ro64.p, e->rptr_.p, (int64_t)(l + 1), s);
-    if (nnz > 0) {
-      upload(e->cidx_.p, ci, nnz * sizeof(int32_t), s);
-      upload(e->rval_.p, vals, nnz * sizeof(double), s);
+    e->rptr_.alloc(l + 1);
+    e->cidx_.alloc(nnz);
+    e->rval_.alloc(nnz);
+    e->cptr_.alloc(n + 1);
+    e->ridx_.alloc(nnz);
+    e->cval_.alloc(nnz);
+    e->y_.alloc(l > 0 ? l : 1);
+    {
+      DevBuf<int64_t> ro64;
+      ro64.alloc(l + 1);
+      upload(ro64.p, ro, (l + 1) * sizeof(int64_t), s);
+      narrow_offsets(ro64.p, e->rptr_.p, (int64_t)(l + 1), s);
+      if (nnz > 0) {
+        upload(e->cidx_.p, ci, nnz * sizeof(int32_t), s);
+        upload(e->rval_.p, vals, nnz * sizeof(double), s);
+      }
+      if (l > 0) upload(e->y_.p, y, l * sizeof(double), s);
     }
-    if (l > 0) upload(e->y_.p, y, l * sizeof(double), s);
+    tr.mark("matrix alloc + H2D issue");
+    valid.get();
+    tr.mark("host validation (overlapped)");
+    e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
+    const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
+    if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
+    e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
+    tr.mark("device CSC build");
+    {
+      // one-time structure analysis of the CSC copy on the host (csc_seg.cu)
+      std::vector<int32_t> cptr_h(n + 1);
+      cuda_check(cudaMemcpyAsync(cptr_h.data(), e->cptr_.p, (n + 1) * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s),
+                 "D2H");
+      cuda_check(cudaStreamSynchronize(s), "cptr download");
+      SegPlanHost P;
+      seg_plan_host(cptr_h.data(), (int64_t)n, nnz, &P);
+      const size_t nch = P.chunk_rank.size();
+      auto up = [&](auto& buf, const auto& vec) {
+        using T = typename std::decay_t<decltype(vec)>::value_type;
+        buf.alloc(std::max<size_t>(vec.size(), 1));
+        if (!vec.empty())
+          cuda_check(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T),
+                                     cudaMemcpyHostToDevice, s),
+                     "H2D");
+      };
+      up(e->chunk_start_, P.chunk_start);
+      up(e->chunk_rank_, P.chunk_rank);
+      up(e->lastbits_, P.lastbits);
+      up(e->nz_col_, P.nz_col);
+      up(e->fix_chunk_, P.fix_chunk);
+      up(e->fix_first_, P.fix_first);
+      e->head_.alloc(std::max<size_t>(nch, 1));
+      e->carry_.alloc(std::max<size_t>(nch, 1));
+      e->plan_.nchunks = (int64_t)nch;
+      e->plan_.nfix = (int64_t)P.fix_chunk.size();
+      e->plan_.chunk_start = e->chunk_start_.p;
+      e->plan_.chunk_rank = e->chunk_rank_.p;
+      e->plan_.lastbits = e->lastbits_.p;
+      e->plan_.nz_col = e->nz_col_.p;
+      e->plan_.fix_chunk = e->fix_chunk_.p;
+      e->plan_.fix_first = e->fix_first_.p;
+      e->plan_.head = e->head_.p;
+      e->plan_.carry = e->carry_.p;
+      cuda_check(cudaStreamSynchronize(s), "seg plan upload");
+    }
+    tr.mark("segmented plan");
+    e->group_ = choose_group((int64_t)l, nnz);
+    cuda_check(cudaStreamSynchronize(s), "csc build");
+    cuda_check(cudaGetLastError(), "csc build");
+    return e;
+  } catch (...) {
+    // an input error outranks a device error met while it was being checked
+    if (valid.valid()) valid.get();
+    throw;
   }
-  tr.mark("matrix alloc + H2D");
-  e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
-  const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
-  if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
-  e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
-  tr.mark("device CSC build");
-  {
-    // one-time structure analysis of the CSC copy on the host (csc_seg.cu)
-    std::vector<int32_t> cptr_h(n + 1);
-    cuda_check(cudaMemcpyAsync(cptr_h.data(), e->cptr_.p, (n + 1) * sizeof(int32_t),
-                               cudaMemcpyDeviceToHost, s),
-               "D2H");
-    cuda_check(cudaStreamSynchronize(s), "cptr download");
-    SegPlanHost P;
-    seg_plan_host(cptr_h.data(), (int64_t)n, nnz, &P);
-    const size_t nch = P.chunk_rank.size();
-    auto up = [&](auto& buf, const auto& vec) {
-      using T = typename std::decay_t<decltype(vec)>::value_type;
-      buf.alloc(std::max<size_t>(vec.size(), 1));
-      if (!vec.empty())
-        cuda_check(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T),
-                                   cudaMemcpyHostToDevice, s),
-                   "H2D");
-    };
-    up(e->chunk_start_, P.chunk_start);
-    up(e->chunk_rank_, P.chunk_rank);
-    up(e->lastbits_, P.lastbits);
-    up(e->nz_col_, P.nz_col);
-    up(e->fix_chunk_, P.fix_chunk);
-    up(e->fix_first_, P.fix_first);
-    e->head_.alloc(std::max<size_t>(nch, 1));
-    e->carry_.alloc(std::max<size_t>(nch, 1));
-    e->plan_.nchunks = (int64_t)nch;
-    e->plan_.nfix = (int64_t)P.fix_chunk.size();
-    e->plan_.chunk_start = e->chunk_start_.p;
-    e->plan_.chunk_rank = e->chunk_rank_.p;
-    e->plan_.lastbits = e->lastbits_.p;
-    e->plan_.nz_col = e->nz_col_.p;
-    e->plan_.fix_chunk = e->fix_chunk_.p;
-    e->plan_.fix_first = e->fix_first_.p;
-    e->plan_.head = e->head_.p;
-    e->plan_.carry = e->carry_.p;
-    cuda_check(cudaStreamSynchronize(s), "seg plan upload");
-  }
-  tr.mark("segmented plan");
-  e->group_ = choose_group((int64_t)l, nnz);
-  cuda_check(cudaStreamSynchronize(s), "csc build");
-  cuda_check(cudaGetLastError(), "csc build");
-  return e;
 }
 
 std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
@@ -356,8 +377,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   PhaseTrace tr("create_dense");
   check_options(loss, opt);
   if (!y || (l * n > 0 && !row_major)) raise(TRON_ERR_ARGUMENT, "null problem array");
-  validate_labels_C(l, y, C);
-  tr.mark("host validation");
+  if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");
   if (n > (uint64_t)kDenseMaxN) {
     // Wide dense problems run through the sparse kernels (explicit entries).
     if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
@@ -382,43 +402,52 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->row_begin_ = opt.row_begin;
   e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
   e->ld_ = dense_ld((int64_t)l);
-  e->common_alloc();
-  cudaStream_t s = e->s_;
-  tr.s = s;
-  tr.mark("context + state alloc");
-  e->Xc_.alloc((size_t)std::max<int64_t>(e->ld_, 1) * (n > 0 ? n : 1));
-  e->y_.alloc((size_t)std::max<int64_t>(e->ld_, 1));
-  cuda_check(cudaMemsetAsync(e->y_.p, 0, e->y_.bytes(), s), "memset");
-  if (n > 0 && e->ld_ > (int64_t)l)
-    cuda_check(cudaMemset2DAsync(e->Xc_.p + l, e->ld_ * sizeof(double), 0,
-                                 (e->ld_ - (int64_t)l) * sizeof(double), n, s),
-               "memset pad");
-  if (l > 0) {
-    upload(e->y_.p, y, l * sizeof(double), s);
-    // chunked row-major upload + on-device transpose to column-major
-    const int64_t chunk_rows =
-        std::max<int64_t>(1, (int64_t{64} << 20) / (int64_t)(sizeof(double) * std::max<uint64_t>(n, 1)));
-    DevBuf<double> stage[2];
-    stage[0].alloc((size_t)chunk_rows * n);
-    stage[1].alloc((size_t)chunk_rows * n);
-    cudaEvent_t ev[2];
-    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
-    int k = 0;
-    bool used[2] = {false, false};
-    for (int64_t r0 = 0; r0 < (int64_t)l; r0 += chunk_rows, k ^= 1) {
-      const int64_t rows = std::min<int64_t>(chunk_rows, (int64_t)l - r0);
-      if (used[k]) cudaEventSynchronize(ev[k]);
-      upload(stage[k].p, row_major + (size_t)r0 * n, rows * n * sizeof(double), s);
-      dense_transpose_chunk(stage[k].p, rows, n, e->Xc_.p, e->ld_, r0, s);
-      cudaEventRecord(ev[k], s);
-      used[k] = true;
+  // labels are checked on the worker pool while the matrix streams in
+  auto labels_ok = std::async(std::launch::async, [&] { validate_labels_C(l, y, C); });
+  try {
+    e->common_alloc();
+    cudaStream_t s = e->s_;
+    tr.s = s;
+    tr.mark("context + state alloc");
+    e->Xc_.alloc((size_t)std::max<int64_t>(e->ld_, 1) * (n > 0 ? n : 1));
+    e->y_.alloc((size_t)std::max<int64_t>(e->ld_, 1));
+    cuda_check(cudaMemsetAsync(e->y_.p, 0, e->y_.bytes(), s), "memset");
+    if (n > 0 && e->ld_ > (int64_t)l)
+      cuda_check(cudaMemset2DAsync(e->Xc_.p + l, e->ld_ * sizeof(double), 0,
+                                   (e->ld_ - (int64_t)l) * sizeof(double), n, s),
+                 "memset pad");
+    if (l > 0) {
+      upload(e->y_.p, y, l * sizeof(double), s);
+      // chunked row-major upload + on-device transpose to column-major
+      const int64_t chunk_rows =
+          std::max<int64_t>(1, (int64_t{64} << 20) / (int64_t)(sizeof(double) * std::max<uint64_t>(n, 1)));
+      DevBuf<double> stage[2];
+      stage[0].alloc((size_t)chunk_rows * n);
+      stage[1].alloc((size_t)chunk_rows * n);
+      cudaEvent_t ev[2];
+      cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+      int k = 0;
+      bool used[2] = {false, false};
+      for (int64_t r0 = 0; r0 < (int64_t)l; r0 += chunk_rows, k ^= 1) {
+        const int64_t rows = std::min<int64_t>(chunk_rows, (int64_t)l - r0);
+        if (used[k]) cudaEventSynchronize(ev[k]);
+        upload(stage[k].p, row_major + (size_t)r0 * n, rows * n * sizeof(double), s);
+        dense_transpose_chunk(stage[k].p, rows, n, e->Xc_.p, e->ld_, r0, s);
+        cudaEventRecord(ev[k], s);
+        used[k] = true;
+      }
+      cuda_check(cudaStreamSynchronize(s), "dense upload");
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
     }
-    cuda_check(cudaStreamSynchronize(s), "dense upload");
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
+    tr.mark("matrix alloc + H2D + transpose");
+    labels_ok.get();  // rethrows a label error found while the matrix was in flight
+    tr.mark("host validation (overlapped)");
+  } catch (...) {
+    if (labels_ok.valid()) labels_ok.get();  // an input error outranks a device error
+    throw;
   }
-  tr.mark("matrix alloc + H2D + transpose");
   if (dense_make_map(&e->xmap_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n) != 0)
     raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the dense matrix");
   if (loss == TRON_LOSS_L2SVM) {

@@ -18,13 +18,20 @@
 #include <cstring>
 #include <vector>
 
+#include "hostio.h"
 #include "tron_b200.h"
 
 namespace {
 
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+
 struct Rng {  // testgen.hpp:14-36
   uint64_t state;
   explicit Rng(uint64_t seed) : state(seed) {}
+  // splitmix64 is a counter generator: the stream after k draws is the
+  // stream seeded with seed + k*golden, so disjoint ranges of a sequential
+  // stream can be produced in parallel, bit for bit.
+  static Rng at(uint64_t seed, uint64_t draws) { return Rng(seed + draws * kGolden); }
   uint64_t next_u64() {
     uint64_t z = (state += 0x9e3779b97f4a7c15ull);
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -36,30 +43,40 @@ struct Rng {  // testgen.hpp:14-36
 };
 
 // testgen.cpp:10-22 labels_from_separator (dense row-major or CSR rows)
-void labels_dense(Rng& rng, size_t l, size_t n, const double* X, double flip, double* y) {
+// Rows are labelled in parallel ranges; row i's flip draw is draw n + i of
+// the label stream (rng's state on entry), as in the sequential loop.
+template <class RowScore>
+void labels_parallel(Rng& rng, size_t l, size_t n, double flip, double* y, RowScore score_of) {
   std::vector<double> w(n);
   for (auto& v : w) v = rng.in(-1.0, 1.0);
-  for (size_t i = 0; i < l; ++i) {
+  const uint64_t base = rng.state;
+  tb::parallel_for(l, 1u << 14, [&](size_t b, size_t e) {
+    Rng r(base + (uint64_t)b * kGolden);
+    for (size_t i = b; i < e; ++i) {
+      double label = score_of(i, w.data()) >= 0.0 ? 1.0 : -1.0;
+      if (r.unit() < flip) label = -label;
+      y[i] = label;
+    }
+  });
+  rng.state = base + (uint64_t)l * kGolden;
+}
+
+void labels_dense(Rng& rng, size_t l, size_t n, const double* X, double flip, double* y) {
+  labels_parallel(rng, l, n, flip, y, [&](size_t i, const double* w) {
     const double* row = X + i * n;
     double score = 0.0;
     for (size_t j = 0; j < n; ++j) score += row[j] * w[j];
-    double label = score >= 0.0 ? 1.0 : -1.0;
-    if (rng.unit() < flip) label = -label;
-    y[i] = label;
-  }
+    return score;
+  });
 }
 
 void labels_csr(Rng& rng, size_t l, size_t n, const int64_t* ro, const int32_t* ci,
                 const double* vals, double flip, double* y) {
-  std::vector<double> w(n);
-  for (auto& v : w) v = rng.in(-1.0, 1.0);
-  for (size_t i = 0; i < l; ++i) {
+  labels_parallel(rng, l, n, flip, y, [&](size_t i, const double* w) {
     double score = 0.0;
     for (int64_t k = ro[i]; k < ro[i + 1]; ++k) score += vals[k] * w[ci[k]];
-    double label = score >= 0.0 ? 1.0 : -1.0;
-    if (rng.unit() < flip) label = -label;
-    y[i] = label;
-  }
+    return score;
+  });
 }
 
 }  // namespace
@@ -145,6 +162,21 @@ int tron_synth_sparse(uint64_t seed, size_t l, size_t n, size_t k, double s, dou
     const double total = cdf[n - 1];
     for (size_t j = 0; j < n; ++j) cdf[j] /= total;
   }
+  // guide[b] = lower_bound(cdf, b/B): u in [b/B, (b+1)/B) has its
+  // lower_bound in [guide[b], guide[b+1]], so the search below returns
+  // exactly std::lower_bound(cdf, u) over a short range.
+  size_t B = 1;
+  while (B < 4 * n && B < (size_t{1} << 24)) B <<= 1;
+  std::vector<uint32_t> guide;
+  if (s != 0.0) {
+    guide.resize(B + 1);
+    size_t j = 0;
+    for (size_t b = 0; b <= B; ++b) {
+      const double t = static_cast<double>(b) / static_cast<double>(B);
+      while (j < n && cdf[j] < t) ++j;
+      guide[b] = static_cast<uint32_t>(j);
+    }
+  }
   std::vector<int32_t> row;
   row.reserve(k);
   ro[0] = 0;
@@ -153,7 +185,11 @@ int tron_synth_sparse(uint64_t seed, size_t l, size_t n, size_t k, double s, dou
     while (row.size() < k) {
       size_t c;
       if (s != 0.0) {
-        c = static_cast<size_t>(std::lower_bound(cdf.begin(), cdf.end(), rng.unit()) - cdf.begin());
+        const double u = rng.unit();
+        const size_t b = static_cast<size_t>(u * static_cast<double>(B));
+        const size_t lo = guide[b], hi = std::min<size_t>(guide[b + 1] + 1, n);
+        c = static_cast<size_t>(std::lower_bound(cdf.begin() + lo, cdf.begin() + hi, u) -
+                                cdf.begin());
         if (c >= n) c = n - 1;
       } else {
         c = static_cast<size_t>(rng.next_u64() % n);
@@ -188,11 +224,16 @@ int tron_synth_dense(uint64_t seed, size_t l, size_t n, double decades, double r
   for (size_t j = 0; j < n; ++j)
     sc[j] = std::pow(10.0, -decades / 2 + decades * static_cast<double>(j) /
                                               static_cast<double>(n - 1));
-  for (size_t i = 0; i < l; ++i) {
-    double g = 2 * rng.unit() - 1;
-    double* row = values + i * n;
-    for (size_t j = 0; j < n; ++j) row[j] = sc[j] * (rho * g + (1 - rho) * (2 * rng.unit() - 1));
-  }
+  // row i consumes draws [i*(n+1), (i+1)*(n+1)): rows are generated in parallel ranges
+  tb::parallel_for(l, 1u << 14, [&](size_t b, size_t e) {
+    Rng r = Rng::at(seed, (uint64_t)b * (n + 1));
+    for (size_t i = b; i < e; ++i) {
+      double g = 2 * r.unit() - 1;
+      double* row = values + i * n;
+      for (size_t j = 0; j < n; ++j) row[j] = sc[j] * (rho * g + (1 - rho) * (2 * r.unit() - 1));
+    }
+  });
+  rng = Rng::at(seed, (uint64_t)l * (n + 1));
   labels_dense(rng, l, n, values, flip, y);
   return TRON_OK;
 }
