@@ -221,6 +221,8 @@ class Reference:
         L.ref_solve.argtypes = [c_int, c_size_t, c_size_t, PI64, PI32, PD, PD, c_double, c_int,
                                 POINTER(or_config), c_int, ctypes.c_uint, PD, PD,
                                 POINTER(or_solve_info), POINTER(or_iteration), c_size_t]
+        L.ref_time_calls.argtypes = [c_int, c_size_t, c_size_t, PI64, PI32, PD, PD, c_double, c_int,
+                                     ctypes.c_uint, c_int, PD]
         L.ref_logistic_fused_pass.restype = c_double
         L.ref_logistic_fused_pass.argtypes = [c_int, c_size_t, c_size_t, PI64, PI32, PD, PD,
                                               c_double, PD, PD, PD, PD, PD]
@@ -257,6 +259,15 @@ class Reference:
         self.lib.ref_solve(*args, loss, ctypes.byref(c), backend, workers, _p(w0a), _p(w),
                            ctypes.byref(info), tr, cap)
         return w, _trace(info, tr, cap)
+
+    def time_calls(self, problem, loss, workers, reps=1):
+        """Per-call ms of the reference evaluator (fun, grad, Hv) at w = 0, parallel(workers)."""
+        args, keep = self._args(problem)
+        out = np.zeros(3)
+        st = self.lib.ref_time_calls(*args, loss, workers, reps, _p(out))
+        if st != 0:
+            raise RuntimeError(f"ref_time_calls failed ({st})")
+        return dict(fun_ms=out[0], grad_ms=out[1], hv_ms=out[2])
 
     def logistic(self, problem, w, v):
         args, keep = self._args(problem)

@@ -5,6 +5,8 @@
 // reference arm call the reference's own tron::solve (backend.cpp:314-318),
 // its loss kernels (loss.cpp) and its deterministic fixture generators
 // (testgen.cpp) on identical inputs.  No reference source is copied here.
+#include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <vector>
@@ -103,6 +105,40 @@ int ref_solve(int layout, size_t l, size_t n, const int64_t* ro, const int32_t* 
     return OR_ERR_NUMERICAL;
   } catch (const tron::BoundsError&) {
     return OR_ERR_BOUNDS;
+  } catch (const std::exception&) {
+    return OR_ERR_DIMENSION;
+  }
+}
+
+// Per-call CPU cost of the reference evaluator under ExecutionPlan::parallel(workers):
+// out_ms = {eval_candidate (fun), commit (gradient), hessian_vec (Hv)}, min over reps,
+// at w = 0 (the first outer iteration's state).  Problem construction is untimed.
+int ref_time_calls(int layout, size_t l, size_t n, const int64_t* ro, const int32_t* ci,
+                   const double* vals, const double* y, double C, int loss, unsigned workers,
+                   int reps, double* out_ms) {
+  try {
+    tron::Problem p = make_problem(layout, l, n, ro, ci, vals, y, C);
+    tron::ExecutionPlan plan = tron::ExecutionPlan::parallel(workers);
+    auto ev = tron::make_evaluator(
+        p, loss == OR_LOGISTIC ? tron::LossKind::Logistic : tron::LossKind::L2Svm, plan);
+    tron::RealVector w(n, 0.0), out;
+    auto ms = [](auto t0, auto t1) {
+      return std::chrono::duration<double, std::milli>(t1 - t0).count();
+    };
+    out_ms[0] = out_ms[1] = out_ms[2] = 1e300;
+    for (int r = 0; r < reps; ++r) {
+      auto t0 = std::chrono::steady_clock::now();
+      ev->eval_candidate(w);
+      auto t1 = std::chrono::steady_clock::now();
+      ev->commit();
+      auto t2 = std::chrono::steady_clock::now();
+      ev->hessian_vec(ev->gradient(), out);
+      auto t3 = std::chrono::steady_clock::now();
+      out_ms[0] = std::min(out_ms[0], ms(t0, t1));
+      out_ms[1] = std::min(out_ms[1], ms(t1, t2));
+      out_ms[2] = std::min(out_ms[2], ms(t2, t3));
+    }
+    return OR_OK;
   } catch (const std::exception&) {
     return OR_ERR_DIMENSION;
   }
