@@ -320,7 +320,17 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
     e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
     tr.mark("device CSC build");
-    {
+    // TRON_B200_SEG_STREAM=1: the TMA-streamed segmented kernels (seg_stream.cu).
+    // Measured slower than the chunk-plan kernels on N1/R1/K1 (gather-bound, see
+    // DESIGN.md §9), so the chunk-plan kernels are the default.
+    const char* ss = std::getenv("TRON_B200_SEG_STREAM");
+    e->use_stream_ = ss && ss[0] == '1';
+    if (e->use_stream_) {
+      // streamed layouts of both orientations, built on the device
+      e->build_stream(e->xs_, e->rptr_.p, (int64_t)l, nnz, e->cidx_.p, e->rval_.p);
+      e->build_stream(e->xts_, e->cptr_.p, (int64_t)n, nnz, e->ridx_.p, e->cval_.p);
+      tr.mark("streamed layouts");
+    } else {
       // one-time structure analysis of the CSC copy on the host (csc_seg.cu)
       std::vector<int32_t> cptr_h(n + 1);
       cuda_check(cudaMemcpyAsync(cptr_h.data(), e->cptr_.p, (n + 1) * sizeof(int32_t),
@@ -357,8 +367,8 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
       cuda_check(cudaStreamSynchronize(s), "seg plan upload");
+      tr.mark("segmented plan");
     }
-    tr.mark("segmented plan");
     e->group_ = choose_group((int64_t)l, nnz);
     cuda_check(cudaStreamSynchronize(s), "csc build");
     cuda_check(cudaGetLastError(), "csc build");
@@ -471,11 +481,41 @@ Engine::~Engine() {
   // DevBuf members queue their frees on s_; stream_owner_ then syncs + destroys it
 }
 
+void Engine::build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64_t nnz,
+                          const int32_t* idx, const double* val) {
+  SegStreamSizes z;
+  seg_stream_sizes(nseg, nnz, &z);
+  B.rec.alloc(std::max<int64_t>(z.rec_bytes, 16));
+  B.off.alloc(z.ntiles + 1);
+  B.nempty.alloc(1);
+  B.empty_seg.alloc(std::max<int64_t>(nseg, 1));
+  B.cta_tail.alloc(kMaxPartialBlocks);
+  B.cta_flags.alloc(kMaxPartialBlocks);
+  B.cta_tag.alloc(kMaxPartialBlocks);
+  B.misc.alloc(2);
+  StreamView& v = B.view;
+  v.nseg = nseg;
+  v.nnz = nnz;
+  v.ntiles = z.ntiles;
+  v.rec = B.rec.p;
+  v.tile_off = B.off.p;
+  v.empty_seg = B.empty_seg.p;
+  v.nempty = B.nempty.p;
+  v.cta_tail = B.cta_tail.p;
+  v.cta_flags = B.cta_flags.p;
+  v.cta_tag = B.cta_tag.p;
+  v.epoch = B.misc.p;
+  v.ticket = B.misc.p + 1;
+  const int rc = seg_stream_build(ptr, nseg, nnz, idx, val, v, s_);
+  if (rc != 0) cuda_check((cudaError_t)rc, "seg_stream_build");
+}
+
 uint64_t Engine::memory_bytes() const {
   uint64_t b = rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
                cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes() + lastbits_.bytes() +
                chunk_rank_.bytes() + chunk_start_.bytes() + fix_chunk_.bytes() +
                fix_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
+  b += xs_.bytes() + xts_.bytes();
   for (const auto& S : slot_)
     b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes() +
          S.gparts.bytes();
@@ -505,6 +545,9 @@ void Engine::forward(Slot& S) {
   if (dense_) {
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
                   S.gparts.p, obj_d_, sc_, s_);
+  } else if (use_stream_) {
+    stream_forward(xs_.view, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_,
+                   sc_, s_);
   } else {
     csr_forward(X_, group_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_,
                 s_);
@@ -552,17 +595,23 @@ double Engine::eval_candidate_host(const double* w) {
 // transposed products: X^T u with epilogue, world-aware
 // ----------------------------------------------------------------------------
 void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out) {
+  auto product = [&](const EpiView& E, double* dst) {
+    if (use_stream_)
+      stream_transposed(xts_.view, u, squared, E, dst, s_);
+    else
+      csc_spmv(Xt_, plan_, u, squared, E, dst, s_);
+    count_launch(use_stream_ ? 1 : 2);
+  };
   if (!comm_.active()) {
-    csc_spmv(Xt_, plan_, u, squared, epi, out, s_);
-    count_launch(2);
+    product(epi, out);
     return;
   }
   EpiView raw;
   raw.kind = EPI_RAW;
-  csc_spmv(Xt_, plan_, u, squared, raw, raw_.p, s_);
+  product(raw, raw_.p);
   comm_.allreduce_sum(raw_.p, n_, s_);
   vec_epilogue(n_, raw_.p, epi, out, s_);
-  count_launch(3);
+  count_launch(1);
 }
 
 // kind = DA_HV / DA_PRECOND (one tiled pass) or -1: finish the gradient
@@ -694,10 +743,12 @@ void Engine::hv_kernels(const double* v, double* out) {
     dense_vector(DA_HV, v, epi, out);
     return;
   }
-  if (loss_ == TRON_LOSS_LOGISTIC)
-    csr_dv(X_, group_, v, S.dvec.p, nullptr, a_.p, s_);
+  const double* dv = loss_ == TRON_LOSS_LOGISTIC ? S.dvec.p : nullptr;
+  const uint8_t* mk = loss_ == TRON_LOSS_LOGISTIC ? nullptr : S.mask.p;
+  if (use_stream_)
+    stream_dv(xs_.view, v, dv, mk, a_.p, s_);
   else
-    csr_dv(X_, group_, v, nullptr, S.mask.p, a_.p, s_);
+    csr_dv(X_, group_, v, dv, mk, a_.p, s_);
   count_launch(1);
   UView u;
   u.kind = U_VEC;
@@ -1113,12 +1164,13 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
     epi.kind = EPI_VEC;
     epi.base = vtmp_.p;
     epi.scale = C_;
-    out->transposed_ms = time_it([&] { csc_spmv(Xt_, plan_, u, false, epi, otmp_.p, s_); });
-    Slot& Cd = slot_[cand_];
-    out->forward_ms = time_it([&] {
-      csr_forward(X_, group_, loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm, S.w.p, y_.p,
-                  C_, Cd.z.p, Cd.zhat.p, Cd.dvec.p, Cd.mask.p, obj_d_, sc_, s_);
+    out->transposed_ms = time_it([&] {
+      if (use_stream_)
+        stream_transposed(xts_.view, u, false, epi, otmp_.p, s_);
+      else
+        csc_spmv(Xt_, plan_, u, false, epi, otmp_.p, s_);
     });
+    out->forward_ms = time_it([&] { forward(slot_[cand_]); });
   } else {
     const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
     out->transposed_ms = time_it([&] {

@@ -80,6 +80,20 @@ class Comm {
 };
 int nccl_unique_id(void* out128);
 
+// Device buffers of one streamed segmented layout (seg_stream.cu).
+struct StreamBufs {
+  DevBuf<unsigned char> rec;
+  DevBuf<long long> off, nempty;
+  DevBuf<double> cta_tail;
+  DevBuf<int32_t> cta_flags, empty_seg;
+  DevBuf<unsigned> cta_tag, misc;
+  StreamView view{};
+  uint64_t bytes() const {
+    return rec.bytes() + off.bytes() + nempty.bytes() + cta_tail.bytes() + cta_flags.bytes() +
+           empty_seg.bytes() + cta_tag.bytes() + misc.bytes();
+  }
+};
+
 struct KernelTimes {
   double hv_ms = 0, transposed_ms = 0, forward_ms = 0, grad_ms = 0;
 };
@@ -145,6 +159,8 @@ class Engine {
   void read_obj();
   void read_cg(CgState* out);
   void build_graph(int slot, bool use_m);
+  void build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64_t nnz,
+                    const int32_t* idx, const double* val);
   void count_launch(uint64_t k) { launches += k; }
 
   int loss_ = 0;
@@ -165,6 +181,8 @@ class Engine {
   DevBuf<int32_t> chunk_start_, fix_chunk_, fix_first_, nz_col_;
   DevBuf<double> head_, carry_;
   CsrView X_{}, Xt_{};
+  StreamBufs xs_, xts_;     // streamed CSR (rows) and CSC (columns) layouts
+  bool use_stream_ = false;  // TRON_B200_SEG_STREAM=1: the streamed segmented kernels
   SegView plan_{};
   int group_ = 4;
   // dense column-major

@@ -49,6 +49,33 @@ struct SegPlanHost {
 };
 void seg_plan_host(const int32_t* ptr, int64_t rows, int64_t nnz, SegPlanHost* out);
 
+// Streamed segmented layout of a compressed matrix (seg_stream.cu): 2048-
+// entry tiles of eight 256-entry pieces, lane-interleaved, with per-lane
+// segment-end bytes, per-tile end ranks and the non-empty segment table,
+// plus the per-CTA records that join segments crossing CTA ranges.
+constexpr int kStreamTilePieces = 8;
+struct StreamView {
+  int64_t nseg = 0, nnz = 0, ntiles = 0;
+  unsigned char* rec = nullptr;       // tile records (see seg_stream.cu)
+  const long long* tile_off = nullptr;  // [ntiles + 1] byte offset of each record
+  const int32_t* empty_seg = nullptr; // [nseg] the empty segments (first *nempty entries)
+  long long* nempty = nullptr;        // device count of empty segments
+  // per-CTA records joining segments that cross CTA ranges
+  double* cta_tail = nullptr;         // [kMaxPartialBlocks] partial open at the CTA's range end
+  int32_t* cta_flags = nullptr;       // bit0: a segment ends in the range
+  unsigned* cta_tag = nullptr;        // launch tag of the record (release/acquire)
+  unsigned* epoch = nullptr;          // launch counter (device-side: CUDA-graph replay safe)
+  unsigned* ticket = nullptr;         // last-CTA ticket
+};
+struct SegStreamSizes {
+  int64_t ntiles = 0, rec_bytes = 0;
+};
+size_t seg_stream_sizes(int64_t nseg, int64_t nnz, SegStreamSizes* z);
+// Builds the layout from segment-ordered device arrays (ptr[nseg+1], idx, val).
+int seg_stream_build(const int32_t* ptr, int64_t nseg, int64_t nnz, const int32_t* idx,
+                     const double* val, const StreamView& A, cudaStream_t s);
+int seg_stream_grid(int64_t ntiles);
+
 // Per-source-row weight u_i used by the transposed product sum_i u_i x_ij.
 enum UKind : int {
   U_VEC = 0,        // u[i]
@@ -130,6 +157,15 @@ void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squar
 int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s);
 // Row-offset narrowing int64 -> int32 (device).
 void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s);
+
+// Streamed versions (seg_stream.cu) of csr_forward / csr_dv / csc_spmv.
+void stream_forward(const StreamView& A, int loss, const double* w, const double* y, double C,
+                    double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
+                    Scratch sc, cudaStream_t s);
+void stream_dv(const StreamView& A, const double* p, const double* dvec, const uint8_t* mask,
+               double* a, cudaStream_t s);
+void stream_transposed(const StreamView& At, const UView& U, bool squared, const EpiView& E,
+                       double* out, cudaStream_t s);
 
 // ---- vector kernels (vec_kernels.cu) -----------------------------------------
 // wc = w + d (d may be null: wc = w); obj->ww = wc.wc
