@@ -20,6 +20,9 @@
 //    memory, no block barriers: results are bit-reproducible run to run.
 //  * each emitted column also writes the empty columns that follow it, so
 //    the epilogue (base_j + scale*sum) covers every j in one pass.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -349,6 +352,135 @@ void seg_plan_host(const int32_t* ptr, int64_t rows, int64_t nnz, SegPlanHost* P
   }
   P->nz_col.push_back((int32_t)rows);
   P->chunk_start.push_back((int32_t)nnz);
+}
+
+// ---------------------------------------------------------------------------
+// Device-built plan with fixed 256-entry chunks (every boundary inside a
+// column becomes a fix-up): fully parallel, no host round trip of the CSC
+// structure -- what context creation uses.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void plan_chunk_start_kernel(int32_t* cs, long long nchunks, long long nnz) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t <= nchunks;
+       t += (long long)gridDim.x * blockDim.x)
+    cs[t] = (int32_t)(t * kSegChunk < nnz ? t * kSegChunk : nnz);
+}
+
+__global__ void plan_cols_kernel(const int32_t* cptr, long long n, uint32_t* lastbits,
+                                 int32_t* nonempty, int32_t* ids, uint8_t* spans) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int b = cptr[c], e = cptr[c + 1];
+    ids[c] = (int32_t)c;
+    nonempty[c] = e > b;
+    spans[c] = e > b && (b / kSegChunk) != ((e - 1) / kSegChunk);
+    if (e > b) atomicOr(lastbits + ((e - 1) >> 5), 1u << ((e - 1) & 31));
+  }
+}
+
+__global__ void plan_chunk_rank_kernel(const int32_t* cptr, long long n, const int32_t* colrank,
+                                       long long nchunks, uint32_t* rank) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nchunks;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long x = t * kSegChunk;
+    long long lo = 0, hi = n + 1;  // upper_bound(cptr[0..n], x) - 1
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (cptr[mid] <= x)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const long long c = lo - 1;
+    rank[t] = (uint32_t)colrank[c] | (cptr[c] < x ? 0x80000000u : 0u);
+  }
+}
+
+__global__ void plan_fix_kernel(const int32_t* cptr, const int32_t* cols, const long long* count,
+                                int32_t* fix_chunk, int32_t* fix_first) {
+  const long long m = *count;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = cols[i];
+    fix_first[i] = cptr[c] / kSegChunk;
+    fix_chunk[i] = (cptr[c + 1] - 1) / kSegChunk;
+  }
+}
+
+__global__ void plan_sentinel_kernel(int32_t* nz_col, const int32_t* colrank, long long n) {
+  nz_col[colrank[n]] = (int32_t)n;
+}
+
+int pgrid(long long n) {
+  long long g = (n + 255) / 256;
+  const long long cap = (long long)device_sm_count() * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, int32_t* chunk_start,
+                    uint32_t* chunk_rank, uint32_t* lastbits, int32_t* nz_col, int32_t* fix_chunk,
+                    int32_t* fix_first, cudaStream_t s) {
+  const int64_t nchunks = (nnz + kSegChunk - 1) / kSegChunk;
+  const size_t n1 = n > 0 ? n : 1;
+  int32_t *nonempty = nullptr, *colrank = nullptr, *ids = nullptr, *cols = nullptr;
+  uint8_t* spans = nullptr;
+  long long *cnt_nz = nullptr, *cnt_fix = nullptr;
+  void* temp = nullptr;
+  size_t tb1 = 0, tb2 = 0, tb3 = 0;
+  cudaError_t e = cudaMallocAsync(&nonempty, (n1 + 1) * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&colrank, (n1 + 1) * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&ids, n1 * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&cols, n1 * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&spans, n1, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&cnt_nz, 2 * sizeof(long long), s);
+  cnt_fix = cnt_nz + 1;
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::ExclusiveSum(nullptr, tb1, nonempty, colrank, (int)(n + 1), s);
+  if (e == cudaSuccess)
+    e = cub::DeviceSelect::Flagged(nullptr, tb2, ids, nonempty, nz_col, cnt_nz, (int)n, s);
+  if (e == cudaSuccess)
+    e = cub::DeviceSelect::Flagged(nullptr, tb3, ids, spans, cols, cnt_fix, (int)n, s);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(&temp, std::max<size_t>(std::max(tb1, std::max(tb2, tb3)), 1), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(nonempty, 0, (n1 + 1) * sizeof(int32_t), s);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(lastbits, 0, (size_t)((nnz + 31) / 32 + 1) * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt_nz, 0, 2 * sizeof(long long), s);
+  if (e == cudaSuccess) {
+    plan_chunk_start_kernel<<<pgrid(nchunks + 1), 256, 0, s>>>(chunk_start, nchunks, nnz);
+    if (n > 0) plan_cols_kernel<<<pgrid(n), 256, 0, s>>>(cptr, n, lastbits, nonempty, ids, spans);
+    e = cub::DeviceScan::ExclusiveSum(temp, tb1, nonempty, colrank, (int)(n + 1), s);
+  }
+  if (e == cudaSuccess && n > 0)
+    e = cub::DeviceSelect::Flagged(temp, tb2, ids, nonempty, nz_col, cnt_nz, (int)n, s);
+  if (e == cudaSuccess && n > 0)
+    e = cub::DeviceSelect::Flagged(temp, tb3, ids, spans, cols, cnt_fix, (int)n, s);
+  if (e == cudaSuccess) {
+    plan_sentinel_kernel<<<1, 1, 0, s>>>(nz_col, colrank, n);
+    if (nchunks > 0)
+      plan_chunk_rank_kernel<<<pgrid(nchunks), 256, 0, s>>>(cptr, n, colrank, nchunks, chunk_rank);
+    plan_fix_kernel<<<pgrid(n), 256, 0, s>>>(cptr, cols, cnt_fix, fix_chunk, fix_first);
+  }
+  long long nfix = 0;
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&nfix, cnt_fix, sizeof(long long), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  for (void* p : {(void*)nonempty, (void*)colrank, (void*)ids, (void*)cols, (void*)spans,
+                  (void*)cnt_nz, temp})
+    if (p) cudaFreeAsync(p, s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  P->nchunks = nchunks;
+  P->nfix = nfix;
+  P->chunk_start = chunk_start;
+  P->chunk_rank = chunk_rank;
+  P->lastbits = lastbits;
+  P->nz_col = nz_col;
+  P->fix_chunk = fix_chunk;
+  P->fix_first = fix_first;
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
 void csc_spmv(const CsrView& At, const SegView& S, const UView& U, bool squared,

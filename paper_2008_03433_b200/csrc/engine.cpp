@@ -106,10 +106,11 @@ namespace {
 // Input validation runs on the worker pool; the first offending row found
 // is re-checked sequentially so the error (class + message) is exactly the
 // one a front-to-back scan reports.
+// grain: items per task (about 64K elementary checks per task)
 template <class Bad>
-uint64_t first_bad(uint64_t count, Bad bad) {
+uint64_t first_bad(uint64_t count, Bad bad, size_t grain = size_t{1} << 16) {
   std::atomic<uint64_t> first{UINT64_MAX};
-  parallel_for(count, 1u << 16, [&](size_t b, size_t e) {
+  parallel_for(count, grain, [&](size_t b, size_t e) {
     for (size_t i = b; i < e && i < first.load(std::memory_order_relaxed); ++i)
       if (bad(i)) {
         uint64_t cur = first.load();
@@ -165,7 +166,9 @@ void validate_csr(uint64_t l, uint64_t n, const int64_t* ro, const int32_t* ci) 
   // offsets first (a decreasing offset makes later rows' ranges meaningless)
   const uint64_t dec = first_bad(l, [&](uint64_t i) { return ro[i] > ro[i + 1]; });
   const uint64_t lim = dec == UINT64_MAX ? l : dec;
-  const uint64_t bad = first_bad(lim, [&](uint64_t i) { return check_row(i, false); });
+  const uint64_t per_row = l > 0 ? std::max<uint64_t>(1, (uint64_t)ro[l] / l) : 1;
+  const uint64_t bad = first_bad(lim, [&](uint64_t i) { return check_row(i, false); },
+                                 std::max<size_t>(1, (size_t{1} << 16) / per_row));
   if (bad != UINT64_MAX) check_row(bad, true);
   if (dec != UINT64_MAX) check_row(dec, true);
 }
@@ -331,42 +334,22 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       e->build_stream(e->xts_, e->cptr_.p, (int64_t)n, nnz, e->ridx_.p, e->cval_.p);
       tr.mark("streamed layouts");
     } else {
-      // one-time structure analysis of the CSC copy on the host (csc_seg.cu)
-      std::vector<int32_t> cptr_h(n + 1);
-      cuda_check(cudaMemcpyAsync(cptr_h.data(), e->cptr_.p, (n + 1) * sizeof(int32_t),
-                                 cudaMemcpyDeviceToHost, s),
-                 "D2H");
-      cuda_check(cudaStreamSynchronize(s), "cptr download");
-      SegPlanHost P;
-      seg_plan_host(cptr_h.data(), (int64_t)n, nnz, &P);
-      const size_t nch = P.chunk_rank.size();
-      auto up = [&](auto& buf, const auto& vec) {
-        using T = typename std::decay_t<decltype(vec)>::value_type;
-        buf.alloc(std::max<size_t>(vec.size(), 1));
-        if (!vec.empty())
-          cuda_check(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T),
-                                     cudaMemcpyHostToDevice, s),
-                     "H2D");
-      };
-      up(e->chunk_start_, P.chunk_start);
-      up(e->chunk_rank_, P.chunk_rank);
-      up(e->lastbits_, P.lastbits);
-      up(e->nz_col_, P.nz_col);
-      up(e->fix_chunk_, P.fix_chunk);
-      up(e->fix_first_, P.fix_first);
-      e->head_.alloc(std::max<size_t>(nch, 1));
-      e->carry_.alloc(std::max<size_t>(nch, 1));
-      e->plan_.nchunks = (int64_t)nch;
-      e->plan_.nfix = (int64_t)P.fix_chunk.size();
-      e->plan_.chunk_start = e->chunk_start_.p;
-      e->plan_.chunk_rank = e->chunk_rank_.p;
-      e->plan_.lastbits = e->lastbits_.p;
-      e->plan_.nz_col = e->nz_col_.p;
-      e->plan_.fix_chunk = e->fix_chunk_.p;
-      e->plan_.fix_first = e->fix_first_.p;
+      // one-time structure analysis of the CSC copy, on the device (csc_seg.cu)
+      const int64_t nch = (nnz + kSegChunk - 1) / kSegChunk;
+      e->chunk_start_.alloc(nch + 1);
+      e->chunk_rank_.alloc(std::max<int64_t>(nch, 1));
+      e->lastbits_.alloc(nnz / 32 + 2);
+      e->nz_col_.alloc(n + 1);
+      e->fix_chunk_.alloc(std::max<uint64_t>(n, 1));
+      e->fix_first_.alloc(std::max<uint64_t>(n, 1));
+      e->head_.alloc(std::max<int64_t>(nch, 1));
+      e->carry_.alloc(std::max<int64_t>(nch, 1));
+      const int prc = seg_plan_device(e->cptr_.p, (int64_t)n, nnz, &e->plan_, e->chunk_start_.p,
+                                      e->chunk_rank_.p, e->lastbits_.p, e->nz_col_.p,
+                                      e->fix_chunk_.p, e->fix_first_.p, s);
+      if (prc != 0) cuda_check((cudaError_t)prc, "seg_plan_device");
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
-      cuda_check(cudaStreamSynchronize(s), "seg plan upload");
       tr.mark("segmented plan");
     }
     e->group_ = choose_group((int64_t)l, nnz);
@@ -586,8 +569,7 @@ double Engine::eval_candidate_dev(const double* d_step) {
 
 double Engine::eval_candidate_host(const double* w) {
   if (n_ > 0)
-    cuda_check(cudaMemcpyAsync(slot_[cand_].w.p, w, n_ * sizeof(double), cudaMemcpyHostToDevice, s_),
-               "H2D");
+    upload(slot_[cand_].w.p, w, n_ * sizeof(double), s_);
   return eval_candidate_dev(nullptr);
 }
 
@@ -725,9 +707,7 @@ void Engine::commit(double* gnorm) {
 
 void Engine::gradient_host(double* g) {
   if (!committed_valid_) raise(TRON_ERR_LOGIC, "gradient() before the first commit()");
-  if (n_ > 0)
-    cuda_check(cudaMemcpyAsync(g, g_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
-  synchronize();
+  download(g, g_.p, n_ * sizeof(double), s_);
 }
 
 // ----------------------------------------------------------------------------
@@ -763,13 +743,9 @@ void Engine::hessian_vec_dev(const double* v, double* out) {
 
 void Engine::hessian_vec_host(const double* v, double* out) {
   if (!committed_valid_) raise(TRON_ERR_LOGIC, "hessian_vec() before the first commit()");
-  if (n_ > 0)
-    cuda_check(cudaMemcpyAsync(vtmp_.p, v, n_ * sizeof(double), cudaMemcpyHostToDevice, s_), "H2D");
+  upload(vtmp_.p, v, n_ * sizeof(double), s_);
   hv_kernels(vtmp_.p, otmp_.p);
-  if (n_ > 0)
-    cuda_check(cudaMemcpyAsync(out, otmp_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, s_),
-               "D2H");
-  synchronize();
+  download(out, otmp_.p, n_ * sizeof(double), s_);
   ledger.concealed_vector_returns++;
 }
 
@@ -799,9 +775,7 @@ void Engine::ensure_precond() {
 
 void Engine::precond_host(double* m) {
   ensure_precond();
-  if (n_ > 0)
-    cuda_check(cudaMemcpyAsync(m, M_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
-  synchronize();
+  download(m, M_.p, n_ * sizeof(double), s_);
 }
 
 // ----------------------------------------------------------------------------
@@ -981,10 +955,7 @@ void Engine::truncated_cg(double delta, const tron_config& cfg, double* d, int32
   if (st.fail)
     raise(TRON_ERR_NUMERICAL,
           "conjugate gradients met non-positive curvature (" + std::to_string(st.php) + ")");
-  if (d && n_ > 0) {
-    cuda_check(cudaMemcpyAsync(d, d_.p, n_ * 8, cudaMemcpyDeviceToHost, s_), "D2H");
-    synchronize();
-  }
+  if (d) download(d, d_.p, n_ * 8, s_);
   if (exit_kind) *exit_kind = st.exit_kind;
   if (iters) *iters = (uint64_t)st.iters;
   if (q) *q = st.q;
@@ -1027,11 +998,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     info->device_ms = ms;
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    if (w_out && n_ > 0) {
-      cuda_check(cudaMemcpyAsync(w_out, slot_[cand_ ^ 1].w.p, n_ * 8, cudaMemcpyDeviceToHost, s_),
-                 "D2H");
-      synchronize();
-    }
+    if (w_out) download(w_out, slot_[cand_ ^ 1].w.p, n_ * 8, s_);
     info->status = status;
     info->hessian_products = hv_count;
     (void)launches0;
@@ -1039,7 +1006,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   Slot& C0 = slot_[cand_];
   if (n_ > 0) {
     if (w0)
-      cuda_check(cudaMemcpyAsync(C0.w.p, w0, n_ * 8, cudaMemcpyHostToDevice, s_), "H2D");
+      upload(C0.w.p, w0, n_ * 8, s_);
     else
       cuda_check(cudaMemsetAsync(C0.w.p, 0, n_ * 8, s_), "memset");
   }

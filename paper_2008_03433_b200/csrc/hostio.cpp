@@ -219,4 +219,43 @@ void upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   // the staging buffers are reused by the next upload only after their events
 }
 
+void download(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) {
+    cuda_check(cudaStreamSynchronize(s), "synchronize");
+    return;
+  }
+  if (is_pinned(dst) || bytes <= (64u << 10)) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "synchronize");
+    return;
+  }
+  Staging& st = staging();
+  std::lock_guard<std::mutex> g(st.mu);
+  if (!st.buf[0]) {
+    for (int k = 0; k < 2; ++k) {
+      cuda_check(cudaMallocHost(&st.buf[k], kStageBytes), "cudaMallocHost");
+      cuda_check(cudaEventCreateWithFlags(&st.ev[k], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  for (int k = 0; k < 2; ++k)  // an upload's copies out of the buffers must be done
+    if (st.used[k]) cuda_check(cudaEventSynchronize(st.ev[k]), "staging wait");
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  const size_t nchunk = (bytes + kStageBytes - 1) / kStageBytes;
+  auto issue = [&](size_t c) {
+    const size_t off = c * kStageBytes, len = std::min(kStageBytes, bytes - off);
+    cuda_check(cudaMemcpyAsync(st.buf[c & 1], in + off, len, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaEventRecord(st.ev[c & 1], s), "event record");
+    st.used[c & 1] = true;
+  };
+  issue(0);
+  for (size_t c = 0; c < nchunk; ++c) {
+    if (c + 1 < nchunk) issue(c + 1);
+    cuda_check(cudaEventSynchronize(st.ev[c & 1]), "D2H wait");
+    const size_t off = c * kStageBytes, len = std::min(kStageBytes, bytes - off);
+    const char* pb = static_cast<const char*>(st.buf[c & 1]);
+    parallel_for(len, 1u << 20, [&](size_t b, size_t e) { std::memcpy(out + off + b, pb + b, e - b); });
+  }
+}
+
 }  // namespace tb

@@ -41,6 +41,10 @@ int host_workers();
 // filled by the worker pool while the previous chunk is in flight.  Returns
 // once the source may be reused (all bytes have left host memory).
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// Device -> host copy in stream order; returns with the bytes in dst (the
+// stream is synchronized).  Pageable destinations are staged through the same
+// pinned buffers, the next chunk's DMA overlapping the previous chunk's copy-out.
+void download(void* dst, const void* src, size_t bytes, cudaStream_t s);
 bool is_pinned(const void* p);
 
 }  // namespace tb

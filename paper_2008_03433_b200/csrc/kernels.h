@@ -48,6 +48,13 @@ struct SegPlanHost {
   std::vector<uint32_t> chunk_rank, lastbits;
 };
 void seg_plan_host(const int32_t* ptr, int64_t rows, int64_t nnz, SegPlanHost* out);
+// Device-built plan with fixed kSegChunk-entry chunks (chunk boundaries inside a
+// row become fix-ups).  Buffers: chunk_start[nchunks+1], chunk_rank[nchunks],
+// lastbits[nnz/32+2], nz_col[rows+1], fix_chunk[rows], fix_first[rows]; P's
+// head / carry are left to the caller.  Synchronizes s (returns nfix in P).
+int seg_plan_device(const int32_t* ptr, int64_t rows, int64_t nnz, SegView* P,
+                    int32_t* chunk_start, uint32_t* chunk_rank, uint32_t* lastbits,
+                    int32_t* nz_col, int32_t* fix_chunk, int32_t* fix_first, cudaStream_t s);
 
 // Streamed segmented layout of a compressed matrix (seg_stream.cu): 2048-
 // entry tiles of eight 256-entry pieces, lane-interleaved, with per-lane
