@@ -98,8 +98,13 @@ struct LaneChunk {
 
 __device__ __forceinline__ void load_chunk(const CsrView& A, const SegView& S, long long t, int lane,
                                            LaneChunk& c) {
-  c.cs = __ldg(S.chunk_start + t);
-  c.ce = __ldg(S.chunk_start + t + 1);
+  if (S.fixed_chunks) {  // device-built plan: chunk t is [256t, 256t + 256), no load on the chain
+    c.cs = (int)(t * kSegChunk);
+    c.ce = (int)min((long long)c.cs + kSegChunk, (long long)A.nnz);
+  } else {
+    c.cs = __ldg(S.chunk_start + t);
+    c.ce = __ldg(S.chunk_start + t + 1);
+  }
   c.base = (long long)(c.cs & ~3) + lane * kSegLaneItems;  // 16-B aligned lanes
   if (c.base + kSegLaneItems <= A.nnz) {
 #pragma unroll
@@ -119,6 +124,90 @@ __device__ __forceinline__ void load_chunk(const CsrView& A, const SegView& S, l
   c.lo_word = any ? __ldg(S.lastbits + (c.base >> 5)) : 0u;
   c.hi_word = any ? __ldg(S.lastbits + (c.base >> 5) + 1) : 0u;
   c.cr = __ldg(S.chunk_rank + t);
+}
+
+// One chunk: gathers, per-lane sequential sums, warp segmented scan, emission.
+template <int UK, bool SQ, int EPI, bool STAGED>
+__device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const UView& U,
+                                              const EpiView& E, double* __restrict__ out,
+                                              const double* su, long long t, const LaneChunk& cur,
+                                              int lane) {
+  // gathers of the current chunk
+  double w[kSegLaneItems];
+#pragma unroll
+  for (int m = 0; m < kSegLaneItems; ++m) {
+    const long long k = cur.base + m;
+    if (STAGED) {
+      const double u = su[cur.ix[m]];
+      const double p = SQ ? (u * cur.v[m]) * cur.v[m] : u * cur.v[m];
+      w[m] = (k >= cur.cs && k < cur.ce) ? p : 0.0;
+    } else {
+      w[m] = (k >= cur.cs && k < cur.ce) ? weight<UK, SQ>(U, cur.ix[m], cur.v[m]) : 0.0;
+    }
+  }
+
+  unsigned bits = 0u;
+  if (cur.base < cur.ce && cur.base + kSegLaneItems > cur.cs) {
+    // base is a multiple of 4: the lane's 8 bits may straddle two words
+    const unsigned long long pair =
+        (unsigned long long)cur.lo_word | ((unsigned long long)cur.hi_word << 32);
+    bits = (unsigned)(pair >> (cur.base & 31)) & 0xffu;
+    const long long lo = cur.cs - cur.base, hi = cur.ce - cur.base;  // keep [cs, ce)
+    if (lo > 0) bits &= ~((1u << lo) - 1u);
+    if (hi < kSegLaneItems) bits &= (1u << hi) - 1u;
+  }
+  const int chunk_rank = (int)(cur.cr & 0x7fffffffu);
+  const bool cont_in = (cur.cr >> 31) != 0;
+
+  // rank of the column containing this lane's first item
+  const int cnt = __popc(bits);
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int r0 = chunk_rank + incl - cnt;
+
+  // sequential pass over the lane's items
+  double acc = 0.0, head_val = 0.0;
+  bool have_head = false;
+  int r = r0;
+#pragma unroll
+  for (int m = 0; m < kSegLaneItems; ++m) {
+    acc += w[m];
+    if (bits & (1u << m)) {
+      if (!have_head) {
+        head_val = acc;
+        have_head = true;
+      } else {
+        emit_rank<EPI>(S, E, out, r, acc);  // column wholly inside this lane
+      }
+      ++r;
+      acc = 0.0;
+    }
+  }
+
+  // warp segmented inclusive scan of the carries, keyed by column rank
+  const int key = r0 + cnt;
+  double val = acc;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int k2 = __shfl_up_sync(0xffffffffu, key, off);
+    const double v2 = __shfl_up_sync(0xffffffffu, val, off);
+    if (lane >= off && k2 == key) val = v2 + val;
+  }
+  const int prev_key = __shfl_up_sync(0xffffffffu, key, 1);
+  const double prev_val = __shfl_up_sync(0xffffffffu, val, 1);
+  if (have_head) {
+    const double tot = (lane > 0 && prev_key == r0) ? prev_val + head_val : head_val;
+    if (r0 == chunk_rank && cont_in)
+      S.head[t] = tot;  // column began in an earlier chunk: finished by the fix-up
+    else
+      emit_rank<EPI>(S, E, out, r0, tot);
+  }
+  if (lane == 31) S.carry[t] = val;
+
 }
 
 // Persistent warps walk chunks t, t+W, ...; the next chunk's operands are
@@ -154,90 +243,32 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
 
   LaneChunk cur;
   load_chunk(A, S, t, lane, cur);
-  for (;;) {
-    // gathers of the current chunk
-    double w[kSegLaneItems];
-#pragma unroll
-    for (int m = 0; m < kSegLaneItems; ++m) {
-      const long long k = cur.base + m;
-      if (STAGED) {
-        const double u = su[cur.ix[m]];
-        const double p = SQ ? (u * cur.v[m]) * cur.v[m] : u * cur.v[m];
-        w[m] = (k >= cur.cs && k < cur.ce) ? p : 0.0;
-      } else {
-        w[m] = (k >= cur.cs && k < cur.ce) ? weight<UK, SQ>(U, cur.ix[m], cur.v[m]) : 0.0;
-      }
+  if (!STAGED) {
+    // one chunk ahead: the next chunk's operands are requested before this
+    // chunk's gathers are consumed
+    for (;;) {
+      const long long tn = t + W;
+      LaneChunk nxt;
+      if (tn < S.nchunks) load_chunk(A, S, tn, lane, nxt);
+      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane);
+      if (tn >= S.nchunks) break;
+      t = tn;
+      cur = nxt;
     }
-    // operands of the next chunk, in flight while this one is reduced
-    const long long tn = t + W;
+  } else {
+    // u in shared memory makes the gathers cheap; with one 16-warp block per
+    // SM, keep two chunks in flight per warp instead
     LaneChunk nxt;
-    if (tn < S.nchunks) load_chunk(A, S, tn, lane, nxt);
-
-    unsigned bits = 0u;
-    if (cur.base < cur.ce && cur.base + kSegLaneItems > cur.cs) {
-      // base is a multiple of 4: the lane's 8 bits may straddle two words
-      const unsigned long long pair =
-          (unsigned long long)cur.lo_word | ((unsigned long long)cur.hi_word << 32);
-      bits = (unsigned)(pair >> (cur.base & 31)) & 0xffu;
-      const long long lo = cur.cs - cur.base, hi = cur.ce - cur.base;  // keep [cs, ce)
-      if (lo > 0) bits &= ~((1u << lo) - 1u);
-      if (hi < kSegLaneItems) bits &= (1u << hi) - 1u;
+    if (t + W < S.nchunks) load_chunk(A, S, t + W, lane, nxt);
+    for (;;) {
+      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane);
+      if (t + W >= S.nchunks) break;
+      if (t + 2 * W < S.nchunks) load_chunk(A, S, t + 2 * W, lane, cur);
+      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t + W, nxt, lane);
+      if (t + 2 * W >= S.nchunks) break;
+      if (t + 3 * W < S.nchunks) load_chunk(A, S, t + 3 * W, lane, nxt);
+      t += 2 * W;
     }
-    const int chunk_rank = (int)(cur.cr & 0x7fffffffu);
-    const bool cont_in = (cur.cr >> 31) != 0;
-
-    // rank of the column containing this lane's first item
-    const int cnt = __popc(bits);
-    int incl = cnt;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += y;
-    }
-    const int r0 = chunk_rank + incl - cnt;
-
-    // sequential pass over the lane's items
-    double acc = 0.0, head_val = 0.0;
-    bool have_head = false;
-    int r = r0;
-#pragma unroll
-    for (int m = 0; m < kSegLaneItems; ++m) {
-      acc += w[m];
-      if (bits & (1u << m)) {
-        if (!have_head) {
-          head_val = acc;
-          have_head = true;
-        } else {
-          emit_rank<EPI>(S, E, out, r, acc);  // column wholly inside this lane
-        }
-        ++r;
-        acc = 0.0;
-      }
-    }
-
-    // warp segmented inclusive scan of the carries, keyed by column rank
-    const int key = r0 + cnt;
-    double val = acc;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int k2 = __shfl_up_sync(0xffffffffu, key, off);
-      const double v2 = __shfl_up_sync(0xffffffffu, val, off);
-      if (lane >= off && k2 == key) val = v2 + val;
-    }
-    const int prev_key = __shfl_up_sync(0xffffffffu, key, 1);
-    const double prev_val = __shfl_up_sync(0xffffffffu, val, 1);
-    if (have_head) {
-      const double tot = (lane > 0 && prev_key == r0) ? prev_val + head_val : head_val;
-      if (r0 == chunk_rank && cont_in)
-        S.head[t] = tot;  // column began in an earlier chunk: finished by the fix-up
-      else
-        emit_rank<EPI>(S, E, out, r0, tot);
-    }
-    if (lane == 31) S.carry[t] = val;
-
-    if (tn >= S.nchunks) break;
-    t = tn;
-    cur = nxt;
   }
 }
 
@@ -474,6 +505,7 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, int
   if (e == cudaSuccess) e = cudaGetLastError();
   P->nchunks = nchunks;
   P->nfix = nfix;
+  P->fixed_chunks = 1;
   P->chunk_start = chunk_start;
   P->chunk_rank = chunk_rank;
   P->lastbits = lastbits;

@@ -50,7 +50,9 @@ template <int G, bool STAGED>
 __device__ __forceinline__ double row_dot_sub(const CsrView& X, long long row, int sub,
                                               const double* __restrict__ v, const double* sv,
                                               int hot) {
-  constexpr int U = 8;  // entries in flight per lane
+  // entries in flight per lane: one 16-warp block per SM when staged, so each
+  // lane keeps twice as many loads in flight
+  constexpr int U = STAGED ? 16 : 8;
   const int beg = X.ptr[row], end = X.ptr[row + 1];
   double s = 0.0;
   for (int k0 = beg + sub; k0 < end; k0 += U * G) {

@@ -244,11 +244,15 @@ void Engine::common_alloc() {
     }
     if (dense_) S.gparts.alloc((size_t)dense_grid(l_, n_) * nn);
   }
-  for (DevBuf<double>* b : {&g_, &M_, &d_, &r0_, &r1_, &p_, &hp_, &vtmp_, &otmp_}) b->alloc(nn);
+  for (DevBuf<double>* b : {&g_, &gspec_, &M_, &d_, &r0_, &r1_, &p_, &hp_, &vtmp_, &otmp_})
+    b->alloc(nn);
   if (comm_.active()) raw_.alloc(nn);
   if (!dense_) a_.alloc(ll);
   if (dense_) parts_.alloc((size_t)dense_grid(l_, n_) * nn);
   small_engine_ = dense_ || n_ <= kSmallCgMaxN;
+  // TRON_B200_CLUSTER_CG=0: the three-kernel large-n CG step for mid-size n too
+  const char* cc = std::getenv("TRON_B200_CLUSTER_CG");
+  mid_engine_ = !small_engine_ && n_ <= kClusterCgMaxN && !(cc && cc[0] == '0');
   // TRON_B200_NO_GRAPH=1 runs the CG loop host-driven (per-kernel profiling:
   // ncu cannot profile kernel nodes of graphs with conditional nodes).
   const char* ng = std::getenv("TRON_B200_NO_GRAPH");
@@ -502,7 +506,7 @@ uint64_t Engine::memory_bytes() const {
   for (const auto& S : slot_)
     b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes() +
          S.gparts.bytes();
-  b += g_.bytes() * 9 + a_.bytes() + parts_.bytes();
+  b += g_.bytes() * 10 + a_.bytes() + parts_.bytes();
   return b;
 }
 
@@ -538,7 +542,7 @@ void Engine::forward(Slot& S) {
   count_launch(1);
 }
 
-double Engine::eval_candidate_dev(const double* d_step) {
+double Engine::eval_candidate_dev(const double* d_step, bool read) {
   Slot& S = slot_[cand_];
   const Slot& W = slot_[cand_ ^ 1];
   if (d_step) {
@@ -550,7 +554,14 @@ double Engine::eval_candidate_dev(const double* d_step) {
   }
   forward(S);
   if (comm_.active()) comm_.allreduce_sum(obj_d_->red, 2, s_);  // per-shard loss sums, |I|
+  if (!read) return 0.0;
   read_obj();
+  return candidate_result();
+}
+
+// Bookkeeping of a candidate whose scalars have been read into obj_h_.
+double Engine::candidate_result() {
+  Slot& S = slot_[cand_];
   double f = obj_h_->f;
   long long nact = obj_h_->nact;
   if (comm_.active()) {
@@ -598,8 +609,9 @@ void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& 
 
 // kind = DA_HV / DA_PRECOND (one tiled pass) or -1: finish the gradient
 // partials the committed slot's margin pass already accumulated.
-void Engine::dense_vector(int kind, const double* v, const EpiView& epi, double* out) {
-  const Slot& S = slot_[cand_ ^ 1];
+void Engine::dense_vector(int kind, const double* v, const EpiView& epi, double* out,
+                          const Slot* grad_slot) {
+  const Slot& S = grad_slot ? *grad_slot : slot_[cand_ ^ 1];
   const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
   const bool gathered = kind == DA_HV && gathered_valid_;
   const double* parts = parts_.p;
@@ -630,14 +642,17 @@ void Engine::dense_vector(int kind, const double* v, const EpiView& epi, double*
 // ----------------------------------------------------------------------------
 // commit + gradient (backend.cpp:165-183 / :249-277; loss.cpp:74-80 / :129-137)
 // ----------------------------------------------------------------------------
-void Engine::gradient_dev() {
-  const Slot& S = slot_[cand_ ^ 1];
+void Engine::gradient_dev() { gradient_into(slot_[cand_ ^ 1], g_.p); }
+
+// g = w + C X^T zhat (LR) / w + 2C X_I^T (z - y)_I (SVM) of slot S into out,
+// then ||out|| and its finiteness into obj (loss.cpp:74-80, :129-137).
+void Engine::gradient_into(const Slot& S, double* out) {
   EpiView epi;
   epi.kind = EPI_VEC;
   epi.base = S.w.p;
   epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
   if (dense_) {
-    dense_vector(-1, nullptr, epi, g_.p);  // partials from the fused margin pass
+    dense_vector(-1, nullptr, epi, out, &S);  // partials from the fused margin pass
   } else {
     UView u;
     if (loss_ == TRON_LOSS_LOGISTIC) {
@@ -649,9 +664,9 @@ void Engine::gradient_dev() {
       u.z = S.z.p;
       u.y = y_.p;
     }
-    transposed_raw_or_epi(u, false, epi, g_.p);
+    transposed_raw_or_epi(u, false, epi, out);
   }
-  vec_norm_check(n_, g_.p, obj_d_, sc_, s_);
+  vec_norm_check(n_, out, obj_d_, sc_, s_);
   count_launch(1);
 }
 
@@ -703,6 +718,22 @@ void Engine::commit(double* gnorm) {
   gnorm_ = obj_h_->gnorm;
   ledger.gradient_materializations++;
   if (gnorm) *gnorm = gnorm_;
+}
+
+// commit() for a candidate whose gradient was computed speculatively into gspec_
+// (its norm already read into obj_h_).
+void Engine::adopt_candidate() {
+  if (!slot_[cand_].valid) raise(TRON_ERR_LOGIC, "commit() without a pending candidate");
+  cand_ ^= 1;
+  slot_[cand_].valid = false;
+  committed_valid_ = true;
+  precond_valid_ = false;
+  gathered_valid_ = false;
+  if (n_ > 0)
+    cuda_check(cudaMemcpyAsync(g_.p, gspec_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_),
+               "D2D");
+  gnorm_ = obj_h_->gnorm;
+  ledger.gradient_materializations++;
 }
 
 void Engine::gradient_host(double* g) {
@@ -859,7 +890,7 @@ void Engine::build_graph(int k, bool use_m) {
   cuda_check(cudaStreamUpdateCaptureDependencies(s_, &cond_node, 1,
                                                  cudaStreamSetCaptureDependencies),
              "update deps");
-  if (!small_engine_) cg_large_post(v, st_d_, sc_, s_);
+  if (!small_engine_ && !mid_engine_) cg_large_post(v, st_d_, sc_, s_);
   cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
 
   cudaGraph_t body = cp.conditional.phGraph_out[0];
@@ -880,6 +911,10 @@ void Engine::build_graph(int k, bool use_m) {
       cg_small_step(v, nullptr, 0, 0.0, st_d_, cond, s_);
       count_launch(1);
     }
+  } else if (mid_engine_) {
+    hv_kernels(p_.p, hp_.p);
+    cg_cluster_step(v, st_d_, cond, s_);
+    count_launch(1);
   } else {
     hv_kernels(p_.p, hp_.p);
     cg_large_php(v, st_d_, sc_, cond, s_);
@@ -896,6 +931,31 @@ void Engine::build_graph(int k, bool use_m) {
   cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
   graph_[k][use_m] = graph;
   graph_exec_[k][use_m] = exec;
+}
+
+// Graph path: enqueues the CG loop and returns without waiting (false); the
+// host-driven path (no graphs / NCCL) runs it to the end and fills *out (true).
+bool Engine::enqueue_cg(double delta, const tron_config& cfg, CgState* out) {
+  if (!use_graphs_) {
+    run_cg(delta, cfg, out);
+    return true;
+  }
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "truncated CG before the first commit()");
+  const bool use_m = cfg.use_preconditioner != 0;
+  if (use_m) ensure_precond();
+  uint64_t max_iters = cfg.max_cg_iters;
+  if (max_iters == 0) max_iters = (uint64_t)n_ < 1000 ? (uint64_t)n_ : 1000;  // tron.cpp:40-41
+  CgState init{};
+  init.delta = delta;
+  init.stop = cfg.cg_tol * gnorm_;  // tron.cpp:55
+  init.max_iters = (long long)max_iters;
+  init.use_m = use_m;
+  *st_h_ = init;
+  cuda_check(cudaMemcpyAsync(st_d_, st_h_, sizeof(CgState), cudaMemcpyHostToDevice, s_), "H2D");
+  const int k = cand_ ^ 1;
+  if (!graph_exec_[k][use_m]) build_graph(k, use_m);
+  cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
+  return false;
 }
 
 void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
@@ -917,7 +977,7 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     if (!graph_exec_[k][use_m]) build_graph(k, use_m);
     cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
     read_cg(out);
-    launches += 1 + (uint64_t)out->iters * body_kernels_ + (small_engine_ ? 0 : 1);
+    launches += 1 + (uint64_t)out->iters * body_kernels_ + (has_post_kernel() ? 1 : 0);
     return;
   }
   // host-driven loop (multi-GPU: NCCL between phases)
@@ -933,6 +993,9 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     if (small_engine_) {
       cg_small_step(v, nullptr, 0, 0.0, st_d_, none, s_);
       count_launch(1);
+    } else if (mid_engine_) {
+      cg_cluster_step(v, st_d_, none, s_);
+      count_launch(1);
     } else {
       cg_large_php(v, st_d_, sc_, none, s_);
       cg_large_update(v, st_d_, sc_, none, s_);
@@ -941,7 +1004,7 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     }
     read_cg(out);
   }
-  if (!small_engine_) {
+  if (has_post_kernel()) {
     cg_large_post(v, st_d_, sc_, s_);
     count_launch(1);
     read_cg(out);
@@ -1034,9 +1097,34 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     return;
   }
   double delta = gnorm0;
+  const bool speculative = !(loss_ == TRON_LOSS_L2SVM && svm_strategy_ == TRON_SVM_GATHERED);
   while (info->n_iterations < cfg.max_outer_iters) {
+    // One host round trip per outer iteration: the CG loop, the candidate's
+    // margin pass and -- speculatively -- the candidate's gradient are queued
+    // back to back; the host reads the CG scalars and f, ||g|| together.
+    // The gradient is adopted only if the step is accepted (the reference's
+    // lazy gradient, backend.cpp:165-183; ledger counts adoptions).
     CgState st;
-    run_cg(delta, cfg, &st);
+    const bool cg_done = enqueue_cg(delta, cfg, &st);
+    double f_cand;
+    if (speculative) {
+      const int k = cand_ ^ 1;
+      f_cand = eval_candidate_dev(d_.p, /*read=*/false);
+      gradient_into(slot_[cand_], gspec_.p);
+      if (!cg_done)
+        cuda_check(cudaMemcpyAsync(st_h_, st_d_, sizeof(CgState), cudaMemcpyDeviceToHost, s_),
+                   "D2H");
+      read_obj();
+      if (!cg_done) {
+        st = *st_h_;
+        launches += 1 + (uint64_t)st.iters * body_kernels_ + (has_post_kernel() ? 1 : 0);
+      }
+      f_cand = candidate_result();
+      (void)k;
+    } else {
+      if (!cg_done) read_cg(&st);
+      f_cand = eval_candidate_dev(d_.p);
+    }
     hv_count += (uint64_t)st.iters;
     if (st.fail) {
       finish(TRON_ERR_NUMERICAL);
@@ -1044,7 +1132,6 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
             "conjugate gradients met non-positive curvature (" + std::to_string(st.php) + ")");
     }
     const double step_norm = st.dnorm;
-    const double f_cand = eval_candidate_dev(d_.p);
     info->objective_evaluations++;
     if (!std::isfinite(f_cand)) {
       finish(TRON_ERR_NUMERICAL);
@@ -1079,7 +1166,10 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     if (accept) {
       f = f_cand;
       info->objective = f;
-      commit(nullptr);
+      if (speculative)
+        adopt_candidate();
+      else
+        commit(nullptr);
       info->accepted_steps++;
       info->gradient_materializations++;
       if (obj_h_->grad_nonfinite) {

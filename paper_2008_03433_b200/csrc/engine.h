@@ -132,7 +132,7 @@ class Engine {
   void synchronize();
 
   // Device-side building blocks (also used by the host-CG adapter).
-  double eval_candidate_dev(const double* d_step);  // slot[cand].w (+ d_step) -> f
+  double eval_candidate_dev(const double* d_step, bool read = true);  // slot[cand].w (+ d_step) -> f
   void hessian_vec_dev(const double* v, double* out);
   void ensure_precond();
   void run_cg(double delta, const tron_config& cfg, CgState* out);
@@ -152,7 +152,12 @@ class Engine {
   void forward(Slot& S);
   void gradient_dev();
   void transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out);
-  void dense_vector(int kind, const double* v, const EpiView& epi, double* out);
+  void dense_vector(int kind, const double* v, const EpiView& epi, double* out,
+                    const Slot* grad_slot = nullptr);
+  void gradient_into(const Slot& S, double* out);
+  bool enqueue_cg(double delta, const tron_config& cfg, CgState* out);
+  double candidate_result();
+  void adopt_candidate();
   void hv_kernels(const double* v, double* out);  // enqueue only
   void gather_active();
   int compact(const Slot& S, DevBuf<int32_t>& idx);
@@ -200,7 +205,7 @@ class Engine {
   Slot slot_[2];
   int cand_ = 0;       // candidate slot index; committed = cand_ ^ 1
   bool committed_valid_ = false;
-  DevBuf<double> g_, M_, d_, r0_, r1_, p_, hp_, a_, raw_, vtmp_, otmp_, parts_;
+  DevBuf<double> g_, gspec_, M_, d_, r0_, r1_, p_, hp_, a_, raw_, vtmp_, otmp_, parts_;
   bool precond_valid_ = false;
   double gnorm_ = 0.0;
 
@@ -219,7 +224,9 @@ class Engine {
   cudaGraphExec_t graph_exec_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   cudaGraph_t graph_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   uint64_t body_kernels_ = 0;
-  bool small_engine_ = false;
+  bool small_engine_ = false;  // n <= kSmallCgMaxN: single-block CG step
+  bool mid_engine_ = false;    // n <= kClusterCgMaxN: one 8-CTA cluster kernel per CG step
+  bool has_post_kernel() const { return !small_engine_ && !mid_engine_; }
   bool use_graphs_ = true;
 };
 

@@ -32,6 +32,7 @@ constexpr int kSegChunk = 32 * kSegLaneItems;
 struct SegView {
   int64_t nchunks = 0;
   int64_t nfix = 0;
+  int fixed_chunks = 0;                  // 1: chunk t = [t*kSegChunk, (t+1)*kSegChunk)
   const int32_t* chunk_start = nullptr;  // [nchunks+1] first entry of each chunk; [nchunks] = nnz
   const uint32_t* chunk_rank = nullptr;  // rank of the row holding the chunk's first entry
                                          // | 0x80000000 when that row began in an earlier chunk
@@ -203,6 +204,11 @@ void cg_large_update(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
 void cg_large_direction(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
                         cudaStream_t s);
 void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s);
+
+// Mid-n CG engine (kSmallCgMaxN < n <= kClusterCgMaxN): one kernel per iteration
+// on a cluster of 8 CTAs (vector phases + scalars; the exit's q(d), ||d|| included).
+constexpr int64_t kClusterCgMaxN = 262144;
+void cg_cluster_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
 
 // Small-n CG engine (n <= kSmallCgMaxN): one single-block kernel per
 // iteration.  When `partials` is non-null, hp_j = p_j + scale*sum_b

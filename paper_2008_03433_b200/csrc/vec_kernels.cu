@@ -15,6 +15,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cooperative_groups.h>
+
 namespace tb {
 
 namespace {
@@ -126,6 +128,12 @@ __global__ void __launch_bounds__(kBlock) cg_init_kernel(CgVectors v, CgState* s
       st->exit_kind = 0;
       const int cont = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
       st->cont = cont;
+      if (!cont) {  // no iteration: d = 0 (tron.cpp:99-106 with q(0) = 0, ||0|| = 0)
+        st->exit_kind = (st->iters >= st->max_iters && st->rnorm > st->stop) ? kCgMaxIters
+                                                                             : kCgConverged;
+        st->q = 0.0;
+        st->dnorm = 0.0;
+      }
       set_cond(cond, cont);
     }
   }
@@ -288,6 +296,158 @@ __global__ void __launch_bounds__(kBlock) cg_post_kernel(CgVectors v, CgState* s
       st->q = 0.5 * (tdg - tdr);  // tron.cpp:106
       st->dnorm = sqrt(tdd);
     }
+  }
+}
+
+// ---------------- mid-n CG: one cluster of 8 CTAs per iteration ----------------
+// For n up to kClusterCgMaxN the CG vector work of an iteration (tron.cpp:70-97:
+// p.Hp, alpha, d, the boundary test and tau, r, z, beta, p) is one kernel on a
+// cluster of 8 CTAs: each CTA owns a contiguous slice of the n-vectors, the
+// dot products are block sums exchanged through distributed shared memory and
+// added in rank order (every CTA holds the identical total), and cluster
+// barriers replace the three kernel boundaries of the large-n engine.
+namespace cgc = cooperative_groups;
+constexpr int kClusterCtas = 8;
+constexpr int kClusterBlock = 1024;
+
+// Sums K values over the whole cluster; identical result in every thread.
+template <int K>
+__device__ __forceinline__ void cluster_sum(double (&v)[K], double* sh, double (*slot)[4]) {
+  cgc::cluster_group cl = cgc::this_cluster();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double b = block_sum<kClusterBlock>(v[k], sh, true);
+    if (threadIdx.x == 0) (*slot)[k] = b;
+  }
+  cl.sync();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double t = 0.0;
+    for (int r = 0; r < kClusterCtas; ++r) t += (*cl.map_shared_rank(slot, r))[k];
+    v[k] = t;
+  }
+  cl.sync();  // the slots may be rewritten by the next sum
+}
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterBlock)
+    cg_cluster_step_kernel(CgVectors v, CgState* st, Cond cond) {
+  __shared__ double sh[kClusterBlock / kWarp + 1];
+  __shared__ double slot[4];
+  const long long n = v.n;
+  const int rank = (int)cgc::this_cluster().block_rank();
+  const long long j0 = n * rank / kClusterCtas, j1 = n * (rank + 1) / kClusterCtas;
+  const double rz_old = st->rz, delta = st->delta;
+  const long long iters = st->iters + 1, max_iters = st->max_iters;
+  const double stop = st->stop;
+  const int rpar = st->rpar;
+  const bool lead = rank == 0 && threadIdx.x == 0;
+  double* r = rpar ? v.r1 : v.r0;
+  // p.Hp (tron.cpp:71-75)
+  double a1[1] = {0.0};
+  for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock) a1[0] += v.p[j] * v.hp[j];
+  cluster_sum<1>(a1, sh, &slot);
+  const double php = a1[0];
+  if (!(php > 0.0)) {
+    if (lead) {
+      st->iters = iters;
+      st->php = php;
+      st->fail = 1;
+      st->cont = 0;
+      set_cond(cond, 0);
+    }
+    return;
+  }
+  const double alpha = rz_old / php;
+  // d += alpha p, ||d|| (tron.cpp:76-78)
+  double a2[1] = {0.0};
+  for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock) {
+    const double dj = v.d[j] + alpha * v.p[j];
+    v.d[j] = dj;
+    a2[0] += dj * dj;
+  }
+  cluster_sum<1>(a2, sh, &slot);
+  if (sqrt(a2[0]) > delta) {
+    // boundary: retreat, then tau on ||d + tau p|| = delta (tron.cpp:78-90)
+    double a3[3] = {0.0, 0.0, 0.0};
+    for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock) {
+      const double pj = v.p[j];
+      const double dj = v.d[j] + (-alpha) * pj;
+      v.d[j] = dj;
+      a3[0] += dj * pj;
+      a3[1] += dj * dj;
+      a3[2] += pj * pj;
+    }
+    cluster_sum<3>(a3, sh, &slot);
+    const double dp = a3[0], dd = a3[1], pp = a3[2];
+    const double rad = sqrt(dp * dp + pp * (delta * delta - dd));
+    const double tau = dp >= 0.0 ? (delta * delta - dd) / (dp + rad) : (rad - dp) / pp;
+    double a4[3] = {0.0, 0.0, 0.0};  // q(d) and ||d|| of the final step (tron.cpp:99-106)
+    for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock) {
+      const double dj = v.d[j] + tau * v.p[j];
+      const double rj = r[j] + (-tau) * v.hp[j];
+      v.d[j] = dj;
+      r[j] = rj;
+      a4[0] += dj * v.g[j];
+      a4[1] += dj * rj;
+      a4[2] += dj * dj;
+    }
+    cluster_sum<3>(a4, sh, &slot);
+    if (lead) {
+      st->iters = iters;
+      st->php = php;
+      st->alpha = alpha;
+      st->tau = tau;
+      st->boundary = 1;
+      st->exit_kind = kCgBoundary;
+      st->q = 0.5 * (a4[0] - a4[1]);
+      st->dnorm = sqrt(a4[2]);
+      st->cont = 0;
+      set_cond(cond, 0);
+    }
+    return;
+  }
+  // r -= alpha Hp, z = M^-1 r (tron.cpp:91-95)
+  double* rn = rpar ? v.r0 : v.r1;
+  double a5[2] = {0.0, 0.0};
+  for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock) {
+    const double rj = r[j] + (-alpha) * v.hp[j];
+    rn[j] = rj;
+    const double z = v.M ? rj / v.M[j] : rj;
+    a5[0] += rj * z;
+    a5[1] += rj * rj;
+  }
+  cluster_sum<2>(a5, sh, &slot);
+  const double rz = a5[0], rnorm = sqrt(a5[1]);
+  const double beta = rz / rz_old;
+  for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock)
+    v.p[j] = zval(rn, v.M, j) + beta * v.p[j];  // tron.cpp:96
+  const int cont = (iters < max_iters) && !(rnorm <= stop);
+  if (!cont) {
+    // exit classification, q(d) = (d.g - d.r)/2, ||d|| (tron.cpp:97-106)
+    double a6[3] = {0.0, 0.0, 0.0};
+    for (long long j = j0 + threadIdx.x; j < j1; j += kClusterBlock) {
+      const double dj = v.d[j];
+      a6[0] += dj * v.g[j];
+      a6[1] += dj * rn[j];
+      a6[2] += dj * dj;
+    }
+    cluster_sum<3>(a6, sh, &slot);
+    if (lead) {
+      st->exit_kind = (iters >= max_iters && rnorm > stop) ? kCgMaxIters : kCgConverged;
+      st->q = 0.5 * (a6[0] - a6[1]);
+      st->dnorm = sqrt(a6[2]);
+    }
+  }
+  if (lead) {
+    st->iters = iters;
+    st->php = php;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->rz = rz;
+    st->rpar = rpar ^ 1;
+    st->rnorm = rnorm;
+    st->cont = cont;
+    set_cond(cond, cont);
   }
 }
 
@@ -481,6 +641,10 @@ void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cud
 
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {
   epilogue_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, raw, epi, out);
+}
+
+void cg_cluster_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s) {
+  cg_cluster_step_kernel<<<kClusterCtas, kClusterBlock, 0, s>>>(v, st, cond);
 }
 
 void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {

@@ -249,6 +249,39 @@ def test_device_cg_matches_host_cg(port, case, precond):
             assert np.linalg.norm(dev.d) <= delta * (1 + 1e-12)
 
 
+# the three CG engines on the same mid-size problem: single cluster kernel per
+# step (default for 4096 < n <= 262144), the three-kernel large-n step, and the
+# host-driven loop (no graph), each against the host restatement
+@pytest.mark.parametrize("engine", ["cluster", "large", "nograph"])
+@pytest.mark.parametrize("precond", [False, True])
+def test_cg_engines_match_host_cg(port, monkeypatch, engine, precond):
+    if engine == "large":
+        monkeypatch.setenv("TRON_B200_CLUSTER_CG", "0")
+    if engine == "nograph":
+        monkeypatch.setenv("TRON_B200_NO_GRAPH", "1")
+    p = synth.synth_sparse(9, 2000, 5000, 37)  # n = 5000 > kSmallCgMaxN
+    w = synth.testgen_random_vector(3007, p.X.cols, 0.3)  # the state of fixture case 7 above
+    with gpu(p, LR) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        g = ev.gradient()
+        M = ev.precond_diagonal() if precond else None
+        for delta in (1e6, 0.5 * np.linalg.norm(g), 1e-3):
+            cfg = TrustRegionConfig(cg_tol=1e-6, use_preconditioner=precond)
+            dev = ev.truncated_cg(delta, cfg)
+            host = port.truncated_cg(g, ev.hessian_vec, delta, M, cg_tol=1e-6)
+            assert dev.iters == host["iters"]
+            assert int(dev.exit) == host["exit"]
+            assert rel_err(dev.d, host["d"]) <= 1e-10
+            assert rel_err(dev.model_value, host["model_value"]) <= 1e-9
+        # the iteration cap ends the loop on the device (exit MaxIters)
+        cfg = TrustRegionConfig(cg_tol=1e-9, max_cg_iters=2, use_preconditioner=precond)
+        dev = ev.truncated_cg(1e6, cfg)
+        host = port.truncated_cg(g, ev.hessian_vec, 1e6, M, cg_tol=1e-9, max_cg_iters=2)
+        assert dev.iters == host["iters"] == 2 and int(dev.exit) == host["exit"]
+        assert rel_err(dev.d, host["d"]) <= 1e-10
+
+
 def test_device_cg_iteration_cap():  # test_tron.cpp:75-90
     p = synth.testgen_dense_problem(1100, 30, 6, 1.0)
     w = synth.testgen_random_vector(1101, 6)
