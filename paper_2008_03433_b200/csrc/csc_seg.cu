@@ -219,8 +219,13 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
 // L1 wavefront (a 32-address LDG costs ~32 L1 wavefronts; measured on N1
 // the gathers, not HBM, bounded this kernel).
 template <int UK, bool SQ, int EPI, bool STAGED>
-__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
+#ifndef TB_SEG_BLOCKS_PER_SM
+#define TB_SEG_BLOCKS_PER_SM 3
+#endif
+__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : TB_SEG_BLOCKS_PER_SM)
     seg_spmv_kernel(CsrView A, SegView S, UView U, EpiView E, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double su[];
   constexpr int BLK = STAGED ? kStagedBlock : kBlock;
   const int lane = threadIdx.x & 31;
@@ -275,6 +280,8 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
 template <int EPI>
 __global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
                                                           double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const long long f = (blockIdx.x * (long long)kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (f >= S.nfix) return;
@@ -298,17 +305,17 @@ void launch_one(const CsrView& A, const SegView& S, const UView& U, const EpiVie
     }
     long long want = (S.nchunks * 32 + kStagedBlock - 1) / kStagedBlock;
     const long long cap = device_sm_count();
-    seg_spmv_kernel<UK, SQ, EPI, true>
-        <<<(int)(want < cap ? want : cap), kStagedBlock, smem, s>>>(A, S, U, E, out);
+    launch_pdl(seg_spmv_kernel<UK, SQ, EPI, true>, dim3((int)(want < cap ? want : cap)),
+               dim3(kStagedBlock), smem, s, A, S, U, E, out);
   } else {
     // persistent: 3 blocks of 8 warps per SM (register-limited), never more than chunks
     long long want = (S.nchunks * 32 + kBlock - 1) / kBlock;
-    const long long cap = (long long)device_sm_count() * 3;
-    seg_spmv_kernel<UK, SQ, EPI, false>
-        <<<(int)(want < cap ? want : cap), kBlock, 0, s>>>(A, S, U, E, out);
+    const long long cap = (long long)device_sm_count() * TB_SEG_BLOCKS_PER_SM;
+    launch_pdl(seg_spmv_kernel<UK, SQ, EPI, false>, dim3((int)(want < cap ? want : cap)),
+               dim3(kBlock), 0, s, A, S, U, E, out);
   }
   const int fgrid = (int)((S.nfix * 32 + kBlock - 1) / kBlock);
-  if (fgrid) seg_fixup_kernel<EPI><<<fgrid, kBlock, 0, s>>>(S, E, out);
+  if (fgrid) launch_pdl(seg_fixup_kernel<EPI>, dim3(fgrid), dim3(kBlock), 0, s, S, E, out);
 }
 
 template <int UK, bool SQ>

@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
                                                             double* __restrict__ dvec,
                                                             uint8_t* __restrict__ mask,
                                                             ObjScalars* obj, Scratch sc) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int BLK = STAGED ? kStagedBlock : kBlock;
   constexpr int RPW = kWarp / G;  // rows per warp
   __shared__ double sh[BLK / kWarp + 1];
@@ -159,6 +161,8 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
                                                        const double* __restrict__ dvec,
                                                        const uint8_t* __restrict__ mask,
                                                        double* __restrict__ a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int BLK = STAGED ? kStagedBlock : kBlock;
   constexpr int RPW = kWarp / G;
   extern __shared__ double sv[];
@@ -249,6 +253,14 @@ int grid_for(long long n, int block = 256) {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRON_B200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int device_sm_count() {
   if (g_sm_count == 0) {
     int dev = 0;
@@ -309,25 +321,29 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
         auto k = csr_forward_kernel<GG, kLossLogistic, true>;
         static bool once = (set_smem(k), true);
         (void)once;
-        k<<<grid, kStagedBlock, smem, s>>>(X, hot, w, y, C, z, zhat, dvec, mask, obj, sc);
+        launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, z, zhat, dvec, mask,
+                   obj, sc);
       });
     } else {
       TB_GROUP_DISPATCH(group, {
         auto k = csr_forward_kernel<GG, kLossSvm, true>;
         static bool once = (set_smem(k), true);
         (void)once;
-        k<<<grid, kStagedBlock, smem, s>>>(X, hot, w, y, C, z, zhat, dvec, mask, obj, sc);
+        launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, z, zhat, dvec, mask,
+                   obj, sc);
       });
     }
     return;
   }
   const int grid = forward_grid(X.rows, group);
   if (loss == kLossLogistic) {
-    TB_GROUP_DISPATCH(group, (csr_forward_kernel<GG, kLossLogistic, false><<<grid, kBlock, 0, s>>>(
-                                 X, 0, w, y, C, z, zhat, dvec, mask, obj, sc)));
+    TB_GROUP_DISPATCH(group, launch_pdl(csr_forward_kernel<GG, kLossLogistic, false>, dim3(grid),
+                                        dim3(kBlock), 0, s, X, 0, w, y, C, z, zhat, dvec, mask, obj,
+                                        sc));
   } else {
-    TB_GROUP_DISPATCH(group, (csr_forward_kernel<GG, kLossSvm, false><<<grid, kBlock, 0, s>>>(
-                                 X, 0, w, y, C, z, zhat, dvec, mask, obj, sc)));
+    TB_GROUP_DISPATCH(group, launch_pdl(csr_forward_kernel<GG, kLossSvm, false>, dim3(grid),
+                                        dim3(kBlock), 0, s, X, 0, w, y, C, z, zhat, dvec, mask, obj,
+                                        sc));
   }
 }
 
@@ -339,12 +355,14 @@ void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, co
       auto k = csr_dv_kernel<GG, true>;
       static bool once = (set_smem(k), true);
       (void)once;
-      k<<<device_sm_count(), kStagedBlock, (size_t)hot * 8, s>>>(X, hot, p, dvec, mask, a);
+      launch_pdl(k, dim3(device_sm_count()), dim3(kStagedBlock), (size_t)hot * 8, s, X, hot, p, dvec,
+                 mask, a);
     });
     return;
   }
   const int grid = forward_grid(X.rows, group);
-  TB_GROUP_DISPATCH(group, (csr_dv_kernel<GG, false><<<grid, kBlock, 0, s>>>(X, 0, p, dvec, mask, a)));
+  TB_GROUP_DISPATCH(group, launch_pdl(csr_dv_kernel<GG, false>, dim3(grid), dim3(kBlock), 0, s, X, 0,
+                                      p, dvec, mask, a));
 }
 
 int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s) {

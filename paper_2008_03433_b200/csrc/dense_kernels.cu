@@ -81,6 +81,8 @@ struct Side {
 template <int NMAX, int T, int MODE, int LOSS>
 __global__ void __launch_bounds__(T + kWarp, 1)
     dense_pass_kernel(const __grid_constant__ CUtensorMap xmap, PassArgs a, int nstages) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long full[4], empty[4];
   __shared__ double s_v[NMAX];
@@ -267,7 +269,7 @@ void launch_pass(const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
     configured = smem;
   }
   const int grid = dense_grid(a.l, a.n);
-  k<<<grid, T + kWarp, smem, s>>>(m, a, ns);
+  launch_pdl(k, dim3(grid), dim3(T + kWarp), smem, s, m, a, ns);
 }
 
 template <int NMAX, int T>
@@ -308,6 +310,8 @@ void launch(int mode, int loss, const CUtensorMap& m, const PassArgs& a, cudaStr
 
 __global__ void __launch_bounds__(1024) dense_finalize_kernel(int n, const double* partials,
                                                              int nparts, EpiView E, double* out) {
+  pdl_wait();
+  pdl_trigger();
   // thread t: coordinate j = t % 64, part group t / 64 (16 groups)
   __shared__ double s_part[1024];
   const int j = threadIdx.x & 63, grp = threadIdx.x >> 6;
@@ -517,7 +521,7 @@ void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X,
 
 void dense_finalize(int64_t n, const double* partials, int nparts, const EpiView& epi, double* out,
                     cudaStream_t s) {
-  dense_finalize_kernel<<<1, 1024, 0, s>>>((int)n, partials, nparts, epi, out);
+  launch_pdl(dense_finalize_kernel, dim3(1), dim3(1024), 0, s, (int)n, partials, nparts, epi, out);
 }
 
 void dense_transpose_chunk(const double* rm, int64_t rows, int64_t n, double* X, int64_t ld,

@@ -42,6 +42,8 @@ __device__ __forceinline__ void set_cond(Cond c, int v) {
 __global__ void __launch_bounds__(kBlock) axpy_dot_kernel(long long n, const double* w,
                                                          const double* d, double* wc,
                                                          ObjScalars* obj, Scratch sc) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double acc = 0.0;
   GRID_STRIDE(j, n) {
@@ -59,6 +61,8 @@ __global__ void __launch_bounds__(kBlock) axpy_dot_kernel(long long n, const dou
 
 __global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const double* g,
                                                            ObjScalars* obj, Scratch sc) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double acc = 0.0, bad = 0.0;
   GRID_STRIDE(j, n) {
@@ -83,6 +87,8 @@ __global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const d
 }
 
 __global__ void epilogue_kernel(long long n, const double* raw, EpiView E, double* out) {
+  pdl_wait();
+  pdl_trigger();
   GRID_STRIDE(j, n) {
     const double s = raw ? raw[j] : 0.0;
     out[j] = E.kind == EPI_VEC ? E.base[j] + E.scale * s
@@ -98,6 +104,8 @@ __device__ __forceinline__ double zval(const double* r, const double* M, long lo
 
 __global__ void __launch_bounds__(kBlock) cg_init_kernel(CgVectors v, CgState* st, Scratch sc,
                                                         Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double rz = 0.0, rr = 0.0;
   GRID_STRIDE(j, v.n) {
@@ -141,6 +149,8 @@ __global__ void __launch_bounds__(kBlock) cg_init_kernel(CgVectors v, CgState* s
 
 __global__ void __launch_bounds__(kBlock) cg_php_kernel(CgVectors v, CgState* st, Scratch sc,
                                                        Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double acc = 0.0;
   GRID_STRIDE(j, v.n) acc += v.p[j] * v.hp[j];
@@ -164,6 +174,8 @@ __global__ void __launch_bounds__(kBlock) cg_php_kernel(CgVectors v, CgState* st
 
 __global__ void __launch_bounds__(kBlock) cg_update_kernel(CgVectors v, CgState* st, Scratch sc,
                                                           Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   if (st->fail) return;  // uniform across the grid
   const double alpha = st->alpha;
@@ -213,6 +225,8 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(CgVectors v, CgState*
 
 __global__ void __launch_bounds__(kBlock) cg_direction_kernel(CgVectors v, CgState* st,
                                                              Scratch sc, Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   if (st->fail) return;
   if (!st->boundary) {
@@ -256,6 +270,8 @@ __global__ void __launch_bounds__(kBlock) cg_direction_kernel(CgVectors v, CgSta
 }
 
 __global__ void __launch_bounds__(kBlock) cg_post_kernel(CgVectors v, CgState* st, Scratch sc) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   const bool boundary = st->boundary && !st->fail;
   const double tau = st->tau;
@@ -331,6 +347,8 @@ __device__ __forceinline__ void cluster_sum(double (&v)[K], double* sh, double (
 
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterBlock)
     cg_cluster_step_kernel(CgVectors v, CgState* st, Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kClusterBlock / kWarp + 1];
   __shared__ double slot[4];
   const long long n = v.n;
@@ -483,6 +501,8 @@ __device__ void small_finish(const CgVectors& v, CgState* st, double* sh) {
 
 __global__ void __launch_bounds__(kSmallBlock) cg_small_init_kernel(CgVectors v, CgState* st,
                                                                     Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kSmallBlock / kWarp + 1];
   double rz = 0.0, rr = 0.0;
   for (long long j = threadIdx.x; j < v.n; j += kSmallBlock) {
@@ -518,6 +538,8 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
                                                                     const double* partials,
                                                                     int nparts, double scale,
                                                                     CgState* st, Cond cond) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sh[kSmallBlock / kWarp + 1];
   __shared__ double s_part[kSmallBlock];
   __shared__ int s_flag;
@@ -632,49 +654,52 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
 
 void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjScalars* obj,
                   Scratch sc, cudaStream_t s) {
-  axpy_dot_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, w, d, wc, obj, sc);
+  launch_pdl(axpy_dot_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, w, d, wc, obj, sc);
 }
 
 void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s) {
-  norm_check_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, g, obj, sc);
+  launch_pdl(norm_check_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, g, obj, sc);
 }
 
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {
-  epilogue_kernel<<<vec_grid(n), kBlock, 0, s>>>(n, raw, epi, out);
+  launch_pdl(epilogue_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, raw, epi, out);
 }
 
 void cg_cluster_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s) {
-  cg_cluster_step_kernel<<<kClusterCtas, kClusterBlock, 0, s>>>(v, st, cond);
+  launch_pdl(cg_cluster_step_kernel, dim3(kClusterCtas), dim3(kClusterBlock), 0, s, v, st, cond);
 }
 
 void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  cg_init_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+  launch_pdl(cg_init_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
 }
 void cg_large_php(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  cg_php_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+  launch_pdl(cg_php_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
 }
 void cg_large_update(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  cg_update_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+  launch_pdl(cg_update_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
 }
 void cg_large_direction(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  cg_direction_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc, cond);
+  launch_pdl(cg_direction_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
 }
 void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s) {
-  cg_post_kernel<<<vec_grid(v.n), kBlock, 0, s>>>(v, st, sc);
+  launch_pdl(cg_post_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc);
 }
 
 void cg_small_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s) {
-  cg_small_init_kernel<<<1, kSmallBlock, 0, s>>>(v, st, cond);
+  launch_pdl(cg_small_init_kernel, dim3(1), dim3(kSmallBlock), 0, s, v, st, cond);
 }
 
 void cg_small_step(const CgVectors& v, const double* partials, int nparts, double scale,
                    CgState* st, Cond cond, cudaStream_t s) {
   if (v.n <= 32)
-    cg_small_step_kernel<16><<<1, kSmallBlock, 0, s>>>(v, partials, nparts, scale, st, cond);
+    launch_pdl(cg_small_step_kernel<16>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
+               st, cond);
   else if (v.n <= 64)
-    cg_small_step_kernel<8><<<1, kSmallBlock, 0, s>>>(v, partials, nparts, scale, st, cond);
+    launch_pdl(cg_small_step_kernel<8>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
+               st, cond);
   else
-    cg_small_step_kernel<1><<<1, kSmallBlock, 0, s>>>(v, partials, nparts, scale, st, cond);
+    launch_pdl(cg_small_step_kernel<1>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
+               st, cond);
 }
 
 }  // namespace tb
