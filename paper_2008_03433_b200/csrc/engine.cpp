@@ -77,11 +77,19 @@ int nccl_unique_id(void* out128) {
 void Comm::init(int rank_, int world_, const void* unique_id, int device) {
   rank = rank_;
   world = world_;
-  if (world <= 1) return;
-  if (!unique_id) raise(TRON_ERR_ARGUMENT, "world > 1 requires an nccl_unique_id");
+  // TRON_B200_FORCE_NCCL=1 runs a single-rank problem through the sharded code
+  // path with a real one-rank NCCL communicator (tests the multi-GPU plumbing
+  // on one GPU: partials, allreduce on the stream, host-driven CG).
+  const char* fe = std::getenv("TRON_B200_FORCE_NCCL");
+  forced = world == 1 && fe && fe[0] == '1';
+  if (world <= 1 && !forced) return;
+  if (!unique_id && world > 1) raise(TRON_ERR_ARGUMENT, "world > 1 requires an nccl_unique_id");
   if (!g_nccl.load()) raise(TRON_ERR_NCCL, "libnccl.so.2 not loadable");
   ncclUniqueId id;
-  std::memcpy(&id, unique_id, sizeof(id));
+  if (unique_id)
+    std::memcpy(&id, unique_id, sizeof(id));
+  else
+    nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   ncclComm_t c;
   nccl_check(g_nccl.CommInitRank(&c, world, id, rank), "ncclCommInitRank");
@@ -93,7 +101,7 @@ Comm::~Comm() {
 }
 
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
-  if (world <= 1 || count == 0) return;
+  if (!active() || count == 0) return;
   nccl_check(g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)comm_, s),
              "ncclAllReduce");
 }
@@ -167,7 +175,19 @@ void validate_csr(uint64_t l, uint64_t n, const int64_t* ro, const int32_t* ci) 
   const uint64_t dec = first_bad(l, [&](uint64_t i) { return ro[i] > ro[i + 1]; });
   const uint64_t lim = dec == UINT64_MAX ? l : dec;
   const uint64_t per_row = l > 0 ? std::max<uint64_t>(1, (uint64_t)ro[l] / l) : 1;
-  const uint64_t bad = first_bad(lim, [&](uint64_t i) { return check_row(i, false); },
+  // screening predicate, branch-free and vectorisable: a row is valid iff its
+  // columns ascend strictly and its first / last column lie in [0, n)
+  auto row_bad = [&](uint64_t i) {
+    const int64_t b = ro[i], e = ro[i + 1];
+    if (e <= b) return false;
+    const int32_t* c = ci + b;
+    const int64_t len = e - b;
+    if (c[0] < 0 || static_cast<uint64_t>(c[len - 1]) >= n) return true;
+    int viol = 0;
+    for (int64_t k = 1; k < len; ++k) viol |= c[k] <= c[k - 1];
+    return viol != 0;
+  };
+  const uint64_t bad = first_bad(lim, row_bad,
                                  std::max<size_t>(1, (size_t{1} << 16) / per_row));
   if (bad != UINT64_MAX) check_row(bad, true);
   if (dec != UINT64_MAX) check_row(dec, true);

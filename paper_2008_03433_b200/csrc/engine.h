@@ -73,7 +73,8 @@ class Comm {
   void init(int rank, int world, const void* unique_id, int device);
   ~Comm();
   void allreduce_sum(double* buf, size_t count, cudaStream_t s);
-  bool active() const { return world > 1; }
+  bool active() const { return world > 1 || forced; }
+  bool forced = false;  // one-rank communicator forced on (TRON_B200_FORCE_NCCL=1)
 
  private:
   void* comm_ = nullptr;

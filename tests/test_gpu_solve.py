@@ -212,3 +212,33 @@ def test_host_cg_ledger_schedule():  # test_backend.cpp:152-184 (staged semantic
     assert pl.ledger.margin_passes == r.trace.objective_evaluations
     assert pl.ledger.bulk_handoffs == r.trace.accepted_steps + 1
     assert any(not it.accepted for it in r.trace.iterations)
+
+
+# The sharded (multi-GPU) code path on one GPU: a real one-rank NCCL
+# communicator (TRON_B200_FORCE_NCCL=1) routes every partial through
+# ncclAllReduce on the solver stream, the epilogues through the raw + vector
+# epilogue kernels and CG through the host-driven loop.  Against the
+# host-driven single-GPU path (same kernels, same order) it must be
+# bit-identical; against the reference, within tolerance.  (The graph path
+# finishes the dense Hv partials in another order; on SYNTH dense SVM the
+# third CG run is chaotic in the last bit -- the reference itself goes
+# [4, 9, 23] -> [4, 9, 19] -> [4, 9, 18] CG steps for C -> C(1+ulp) -> C(1+2ulp).)
+@pytest.mark.parametrize("case", ["sparse_lr", "dense_svm", "dense_lr"])
+def test_sharded_path_single_rank_nccl(ref, monkeypatch, case):
+    p, loss = {
+        "sparse_lr": (synth.synth_sparse(9, 2000, 5000, 37), LossKind.Logistic),
+        "dense_svm": (synth.testgen_dense_problem(3001, 200, 20, 1.0), LossKind.L2Svm),
+        "dense_lr": (synth.testgen_dense_problem(2001, 200, 20, 1.0), LossKind.Logistic),
+    }[case]
+    cfg = TrustRegionConfig(eps=0.01)
+    monkeypatch.setenv("TRON_B200_NO_GRAPH", "1")
+    base = solve(p, loss, cfg, ExecutionPlan.gpu())
+    monkeypatch.delenv("TRON_B200_NO_GRAPH")
+    monkeypatch.setenv("TRON_B200_FORCE_NCCL", "1")
+    got = solve(p, loss, cfg, ExecutionPlan.gpu())
+    assert got.objective == base.objective
+    assert np.array_equal(got.w, base.w)
+    assert [it.cg_iters for it in got.trace.iterations] == [it.cg_iters for it in base.trace.iterations]
+    w_ref, t_ref = ref.solve(p, 0 if loss == LossKind.Logistic else 1, cfg)
+    assert rel_err(got.objective, t_ref["objective"]) <= 1e-6
+    assert rel_err(got.w, w_ref) <= 1e-6
