@@ -276,7 +276,11 @@ void Engine::common_alloc() {
   // TRON_B200_NO_GRAPH=1 runs the CG loop host-driven (per-kernel profiling:
   // ncu cannot profile kernel nodes of graphs with conditional nodes).
   const char* ng = std::getenv("TRON_B200_NO_GRAPH");
-  use_graphs_ = !comm_.active() && !(ng && ng[0] == '1');
+  // Sharded: the NCCL allreduces are captured inside the CG while-graph (every
+  // rank's CG state is identical, so every rank runs the same number of
+  // allreduces); TRON_B200_NCCL_GRAPH=0 selects the host-driven CG loop.
+  const char* cg = std::getenv("TRON_B200_NCCL_GRAPH");
+  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !(ng && ng[0] == '1');
 }
 
 std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, const int64_t* ro,

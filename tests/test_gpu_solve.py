@@ -235,7 +235,12 @@ def test_sharded_path_single_rank_nccl(ref, monkeypatch, case):
     base = solve(p, loss, cfg, ExecutionPlan.gpu())
     monkeypatch.delenv("TRON_B200_NO_GRAPH")
     monkeypatch.setenv("TRON_B200_FORCE_NCCL", "1")
+    monkeypatch.setenv("TRON_B200_NCCL_GRAPH", "0")  # host-driven CG loop
     got = solve(p, loss, cfg, ExecutionPlan.gpu())
+    monkeypatch.setenv("TRON_B200_NCCL_GRAPH", "1")  # allreduces inside the CG graph
+    in_graph = solve(p, loss, cfg, ExecutionPlan.gpu())
+    assert [it.cg_iters for it in in_graph.trace.iterations] == [it.cg_iters for it in base.trace.iterations]
+    assert rel_err(in_graph.w, base.w) <= 1e-12
     assert got.objective == base.objective
     assert np.array_equal(got.w, base.w)
     assert [it.cg_iters for it in got.trace.iterations] == [it.cg_iters for it in base.trace.iterations]
