@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kBlock = 256;         // 8 warps = 8 chunks per block
 constexpr int kStagedBlock = 512;   // one 16-warp block per SM holding u in shared memory
-constexpr long long kStageMaxBytes = 200 * 1024;
+constexpr long long kStageMaxBytes = 190 * 1024;  // + 32 KB of static emission buffers
 
 __device__ __forceinline__ void ld2(const double* p, double& a, double& b) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
@@ -131,7 +131,7 @@ template <int UK, bool SQ, int EPI, bool STAGED>
 __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const UView& U,
                                               const EpiView& E, double* __restrict__ out,
                                               const double* su, long long t, const LaneChunk& cur,
-                                              int lane) {
+                                              int lane, double* ebuf) {
   // gathers of the current chunk
   double w[kSegLaneItems];
 #pragma unroll
@@ -169,10 +169,11 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
   }
   const int r0 = chunk_rank + incl - cnt;
 
-  // sequential pass over the lane's items
+  // sequential pass over the lane's items; the sums of the columns ending
+  // here go to the warp's buffer, indexed by their order in the chunk
   double acc = 0.0, head_val = 0.0;
   bool have_head = false;
-  int r = r0;
+  int k = incl - cnt;
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; ++m) {
     acc += w[m];
@@ -181,9 +182,9 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
         head_val = acc;
         have_head = true;
       } else {
-        emit_rank<EPI>(S, E, out, r, acc);  // column wholly inside this lane
+        ebuf[k] = acc;  // column wholly inside this lane
       }
-      ++r;
+      ++k;
       acc = 0.0;
     }
   }
@@ -199,14 +200,21 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
   }
   const int prev_key = __shfl_up_sync(0xffffffffu, key, 1);
   const double prev_val = __shfl_up_sync(0xffffffffu, val, 1);
-  if (have_head) {
-    const double tot = (lane > 0 && prev_key == r0) ? prev_val + head_val : head_val;
-    if (r0 == chunk_rank && cont_in)
-      S.head[t] = tot;  // column began in an earlier chunk: finished by the fix-up
-    else
-      emit_rank<EPI>(S, E, out, r0, tot);
-  }
+  if (have_head) ebuf[incl - cnt] = (lane > 0 && prev_key == r0) ? prev_val + head_val : head_val;
   if (lane == 31) S.carry[t] = val;
+  // emission, warp-cooperative: consecutive columns to consecutive lanes, so
+  // the nz_col / base loads and the stores of a chunk are coalesced and no
+  // lane walks a chain of dependent loads
+  __syncwarp();
+  const int nend = __shfl_sync(0xffffffffu, incl, 31);
+  for (int q = lane; q < nend; q += 32) {
+    const double v = ebuf[q];
+    if (q == 0 && cont_in)
+      S.head[t] = v;  // column began in an earlier chunk: finished by the fix-up
+    else
+      emit_rank<EPI>(S, E, out, chunk_rank + q, v);
+  }
+  __syncwarp();  // the buffer is reused by the warp's next chunk
 
 }
 
@@ -222,13 +230,18 @@ template <int UK, bool SQ, int EPI, bool STAGED>
 #ifndef TB_SEG_BLOCKS_PER_SM
 #define TB_SEG_BLOCKS_PER_SM 3
 #endif
+#ifndef TB_SEG_PREFETCH2
+#define TB_SEG_PREFETCH2 0
+#endif
 __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : TB_SEG_BLOCKS_PER_SM)
     seg_spmv_kernel(CsrView A, SegView S, UView U, EpiView E, double* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double su[];
   constexpr int BLK = STAGED ? kStagedBlock : kBlock;
+  __shared__ double ebuf_all[BLK / kWarp][kSegChunk];
   const int lane = threadIdx.x & 31;
+  double* ebuf = ebuf_all[threadIdx.x >> 5];
   if (STAGED) {
     if (UK == U_VEC) {
       bulk_stage_f64(su, U.u, A.cols);  // TMA bulk copy (UBLKCP)
@@ -248,14 +261,14 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : T
 
   LaneChunk cur;
   load_chunk(A, S, t, lane, cur);
-  if (!STAGED) {
+  if (!STAGED && !TB_SEG_PREFETCH2) {
     // one chunk ahead: the next chunk's operands are requested before this
     // chunk's gathers are consumed
     for (;;) {
       const long long tn = t + W;
       LaneChunk nxt;
       if (tn < S.nchunks) load_chunk(A, S, tn, lane, nxt);
-      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane);
+      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane, ebuf);
       if (tn >= S.nchunks) break;
       t = tn;
       cur = nxt;
@@ -266,10 +279,10 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : T
     LaneChunk nxt;
     if (t + W < S.nchunks) load_chunk(A, S, t + W, lane, nxt);
     for (;;) {
-      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane);
+      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane, ebuf);
       if (t + W >= S.nchunks) break;
       if (t + 2 * W < S.nchunks) load_chunk(A, S, t + 2 * W, lane, cur);
-      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t + W, nxt, lane);
+      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t + W, nxt, lane, ebuf);
       if (t + 2 * W >= S.nchunks) break;
       if (t + 3 * W < S.nchunks) load_chunk(A, S, t + 3 * W, lane, nxt);
       t += 2 * W;
