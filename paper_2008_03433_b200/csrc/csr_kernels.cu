@@ -243,6 +243,32 @@ __global__ void narrow_kernel(const int64_t* in, int32_t* out, long long n) {
     out[i] = (int32_t)in[i];
 }
 
+// Input screening on the device (the host re-checks the first offending row
+// sequentially to report the reference's exact error): one warp per row,
+// valid iff the columns ascend strictly within [0, n).
+__global__ void csr_screen_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                  long long rows, long long n, unsigned long long* first_bad) {
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = gw; r < rows; r += nw) {
+    const int b = ptr[r], e = ptr[r + 1];
+    bool bad = false;
+    for (int k = b + lane; k < e; k += 32) {
+      const int c = idx[k];
+      bad |= c < 0 || c >= n || (k > b && c <= idx[k - 1]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(first_bad, (unsigned long long)r);
+  }
+}
+
+__global__ void labels_screen_kernel(const double* __restrict__ y, long long l,
+                                     unsigned long long* first_bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < l;
+       i += (long long)gridDim.x * blockDim.x)
+    if (y[i] != 1.0 && y[i] != -1.0) atomicMin(first_bad, (unsigned long long)i);
+}
+
 int grid_for(long long n, int block = 256) {
   long long g = (n + block - 1) / block;
   long long cap = (long long)device_sm_count() * 16;
@@ -402,6 +428,14 @@ int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cuda
   if (temp) cudaFreeAsync(temp, s);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+void screen_inputs(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n,
+                   const double* y, int64_t l, unsigned long long* first_bad2, cudaStream_t s) {
+  cudaMemsetAsync(first_bad2, 0xff, 2 * sizeof(unsigned long long), s);
+  if (ptr && rows > 0)
+    csr_screen_kernel<<<grid_for(rows * 32), 256, 0, s>>>(ptr, idx, rows, n, first_bad2);
+  if (l > 0) labels_screen_kernel<<<grid_for(l), 256, 0, s>>>(y, l, first_bad2 + 1);
 }
 
 void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s) {

@@ -291,8 +291,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
   check_options(loss, opt);
   if (!ro || !y || (l > 0 && ro[l] > 0 && (!ci || !vals)))
     raise(TRON_ERR_ARGUMENT, "null problem array");
-  // offsets first (they size the device arrays); the O(nnz) column checks and
-  // the labels run on the worker pool while the uploads are in flight
+  // offsets first (they size the device arrays and bound the device screening)
   validate_offsets(l, ro);
   const int64_t nnz = ro[l];
   if (nnz >= (int64_t{1} << 31) || n >= (uint64_t{1} << 31) || l >= (uint64_t{1} << 31))
@@ -303,11 +302,6 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     raise(TRON_ERR_STRATEGY,
           "gathered L2-SVM strategy needs dense features on the GPU backend; use Indirect "
           "(masked CSR/CSC traversal)");
-  // column + label checks run on the worker pool while the uploads are in flight
-  auto valid = std::async(std::launch::async, [&] {
-    validate_csr(l, n, ro, ci);
-    validate_labels_C(l, y, C);
-  });
   try {
     std::unique_ptr<Engine> e(new Engine());
     e->loss_ = loss;
@@ -344,8 +338,15 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       if (l > 0) upload(e->y_.p, y, l * sizeof(double), s);
     }
     tr.mark("matrix alloc + H2D issue");
-    valid.get();
-    tr.mark("host validation (overlapped)");
+    // O(nnz) column checks and the labels on the device; the host re-checks
+    // the first offending row to raise the reference's exact error
+    e->screen(e->rptr_.p, e->cidx_.p, (int64_t)l, (int64_t)n,
+              [&](uint64_t bad_row, uint64_t bad_label) {
+                if (bad_row != UINT64_MAX) validate_csr(l, n, ro, ci);  // raises the exact error
+                if (bad_label != UINT64_MAX) validate_labels_C(l, y, C);
+              });
+    if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");  // loss.cpp:30
+    tr.mark("device validation");
     e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
     const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
     if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
@@ -384,9 +385,13 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     cuda_check(cudaStreamSynchronize(s), "csc build");
     cuda_check(cudaGetLastError(), "csc build");
     return e;
-  } catch (...) {
-    // an input error outranks a device error met while it was being checked
-    if (valid.valid()) valid.get();
+  } catch (const StatusError& err) {
+    // no usable device: the inputs are still checked, and an input error
+    // outranks the device error (the reference has no device to fail)
+    if (err.status == TRON_ERR_CUDA || err.status == TRON_ERR_OOM) {
+      validate_csr(l, n, ro, ci);
+      validate_labels_C(l, y, C);
+    }
     throw;
   }
 }
@@ -398,7 +403,6 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   PhaseTrace tr("create_dense");
   check_options(loss, opt);
   if (!y || (l * n > 0 && !row_major)) raise(TRON_ERR_ARGUMENT, "null problem array");
-  if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");
   if (n > (uint64_t)kDenseMaxN) {
     // Wide dense problems run through the sparse kernels (explicit entries).
     if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
@@ -424,7 +428,6 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
   e->ld_ = dense_ld((int64_t)l);
   // labels are checked on the worker pool while the matrix streams in
-  auto labels_ok = std::async(std::launch::async, [&] { validate_labels_C(l, y, C); });
   try {
     e->common_alloc();
     cudaStream_t s = e->s_;
@@ -463,10 +466,13 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       cudaEventDestroy(ev[1]);
     }
     tr.mark("matrix alloc + H2D + transpose");
-    labels_ok.get();  // rethrows a label error found while the matrix was in flight
-    tr.mark("host validation (overlapped)");
-  } catch (...) {
-    if (labels_ok.valid()) labels_ok.get();  // an input error outranks a device error
+    e->screen(nullptr, nullptr, 0, (int64_t)n, [&](uint64_t, uint64_t bad_label) {
+      if (bad_label != UINT64_MAX) validate_labels_C(l, y, C);  // raises the exact error
+    });
+    if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");  // loss.cpp:30
+    tr.mark("device validation");
+  } catch (const StatusError& err) {
+    if (err.status == TRON_ERR_CUDA || err.status == TRON_ERR_OOM) validate_labels_C(l, y, C);
     throw;
   }
   if (dense_make_map(&e->xmap_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n) != 0)
@@ -490,6 +496,19 @@ Engine::~Engine() {
   pinned_block_put(obj_h_);
   pinned_block_put(st_h_);
   // DevBuf members queue their frees on s_; stream_owner_ then syncs + destroys it
+}
+
+// Device screening of the uploaded inputs (screen_inputs); on a hit, report()
+// re-runs the host check that raises the exact error.
+template <class Report>
+void Engine::screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n, Report report) {
+  DevBuf<unsigned long long> flags;
+  flags.alloc(2);
+  screen_inputs(ptr, idx, rows, n, y_.p, l_, flags.p, s_);
+  unsigned long long h[2];
+  cuda_check(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, s_), "D2H");
+  synchronize();
+  if (h[0] != ~0ull || h[1] != ~0ull) report((uint64_t)h[0], (uint64_t)h[1]);
 }
 
 void Engine::build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64_t nnz,

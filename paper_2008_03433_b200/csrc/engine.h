@@ -165,6 +165,8 @@ class Engine {
   void read_obj();
   void read_cg(CgState* out);
   void build_graph(int slot, bool use_m);
+  template <class Report>
+  void screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n, Report report);
   void build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64_t nnz,
                     const int32_t* idx, const double* val);
   void count_launch(uint64_t k) { launches += k; }

@@ -163,6 +163,11 @@ void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squar
 // Device CSC construction from device CSR (stable in row order).
 // Returns 0 on success; temp storage allocated internally.
 int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s);
+// Input screening: first_bad2[0] = first row whose columns are not strictly
+// ascending within [0, n) (ptr may be null: no matrix check), first_bad2[1] =
+// first label not in {-1, +1}; ~0 when none.  Offsets must already be valid.
+void screen_inputs(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n,
+                   const double* y, int64_t l, unsigned long long* first_bad2, cudaStream_t s);
 // Row-offset narrowing int64 -> int32 (device).
 void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s);
 
