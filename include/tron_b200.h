@@ -35,7 +35,9 @@ typedef enum {
   TRON_ERR_CUDA = 7,
   TRON_ERR_NCCL = 8,
   TRON_ERR_OOM = 9,
-  TRON_ERR_ARGUMENT = 10
+  TRON_ERR_ARGUMENT = 10,
+  TRON_ERR_PARSE = 11,             /* ParseError (error.hpp:28-38) */
+  TRON_ERR_UNSUPPORTED_LABEL = 12  /* UnsupportedLabelError (error.hpp:40-43) */
 } tron_status;
 
 typedef enum { TRON_LOSS_LOGISTIC = 0, TRON_LOSS_L2SVM = 1 } tron_loss; /* loss.hpp:11 */
@@ -164,6 +166,20 @@ int tron_gpu_synchronize(tron_gpu_ctx *ctx);
 
 /* ncclGetUniqueId via the lazily loaded NCCL (128 bytes). */
 int tron_gpu_nccl_unique_id(void *out128);
+
+/* ---- LIBSVM ingestion (io.cpp:54-132, parse_libsvm) ----
+ * A parallel host parser with the reference's exact semantics and error
+ * messages; the arrays feed tron_gpu_create_csr.  On a parse error the status
+ * is TRON_ERR_PARSE / TRON_ERR_UNSUPPORTED_LABEL, tron_gpu_last_error() holds
+ * "line N: ..." and tron_gpu_last_error_line() the 1-based line (0: none). */
+typedef struct tron_parsed tron_parsed;
+int tron_parse_libsvm(const char *text, uint64_t len, uint64_t n_override, tron_parsed **out);
+int tron_parse_libsvm_file(const char *path, uint64_t n_override, tron_parsed **out);
+int tron_parsed_sizes(const tron_parsed *p, uint64_t *rows, uint64_t *cols, uint64_t *nnz);
+int tron_parsed_copy(const tron_parsed *p, int64_t *row_offsets, int32_t *col_indices,
+                     double *values, double *y);
+void tron_parsed_free(tron_parsed *p);
+uint64_t tron_gpu_last_error_line(void);
 
 /* ---- deterministic synthetic inputs (host-side tooling) ---- */
 void tron_testgen_dense_problem(uint64_t seed, size_t l, size_t n, double flip, double *values,

@@ -260,6 +260,37 @@ class Reference:
                            ctypes.byref(info), tr, cap)
         return w, _trace(info, tr, cap)
 
+    def parse_libsvm(self, text: bytes, n_override=0):
+        """The reference's parse_libsvm (io.cpp:54-132) on an in-memory text:
+        ('ok', (ro, ci, vals, y, n)) or (kind, (message, line)), kind in
+        'parse' / 'label' / 'other'."""
+        L = self.lib
+        if not getattr(self, "_parse_bound", False):
+            L.ref_parse_libsvm.argtypes = [ctypes.c_char_p, c_size_t, c_size_t,
+                                           ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p, c_size_t,
+                                           POINTER(c_size_t)]
+            L.ref_parsed_sizes.argtypes = [ctypes.c_void_p, POINTER(c_size_t), POINTER(c_size_t),
+                                           POINTER(c_size_t)]
+            L.ref_parsed_copy.argtypes = [ctypes.c_void_p, PI64, PI32, PD, PD]
+            L.ref_parsed_free.argtypes = [ctypes.c_void_p]
+            self._parse_bound = True
+        h = ctypes.c_void_p()
+        msg = ctypes.create_string_buffer(512)
+        line = c_size_t()
+        rc = L.ref_parse_libsvm(text, len(text), n_override, ctypes.byref(h), msg, 512,
+                                ctypes.byref(line))
+        if rc != 0:
+            return {1: "parse", 2: "label"}.get(rc, "other"), (msg.value.decode(), line.value)
+        r, c, z = c_size_t(), c_size_t(), c_size_t()
+        L.ref_parsed_sizes(h, ctypes.byref(r), ctypes.byref(c), ctypes.byref(z))
+        ro = np.empty(r.value + 1, dtype=np.int64)
+        ci = np.empty(z.value, dtype=np.int32)
+        vals = np.empty(z.value)
+        y = np.empty(r.value)
+        L.ref_parsed_copy(h, _p(ro, PI64), _p(ci, PI32), _p(vals), _p(y))
+        L.ref_parsed_free(h)
+        return "ok", (ro, ci, vals, y, c.value)
+
     def time_calls(self, problem, loss, workers, reps=1):
         """Per-call ms of the reference evaluator (fun, grad, Hv) at w = 0, parallel(workers)."""
         args, keep = self._args(problem)

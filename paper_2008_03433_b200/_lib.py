@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libtron_b200.so")
 
 # tron_status
 OK, ERR_DIMENSION, ERR_BOUNDS, ERR_STRATEGY, ERR_BUDGET, ERR_NUMERICAL, ERR_LOGIC, ERR_CUDA, \
-    ERR_NCCL, ERR_OOM, ERR_ARGUMENT = range(11)
+    ERR_NCCL, ERR_OOM, ERR_ARGUMENT, ERR_PARSE, ERR_UNSUPPORTED_LABEL = range(13)
 LOSS_LOGISTIC, LOSS_L2SVM = 0, 1
 SVM_GATHERED, SVM_INDIRECT = 0, 1
 SOLVE_DEVICE, SOLVE_HOST_CG = 0, 1
@@ -101,6 +101,13 @@ SIGNATURES = [
                                   PI32, PD, PD]),
     ("tron_synth_dense", c_int, [c_uint64, c_size_t, c_size_t, c_double, c_double, c_double, PD,
                                  PD]),
+    ("tron_parse_libsvm", c_int, [ctypes.c_char_p, c_uint64, c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    ("tron_parse_libsvm_file", c_int, [ctypes.c_char_p, c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    ("tron_parsed_sizes", c_int, [ctypes.c_void_p, ctypes.POINTER(c_uint64), ctypes.POINTER(c_uint64),
+                                  ctypes.POINTER(c_uint64)]),
+    ("tron_parsed_copy", c_int, [ctypes.c_void_p, PI64, PI32, PD, PD]),
+    ("tron_parsed_free", None, [ctypes.c_void_p]),
+    ("tron_gpu_last_error_line", c_uint64, []),
 ]
 
 

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "engine.h"
+#include "ingest.h"
 #include "tron_b200.h"
 #include "tron_b200.hpp"
 
@@ -14,12 +15,18 @@ struct tron_gpu_ctx {
   std::unique_ptr<tb::Engine> engine;
 };
 
+struct tron_parsed {
+  tb::ParsedProblem p;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
+thread_local uint64_t g_last_error_line = 0;
 
 int fail(int status, const std::string& msg) {
   g_last_error = msg;
+  g_last_error_line = 0;
   return status;
 }
 
@@ -31,6 +38,10 @@ int guarded(F&& fn) {
     return TRON_OK;
   } catch (const tb::StatusError& e) {
     return fail(e.status, e.what());
+  } catch (const tb::ParseFailure& e) {
+    const int st = fail(e.status, e.what());
+    g_last_error_line = e.line;
+    return st;
   } catch (const tron_b200::NumericalFailureError& e) {
     return fail(TRON_ERR_NUMERICAL, e.what());
   } catch (const tron_b200::BudgetExceededError& e) {
@@ -156,6 +167,48 @@ void tron_gpu_default_options(tron_gpu_options* o) {
 }
 
 const char* tron_gpu_last_error(void) { return g_last_error.c_str(); }
+uint64_t tron_gpu_last_error_line(void) { return g_last_error_line; }
+
+int tron_parse_libsvm(const char* text, uint64_t len, uint64_t n_override, tron_parsed** out) {
+  if (!out || (!text && len > 0)) return fail(TRON_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<tron_parsed>();
+    h->p = tb::parse_libsvm_buffer(text ? text : "", len, n_override);
+    *out = h.release();
+  });
+}
+
+int tron_parse_libsvm_file(const char* path, uint64_t n_override, tron_parsed** out) {
+  if (!out || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<tron_parsed>();
+    h->p = tb::parse_libsvm_file(path, n_override);
+    *out = h.release();
+  });
+}
+
+int tron_parsed_sizes(const tron_parsed* p, uint64_t* rows, uint64_t* cols, uint64_t* nnz) {
+  if (!p) return fail(TRON_ERR_ARGUMENT, "null parse handle");
+  if (rows) *rows = p->p.y.size();
+  if (cols) *cols = p->p.cols;
+  if (nnz) *nnz = p->p.values.size();
+  return TRON_OK;
+}
+
+int tron_parsed_copy(const tron_parsed* p, int64_t* row_offsets, int32_t* col_indices,
+                     double* values, double* y) {
+  if (!p) return fail(TRON_ERR_ARGUMENT, "null parse handle");
+  const auto& q = p->p;
+  if (row_offsets) std::memcpy(row_offsets, q.row_offsets.data(), q.row_offsets.size() * 8);
+  if (col_indices) std::memcpy(col_indices, q.col_indices.data(), q.col_indices.size() * 4);
+  if (values) std::memcpy(values, q.values.data(), q.values.size() * 8);
+  if (y) std::memcpy(y, q.y.data(), q.y.size() * 8);
+  return TRON_OK;
+}
+
+void tron_parsed_free(tron_parsed* p) { delete p; }
 
 int tron_gpu_device_count(int* count) {
   int c = 0;
