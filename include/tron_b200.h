@@ -164,6 +164,11 @@ int tron_gpu_launch_count(tron_gpu_ctx *ctx, uint64_t *count);
 /* Stream synchronize (for timing harnesses). */
 int tron_gpu_synchronize(tron_gpu_ctx *ctx);
 
+/* Page-locked host memory from a process-wide pool (recycled on free): a
+ * result buffer here (e.g. tron_gpu_solve's w_out) is filled by a plain DMA. */
+void *tron_host_alloc(uint64_t bytes);
+void tron_host_free(void *p);
+
 /* ncclGetUniqueId via the lazily loaded NCCL (128 bytes). */
 int tron_gpu_nccl_unique_id(void *out128);
 

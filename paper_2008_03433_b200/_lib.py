@@ -8,6 +8,9 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
+
+import numpy as np
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -108,6 +111,8 @@ SIGNATURES = [
     ("tron_parsed_copy", c_int, [ctypes.c_void_p, PI64, PI32, PD, PD]),
     ("tron_parsed_free", None, [ctypes.c_void_p]),
     ("tron_gpu_last_error_line", c_uint64, []),
+    ("tron_host_alloc", c_void_p, [c_uint64]),
+    ("tron_host_free", None, [c_void_p]),
 ]
 
 
@@ -125,6 +130,21 @@ def _load():
 
 
 lib = _load()
+
+
+def pinned_array(n: int, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked memory from the library's pool (returned to
+    the pool when the array is garbage collected); device results land in it
+    with a plain DMA."""
+    dt = np.dtype(dtype)
+    nbytes = max(int(n) * dt.itemsize, 1)
+    ptr = lib.tron_host_alloc(nbytes)
+    if not ptr:
+        raise MemoryError(last_error())
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    arr = np.frombuffer(buf, dtype=dt, count=int(n))
+    weakref.finalize(buf, lib.tron_host_free, ptr)
+    return arr
 
 
 def last_error() -> str:

@@ -210,6 +210,17 @@ int tron_parsed_copy(const tron_parsed* p, int64_t* row_offsets, int32_t* col_in
 
 void tron_parsed_free(tron_parsed* p) { delete p; }
 
+void* tron_host_alloc(uint64_t bytes) {
+  try {
+    return tb::pinned_pool_get((size_t)bytes);
+  } catch (const std::exception& e) {
+    fail(TRON_ERR_OOM, e.what());
+    return nullptr;
+  }
+}
+
+void tron_host_free(void* p) { tb::pinned_pool_put(p); }
+
 int tron_gpu_device_count(int* count) {
   int c = 0;
   cudaError_t e = cudaGetDeviceCount(&c);

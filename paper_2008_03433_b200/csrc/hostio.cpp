@@ -69,6 +69,44 @@ void pinned_block_put(void* p) {
 }
 
 // ---------------------------------------------------------------------------
+// pinned buffer pool
+// ---------------------------------------------------------------------------
+namespace {
+std::mutex g_pool_mu;
+std::vector<std::pair<size_t, void*>> g_pool_free;   // (capacity, pointer)
+std::vector<std::pair<void*, size_t>> g_pool_live;   // pointer -> capacity
+}  // namespace
+
+void* pinned_pool_get(size_t bytes) {
+  const size_t cap = ((bytes + (1u << 20) - 1) >> 20 << 20) + (1u << 20) * (bytes == 0);
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  for (size_t k = 0; k < g_pool_free.size(); ++k) {
+    if (g_pool_free[k].first == cap) {
+      void* p = g_pool_free[k].second;
+      g_pool_free.erase(g_pool_free.begin() + k);
+      g_pool_live.emplace_back(p, cap);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cuda_check(cudaMallocHost(&p, cap), "cudaMallocHost");
+  g_pool_live.emplace_back(p, cap);
+  return p;
+}
+
+void pinned_pool_put(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  for (size_t k = 0; k < g_pool_live.size(); ++k) {
+    if (g_pool_live[k].first == p) {
+      g_pool_free.emplace_back(g_pool_live[k].second, p);
+      g_pool_live.erase(g_pool_live.begin() + k);
+      return;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // worker pool
 // ---------------------------------------------------------------------------
 namespace {

@@ -30,6 +30,12 @@ struct AllocScope {
 void* pinned_block_get();
 void pinned_block_put(void* p);
 
+// Page-locked host buffers from a process-wide pool (size classes of 1 MB),
+// handed to callers that receive large results (so the copy back is a plain
+// DMA) and recycled when released.
+void* pinned_pool_get(size_t bytes);
+void pinned_pool_put(void* p);
+
 // Runs fn(begin, end) over [0, count) split into contiguous ranges on the
 // worker pool (at most `max_parts` ranges; the caller's thread takes one).
 void parallel_for(size_t count, size_t min_grain,

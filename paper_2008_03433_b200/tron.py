@@ -426,7 +426,7 @@ class GpuEvaluator:
     def solve(self, cfg: TrustRegionConfig, warm_start=None, mode: Optional[str] = None) -> SolveResult:
         mode = mode or self.plan.solve_mode
         c = cfg.to_c(_lib.SOLVE_HOST_CG if mode == "host_cg" else _lib.SOLVE_DEVICE)
-        w = np.zeros(self.n)
+        w = _lib.pinned_array(self.n)  # page-locked: the result comes back by one DMA
         w0 = None
         if warm_start is not None:
             w0 = _f64(warm_start)
