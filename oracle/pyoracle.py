@@ -260,6 +260,26 @@ class Reference:
                            ctypes.byref(info), tr, cap)
         return w, _trace(info, tr, cap)
 
+    def solve_with_gpu_evaluator(self, lib_path, problem, loss, cfg=None, cap=4096, **over):
+        """The reference's own tron::solve driving a LossEvaluator that forwards
+        every call to the B200 C ABI (INTEGRATION.md's binding), in this process."""
+        L = self.lib
+        L.ref_solve_with_gpu_evaluator.argtypes = [
+            ctypes.c_char_p, c_int, c_size_t, c_size_t, PI64, PI32, PD, PD, c_double, c_int,
+            POINTER(or_config), PD, POINTER(or_solve_info), POINTER(or_iteration), c_size_t,
+            ctypes.c_char_p, c_size_t]
+        args, keep = self._args(problem)
+        c = make_config(cfg, **over)
+        w = np.zeros(problem.X.cols)
+        info = or_solve_info()
+        tr = (or_iteration * cap)()
+        msg = ctypes.create_string_buffer(512)
+        st = L.ref_solve_with_gpu_evaluator(os.fsencode(lib_path), *args, loss, ctypes.byref(c),
+                                            _p(w), ctypes.byref(info), tr, cap, msg, 512)
+        if st != 0:
+            raise RuntimeError(f"ref_solve_with_gpu_evaluator: {msg.value.decode()}")
+        return w, _trace(info, tr, cap)
+
     def parse_libsvm(self, text: bytes, n_override=0):
         """The reference's parse_libsvm (io.cpp:54-132) on an in-memory text:
         ('ok', (ro, ci, vals, y, n)) or (kind, (message, line)), kind in

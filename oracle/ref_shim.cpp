@@ -5,11 +5,15 @@
 // reference arm call the reference's own tron::solve (backend.cpp:314-318),
 // its loss kernels (loss.cpp) and its deterministic fixture generators
 // (testgen.cpp) on identical inputs.  No reference source is copied here.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <sstream>
+#include <stdexcept>
+#include <type_traits>
 #include <exception>
 #include <vector>
 
@@ -243,6 +247,113 @@ size_t ref_testgen_random_index_set(uint64_t seed, size_t l, double fraction, in
   if (out)
     for (size_t k = 0; k < s.size(); ++k) out[k] = s[k];
   return s.size();
+}
+
+// The drop-in boundary exercised literally: the
+// REFERENCE's own tron::solve(LossEvaluator&) (tron.cpp:127-217) driving a
+// LossEvaluator whose every method forwards to the B200 C ABI
+// (include/tron_b200.h), loaded with dlopen from `lib_path`.
+namespace {
+struct GpuAbi {
+  void* h = nullptr;
+  int (*create_csr)(int, uint64_t, uint64_t, const int64_t*, const int32_t*, const double*,
+                    const double*, double, const void*, void**) = nullptr;
+  int (*create_dense)(int, uint64_t, uint64_t, const double*, const double*, double, const void*,
+                      void**) = nullptr;
+  void (*destroy)(void*) = nullptr;
+  int (*eval_candidate)(void*, const double*, double*) = nullptr;
+  int (*commit)(void*, double*) = nullptr;
+  int (*gradient)(void*, double*) = nullptr;
+  int (*hessian_vec)(void*, const double*, double*) = nullptr;
+  int (*precond)(void*, double*) = nullptr;
+  const char* (*last_error)() = nullptr;
+  void (*default_options)(void*) = nullptr;
+  bool load(const char* path) {
+    h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) return false;
+    auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::decay_t<decltype(f)>>(dlsym(h, name)); };
+    sym(create_csr, "tron_gpu_create_csr");
+    sym(create_dense, "tron_gpu_create_dense");
+    sym(destroy, "tron_gpu_destroy");
+    sym(eval_candidate, "tron_gpu_eval_candidate");
+    sym(commit, "tron_gpu_commit");
+    sym(gradient, "tron_gpu_gradient");
+    sym(hessian_vec, "tron_gpu_hessian_vec");
+    sym(precond, "tron_gpu_precond_diagonal");
+    sym(last_error, "tron_gpu_last_error");
+    sym(default_options, "tron_gpu_default_options");
+    return create_csr && create_dense && destroy && eval_candidate && commit && gradient &&
+           hessian_vec && precond && last_error && default_options;
+  }
+};
+
+class AbiEvaluator final : public tron::LossEvaluator {
+ public:
+  AbiEvaluator(GpuAbi& abi, void* ctx, size_t n) : abi_(abi), ctx_(ctx), g_(n), m_(n) {}
+  ~AbiEvaluator() override { abi_.destroy(ctx_); }
+  std::size_t dimension() const override { return g_.size(); }
+  double eval_candidate(const tron::RealVector& w) override {
+    double f = 0.0;
+    check(abi_.eval_candidate(ctx_, w.data(), &f));
+    return f;
+  }
+  void commit() override {
+    check(abi_.commit(ctx_, nullptr));
+    check(abi_.gradient(ctx_, g_.data()));
+  }
+  const tron::RealVector& gradient() const override { return g_; }
+  void hessian_vec(const tron::RealVector& v, tron::RealVector& out) override {
+    out.resize(v.size());
+    check(abi_.hessian_vec(ctx_, v.data(), out.data()));
+  }
+  const tron::RealVector& precond_diagonal() override {
+    check(abi_.precond(ctx_, m_.data()));
+    return m_;
+  }
+
+ private:
+  void check(int st) const {
+    if (st != 0) throw std::runtime_error(abi_.last_error());
+  }
+  GpuAbi& abi_;
+  void* ctx_;
+  tron::RealVector g_, m_;
+};
+}  // namespace
+
+int ref_solve_with_gpu_evaluator(const char* lib_path, int layout, size_t l, size_t n,
+                                 const int64_t* ro, const int32_t* ci, const double* vals,
+                                 const double* y, double C, int loss, const or_config* c,
+                                 double* w_out, or_solve_info* info, or_iteration* trace,
+                                 size_t cap, char* msg, size_t msglen) {
+  std::memset(info, 0, sizeof(*info));
+  if (msglen) msg[0] = 0;
+  static GpuAbi abi;
+  if (!abi.h && !abi.load(lib_path)) {
+    std::snprintf(msg, msglen, "cannot load %s", lib_path);
+    return OR_ERR_DIMENSION;
+  }
+  try {
+    alignas(16) unsigned char opt[256];
+    std::memset(opt, 0, sizeof(opt));
+    abi.default_options(opt);
+    void* ctx = nullptr;
+    const int st = layout == OR_SPARSE_CSR
+                       ? abi.create_csr(loss, l, n, ro, ci, vals, y, C, opt, &ctx)
+                       : abi.create_dense(loss, l, n, vals, y, C, opt, &ctx);
+    if (st != 0) throw std::runtime_error(abi.last_error());
+    AbiEvaluator ev(abi, ctx, n);
+    auto res = tron::solve(ev, make_cfg(c));  // the reference's own solver loop
+    std::memcpy(w_out, res.w.data(), n * sizeof(double));
+    fill_trace(res.trace, info, trace, cap);
+    info->objective = res.objective;
+    info->converged = res.converged;
+    info->status = OR_OK;
+    return OR_OK;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, msglen, "%s", e.what());
+    return OR_ERR_NUMERICAL;
+  }
 }
 
 // parse_libsvm (io.cpp:54-132) on an in-memory text: 0 ok, 1 ParseError,

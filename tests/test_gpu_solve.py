@@ -247,3 +247,24 @@ def test_sharded_path_single_rank_nccl(ref, monkeypatch, case):
     w_ref, t_ref = ref.solve(p, 0 if loss == LossKind.Logistic else 1, cfg)
     assert rel_err(got.objective, t_ref["objective"]) <= 1e-6
     assert rel_err(got.w, w_ref) <= 1e-6
+
+
+# The drop-in boundary, literally: the reference's own tron::solve
+# (tron.cpp:127-217, compiled from /root/reference into oracle/_ref) driving a
+# tron::LossEvaluator whose every method forwards to the C ABI of
+# libtron_b200.so -- the binding INTEGRATION.md §1 proposes for backend.cpp.
+@pytest.mark.parametrize("case", ["sparse_lr", "dense_svm", "sparse_svm_precond"])
+def test_reference_solver_drives_the_gpu_evaluator(ref, case):
+    from paper_2008_03433_b200 import LIB_PATH
+    p, loss, over = {
+        "sparse_lr": (synth.synth_sparse(1, 20242, 47236, 74), 0, {}),
+        "dense_svm": (synth.testgen_dense_problem(3001, 200, 20, 1.0), 1, dict(eps=1e-8)),
+        "sparse_svm_precond": (synth.testgen_sparse_problem(3400, 400, 60, 2.0, 0.15), 1,
+                               dict(eps=1e-7, use_preconditioner=True)),
+    }[case]
+    cfg = TrustRegionConfig(eps=over.pop("eps", 0.01), **over)
+    w_gpu, t_gpu = ref.solve_with_gpu_evaluator(LIB_PATH, p, loss, cfg)
+    w_ref, t_ref = ref.solve(p, loss, cfg)
+    assert rel_err(t_gpu["objective"], t_ref["objective"]) <= 1e-9
+    assert rel_err(w_gpu, w_ref) <= 1e-6
+    assert [it["cg_iters"] for it in t_gpu["iterations"]] == [it["cg_iters"] for it in t_ref["iterations"]]
