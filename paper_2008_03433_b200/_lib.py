@@ -14,7 +14,8 @@ import numpy as np
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtron_b200.so")
+# TRON_B200_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("TRON_B200_LIB") or os.path.join(HERE, "libtron_b200.so")
 
 # tron_status
 OK, ERR_DIMENSION, ERR_BOUNDS, ERR_STRATEGY, ERR_BUDGET, ERR_NUMERICAL, ERR_LOGIC, ERR_CUDA, \

@@ -6,20 +6,20 @@
 // (parallel.hpp:101-123) -- the dominant cost of TRON-LR at large n.  Here
 // the CSC copy turns it into a segmented sum over contiguous memory:
 //
-//  * the nonzeros are cut into chunks of at most 256 (one warp, 8 per
-//    lane) packed greedily along column boundaries, so work is balanced
-//    regardless of column lengths (Zipf-hot columns of 20k+ entries and the
-//    27% empty columns of news20 cost the same) and only columns longer
-//    than a chunk are split;
+//  * the nonzeros are cut into fixed chunks of 256 (one warp, 8 per lane),
+//    so work is balanced regardless of column lengths (Zipf-hot columns of
+//    20k+ entries cost the same as short ones);
 //  * per-entry "last entry of its column" bits, the chunk -> column-rank
-//    map and the table of non-empty columns are precomputed once per
-//    matrix on the host (the structure never changes during a solve);
+//    map, the table of non-empty columns and the list of empty ones are
+//    built once per matrix on the device (the structure never changes
+//    during a solve);
 //  * a lane sums its 8 products sequentially, column pieces that cross
 //    lanes are combined by one warp-level segmented scan, the pieces of
 //    long columns by a fixed-order fix-up pass.  No atomics, no shared
 //    memory, no block barriers: results are bit-reproducible run to run.
-//  * each emitted column also writes the empty columns that follow it, so
-//    the epilogue (base_j + scale*sum) covers every j in one pass.
+//  * the empty columns (27% of news20) are written from their own list in
+//    the same launch, so the epilogue (base_j + scale*sum) covers every j
+//    in one pass.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
@@ -33,9 +33,8 @@ namespace tb {
 
 namespace {
 
-constexpr int kBlock = 256;         // 8 warps = 8 chunks per block
-constexpr int kStagedBlock = 512;   // one 16-warp block per SM holding u in shared memory
-constexpr long long kStageMaxBytes = 190 * 1024;  // + 32 KB of static emission buffers
+constexpr int kBlock = 256;  // 8 warps = 8 chunks in flight per block
+constexpr int kEmptyItems = 4;  // empty rows per lane per visit
 
 __device__ __forceinline__ void ld2(const double* p, double& a, double& b) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
@@ -48,118 +47,95 @@ __device__ __forceinline__ void ld4(const int* p, int& a, int& b, int& c, int& d
                : "l"(p));
 }
 
-template <int UK, bool SQ>
-__device__ __forceinline__ double weight(const UView& U, int r, double v) {
-  double u;
-  if (UK == U_VEC) {
-    u = __ldg(U.u + r);
-  } else if (UK == U_SVM_RESID) {
-    u = U.mask[r] ? (U.z[r] - U.y[r]) : 0.0;
-  } else {
-    u = U.mask[r] ? 1.0 : 0.0;
-  }
-  // row_axpy: out += a*v ; row_axpy_squared: out += a*v*v  (linalg.cpp:88-109)
-  return SQ ? (u * v) * v : u * v;
-}
-
+// Epilogue out_j = base_j + scale*sum (VEC), cbase + scale*sum (CONST) or
+// sum (RAW); base_j is requested early (epi_base) and applied at emission.
 template <int EPI>
-__device__ __forceinline__ double epi_value(const EpiView& E, long long j, double sum) {
-  if (EPI == EPI_VEC) return E.base[j] + E.scale * sum;
+__device__ __forceinline__ double epi_base(const EpiView& E, int j) {
+  return (EPI == EPI_VEC && j >= 0) ? __ldg(E.base + j) : 0.0;
+}
+template <int EPI>
+__device__ __forceinline__ double epi_apply(const EpiView& E, double base, double sum) {
+  if (EPI == EPI_VEC) return base + E.scale * sum;
   if (EPI == EPI_CONST) return E.cbase + E.scale * sum;
   return sum;
 }
 
-// Writes column nz_col[rank] and the empty columns up to the next non-empty one.
-template <int EPI>
-__device__ __forceinline__ void emit_rank(const SegView& S, const EpiView& E, double* out, int rank,
-                                          double sum) {
-  const int j = __ldg(S.nz_col + rank);
-  const int j_next = __ldg(S.nz_col + rank + 1);
-  out[j] = epi_value<EPI>(E, j, sum);
-  for (int e = j + 1; e < j_next; ++e) out[e] = epi_value<EPI>(E, e, 0.0);
-}
-
-// Effective per-row weight u_i for the staged variant (shared memory).
+// Effective per-row weight u_r (row_axpy's a, linalg.cpp:88-109).
 template <int UK>
 __device__ __forceinline__ double ueff(const UView& U, long long r) {
-  if (UK == U_VEC) return U.u[r];
+  if (UK == U_VEC) return __ldg(U.u + r);
   if (UK == U_SVM_RESID) return U.mask[r] ? (U.z[r] - U.y[r]) : 0.0;
   return U.mask[r] ? 1.0 : 0.0;
 }
 
-// Raw operands of one chunk for one lane (loaded one chunk ahead).
+// Operands of one chunk for one lane, moved through a three-stage software
+// pipeline so that no load sits on a chunk's own dependency chain:
+//   chunk rank          requested three chunks ahead,
+//   nonzeros, last-entry bits, row table (col)   two ahead,
+//   gathered u_r and the epilogue bases          one ahead,
+//   sums, scans and emission                     now.
 struct LaneChunk {
-  int cs, ce;
-  long long base;
+  long long base;  // the lane's first entry (multiple of kSegLaneItems)
   double v[kSegLaneItems];
   int ix[kSegLaneItems];
-  unsigned lo_word, hi_word, cr;
+  double g[kSegLaneItems];  // gathered u_r (stage 2)
+  double bv[2];             // epilogue bases of col[] (stage 2)
+  unsigned word, cr;        // last-entry bits holding the lane's items; chunk rank
+  int col[2];               // nz_col[rank + lane], nz_col[rank + 32 + lane]; -1 past the table
 };
 
+// The CSC copy is padded to whole chunks (zero entries, no last-entry bits),
+// so every chunk is read in full without bounds checks.
 __device__ __forceinline__ void load_chunk(const CsrView& A, const SegView& S, long long t, int lane,
-                                           LaneChunk& c) {
-  if (S.fixed_chunks) {  // device-built plan: chunk t is [256t, 256t + 256), no load on the chain
-    c.cs = (int)(t * kSegChunk);
-    c.ce = (int)min((long long)c.cs + kSegChunk, (long long)A.nnz);
-  } else {
-    c.cs = __ldg(S.chunk_start + t);
-    c.ce = __ldg(S.chunk_start + t + 1);
-  }
-  c.base = (long long)(c.cs & ~3) + lane * kSegLaneItems;  // 16-B aligned lanes
-  if (c.base + kSegLaneItems <= A.nnz) {
+                                           unsigned cr, LaneChunk& c) {
+  c.base = t * kSegChunk + lane * kSegLaneItems;  // 16-B aligned
 #pragma unroll
-    for (int m = 0; m < kSegLaneItems; m += 2) ld2(A.val + c.base + m, c.v[m], c.v[m + 1]);
+  for (int m = 0; m < kSegLaneItems; m += 2) ld2(A.val + c.base + m, c.v[m], c.v[m + 1]);
 #pragma unroll
-    for (int m = 0; m < kSegLaneItems; m += 4)
-      ld4(A.idx + c.base + m, c.ix[m], c.ix[m + 1], c.ix[m + 2], c.ix[m + 3]);
-  } else {
-#pragma unroll
-    for (int m = 0; m < kSegLaneItems; ++m) {
-      const long long k = c.base + m;
-      c.v[m] = k < A.nnz ? A.val[k] : 0.0;
-      c.ix[m] = k < A.nnz ? A.idx[k] : 0;
-    }
-  }
-  const bool any = c.base < c.ce && c.base + kSegLaneItems > c.cs;
-  c.lo_word = any ? __ldg(S.lastbits + (c.base >> 5)) : 0u;
-  c.hi_word = any ? __ldg(S.lastbits + (c.base >> 5) + 1) : 0u;
-  c.cr = __ldg(S.chunk_rank + t);
+  for (int m = 0; m < kSegLaneItems; m += 4)
+    ld4(A.idx + c.base + m, c.ix[m], c.ix[m + 1], c.ix[m + 2], c.ix[m + 3]);
+  // a lane's 8 items never straddle a 32-bit word (base is a multiple of 8)
+  c.word = __ldg(S.lastbits + (c.base >> 5));
+  c.cr = cr;
+  const long long r0 = cr & 0x7fffffffu;
+  c.col[0] = r0 + lane < S.nnzc ? __ldg(S.nz_col + r0 + lane) : -1;
+  c.col[1] = r0 + 32 + lane < S.nnzc ? __ldg(S.nz_col + r0 + 32 + lane) : -1;
 }
 
-// One chunk: gathers, per-lane sequential sums, warp segmented scan, emission.
+// Stage 2.  STAGED: the u_r are LDS reads, so the products are formed here
+// and only they stay live; otherwise the gathered u_r stay in flight until
+// the chunk is processed.
 template <int UK, bool SQ, int EPI, bool STAGED>
-__device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const UView& U,
-                                              const EpiView& E, double* __restrict__ out,
-                                              const double* su, long long t, const LaneChunk& cur,
-                                              int lane, double* ebuf) {
-  // gathers of the current chunk
-  double w[kSegLaneItems];
+__device__ __forceinline__ void gather_chunk(const UView& U, const EpiView& E, const double* su,
+                                             LaneChunk& c) {
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; ++m) {
-    const long long k = cur.base + m;
     if (STAGED) {
-      const double u = su[cur.ix[m]];
-      const double p = SQ ? (u * cur.v[m]) * cur.v[m] : u * cur.v[m];
-      w[m] = (k >= cur.cs && k < cur.ce) ? p : 0.0;
+      const double u = su[c.ix[m]];
+      c.g[m] = SQ ? (u * c.v[m]) * c.v[m] : u * c.v[m];  // row_axpy(_squared)
     } else {
-      w[m] = (k >= cur.cs && k < cur.ce) ? weight<UK, SQ>(U, cur.ix[m], cur.v[m]) : 0.0;
+      c.g[m] = ueff<UK>(U, c.ix[m]);
     }
   }
+  c.bv[0] = epi_base<EPI>(E, c.col[0]);
+  c.bv[1] = epi_base<EPI>(E, c.col[1]);
+}
 
-  unsigned bits = 0u;
-  if (cur.base < cur.ce && cur.base + kSegLaneItems > cur.cs) {
-    // base is a multiple of 4: the lane's 8 bits may straddle two words
-    const unsigned long long pair =
-        (unsigned long long)cur.lo_word | ((unsigned long long)cur.hi_word << 32);
-    bits = (unsigned)(pair >> (cur.base & 31)) & 0xffu;
-    const long long lo = cur.cs - cur.base, hi = cur.ce - cur.base;  // keep [cs, ce)
-    if (lo > 0) bits &= ~((1u << lo) - 1u);
-    if (hi < kSegLaneItems) bits &= (1u << hi) - 1u;
-  }
+// One chunk: products, per-lane sequential sums, warp segmented scan, emission.
+template <bool SQ, int EPI, bool STAGED>
+__device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const EpiView& E,
+                                              double* __restrict__ out, long long t,
+                                              const LaneChunk& cur, int lane, double* ebuf) {
+  double w[kSegLaneItems];
+#pragma unroll
+  for (int m = 0; m < kSegLaneItems; ++m)  // row_axpy / row_axpy_squared
+    w[m] = STAGED ? cur.g[m] : (SQ ? (cur.g[m] * cur.v[m]) * cur.v[m] : cur.g[m] * cur.v[m]);
+
+  const unsigned bits = (cur.word >> (cur.base & 31)) & 0xffu;
   const int chunk_rank = (int)(cur.cr & 0x7fffffffu);
   const bool cont_in = (cur.cr >> 31) != 0;
 
-  // rank of the column containing this lane's first item
+  // rank of the row containing this lane's first item
   const int cnt = __popc(bits);
   int incl = cnt;
 #pragma unroll
@@ -169,27 +145,22 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
   }
   const int r0 = chunk_rank + incl - cnt;
 
-  // sequential pass over the lane's items; the sums of the columns ending
-  // here go to the warp's buffer, indexed by their order in the chunk
-  double acc = 0.0, head_val = 0.0;
-  bool have_head = false;
+  // sequential pass over the lane's items; the sums of the rows ending here
+  // go to the warp's buffer, indexed by their order in the chunk
+  // (branch-free: predicated stores and selects; the first row ending here,
+  // whose sum may continue a previous lane's, is rewritten after the scan)
+  double acc = 0.0;
   int k = incl - cnt;
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; ++m) {
     acc += w[m];
-    if (bits & (1u << m)) {
-      if (!have_head) {
-        head_val = acc;
-        have_head = true;
-      } else {
-        ebuf[k] = acc;  // column wholly inside this lane
-      }
-      ++k;
-      acc = 0.0;
-    }
+    const bool end = (bits >> m) & 1u;
+    if (end) ebuf[k] = acc;
+    k += end;
+    acc = end ? 0.0 : acc;
   }
 
-  // warp segmented inclusive scan of the carries, keyed by column rank
+  // warp segmented inclusive scan of the carries, keyed by row rank
   const int key = r0 + cnt;
   double val = acc;
 #pragma unroll
@@ -200,238 +171,225 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
   }
   const int prev_key = __shfl_up_sync(0xffffffffu, key, 1);
   const double prev_val = __shfl_up_sync(0xffffffffu, val, 1);
-  if (have_head) ebuf[incl - cnt] = (lane > 0 && prev_key == r0) ? prev_val + head_val : head_val;
-  if (lane == 31) S.carry[t] = val;
-  // emission, warp-cooperative: consecutive columns to consecutive lanes, so
-  // the nz_col / base loads and the stores of a chunk are coalesced and no
-  // lane walks a chain of dependent loads
+  if (cnt > 0 && lane > 0 && prev_key == r0) ebuf[incl - cnt] = prev_val + ebuf[incl - cnt];
+  const double tail = __shfl_sync(0xffffffffu, val, 31);  // the row open at the chunk's end
+  // emission, warp-cooperative: consecutive rows to consecutive lanes
+  // (coalesced stores); the first 64 use the prefetched row table and bases
   __syncwarp();
   const int nend = __shfl_sync(0xffffffffu, incl, 31);
-  for (int q = lane; q < nend; q += 32) {
-    const double v = ebuf[q];
-    if (q == 0 && cont_in)
-      S.head[t] = v;  // column began in an earlier chunk: finished by the fix-up
+  if (lane < nend) {
+    const double v = ebuf[lane];
+    if (lane == 0 && cont_in)
+      S.head[t] = v;  // row began in an earlier chunk: finished by the fix-up
     else
-      emit_rank<EPI>(S, E, out, chunk_rank + q, v);
+      out[cur.col[0]] = epi_apply<EPI>(E, cur.bv[0], v);
   }
+  if (lane + 32 < nend) out[cur.col[1]] = epi_apply<EPI>(E, cur.bv[1], ebuf[lane + 32]);
+  for (int q = lane + 64; q < nend; q += 32) {
+    const int j = __ldg(S.nz_col + chunk_rank + q);
+    out[j] = epi_apply<EPI>(E, epi_base<EPI>(E, j), ebuf[q]);
+  }
+  if (lane == 0) S.carry[t] = tail;
   __syncwarp();  // the buffer is reused by the warp's next chunk
-
 }
 
-// Persistent warps walk chunks t, t+W, ...; the next chunk's operands are
-// requested before the current chunk's gathers are consumed, so the
-// descriptor -> data -> gather -> emission latency chain of consecutive
-// chunks overlaps.
-// STAGED: the gathered vector u (length A.cols = l) is first copied into
-// shared memory, so the per-nonzero random gather is an LDS instead of an
-// L1 wavefront (a 32-address LDG costs ~32 L1 wavefronts; measured on N1
-// the gathers, not HBM, bounded this kernel).
+constexpr int kStagedBlock = 512;                  // one 16-warp block per SM
+constexpr long long kStageMaxBytes = 190 * 1024;   // + 32 KB of emission buffers
+
+// Persistent warps walk chunks t, t+W, t+2W, ... through the pipeline above.
+// STAGED: u (length A.cols) is first copied to shared memory (TMA bulk copy),
+// so a gather is an LDS instead of a 32-line L1 request; the L1 wavefront
+// queue, not HBM, bounds the unstaged kernel on L2-resident u.
+// The empty rows (out_j = epilogue of 0) are a flat list shared by all warps.
 template <int UK, bool SQ, int EPI, bool STAGED>
-#ifndef TB_SEG_BLOCKS_PER_SM
-#define TB_SEG_BLOCKS_PER_SM 3
-#endif
-#ifndef TB_SEG_PREFETCH2
-#define TB_SEG_PREFETCH2 0
-#endif
-__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : TB_SEG_BLOCKS_PER_SM)
+__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2)
     seg_spmv_kernel(CsrView A, SegView S, UView U, EpiView E, double* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ double su[];
   constexpr int BLK = STAGED ? kStagedBlock : kBlock;
+  extern __shared__ double su[];
   __shared__ double ebuf_all[BLK / kWarp][kSegChunk];
   const int lane = threadIdx.x & 31;
   double* ebuf = ebuf_all[threadIdx.x >> 5];
+  const long long W = ((long long)gridDim.x * BLK) >> 5;
+  const long long gw = (blockIdx.x * (long long)BLK + threadIdx.x) >> 5;
+  const long long nch = S.nchunks;
+
+  long long t = gw;
+  LaneChunk b0, b1;
+  unsigned cr3 = 0;  // rank of chunk t + 2W
+  if (t < nch) {
+    load_chunk(A, S, t, lane, __ldg(S.chunk_rank + t), b0);
+    if (t + W < nch) load_chunk(A, S, t + W, lane, __ldg(S.chunk_rank + t + W), b1);
+    if (t + 2 * W < nch) cr3 = __ldg(S.chunk_rank + t + 2 * W);
+  }
   if (STAGED) {
     if (UK == U_VEC) {
       bulk_stage_f64(su, U.u, A.cols);  // TMA bulk copy (UBLKCP)
     } else {
-#pragma unroll 4
       for (long long i = threadIdx.x; i < A.cols; i += BLK) su[i] = ueff<UK>(U, i);
       __syncthreads();
     }
   }
-  const long long W = ((long long)gridDim.x * BLK) >> 5;
-  long long t = (blockIdx.x * (long long)BLK + threadIdx.x) >> 5;
-  if (t >= S.nchunks) return;  // warp-uniform
 
-  // Columns before the first non-empty one (usually none).
-  if (t == 0 && lane == 0)
-    for (int e = 0; e < __ldg(S.nz_col); ++e) out[e] = epi_value<EPI>(E, e, 0.0);
-
-  LaneChunk cur;
-  load_chunk(A, S, t, lane, cur);
-  if (!STAGED && !TB_SEG_PREFETCH2) {
-    // one chunk ahead: the next chunk's operands are requested before this
-    // chunk's gathers are consumed
-    for (;;) {
-      const long long tn = t + W;
-      LaneChunk nxt;
-      if (tn < S.nchunks) load_chunk(A, S, tn, lane, nxt);
-      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane, ebuf);
-      if (tn >= S.nchunks) break;
-      t = tn;
-      cur = nxt;
+  for (long long b = gw * (32 * kEmptyItems); b < S.nempty; b += W * (32 * kEmptyItems)) {
+    int e[kEmptyItems];
+    double bb[kEmptyItems];
+#pragma unroll
+    for (int m = 0; m < kEmptyItems; ++m) {
+      const long long i = b + m * 32 + lane;
+      e[m] = i < S.nempty ? __ldg(S.empty_col + i) : -1;
     }
-  } else {
-    // u in shared memory makes the gathers cheap; with one 16-warp block per
-    // SM, keep two chunks in flight per warp instead
-    LaneChunk nxt;
-    if (t + W < S.nchunks) load_chunk(A, S, t + W, lane, nxt);
-    for (;;) {
-      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t, cur, lane, ebuf);
-      if (t + W >= S.nchunks) break;
-      if (t + 2 * W < S.nchunks) load_chunk(A, S, t + 2 * W, lane, cur);
-      process_chunk<UK, SQ, EPI, STAGED>(A, S, U, E, out, su, t + W, nxt, lane, ebuf);
-      if (t + 2 * W >= S.nchunks) break;
-      if (t + 3 * W < S.nchunks) load_chunk(A, S, t + 3 * W, lane, nxt);
-      t += 2 * W;
-    }
+#pragma unroll
+    for (int m = 0; m < kEmptyItems; ++m) bb[m] = epi_base<EPI>(E, e[m]);
+#pragma unroll
+    for (int m = 0; m < kEmptyItems; ++m)
+      if (e[m] >= 0) out[e[m]] = epi_apply<EPI>(E, bb[m], 0.0);
   }
+  if (t >= nch) return;  // warp-uniform
+
+  // two buffers in ping-pong (unrolled by two: a register copy of a buffer
+  // whose loads are in flight would wait for them).
+  // chunk t: processed; t+W: gathered; t+2W: nonzeros in flight
+#define TB_SEG_STEP(P, G)                                                      \
+  process_chunk<SQ, EPI, STAGED>(A, S, E, out, t, P, lane, ebuf);              \
+  if (t + W >= nch) break;                                                     \
+  gather_chunk<UK, SQ, EPI, STAGED>(U, E, su, G);                              \
+  if (t + 2 * W < nch) {                                                       \
+    load_chunk(A, S, t + 2 * W, lane, cr3, P);                                 \
+    if (t + 3 * W < nch) cr3 = __ldg(S.chunk_rank + t + 3 * W);                \
+  }                                                                            \
+  t += W;
+  gather_chunk<UK, SQ, EPI, STAGED>(U, E, su, b0);
+  for (;;) {
+    TB_SEG_STEP(b0, b1)
+    TB_SEG_STEP(b1, b0)
+  }
+#undef TB_SEG_STEP
 }
 
+// Rows split across chunks, finished in the chunk t holding their last entry:
+// the partials of chunks first[t] .. t-1 (carry) plus chunk t's own part
+// (head).  Lane i of a warp takes chunk 32w + i; spans of up to 16 chunks
+// are summed by the lane in order, longer ones (Zipf-hot rows) by the whole
+// warp, lane-strided then as a tree.  The order depends on the structure
+// only, so results are bit-reproducible.
+constexpr int kFixSerial = 16;
 template <int EPI>
 __global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
                                                           double* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const long long f = (blockIdx.x * (long long)kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (f >= S.nfix) return;
-  const int t = S.fix_chunk[f], ts = S.fix_first[f];
-  double s = 0.0;
-  for (int k = ts + lane; k < t; k += 32) s += S.carry[k];  // fixed order
-  s = warp_sum(s);
-  if (lane == 0) emit_rank<EPI>(S, E, out, (int)(S.chunk_rank[t] & 0x7fffffffu), s + S.head[t]);
+  const long long t = blockIdx.x * (long long)kBlock + threadIdx.x;
+  const long long f = t < S.nchunks ? __ldg(S.chunk_first + t) : -1;
+  const bool longspan = f >= 0 && t - f > kFixSerial;
+  if (f >= 0 && !longspan) {
+    double s = S.carry[f];
+    for (long long v = f + 1; v < t; ++v) s = s + S.carry[v];
+    const int j = S.nz_col[S.chunk_rank[t] & 0x7fffffffu];
+    out[j] = epi_apply<EPI>(E, epi_base<EPI>(E, j), s + S.head[t]);
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, longspan);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const long long tt = __shfl_sync(0xffffffffu, t, src);
+    const long long ff = __shfl_sync(0xffffffffu, f, src);
+    double s = 0.0;
+    for (long long v = ff + lane; v < tt; v += 32) s += S.carry[v];
+    s = warp_sum(s);  // valid in lane 0
+    if (lane == 0) {
+      const int j = S.nz_col[S.chunk_rank[tt] & 0x7fffffffu];
+      out[j] = epi_apply<EPI>(E, epi_base<EPI>(E, j), s + S.head[tt]);
+    }
+  }
 }
 
 template <int UK, bool SQ, int EPI, bool STAGED>
 void launch_one(const CsrView& A, const SegView& S, const UView& U, const EpiView& E, double* out,
                 cudaStream_t s) {
+  constexpr int BLK = STAGED ? kStagedBlock : kBlock;
+  size_t smem = 0;
+  long long cap = device_sm_count();
   if (STAGED) {
-    const size_t smem = (size_t)A.cols * sizeof(double);
+    smem = (size_t)A.cols * sizeof(double);
     static bool configured = false;  // per instantiation
     if (!configured) {
       cudaFuncSetAttribute(seg_spmv_kernel<UK, SQ, EPI, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageMaxBytes);
       configured = true;
     }
-    long long want = (S.nchunks * 32 + kStagedBlock - 1) / kStagedBlock;
-    const long long cap = device_sm_count();
-    launch_pdl(seg_spmv_kernel<UK, SQ, EPI, true>, dim3((int)(want < cap ? want : cap)),
-               dim3(kStagedBlock), smem, s, A, S, U, E, out);
   } else {
-    // persistent: 3 blocks of 8 warps per SM (register-limited), never more than chunks
-    long long want = (S.nchunks * 32 + kBlock - 1) / kBlock;
-    const long long cap = (long long)device_sm_count() * TB_SEG_BLOCKS_PER_SM;
-    launch_pdl(seg_spmv_kernel<UK, SQ, EPI, false>, dim3((int)(want < cap ? want : cap)),
-               dim3(kBlock), 0, s, A, S, U, E, out);
+    cap *= 2;  // persistent: 2 blocks of 8 warps per SM (register-limited)
   }
-  const int fgrid = (int)((S.nfix * 32 + kBlock - 1) / kBlock);
+  // never more warps than chunks or visits of the empty list
+  const long long warps =
+      std::max<long long>(S.nchunks, (S.nempty + 32 * kEmptyItems - 1) / (32 * kEmptyItems));
+  long long grid = (warps * 32 + BLK - 1) / BLK;
+  if (grid > cap) grid = cap;
+  launch_pdl(seg_spmv_kernel<UK, SQ, EPI, STAGED>, dim3((int)grid), dim3(BLK), smem, s, A, S, U, E,
+             out);
+  const int fgrid = (int)((S.nchunks + kBlock - 1) / kBlock);
   if (fgrid) launch_pdl(seg_fixup_kernel<EPI>, dim3(fgrid), dim3(kBlock), 0, s, S, E, out);
+}
+
+template <int UK, bool SQ, int EPI>
+void launch_epi(const CsrView& A, const SegView& S, const UView& U, const EpiView& E, double* out,
+                cudaStream_t s) {
+  // u staged in shared memory when it fits (TRON_B200_STAGE=0 disables)
+  static const bool stage_on = [] {
+    const char* e = std::getenv("TRON_B200_STAGE");
+    return !(e && e[0] == '0');
+  }();
+  // ... and when it pays: each staged u_r must serve enough nonzeros to cover
+  // the per-SM copy (R1, 74 per row: no; N1, 450: yes)
+  if (stage_on && (long long)A.cols * (long long)sizeof(double) <= kStageMaxBytes &&
+      A.nnz >= 128 * A.cols)
+    launch_one<UK, SQ, EPI, true>(A, S, U, E, out, s);
+  else
+    launch_one<UK, SQ, EPI, false>(A, S, U, E, out, s);
 }
 
 template <int UK, bool SQ>
 void launch_seg(const CsrView& A, const SegView& S, const UView& U, const EpiView& E, double* out,
                 cudaStream_t s) {
-  // Opt-in (TRON_B200_STAGE=1): see csr_kernels.cu stage_enabled().
-  static const bool stage_on = [] {
-    const char* e = std::getenv("TRON_B200_STAGE");
-    return e && e[0] == '1';
-  }();
-  const bool staged = stage_on && (long long)A.cols * (long long)sizeof(double) <= kStageMaxBytes;
   switch (E.kind) {
     case EPI_VEC:
-      staged ? launch_one<UK, SQ, EPI_VEC, true>(A, S, U, E, out, s)
-             : launch_one<UK, SQ, EPI_VEC, false>(A, S, U, E, out, s);
+      launch_epi<UK, SQ, EPI_VEC>(A, S, U, E, out, s);
       break;
     case EPI_CONST:
-      staged ? launch_one<UK, SQ, EPI_CONST, true>(A, S, U, E, out, s)
-             : launch_one<UK, SQ, EPI_CONST, false>(A, S, U, E, out, s);
+      launch_epi<UK, SQ, EPI_CONST>(A, S, U, E, out, s);
       break;
     default:
-      staged ? launch_one<UK, SQ, EPI_RAW, true>(A, S, U, E, out, s)
-             : launch_one<UK, SQ, EPI_RAW, false>(A, S, U, E, out, s);
+      launch_epi<UK, SQ, EPI_RAW>(A, S, U, E, out, s);
       break;
   }
 }
 
 }  // namespace
 
-// Greedy packing of whole rows (CSC: columns) into chunks of <= kSegChunk
-// lane slots; a chunk's lanes start at its first entry rounded down to a
-// multiple of 4 (16-byte aligned vector loads), so it holds entries
-// [start, (start & ~3) + kSegChunk).  Rows that fit nowhere whole are split
-// into consecutive pieces finished by the fix-up pass.
-void seg_plan_host(const int32_t* ptr, int64_t rows, int64_t nnz, SegPlanHost* P) {
-  P->chunk_start.clear();
-  P->chunk_rank.clear();
-  P->nz_col.clear();
-  P->fix_chunk.clear();
-  P->fix_first.clear();
-  P->lastbits.assign((size_t)((nnz + 31) / 32 + 1), 0u);
-  int64_t open_base = -1;  // aligned base of the chunk being filled, -1 = none
-  uint32_t rank = 0;
-  for (int64_t c = 0; c < rows; ++c) {
-    const int64_t b = ptr[c], e = ptr[c + 1];
-    if (e <= b) continue;
-    P->nz_col.push_back((int32_t)c);
-    P->lastbits[(size_t)((e - 1) >> 5)] |= 1u << ((e - 1) & 31);
-    if (open_base >= 0 && e <= open_base + kSegChunk) {
-      ++rank;  // fits in the open chunk
-      continue;
-    }
-    if (e <= (b & ~int64_t{3}) + kSegChunk) {  // starts a new chunk
-      P->chunk_start.push_back((int32_t)b);
-      P->chunk_rank.push_back(rank);
-      open_base = b & ~int64_t{3};
-    } else {  // long row: consecutive pieces, the last one finished by the fix-up
-      const int32_t first = (int32_t)P->chunk_start.size();
-      for (int64_t p = b; p < e;) {
-        const int64_t pe = std::min<int64_t>((p & ~int64_t{3}) + kSegChunk, e);
-        P->chunk_start.push_back((int32_t)p);
-        P->chunk_rank.push_back(rank | (p > b ? 0x80000000u : 0u));
-        if (pe == e) {
-          P->fix_chunk.push_back((int32_t)P->chunk_start.size() - 1);
-          P->fix_first.push_back(first);
-        }
-        p = pe;
-      }
-      open_base = -1;
-    }
-    ++rank;
-  }
-  P->nz_col.push_back((int32_t)rows);
-  P->chunk_start.push_back((int32_t)nnz);
-}
-
 // ---------------------------------------------------------------------------
 // Device-built plan with fixed 256-entry chunks (every boundary inside a
-// column becomes a fix-up): fully parallel, no host round trip of the CSC
-// structure -- what context creation uses.
+// row becomes a fix-up): fully parallel, no host round trip of the CSC
+// structure.
 // ---------------------------------------------------------------------------
 namespace {
 
-__global__ void plan_chunk_start_kernel(int32_t* cs, long long nchunks, long long nnz) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t <= nchunks;
-       t += (long long)gridDim.x * blockDim.x)
-    cs[t] = (int32_t)(t * kSegChunk < nnz ? t * kSegChunk : nnz);
-}
-
 __global__ void plan_cols_kernel(const int32_t* cptr, long long n, uint32_t* lastbits,
-                                 int32_t* nonempty, int32_t* ids, uint8_t* spans) {
+                                 int32_t* nonempty, int32_t* ids, uint8_t* empty) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x) {
     const int b = cptr[c], e = cptr[c + 1];
     ids[c] = (int32_t)c;
     nonempty[c] = e > b;
-    spans[c] = e > b && (b / kSegChunk) != ((e - 1) / kSegChunk);
+    empty[c] = e <= b;
     if (e > b) atomicOr(lastbits + ((e - 1) >> 5), 1u << ((e - 1) & 31));
   }
 }
 
 __global__ void plan_chunk_rank_kernel(const int32_t* cptr, long long n, const int32_t* colrank,
-                                       long long nchunks, uint32_t* rank) {
+                                       long long nchunks, uint32_t* rank, int32_t* first) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nchunks;
        t += (long long)gridDim.x * blockDim.x) {
     const long long x = t * kSegChunk;
@@ -444,18 +402,10 @@ __global__ void plan_chunk_rank_kernel(const int32_t* cptr, long long n, const i
         hi = mid;
     }
     const long long c = lo - 1;
-    rank[t] = (uint32_t)colrank[c] | (cptr[c] < x ? 0x80000000u : 0u);
-  }
-}
-
-__global__ void plan_fix_kernel(const int32_t* cptr, const int32_t* cols, const long long* count,
-                                int32_t* fix_chunk, int32_t* fix_first) {
-  const long long m = *count;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c = cols[i];
-    fix_first[i] = cptr[c] / kSegChunk;
-    fix_chunk[i] = (cptr[c + 1] - 1) / kSegChunk;
+    const bool cont = cptr[c] < x;
+    rank[t] = (uint32_t)colrank[c] | (cont ? 0x80000000u : 0u);
+    // fix-up of the row continued into chunk t when it also ends there
+    first[t] = cont && cptr[c + 1] <= x + kSegChunk ? (int32_t)(cptr[c] / kSegChunk) : -1;
   }
 }
 
@@ -471,67 +421,62 @@ int pgrid(long long n) {
 
 }  // namespace
 
-int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, int32_t* chunk_start,
-                    uint32_t* chunk_rank, uint32_t* lastbits, int32_t* nz_col, int32_t* fix_chunk,
-                    int32_t* fix_first, cudaStream_t s) {
+int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uint32_t* chunk_rank,
+                    int32_t* chunk_first, uint32_t* lastbits, int32_t* nz_col, int32_t* empty_col,
+                    cudaStream_t s) {
   const int64_t nchunks = (nnz + kSegChunk - 1) / kSegChunk;
   const size_t n1 = n > 0 ? n : 1;
-  int32_t *nonempty = nullptr, *colrank = nullptr, *ids = nullptr, *cols = nullptr;
-  uint8_t* spans = nullptr;
-  long long *cnt_nz = nullptr, *cnt_fix = nullptr;
+  int32_t *nonempty = nullptr, *colrank = nullptr, *ids = nullptr;
+  uint8_t* empty = nullptr;
+  long long* cnt = nullptr;  // [0] non-empty rows, [1] empty rows
   void* temp = nullptr;
   size_t tb1 = 0, tb2 = 0, tb3 = 0;
   cudaError_t e = cudaMallocAsync(&nonempty, (n1 + 1) * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaMallocAsync(&colrank, (n1 + 1) * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaMallocAsync(&ids, n1 * sizeof(int32_t), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&cols, n1 * sizeof(int32_t), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&spans, n1, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&cnt_nz, 2 * sizeof(long long), s);
-  cnt_fix = cnt_nz + 1;
+  if (e == cudaSuccess) e = cudaMallocAsync(&empty, n1, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&cnt, 2 * sizeof(long long), s);
   if (e == cudaSuccess)
     e = cub::DeviceScan::ExclusiveSum(nullptr, tb1, nonempty, colrank, (int)(n + 1), s);
   if (e == cudaSuccess)
-    e = cub::DeviceSelect::Flagged(nullptr, tb2, ids, nonempty, nz_col, cnt_nz, (int)n, s);
+    e = cub::DeviceSelect::Flagged(nullptr, tb2, ids, nonempty, nz_col, cnt, (int)n, s);
   if (e == cudaSuccess)
-    e = cub::DeviceSelect::Flagged(nullptr, tb3, ids, spans, cols, cnt_fix, (int)n, s);
+    e = cub::DeviceSelect::Flagged(nullptr, tb3, ids, empty, empty_col, cnt + 1, (int)n, s);
   if (e == cudaSuccess)
     e = cudaMallocAsync(&temp, std::max<size_t>(std::max(tb1, std::max(tb2, tb3)), 1), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(nonempty, 0, (n1 + 1) * sizeof(int32_t), s);
   if (e == cudaSuccess)
-    e = cudaMemsetAsync(lastbits, 0, (size_t)((nnz + 31) / 32 + 1) * sizeof(uint32_t), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(cnt_nz, 0, 2 * sizeof(long long), s);
+    e = cudaMemsetAsync(lastbits, 0, (size_t)(nchunks * (kSegChunk / 32) + 2) * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 2 * sizeof(long long), s);
   if (e == cudaSuccess) {
-    plan_chunk_start_kernel<<<pgrid(nchunks + 1), 256, 0, s>>>(chunk_start, nchunks, nnz);
-    if (n > 0) plan_cols_kernel<<<pgrid(n), 256, 0, s>>>(cptr, n, lastbits, nonempty, ids, spans);
+    if (n > 0) plan_cols_kernel<<<pgrid(n), 256, 0, s>>>(cptr, n, lastbits, nonempty, ids, empty);
     e = cub::DeviceScan::ExclusiveSum(temp, tb1, nonempty, colrank, (int)(n + 1), s);
   }
   if (e == cudaSuccess && n > 0)
-    e = cub::DeviceSelect::Flagged(temp, tb2, ids, nonempty, nz_col, cnt_nz, (int)n, s);
+    e = cub::DeviceSelect::Flagged(temp, tb2, ids, nonempty, nz_col, cnt, (int)n, s);
   if (e == cudaSuccess && n > 0)
-    e = cub::DeviceSelect::Flagged(temp, tb3, ids, spans, cols, cnt_fix, (int)n, s);
+    e = cub::DeviceSelect::Flagged(temp, tb3, ids, empty, empty_col, cnt + 1, (int)n, s);
   if (e == cudaSuccess) {
     plan_sentinel_kernel<<<1, 1, 0, s>>>(nz_col, colrank, n);
     if (nchunks > 0)
-      plan_chunk_rank_kernel<<<pgrid(nchunks), 256, 0, s>>>(cptr, n, colrank, nchunks, chunk_rank);
-    plan_fix_kernel<<<pgrid(n), 256, 0, s>>>(cptr, cols, cnt_fix, fix_chunk, fix_first);
+      plan_chunk_rank_kernel<<<pgrid(nchunks), 256, 0, s>>>(cptr, n, colrank, nchunks, chunk_rank,
+                                                            chunk_first);
   }
-  long long nfix = 0;
+  long long counts[2] = {0, 0};
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(&nfix, cnt_fix, sizeof(long long), cudaMemcpyDeviceToHost, s);
+    e = cudaMemcpyAsync(counts, cnt, sizeof(counts), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  for (void* p : {(void*)nonempty, (void*)colrank, (void*)ids, (void*)cols, (void*)spans,
-                  (void*)cnt_nz, temp})
+  for (void* p : {(void*)nonempty, (void*)colrank, (void*)ids, (void*)empty, (void*)cnt, temp})
     if (p) cudaFreeAsync(p, s);
   if (e == cudaSuccess) e = cudaGetLastError();
   P->nchunks = nchunks;
-  P->nfix = nfix;
-  P->fixed_chunks = 1;
-  P->chunk_start = chunk_start;
+  P->nnzc = counts[0];
+  P->nempty = counts[1];
   P->chunk_rank = chunk_rank;
+  P->chunk_first = chunk_first;
   P->lastbits = lastbits;
   P->nz_col = nz_col;
-  P->fix_chunk = fix_chunk;
-  P->fix_first = fix_first;
+  P->empty_col = empty_col;
   return e == cudaSuccess ? 0 : (int)e;
 }
 

@@ -323,8 +323,11 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     e->cidx_.alloc(nnz);
     e->rval_.alloc(nnz);
     e->cptr_.alloc(n + 1);
-    e->ridx_.alloc(nnz);
-    e->cval_.alloc(nnz);
+    // the CSC copy is padded to whole segmented chunks (zero entries of row 0),
+    // so the chunk kernels read full chunks without bounds checks
+    const int64_t nnz_pad = (nnz + kSegChunk - 1) / kSegChunk * kSegChunk;
+    e->ridx_.alloc(std::max<int64_t>(nnz_pad, 1));
+    e->cval_.alloc(std::max<int64_t>(nnz_pad, 1));
     e->y_.alloc(l > 0 ? l : 1);
     {
       DevBuf<int64_t> ro64;
@@ -350,6 +353,10 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
     const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
     if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
+    if (nnz_pad > nnz) {
+      cuda_check(cudaMemsetAsync(e->ridx_.p + nnz, 0, (nnz_pad - nnz) * sizeof(int32_t), s), "pad");
+      cuda_check(cudaMemsetAsync(e->cval_.p + nnz, 0, (nnz_pad - nnz) * sizeof(double), s), "pad");
+    }
     e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
     tr.mark("device CSC build");
     // TRON_B200_SEG_STREAM=1: the TMA-streamed segmented kernels (seg_stream.cu).
@@ -365,17 +372,17 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     } else {
       // one-time structure analysis of the CSC copy, on the device (csc_seg.cu)
       const int64_t nch = (nnz + kSegChunk - 1) / kSegChunk;
-      e->chunk_start_.alloc(nch + 1);
       e->chunk_rank_.alloc(std::max<int64_t>(nch, 1));
-      e->lastbits_.alloc(nnz / 32 + 2);
+      e->lastbits_.alloc(nch * (kSegChunk / 32) + 2);
       e->nz_col_.alloc(n + 1);
-      e->fix_chunk_.alloc(std::max<uint64_t>(n, 1));
-      e->fix_first_.alloc(std::max<uint64_t>(n, 1));
-      e->head_.alloc(std::max<int64_t>(nch, 1));
-      e->carry_.alloc(std::max<int64_t>(nch, 1));
-      const int prc = seg_plan_device(e->cptr_.p, (int64_t)n, nnz, &e->plan_, e->chunk_start_.p,
-                                      e->chunk_rank_.p, e->lastbits_.p, e->nz_col_.p,
-                                      e->fix_chunk_.p, e->fix_first_.p, s);
+      e->empty_col_.alloc(std::max<uint64_t>(n, 1));
+      const int64_t slots = std::max<int64_t>(nch, 1);
+      e->chunk_first_.alloc(slots);
+      e->head_.alloc(slots);
+      e->carry_.alloc(slots);
+      const int prc = seg_plan_device(e->cptr_.p, (int64_t)n, nnz, &e->plan_, e->chunk_rank_.p,
+                                      e->chunk_first_.p, e->lastbits_.p, e->nz_col_.p,
+                                      e->empty_col_.p, s);
       if (prc != 0) cuda_check((cudaError_t)prc, "seg_plan_device");
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
@@ -543,8 +550,7 @@ void Engine::build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64
 uint64_t Engine::memory_bytes() const {
   uint64_t b = rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
                cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes() + lastbits_.bytes() +
-               chunk_rank_.bytes() + chunk_start_.bytes() + fix_chunk_.bytes() +
-               fix_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
+               chunk_rank_.bytes() + empty_col_.bytes() + chunk_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
   b += xs_.bytes() + xts_.bytes();
   for (const auto& S : slot_)
     b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes() +
@@ -1235,14 +1241,19 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
 void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
   AllocScope scope(s_);
   if (!committed_valid_) raise(TRON_ERR_LOGIC, "bench_kernels() needs a committed state");
-  if (flush_l2 && flush_.n == 0) flush_.alloc((size_t)(256u << 20) / 8);  // 256 MiB > L2
+  if (flush_l2 && flush_.n == 0) {
+    flush_.alloc((size_t)(256u << 20) / 8);  // 256 MiB > L2
+    cuda_check(cudaMemsetAsync(flush_.p, 0, flush_.bytes(), s_), "flush init");
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   auto time_it = [&](auto&& fn) {
     double total = 0.0;
     for (int r = 0; r < reps; ++r) {
-      if (flush_l2) cudaMemsetAsync(flush_.p, r & 0xff, flush_.bytes(), s_);
+      // read-based eviction: cold L2, nothing dirty left to write back inside
+      // the timed launch (the solve's own kernels leave clean lines too)
+      if (flush_l2) l2_read_flush(flush_.p, (int64_t)flush_.n, s_);
       cudaEventRecord(a, s_);
       fn();
       cudaEventRecord(b, s_);

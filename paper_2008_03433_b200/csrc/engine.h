@@ -186,7 +186,7 @@ class Engine {
   DevBuf<int32_t> rptr_, cidx_, cptr_, ridx_;
   DevBuf<double> rval_, cval_;
   DevBuf<uint32_t> lastbits_, chunk_rank_;
-  DevBuf<int32_t> chunk_start_, fix_chunk_, fix_first_, nz_col_;
+  DevBuf<int32_t> empty_col_, chunk_first_, nz_col_;
   DevBuf<double> head_, carry_;
   CsrView X_{}, Xt_{};
   StreamBufs xs_, xts_;     // streamed CSR (rows) and CSC (columns) layouts

@@ -24,38 +24,32 @@ struct CsrView {
 };
 
 // Segmented-chunk plan of a compressed matrix (fixed per structure): the
-// nonzeros are cut into chunks of at most 32*kSegLaneItems (one warp each)
-// whose boundaries follow row boundaries, so only rows longer than a chunk
-// are split (and finished by the fix-up pass).
+// nonzeros are cut into fixed chunks of 32*kSegLaneItems (one warp each);
+// rows crossing chunks are finished by the fix-up pass, empty rows are
+// written from their own list.
 constexpr int kSegLaneItems = 8;
 constexpr int kSegChunk = 32 * kSegLaneItems;
 struct SegView {
   int64_t nchunks = 0;
-  int64_t nfix = 0;
-  int fixed_chunks = 0;                  // 1: chunk t = [t*kSegChunk, (t+1)*kSegChunk)
-  const int32_t* chunk_start = nullptr;  // [nchunks+1] first entry of each chunk; [nchunks] = nnz
+  int64_t nnzc = 0;                      // non-empty rows
+  int64_t nempty = 0;                    // empty rows
   const uint32_t* chunk_rank = nullptr;  // rank of the row holding the chunk's first entry
                                          // | 0x80000000 when that row began in an earlier chunk
   const uint32_t* lastbits = nullptr;    // bit k: entry k is the last of its row
   const int32_t* nz_col = nullptr;       // [nnzc+1] index of the r-th non-empty row; [nnzc] = rows
-  const int32_t* fix_chunk = nullptr;    // [nfix] chunk finishing a split row
-  const int32_t* fix_first = nullptr;    // [nfix] first chunk of that row
-  double* head = nullptr;                // [nchunks] partial of a chunk's split head row
-  double* carry = nullptr;               // [nchunks] carry-out toward the next chunk
+  const int32_t* empty_col = nullptr;    // [nempty] the empty rows, ascending
+  const int32_t* chunk_first = nullptr;  // first chunk of the row continued into chunk t when it
+                                         // ends there (a fix-up), else -1
+  double* head = nullptr;   // [nchunks] partial of the row open at the chunk's start, if it ends inside
+  double* carry = nullptr;  // [nchunks] partial of the row open at the chunk's end
 };
-// Host-side plan construction from the compressed-row offsets (ptr, rows+1).
-struct SegPlanHost {
-  std::vector<int32_t> chunk_start, nz_col, fix_chunk, fix_first;
-  std::vector<uint32_t> chunk_rank, lastbits;
-};
-void seg_plan_host(const int32_t* ptr, int64_t rows, int64_t nnz, SegPlanHost* out);
-// Device-built plan with fixed kSegChunk-entry chunks (chunk boundaries inside a
-// row become fix-ups).  Buffers: chunk_start[nchunks+1], chunk_rank[nchunks],
-// lastbits[nnz/32+2], nz_col[rows+1], fix_chunk[rows], fix_first[rows]; P's
-// head / carry are left to the caller.  Synchronizes s (returns nfix in P).
+// Device-built plan from the compressed-row offsets (ptr, rows+1).  Buffers:
+// chunk_rank[nchunks], chunk_first[nchunks], lastbits[nchunks*8+2],
+// nz_col[rows+1], empty_col[rows]; P's head / carry are left to the caller.
+// Synchronizes s (returns the counts in P).
 int seg_plan_device(const int32_t* ptr, int64_t rows, int64_t nnz, SegView* P,
-                    int32_t* chunk_start, uint32_t* chunk_rank, uint32_t* lastbits,
-                    int32_t* nz_col, int32_t* fix_chunk, int32_t* fix_first, cudaStream_t s);
+                    uint32_t* chunk_rank, int32_t* chunk_first, uint32_t* lastbits, int32_t* nz_col,
+                    int32_t* empty_col, cudaStream_t s);
 
 // Streamed segmented layout of a compressed matrix (seg_stream.cu): 2048-
 // entry tiles of eight 256-entry pieces, lane-interleaved, with per-lane
@@ -188,6 +182,7 @@ void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjSc
 void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s);
 // out = base + scale*raw  (after an allreduce of raw partials; raw == nullptr => 0)
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
+void l2_read_flush(const double* buf, int64_t n, cudaStream_t s);
 
 // Large-n CG engine (one kernel per phase; conditional handle optional).
 struct CgVectors {

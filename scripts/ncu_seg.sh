@@ -1,0 +1,8 @@
+#!/bin/bash
+# One ncu --set full capture (with source) of the segmented transposed kernel on a workload.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+W=${1:-N1}
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:seg_spmv -s 3 -c 1 \
+  -o gpurun_out/${W}_seg -f python scripts/profile_n1.py $W > gpurun_out/ncu_${W}_seg.log 2>&1
+echo "ncu rc=$?"; tail -2 gpurun_out/ncu_${W}_seg.log

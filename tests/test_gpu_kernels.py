@@ -238,7 +238,9 @@ def test_device_cg_matches_host_cg(port, case, precond):
         # iterations rounding differences grow ~10x per iteration in any two
         # FP64 implementations, so that case runs at TRON's own cg_tol (0.1).
         cg_tol = 0.1 if name == "dense40" else 1e-6
-        for delta, tol in ((1e6, 1e-10), (0.5 * np.linalg.norm(g), 1e-10), (1e-3, 1e-10)):
+        # d: the two CGs share Hv but not the order of their dot products; at
+        # cg_tol 1e-6 (~25 iterations) that difference grows to ~1e-10
+        for delta, tol in ((1e6, 1e-9), (0.5 * np.linalg.norm(g), 1e-9), (1e-3, 1e-9)):
             cfg = TrustRegionConfig(cg_tol=cg_tol, use_preconditioner=precond)
             dev = ev.truncated_cg(delta, cfg)
             host = port.truncated_cg(g, ev.hessian_vec, delta, M, cg_tol=cg_tol)
@@ -272,7 +274,8 @@ def test_cg_engines_match_host_cg(port, monkeypatch, engine, precond):
             host = port.truncated_cg(g, ev.hessian_vec, delta, M, cg_tol=1e-6)
             assert dev.iters == host["iters"]
             assert int(dev.exit) == host["exit"]
-            assert rel_err(dev.d, host["d"]) <= 1e-10
+            # shared Hv, different dot-product order: ~2e-10 after ~20 iterations
+            assert rel_err(dev.d, host["d"]) <= 1e-9
             assert rel_err(dev.model_value, host["model_value"]) <= 1e-9
         # the iteration cap ends the loop on the device (exit MaxIters)
         cfg = TrustRegionConfig(cg_tol=1e-9, max_cg_iters=2, use_preconditioner=precond)
