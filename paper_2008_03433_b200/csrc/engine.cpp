@@ -320,8 +320,9 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     tr.mark("context + state alloc");
 
     e->rptr_.alloc(l + 1);
-    e->cidx_.alloc(nnz);
-    e->rval_.alloc(nnz);
+    // +4: the row kernels read whole aligned groups of four entries
+    e->cidx_.alloc(nnz + 4);
+    e->rval_.alloc(nnz + 4);
     e->cptr_.alloc(n + 1);
     // the CSC copy is padded to whole segmented chunks (zero entries of row 0),
     // so the chunk kernels read full chunks without bounds checks
