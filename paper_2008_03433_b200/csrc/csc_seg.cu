@@ -23,8 +23,11 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "rowdot.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -49,9 +52,26 @@ __device__ __forceinline__ void ld4(const int* p, int& a, int& b, int& c, int& d
 
 // Epilogue out_j = base_j + scale*sum (VEC), cbase + scale*sum (CONST) or
 // sum (RAW); base_j is requested early (epi_base) and applied at emission.
-template <int EPI>
+// COH (persistent CG kernel): the vector is written inside the same kernel by
+// other CTAs, so it is read through L2 (ld.global.cg), never the
+// non-coherent path.
+#ifndef TB_COH_LOAD
+#define TB_COH_LOAD 1  // 0: ld.global.cg (L2 only), 1: plain ld.global (ordered by grid.sync)
+#endif
+__device__ __forceinline__ double ld_coh(const double* p) {
+#if TB_COH_LOAD
+  return *p;
+#else
+  return __ldcg(p);
+#endif
+}
+template <bool COH>
+__device__ __forceinline__ double ldv(const double* p) {
+  return COH ? ld_coh(p) : __ldg(p);
+}
+template <int EPI, bool COH = false>
 __device__ __forceinline__ double epi_base(const EpiView& E, int j) {
-  return (EPI == EPI_VEC && j >= 0) ? __ldg(E.base + j) : 0.0;
+  return (EPI == EPI_VEC && j >= 0) ? ldv<COH>(E.base + j) : 0.0;
 }
 template <int EPI>
 __device__ __forceinline__ double epi_apply(const EpiView& E, double base, double sum) {
@@ -61,9 +81,9 @@ __device__ __forceinline__ double epi_apply(const EpiView& E, double base, doubl
 }
 
 // Effective per-row weight u_r (row_axpy's a, linalg.cpp:88-109).
-template <int UK>
+template <int UK, bool COH = false>
 __device__ __forceinline__ double ueff(const UView& U, long long r) {
-  if (UK == U_VEC) return __ldg(U.u + r);
+  if (UK == U_VEC) return ldv<COH>(U.u + r);
   if (UK == U_SVM_RESID) return U.mask[r] ? (U.z[r] - U.y[r]) : 0.0;
   return U.mask[r] ? 1.0 : 0.0;
 }
@@ -105,7 +125,7 @@ __device__ __forceinline__ void load_chunk(const CsrView& A, const SegView& S, l
 // Stage 2.  STAGED: the u_r are LDS reads, so the products are formed here
 // and only they stay live; otherwise the gathered u_r stay in flight until
 // the chunk is processed.
-template <int UK, bool SQ, int EPI, bool STAGED>
+template <int UK, bool SQ, int EPI, bool STAGED, bool COH>
 __device__ __forceinline__ void gather_chunk(const UView& U, const EpiView& E, const double* su,
                                              LaneChunk& c) {
 #pragma unroll
@@ -114,15 +134,15 @@ __device__ __forceinline__ void gather_chunk(const UView& U, const EpiView& E, c
       const double u = su[c.ix[m]];
       c.g[m] = SQ ? (u * c.v[m]) * c.v[m] : u * c.v[m];  // row_axpy(_squared)
     } else {
-      c.g[m] = ueff<UK>(U, c.ix[m]);
+      c.g[m] = ueff<UK, COH>(U, c.ix[m]);
     }
   }
-  c.bv[0] = epi_base<EPI>(E, c.col[0]);
-  c.bv[1] = epi_base<EPI>(E, c.col[1]);
+  c.bv[0] = epi_base<EPI, COH>(E, c.col[0]);
+  c.bv[1] = epi_base<EPI, COH>(E, c.col[1]);
 }
 
 // One chunk: products, per-lane sequential sums, warp segmented scan, emission.
-template <bool SQ, int EPI, bool STAGED>
+template <bool SQ, int EPI, bool STAGED, bool COH>
 __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const EpiView& E,
                                               double* __restrict__ out, long long t,
                                               const LaneChunk& cur, int lane, double* ebuf) {
@@ -187,7 +207,7 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
   if (lane + 32 < nend) out[cur.col[1]] = epi_apply<EPI>(E, cur.bv[1], ebuf[lane + 32]);
   for (int q = lane + 64; q < nend; q += 32) {
     const int j = __ldg(S.nz_col + chunk_rank + q);
-    out[j] = epi_apply<EPI>(E, epi_base<EPI>(E, j), ebuf[q]);
+    out[j] = epi_apply<EPI>(E, epi_base<EPI, COH>(E, j), ebuf[q]);
   }
   if (lane == 0) S.carry[t] = tail;
   __syncwarp();  // the buffer is reused by the warp's next chunk
@@ -201,27 +221,32 @@ constexpr long long kStageMaxBytes = 190 * 1024;   // + 32 KB of emission buffer
 // so a gather is an LDS instead of a 32-line L1 request; the L1 wavefront
 // queue, not HBM, bounds the unstaged kernel on L2-resident u.
 // The empty rows (out_j = epilogue of 0) are a flat list shared by all warps.
-template <int UK, bool SQ, int EPI, bool STAGED>
-__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2)
-    seg_spmv_kernel(CsrView A, SegView S, UView U, EpiView E, double* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int BLK = STAGED ? kStagedBlock : kBlock;
-  extern __shared__ double su[];
-  __shared__ double ebuf_all[BLK / kWarp][kSegChunk];
-  const int lane = threadIdx.x & 31;
-  double* ebuf = ebuf_all[threadIdx.x >> 5];
-  const long long W = ((long long)gridDim.x * BLK) >> 5;
-  const long long gw = (blockIdx.x * (long long)BLK + threadIdx.x) >> 5;
+// Body shared with the persistent CG kernel (which runs it with COH and
+// without STAGED); every thread of the block calls it.
+template <int UK, bool SQ, int EPI, bool STAGED, bool COH, int BLK>
+__device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, const UView& U,
+                                         const EpiView& E, double* __restrict__ out, double* su,
+                                         double* ebuf, long long gw, long long W, int lane) {
   const long long nch = S.nchunks;
 
   long long t = gw;
+  // chunk ranks of the warp's next 32 chunks (t, t+W, ...), one per lane,
+  // refilled every 32 chunks: a chunk's row-table loads never wait for its rank
+  long long cr_base = t;
+  unsigned crv = t + lane * W < nch ? __ldg(S.chunk_rank + t + lane * W) : 0u;
+  auto rank_of = [&](long long tt) -> unsigned {
+    long long k = (tt - cr_base) / W;
+    if (k >= 32) {  // warp-uniform
+      cr_base = tt;
+      crv = tt + lane * W < nch ? __ldg(S.chunk_rank + tt + lane * W) : 0u;
+      k = 0;
+    }
+    return __shfl_sync(0xffffffffu, crv, (int)k);
+  };
   LaneChunk b0, b1;
-  unsigned cr3 = 0;  // rank of chunk t + 2W
   if (t < nch) {
-    load_chunk(A, S, t, lane, __ldg(S.chunk_rank + t), b0);
-    if (t + W < nch) load_chunk(A, S, t + W, lane, __ldg(S.chunk_rank + t + W), b1);
-    if (t + 2 * W < nch) cr3 = __ldg(S.chunk_rank + t + 2 * W);
+    load_chunk(A, S, t, lane, rank_of(t), b0);
+    if (t + W < nch) load_chunk(A, S, t + W, lane, rank_of(t + W), b1);
   }
   if (STAGED) {
     if (UK == U_VEC) {
@@ -241,7 +266,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2
       e[m] = i < S.nempty ? __ldg(S.empty_col + i) : -1;
     }
 #pragma unroll
-    for (int m = 0; m < kEmptyItems; ++m) bb[m] = epi_base<EPI>(E, e[m]);
+    for (int m = 0; m < kEmptyItems; ++m) bb[m] = epi_base<EPI, COH>(E, e[m]);
 #pragma unroll
     for (int m = 0; m < kEmptyItems; ++m)
       if (e[m] >= 0) out[e[m]] = epi_apply<EPI>(E, bb[m], 0.0);
@@ -252,20 +277,32 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2
   // whose loads are in flight would wait for them).
   // chunk t: processed; t+W: gathered; t+2W: nonzeros in flight
 #define TB_SEG_STEP(P, G)                                                      \
-  process_chunk<SQ, EPI, STAGED>(A, S, E, out, t, P, lane, ebuf);              \
+  process_chunk<SQ, EPI, STAGED, COH>(A, S, E, out, t, P, lane, ebuf);         \
   if (t + W >= nch) break;                                                     \
-  gather_chunk<UK, SQ, EPI, STAGED>(U, E, su, G);                              \
-  if (t + 2 * W < nch) {                                                       \
-    load_chunk(A, S, t + 2 * W, lane, cr3, P);                                 \
-    if (t + 3 * W < nch) cr3 = __ldg(S.chunk_rank + t + 3 * W);                \
-  }                                                                            \
+  gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, G);                         \
+  if (t + 2 * W < nch) load_chunk(A, S, t + 2 * W, lane, rank_of(t + 2 * W), P); \
   t += W;
-  gather_chunk<UK, SQ, EPI, STAGED>(U, E, su, b0);
+  gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, b0);
   for (;;) {
     TB_SEG_STEP(b0, b1)
     TB_SEG_STEP(b1, b0)
   }
 #undef TB_SEG_STEP
+}
+
+template <int UK, bool SQ, int EPI, bool STAGED>
+__global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2)
+    seg_spmv_kernel(CsrView A, SegView S, UView U, EpiView E, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int BLK = STAGED ? kStagedBlock : kBlock;
+  extern __shared__ double su[];
+  __shared__ double ebuf_all[BLK / kWarp][kSegChunk];
+  const int lane = threadIdx.x & 31;
+  const long long W = ((long long)gridDim.x * BLK) >> 5;
+  const long long gw = (blockIdx.x * (long long)BLK + threadIdx.x) >> 5;
+  seg_body<UK, SQ, EPI, STAGED, false, BLK>(A, S, U, E, out, su, ebuf_all[threadIdx.x >> 5], gw, W,
+                                             lane);
 }
 
 // Rows split across chunks, finished in the chunk t holding their last entry:
@@ -275,20 +312,16 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2
 // warp, lane-strided then as a tree.  The order depends on the structure
 // only, so results are bit-reproducible.
 constexpr int kFixSerial = 16;
-template <int EPI>
-__global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
-                                                          double* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  const int lane = threadIdx.x & 31;
-  const long long t = blockIdx.x * (long long)kBlock + threadIdx.x;
+template <int EPI, bool COH>
+__device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
+                                          double* __restrict__ out, long long t, int lane) {
   const long long f = t < S.nchunks ? __ldg(S.chunk_first + t) : -1;
   const bool longspan = f >= 0 && t - f > kFixSerial;
   if (f >= 0 && !longspan) {
-    double s = S.carry[f];
-    for (long long v = f + 1; v < t; ++v) s = s + S.carry[v];
+    double s = COH ? ld_coh(S.carry + f) : S.carry[f];
+    for (long long v = f + 1; v < t; ++v) s = s + (COH ? ld_coh(S.carry + v) : S.carry[v]);
     const int j = S.nz_col[S.chunk_rank[t] & 0x7fffffffu];
-    out[j] = epi_apply<EPI>(E, epi_base<EPI>(E, j), s + S.head[t]);
+    out[j] = epi_apply<EPI>(E, epi_base<EPI, COH>(E, j), s + (COH ? ld_coh(S.head + t) : S.head[t]));
   }
   unsigned todo = __ballot_sync(0xffffffffu, longspan);
   while (todo) {
@@ -297,13 +330,22 @@ __global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
     const long long tt = __shfl_sync(0xffffffffu, t, src);
     const long long ff = __shfl_sync(0xffffffffu, f, src);
     double s = 0.0;
-    for (long long v = ff + lane; v < tt; v += 32) s += S.carry[v];
+    for (long long v = ff + lane; v < tt; v += 32) s += COH ? ld_coh(S.carry + v) : S.carry[v];
     s = warp_sum(s);  // valid in lane 0
     if (lane == 0) {
       const int j = S.nz_col[S.chunk_rank[tt] & 0x7fffffffu];
-      out[j] = epi_apply<EPI>(E, epi_base<EPI>(E, j), s + S.head[tt]);
+      out[j] = epi_apply<EPI>(E, epi_base<EPI, COH>(E, j),
+                              s + (COH ? ld_coh(S.head + tt) : S.head[tt]));
     }
   }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
+                                                          double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  fixup_one<EPI, false>(S, E, out, blockIdx.x * (long long)kBlock + threadIdx.x, threadIdx.x & 31);
 }
 
 template <int UK, bool SQ, int EPI, bool STAGED>
@@ -478,6 +520,291 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uin
   P->nz_col = nz_col;
   P->empty_col = empty_col;
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent CG (tron.cpp:37-108) for sparse problems: one cooperative launch
+// runs every CG iteration -- a = D(Xp) over the CSR, hp = p + scale X^T a over
+// the CSC (the segmented body above), the fix-ups and the CG vector step --
+// with grid barriers instead of kernel boundaries.  What a CG iteration costs
+// on L2-resident problems (R1) is the latency of its phases, not bytes.
+// Scalars are reduced per CTA, then every CTA sums all CTA partials in the
+// same fixed order, so all CTAs hold identical alpha / beta / norms and take
+// the same branches.  The per-entry arithmetic is cg_cluster_step_kernel's.
+// ---------------------------------------------------------------------------
+namespace {
+
+namespace cgrp = cooperative_groups;
+constexpr int kFusedBlock = 256;
+#ifndef TB_FUSED_PROF
+#define TB_FUSED_PROF 0
+#endif
+#ifndef TB_FUSED_NG
+#define TB_FUSED_NG 2  // groups of four per lane in flight (16 warps per SM here, not 64)
+#endif
+
+struct FusedCg {
+  CsrView X, At;
+  SegView S;
+  CgVectors v;
+  const double* dvec;   // LR: D
+  const uint8_t* mask;  // SVM on CSR: active set
+  double* a;            // l-length: D (X p)
+  double scale;         // C (LR) or 2C (SVM)
+  double* parts;        // [2][grid][4] CTA partials
+  CgState* st;
+};
+
+template <int K>
+__device__ __forceinline__ void fused_sums(double (&x)[K], double* parts, int& buf, double* sh,
+                                           double* red, cgrp::grid_group& grid) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = block_sum<kFusedBlock>(x[k], sh);  // thread 0
+  double* P = parts + (size_t)buf * gridDim.x * 4;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) P[blockIdx.x * 4 + k] = x[k];
+  }
+  grid.sync();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double t = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(P + b * 4 + k);
+      t = warp_allsum(t);
+      if (threadIdx.x == 0) red[k] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = red[k];
+  __syncthreads();
+  buf ^= 1;  // the other buffer is free: every CTA read it before this barrier
+}
+
+template <int G>
+__global__ void __launch_bounds__(kFusedBlock, 2) cg_fused_kernel(FusedCg F) {
+  cgrp::grid_group grid = cgrp::this_grid();
+  __shared__ double ebuf_all[kFusedBlock / kWarp][kSegChunk];
+  __shared__ double sh[kFusedBlock / kWarp + 1];
+  __shared__ double red[4];
+  const int lane = threadIdx.x & 31;
+  const long long W = ((long long)gridDim.x * kFusedBlock) >> 5;
+  const long long gw = (blockIdx.x * (long long)kFusedBlock + threadIdx.x) >> 5;
+  const long long gt = blockIdx.x * (long long)kFusedBlock + threadIdx.x;
+  const long long NT = (long long)gridDim.x * kFusedBlock;
+  CgState* st = F.st;
+  const CgVectors v = F.v;
+  if (!st->cont) return;  // the init kernel ended the loop (uniform)
+  double rz_old = st->rz;
+  const double delta = st->delta, stop = st->stop;
+  long long iters = st->iters;
+  const long long max_iters = st->max_iters;
+  int rpar = st->rpar;
+  int buf = 0;
+  UView U;
+  U.kind = U_VEC;
+  U.u = F.a;
+  EpiView E;
+  E.kind = EPI_VEC;
+  E.base = v.p;
+  E.scale = F.scale;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  constexpr int RPW = kWarp / G;
+  const int sub = lane % G;
+#if TB_FUSED_PROF
+  unsigned long long tp[8];
+  auto stamp = [&](int i) {
+    unsigned long long x;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x));
+    tp[i] = x;
+  };
+#else
+  auto stamp = [](int) {};
+#endif
+  for (;;) {
+    ++iters;
+    stamp(0);
+    // a = D (X p) (loss.cpp:86-89; csr_dv_kernel)
+    for (long long r0 = gw * RPW; r0 < F.X.rows; r0 += W * RPW) {
+      const long long row = r0 + lane / G;
+      bool active = row < F.X.rows;
+      if (active && F.mask) active = F.mask[row] != 0;
+      double s = 0.0;
+      if (active) s = row_dot_vec<G, true, TB_FUSED_NG>(F.X, row, sub, v.p);
+      s = group_sum<G>(s);
+      if (sub == 0 && row < F.X.rows) F.a[row] = F.mask ? (active ? s : 0.0) : s * F.dvec[row];
+    }
+    stamp(1);
+    grid.sync();
+    stamp(2);
+    // hp = p + scale X^T a, then the rows split across chunks
+    seg_body<U_VEC, false, EPI_VEC, false, true, kFusedBlock>(F.At, F.S, U, E, v.hp, nullptr,
+                                                              ebuf_all[threadIdx.x >> 5], gw, W,
+                                                              lane);
+    stamp(3);
+    grid.sync();
+    stamp(4);
+    for (long long b = gw * 32; b < F.S.nchunks; b += W * 32)
+      fixup_one<EPI_VEC, true>(F.S, E, v.hp, b + lane, lane);
+    grid.sync();
+    stamp(5);
+    // p.Hp (tron.cpp:71-75)
+    double* r = rpar ? v.r1 : v.r0;
+    double x1[1] = {0.0};
+    for (long long j = gt; j < v.n; j += NT) x1[0] += ld_coh(v.p + j) * ld_coh(v.hp + j);
+    fused_sums<1>(x1, F.parts, buf, sh, red, grid);
+    const double php = x1[0];
+    if (!(php > 0.0)) {
+      if (lead) {
+        st->iters = iters;
+        st->php = php;
+        st->fail = 1;
+        st->cont = 0;
+      }
+      return;
+    }
+    const double alpha = rz_old / php;
+    // d += alpha p, ||d|| (tron.cpp:76-78), and speculatively r -= alpha Hp,
+    // z = M^-1 r (tron.cpp:91-95) into the other parity buffer, so one
+    // barrier serves both (on the boundary exit rn is simply not used)
+    double* rn = rpar ? v.r0 : v.r1;
+    double x2[3] = {0.0, 0.0, 0.0};
+    for (long long j = gt; j < v.n; j += NT) {
+      const double dj = v.d[j] + alpha * v.p[j];
+      v.d[j] = dj;
+      x2[0] += dj * dj;
+      const double rj = r[j] + (-alpha) * ld_coh(v.hp + j);
+      rn[j] = rj;
+      const double z = v.M ? rj / v.M[j] : rj;
+      x2[1] += rj * z;
+      x2[2] += rj * rj;
+    }
+    fused_sums<3>(x2, F.parts, buf, sh, red, grid);
+    if (sqrt(x2[0]) > delta) {
+      // boundary: retreat, then tau on ||d + tau p|| = delta (tron.cpp:78-90)
+      double x3[3] = {0.0, 0.0, 0.0};
+      for (long long j = gt; j < v.n; j += NT) {
+        const double pj = v.p[j];
+        const double dj = v.d[j] + (-alpha) * pj;
+        v.d[j] = dj;
+        x3[0] += dj * pj;
+        x3[1] += dj * dj;
+        x3[2] += pj * pj;
+      }
+      fused_sums<3>(x3, F.parts, buf, sh, red, grid);
+      const double dp = x3[0], dd = x3[1], pp = x3[2];
+      const double rad = sqrt(dp * dp + pp * (delta * delta - dd));
+      const double tau = dp >= 0.0 ? (delta * delta - dd) / (dp + rad) : (rad - dp) / pp;
+      double x4[3] = {0.0, 0.0, 0.0};  // q(d) and ||d|| of the final step (tron.cpp:99-106)
+      for (long long j = gt; j < v.n; j += NT) {
+        const double dj = v.d[j] + tau * v.p[j];
+        const double rj = r[j] + (-tau) * ld_coh(v.hp + j);
+        v.d[j] = dj;
+        r[j] = rj;
+        x4[0] += dj * v.g[j];
+        x4[1] += dj * rj;
+        x4[2] += dj * dj;
+      }
+      fused_sums<3>(x4, F.parts, buf, sh, red, grid);
+      if (lead) {
+        st->iters = iters;
+        st->php = php;
+        st->alpha = alpha;
+        st->tau = tau;
+        st->boundary = 1;
+        st->exit_kind = kCgBoundary;
+        st->q = 0.5 * (x4[0] - x4[1]);
+        st->dnorm = sqrt(x4[2]);
+        st->cont = 0;
+      }
+      return;
+    }
+    const double rz = x2[1], rnorm = sqrt(x2[2]);
+    stamp(6);
+    const double beta = rz / rz_old;
+    for (long long j = gt; j < v.n; j += NT)
+      v.p[j] = (v.M ? rn[j] / v.M[j] : rn[j]) + beta * v.p[j];  // tron.cpp:96
+    const int cont = (iters < max_iters) && !(rnorm <= stop);
+    if (!cont) {
+      // exit classification, q(d) = (d.g - d.r)/2, ||d|| (tron.cpp:97-106)
+      double x6[3] = {0.0, 0.0, 0.0};
+      for (long long j = gt; j < v.n; j += NT) {
+        const double dj = v.d[j];
+        x6[0] += dj * v.g[j];
+        x6[1] += dj * rn[j];
+        x6[2] += dj * dj;
+      }
+      fused_sums<3>(x6, F.parts, buf, sh, red, grid);
+      if (lead) {
+        st->exit_kind = (iters >= max_iters && rnorm > stop) ? kCgMaxIters : kCgConverged;
+        st->q = 0.5 * (x6[0] - x6[1]);
+        st->dnorm = sqrt(x6[2]);
+      }
+    }
+    if (lead) {
+      st->iters = iters;
+      st->php = php;
+      st->alpha = alpha;
+      st->beta = beta;
+      st->rz = rz;
+      st->rpar = rpar ^ 1;
+      st->rnorm = rnorm;
+      st->cont = cont;
+    }
+    if (!cont) return;
+    rz_old = rz;
+    rpar ^= 1;
+    grid.sync();  // p complete before the next row phase gathers it
+#if TB_FUSED_PROF
+    stamp(7);
+    if (lead && iters == 3)
+      printf("fused phases us: rows %.2f sync %.2f seg %.2f sync+fix+sync %.2f cg2sums %.2f p+sync %.2f\n",
+             (tp[1] - tp[0]) * 1e-3, (tp[2] - tp[1]) * 1e-3, (tp[3] - tp[2]) * 1e-3,
+             (tp[5] - tp[3]) * 1e-3, (tp[6] - tp[5]) * 1e-3, (tp[7] - tp[6]) * 1e-3);
+#endif
+  }
+}
+
+template <int G>
+int fused_grid() {
+  static int g = [] {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel<G>, kFusedBlock, 0);
+    return per_sm * device_sm_count();
+  }();
+  return g;
+}
+
+template <int G>
+void launch_fused(const FusedCg& F, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)fused_grid<G>());
+  cfg.blockDim = dim3(kFusedBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, cg_fused_kernel<G>, F);
+}
+
+}  // namespace
+
+int cg_fused_max_grid() { return 2 * device_sm_count(); }
+
+void cg_fused(const CsrView& X, const CsrView& At, const SegView& S, int group, const CgVectors& v,
+              const double* dvec, const uint8_t* mask, double* a, double scale, double* parts,
+              CgState* st, cudaStream_t s) {
+  FusedCg F{X, At, S, v, dvec, mask, a, scale, parts, st};
+  switch (group) {
+    case 32: launch_fused<32>(F, s); break;
+    case 16: launch_fused<16>(F, s); break;
+    case 8: launch_fused<8>(F, s); break;
+    case 4: launch_fused<4>(F, s); break;
+    default: launch_fused<2>(F, s); break;
+  }
 }
 
 void csc_spmv(const CsrView& At, const SegView& S, const UView& U, bool squared,

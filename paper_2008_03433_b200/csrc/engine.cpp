@@ -390,6 +390,13 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       tr.mark("segmented plan");
     }
     e->group_ = choose_group((int64_t)l, nnz);
+    // The persistent cooperative CG (cg_fused), opt-in (TRON_B200_FUSED_CG=1,
+    // any n above the single-block engine): measured 47 us per R1 CG iteration
+    // against 40 us for the kernel-per-phase graph.
+    const char* fc = std::getenv("TRON_B200_FUSED_CG");
+    e->fused_engine_ = !e->use_stream_ && !e->comm_.active() && !e->small_engine_ && fc &&
+                       fc[0] == '1';
+    if (e->fused_engine_) e->fused_parts_.alloc((size_t)8 * cg_fused_max_grid());
     cuda_check(cudaStreamSynchronize(s), "csc build");
     cuda_check(cudaGetLastError(), "csc build");
     return e;
@@ -903,7 +910,29 @@ void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint
 // ----------------------------------------------------------------------------
 // device-resident truncated CG (tron.cpp:37-108)
 // ----------------------------------------------------------------------------
+void Engine::launch_fused_cg(int k, bool use_m) {
+  CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
+  const Slot& S = slot_[k];
+  const bool lr = loss_ == TRON_LOSS_LOGISTIC;
+  Cond none;
+  cg_large_init(v, st_d_, sc_, none, s_);
+  cg_fused(X_, Xt_, plan_, group_, v, lr ? S.dvec.p : nullptr, lr ? nullptr : S.mask.p, a_.p,
+           lr ? C_ : 2.0 * C_, fused_parts_.p, st_d_, s_);
+}
+
 void Engine::build_graph(int k, bool use_m) {
+  if (fused_engine_) {  // init + one persistent kernel: no device-side loop node
+    cudaGraph_t graph;
+    cuda_check(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal), "begin capture");
+    launch_fused_cg(k, use_m);
+    cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
+    cudaGraphExec_t exec;
+    cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    graph_[k][use_m] = graph;
+    graph_exec_[k][use_m] = exec;
+    body_kernels_ = 0;
+    return;
+  }
   // Captured against committed slot k; CG vectors are fixed buffers.
   cudaGraph_t graph;
   cuda_check(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
@@ -1028,6 +1057,12 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
     read_cg(out);
     launches += 1 + (uint64_t)out->iters * body_kernels_ + (has_post_kernel() ? 1 : 0);
+    return;
+  }
+  if (fused_engine_) {
+    launch_fused_cg(k, use_m);
+    count_launch(2);
+    read_cg(out);
     return;
   }
   // host-driven loop (multi-GPU: NCCL between phases)

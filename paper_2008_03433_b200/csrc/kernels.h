@@ -208,6 +208,13 @@ void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s);
 // Mid-n CG engine (kSmallCgMaxN < n <= kClusterCgMaxN): one kernel per iteration
 // on a cluster of 8 CTAs (vector phases + scalars; the exit's q(d), ||d|| included).
 constexpr int64_t kClusterCgMaxN = 262144;
+// Persistent cooperative CG over a sparse problem (csc_seg.cu): every CG
+// iteration of one truncated_cg in a single launch.  parts: 2 * 4 *
+// cg_fused_max_grid() doubles.  The caller runs cg_large_init first.
+int cg_fused_max_grid();
+void cg_fused(const CsrView& X, const CsrView& At, const SegView& S, int group, const CgVectors& v,
+              const double* dvec, const uint8_t* mask, double* a, double scale, double* parts,
+              CgState* st, cudaStream_t s);
 void cg_cluster_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
 
 // Small-n CG engine (n <= kSmallCgMaxN): one single-block kernel per

@@ -251,15 +251,18 @@ def test_device_cg_matches_host_cg(port, case, precond):
             assert np.linalg.norm(dev.d) <= delta * (1 + 1e-12)
 
 
-# the three CG engines on the same mid-size problem: single cluster kernel per
-# step (default for 4096 < n <= 262144), the three-kernel large-n step, and the
+# the CG engines on the same mid-size problem: the persistent cooperative
+# kernel (opt-in; in a graph and host-launched), single cluster kernel per step
+# (default for 4096 < n <= 262144), the three-kernel large-n step, and the
 # host-driven loop (no graph), each against the host restatement
-@pytest.mark.parametrize("engine", ["cluster", "large", "nograph"])
+@pytest.mark.parametrize("engine", ["fused", "fused_nograph", "cluster", "large", "nograph"])
 @pytest.mark.parametrize("precond", [False, True])
 def test_cg_engines_match_host_cg(port, monkeypatch, engine, precond):
+    if engine.startswith("fused"):
+        monkeypatch.setenv("TRON_B200_FUSED_CG", "1")
     if engine == "large":
         monkeypatch.setenv("TRON_B200_CLUSTER_CG", "0")
-    if engine == "nograph":
+    if engine in ("nograph", "fused_nograph"):
         monkeypatch.setenv("TRON_B200_NO_GRAPH", "1")
     p = synth.synth_sparse(9, 2000, 5000, 37)  # n = 5000 > kSmallCgMaxN
     w = synth.testgen_random_vector(3007, p.X.cols, 0.3)  # the state of fixture case 7 above
