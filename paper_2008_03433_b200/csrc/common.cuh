@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <utility>
 
 namespace tb {
@@ -57,6 +58,38 @@ __device__ __forceinline__ double block_sum(double v, double* sh, bool broadcast
   double r = broadcast ? sh[NW] : (threadIdx.x == 0 ? sh[NW] : 0.0);
   if (broadcast) __syncthreads();
   return r;
+}
+
+// Grid-wide sums of K values in a cooperative kernel: block sums, one
+// partial per CTA, a grid barrier, then every CTA adds all CTA partials in the
+// same fixed order, so all CTAs hold identical totals.  parts: [2][grid][4]
+// doubles used alternately (`buf` flips), so a CTA never overwrites a slot
+// another CTA may still be reading.  sh: BLOCK/32 + 1 doubles, red: 4.
+template <int BLOCK, int K>
+__device__ __forceinline__ void grid_sums(double (&x)[K], double* parts, int& buf, double* sh,
+                                          double* red, cooperative_groups::grid_group& grid) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = block_sum<BLOCK>(x[k], sh);  // thread 0
+  double* P = parts + (size_t)buf * gridDim.x * 4;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) P[blockIdx.x * 4 + k] = x[k];
+  }
+  grid.sync();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double t = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(P + b * 4 + k);
+      t = warp_allsum(t);
+      if (threadIdx.x == 0) red[k] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = red[k];
+  __syncthreads();
+  buf ^= 1;
 }
 
 // Ticket: returns true in exactly one block (the last to arrive) after all

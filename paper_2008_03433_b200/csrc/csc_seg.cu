@@ -558,28 +558,7 @@ struct FusedCg {
 template <int K>
 __device__ __forceinline__ void fused_sums(double (&x)[K], double* parts, int& buf, double* sh,
                                            double* red, cgrp::grid_group& grid) {
-#pragma unroll
-  for (int k = 0; k < K; ++k) x[k] = block_sum<kFusedBlock>(x[k], sh);  // thread 0
-  double* P = parts + (size_t)buf * gridDim.x * 4;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) P[blockIdx.x * 4 + k] = x[k];
-  }
-  grid.sync();
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double t = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(P + b * 4 + k);
-      t = warp_allsum(t);
-      if (threadIdx.x == 0) red[k] = t;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < K; ++k) x[k] = red[k];
-  __syncthreads();
-  buf ^= 1;  // the other buffer is free: every CTA read it before this barrier
+  grid_sums<kFusedBlock, K>(x, parts, buf, sh, red, grid);
 }
 
 template <int G>

@@ -270,9 +270,14 @@ void Engine::common_alloc() {
   if (!dense_) a_.alloc(ll);
   if (dense_) parts_.alloc((size_t)dense_grid(l_, n_) * nn);
   small_engine_ = dense_ || n_ <= kSmallCgMaxN;
+  // large n: one cooperative kernel per CG iteration (TRON_B200_COOP_CG=0: the
+  // three-kernel php / update / direction sequence)
+  const char* co = std::getenv("TRON_B200_COOP_CG");
+  coop_parts_.alloc((size_t)8 * std::max(cg_coop_grid(), cg_fused_max_grid()));
   // TRON_B200_CLUSTER_CG=0: the three-kernel large-n CG step for mid-size n too
   const char* cc = std::getenv("TRON_B200_CLUSTER_CG");
   mid_engine_ = !small_engine_ && n_ <= kClusterCgMaxN && !(cc && cc[0] == '0');
+  coop_engine_ = !small_engine_ && !mid_engine_ && !(co && co[0] == '0');
   // TRON_B200_NO_GRAPH=1 runs the CG loop host-driven (per-kernel profiling:
   // ncu cannot profile kernel nodes of graphs with conditional nodes).
   const char* ng = std::getenv("TRON_B200_NO_GRAPH");
@@ -396,7 +401,6 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     const char* fc = std::getenv("TRON_B200_FUSED_CG");
     e->fused_engine_ = !e->use_stream_ && !e->comm_.active() && !e->small_engine_ && fc &&
                        fc[0] == '1';
-    if (e->fused_engine_) e->fused_parts_.alloc((size_t)8 * cg_fused_max_grid());
     cuda_check(cudaStreamSynchronize(s), "csc build");
     cuda_check(cudaGetLastError(), "csc build");
     return e;
@@ -917,7 +921,7 @@ void Engine::launch_fused_cg(int k, bool use_m) {
   Cond none;
   cg_large_init(v, st_d_, sc_, none, s_);
   cg_fused(X_, Xt_, plan_, group_, v, lr ? S.dvec.p : nullptr, lr ? nullptr : S.mask.p, a_.p,
-           lr ? C_ : 2.0 * C_, fused_parts_.p, st_d_, s_);
+           lr ? C_ : 2.0 * C_, coop_parts_.p, st_d_, s_);
 }
 
 void Engine::build_graph(int k, bool use_m) {
@@ -969,7 +973,7 @@ void Engine::build_graph(int k, bool use_m) {
   cuda_check(cudaStreamUpdateCaptureDependencies(s_, &cond_node, 1,
                                                  cudaStreamSetCaptureDependencies),
              "update deps");
-  if (!small_engine_ && !mid_engine_) cg_large_post(v, st_d_, sc_, s_);
+  if (has_post_kernel()) cg_large_post(v, st_d_, sc_, s_);
   cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
 
   cudaGraph_t body = cp.conditional.phGraph_out[0];
@@ -993,6 +997,10 @@ void Engine::build_graph(int k, bool use_m) {
   } else if (mid_engine_) {
     hv_kernels(p_.p, hp_.p);
     cg_cluster_step(v, st_d_, cond, s_);
+    count_launch(1);
+  } else if (coop_engine_) {
+    hv_kernels(p_.p, hp_.p);
+    cg_coop_step(v, st_d_, coop_parts_.p, cond, s_);
     count_launch(1);
   } else {
     hv_kernels(p_.p, hp_.p);
@@ -1080,6 +1088,9 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
       count_launch(1);
     } else if (mid_engine_) {
       cg_cluster_step(v, st_d_, none, s_);
+      count_launch(1);
+    } else if (coop_engine_) {
+      cg_coop_step(v, st_d_, coop_parts_.p, none, s_);
       count_launch(1);
     } else {
       cg_large_php(v, st_d_, sc_, none, s_);

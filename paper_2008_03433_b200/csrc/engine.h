@@ -229,11 +229,14 @@ class Engine {
   uint64_t body_kernels_ = 0;
   bool small_engine_ = false;  // n <= kSmallCgMaxN: single-block CG step
   bool mid_engine_ = false;    // n <= kClusterCgMaxN: one 8-CTA cluster kernel per CG step
+  bool coop_engine_ = false;   // large n: one cooperative kernel per CG step (cg_coop_step)
   bool fused_engine_ = false;  // persistent cooperative CG kernel (cg_fused)
-  DevBuf<double> fused_parts_;
+  DevBuf<double> coop_parts_;  // CTA partials of both cooperative engines
   void launch_fused_cg(int k, bool use_m);
   // kernels after the loop body: cg_large_post, or the persistent kernel itself
-  bool has_post_kernel() const { return fused_engine_ || (!small_engine_ && !mid_engine_); }
+  bool has_post_kernel() const {
+    return fused_engine_ || (!small_engine_ && !mid_engine_ && !coop_engine_);
+  }
   bool use_graphs_ = true;
 };
 

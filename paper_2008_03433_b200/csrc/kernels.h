@@ -208,6 +208,10 @@ void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s);
 // Mid-n CG engine (kSmallCgMaxN < n <= kClusterCgMaxN): one kernel per iteration
 // on a cluster of 8 CTAs (vector phases + scalars; the exit's q(d), ||d|| included).
 constexpr int64_t kClusterCgMaxN = 262144;
+// One large-n CG iteration as a single cooperative kernel (vec_kernels.cu);
+// parts: 8 * cg_coop_grid() doubles.  Ends the loop itself (no post kernel).
+int cg_coop_grid();
+void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s);
 // Persistent cooperative CG over a sparse problem (csc_seg.cu): every CG
 // iteration of one truncated_cg in a single launch.  parts: 2 * 4 *
 // cg_fused_max_grid() doubles.  The caller runs cg_large_init first.

@@ -12,6 +12,8 @@
 //    not bandwidth, is the cost.
 // Both can run under a CUDA-graph while node: the kernel that decides
 // whether CG continues sets the conditional handle.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -659,6 +661,167 @@ void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjSc
 
 void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s) {
   launch_pdl(norm_check_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, g, obj, sc);
+}
+
+// ---------------- large-n CG: one cooperative kernel per iteration ----------------
+// The vector work of a CG iteration (tron.cpp:70-106) for n too large for one
+// cluster: p.Hp, then d += alpha p together with a speculative r -= alpha Hp
+// into the other parity buffer (one barrier serves ||d||, r.z and r.r), then
+// beta and p -- grid barriers instead of the three kernels and last-block
+// tickets of the cg_php / cg_update / cg_direction sequence.  Per-entry
+// arithmetic is theirs; totals come from grid_sums (fixed order).
+namespace {
+constexpr int kCoopBlock = 256;
+namespace cgg = cooperative_groups;
+
+__global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, CgState* st,
+                                                                 double* parts, Cond cond) {
+  cgg::grid_group grid = cgg::this_grid();
+  __shared__ double sh[kCoopBlock / kWarp + 1];
+  __shared__ double red[4];
+  const long long gt = blockIdx.x * (long long)kCoopBlock + threadIdx.x;
+  const long long NT = (long long)gridDim.x * kCoopBlock;
+  const double rz_old = st->rz, delta = st->delta, stop = st->stop;
+  const long long iters = st->iters + 1, max_iters = st->max_iters;
+  const int rpar = st->rpar;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  int buf = 0;
+  double* r = rpar ? v.r1 : v.r0;
+  double* rn = rpar ? v.r0 : v.r1;
+  // p.Hp (tron.cpp:71-75)
+  double x1[1] = {0.0};
+#pragma unroll 4
+  for (long long j = gt; j < v.n; j += NT) x1[0] += v.p[j] * v.hp[j];
+  grid_sums<kCoopBlock, 1>(x1, parts, buf, sh, red, grid);
+  const double php = x1[0];
+  if (!(php > 0.0)) {
+    if (lead) {
+      st->iters = iters;
+      st->php = php;
+      st->fail = 1;
+      st->cont = 0;
+      set_cond(cond, 0);
+    }
+    return;
+  }
+  const double alpha = rz_old / php;
+  // d += alpha p (tron.cpp:76-78); r -= alpha Hp, z = M^-1 r (tron.cpp:91-95)
+  double x2[3] = {0.0, 0.0, 0.0};
+#pragma unroll 4
+  for (long long j = gt; j < v.n; j += NT) {
+    const double dj = v.d[j] + alpha * v.p[j];
+    v.d[j] = dj;
+    x2[0] += dj * dj;
+    const double rj = r[j] + (-alpha) * v.hp[j];
+    rn[j] = rj;
+    const double z = v.M ? rj / v.M[j] : rj;
+    x2[1] += rj * z;
+    x2[2] += rj * rj;
+  }
+  grid_sums<kCoopBlock, 3>(x2, parts, buf, sh, red, grid);
+  if (sqrt(x2[0]) > delta) {
+    // boundary: retreat, then tau on ||d + tau p|| = delta (tron.cpp:78-90)
+    double x3[3] = {0.0, 0.0, 0.0};
+  #pragma unroll 4
+  for (long long j = gt; j < v.n; j += NT) {
+      const double pj = v.p[j];
+      const double dj = v.d[j] + (-alpha) * pj;
+      v.d[j] = dj;
+      x3[0] += dj * pj;
+      x3[1] += dj * dj;
+      x3[2] += pj * pj;
+    }
+    grid_sums<kCoopBlock, 3>(x3, parts, buf, sh, red, grid);
+    const double dp = x3[0], dd = x3[1], pp = x3[2];
+    const double rad = sqrt(dp * dp + pp * (delta * delta - dd));
+    const double tau = dp >= 0.0 ? (delta * delta - dd) / (dp + rad) : (rad - dp) / pp;
+    double x4[3] = {0.0, 0.0, 0.0};  // q(d) and ||d|| of the final step (tron.cpp:99-106)
+  #pragma unroll 4
+  for (long long j = gt; j < v.n; j += NT) {
+      const double dj = v.d[j] + tau * v.p[j];
+      const double rj = r[j] + (-tau) * v.hp[j];
+      v.d[j] = dj;
+      r[j] = rj;
+      x4[0] += dj * v.g[j];
+      x4[1] += dj * rj;
+      x4[2] += dj * dj;
+    }
+    grid_sums<kCoopBlock, 3>(x4, parts, buf, sh, red, grid);
+    if (lead) {
+      st->iters = iters;
+      st->php = php;
+      st->alpha = alpha;
+      st->tau = tau;
+      st->boundary = 1;
+      st->exit_kind = kCgBoundary;
+      st->q = 0.5 * (x4[0] - x4[1]);
+      st->dnorm = sqrt(x4[2]);
+      st->cont = 0;
+      set_cond(cond, 0);
+    }
+    return;
+  }
+  const double rz = x2[1], rnorm = sqrt(x2[2]);
+  const double beta = rz / rz_old;
+#pragma unroll 4
+  for (long long j = gt; j < v.n; j += NT) v.p[j] = zval(rn, v.M, j) + beta * v.p[j];  // tron.cpp:96
+  const int cont = (iters < max_iters) && !(rnorm <= stop);
+  if (!cont) {
+    // exit classification, q(d) = (d.g - d.r)/2, ||d|| (tron.cpp:97-106)
+    double x6[3] = {0.0, 0.0, 0.0};
+  #pragma unroll 4
+  for (long long j = gt; j < v.n; j += NT) {
+      const double dj = v.d[j];
+      x6[0] += dj * v.g[j];
+      x6[1] += dj * rn[j];
+      x6[2] += dj * dj;
+    }
+    grid_sums<kCoopBlock, 3>(x6, parts, buf, sh, red, grid);
+    if (lead) {
+      st->exit_kind = (iters >= max_iters && rnorm > stop) ? kCgMaxIters : kCgConverged;
+      st->q = 0.5 * (x6[0] - x6[1]);
+      st->dnorm = sqrt(x6[2]);
+    }
+  }
+  if (lead) {
+    st->iters = iters;
+    st->php = php;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->rz = rz;
+    st->rpar = rpar ^ 1;
+    st->rnorm = rnorm;
+    st->cont = cont;
+    set_cond(cond, cont);
+  }
+}
+}  // namespace
+
+#ifndef TB_COOP_PER_SM
+#define TB_COOP_PER_SM 4
+#endif
+// 4 CTAs of 8 warps per SM: the passes stream ~10 n-vectors from HBM and need
+// the loads in flight; more CTAs make each grid barrier dearer
+int cg_coop_grid() {
+  static const int g = [] {
+    int per_sm = 0;  // a cooperative grid must be co-resident
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_coop_step_kernel, kCoopBlock, 0);
+    return std::max(1, std::min(per_sm, TB_COOP_PER_SM)) * device_sm_count();
+  }();
+  return g;
+}
+
+void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cg_coop_grid());
+  cfg.blockDim = dim3(kCoopBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, cg_coop_step_kernel, v, st, parts, cond);
 }
 
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {

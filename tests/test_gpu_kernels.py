@@ -253,15 +253,18 @@ def test_device_cg_matches_host_cg(port, case, precond):
 
 # the CG engines on the same mid-size problem: the persistent cooperative
 # kernel (opt-in; in a graph and host-launched), single cluster kernel per step
-# (default for 4096 < n <= 262144), the three-kernel large-n step, and the
-# host-driven loop (no graph), each against the host restatement
-@pytest.mark.parametrize("engine", ["fused", "fused_nograph", "cluster", "large", "nograph"])
+# (default for 4096 < n <= 262144), the cooperative large-n step (default above),
+# the three-kernel large-n step, and the host-driven loop (no graph), each
+# against the host restatement
+@pytest.mark.parametrize("engine", ["fused", "fused_nograph", "cluster", "coop", "large", "nograph"])
 @pytest.mark.parametrize("precond", [False, True])
 def test_cg_engines_match_host_cg(port, monkeypatch, engine, precond):
     if engine.startswith("fused"):
         monkeypatch.setenv("TRON_B200_FUSED_CG", "1")
-    if engine == "large":
+    if engine in ("coop", "large"):
         monkeypatch.setenv("TRON_B200_CLUSTER_CG", "0")
+    if engine == "large":
+        monkeypatch.setenv("TRON_B200_COOP_CG", "0")
     if engine in ("nograph", "fused_nograph"):
         monkeypatch.setenv("TRON_B200_NO_GRAPH", "1")
     p = synth.synth_sparse(9, 2000, 5000, 37)  # n = 5000 > kSmallCgMaxN
