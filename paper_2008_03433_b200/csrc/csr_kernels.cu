@@ -188,10 +188,17 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
   }
 }
 
-int forward_grid(int64_t rows, int group) {
+// Rows are grid-strided, so the grid is capped at one wave of resident CTAs
+// of this kernel (a partial second wave would be a tail: measured on N1, the
+// forward kernel at 40 registers holds 6 CTAs per SM, not 8).
+template <class Kernel>
+int forward_grid(Kernel k, int64_t rows, int group) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, 0);
+  if (per_sm < 1) per_sm = 1;
   const int64_t rows_per_block = kBlock / group;
   int64_t want = (rows + rows_per_block - 1) / rows_per_block;
-  int64_t cap = (int64_t)device_sm_count() * 8;
+  const int64_t cap = (int64_t)device_sm_count() * per_sm;
   if (want > cap) want = cap;
   if (want < 1) want = 1;
   return (int)want;
@@ -362,15 +369,18 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
     }
     return;
   }
-  const int grid = forward_grid(X.rows, group);
   if (loss == kLossLogistic) {
-    TB_GROUP_DISPATCH(group, launch_pdl(csr_forward_kernel<GG, kLossLogistic, false>, dim3(grid),
-                                        dim3(kBlock), 0, s, X, 0, w, y, C, z, zhat, dvec, mask, obj,
-                                        sc));
+    TB_GROUP_DISPATCH(group, {
+      auto k = csr_forward_kernel<GG, kLossLogistic, false>;
+      launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, w, y, C, z,
+                 zhat, dvec, mask, obj, sc);
+    });
   } else {
-    TB_GROUP_DISPATCH(group, launch_pdl(csr_forward_kernel<GG, kLossSvm, false>, dim3(grid),
-                                        dim3(kBlock), 0, s, X, 0, w, y, C, z, zhat, dvec, mask, obj,
-                                        sc));
+    TB_GROUP_DISPATCH(group, {
+      auto k = csr_forward_kernel<GG, kLossSvm, false>;
+      launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, w, y, C, z,
+                 zhat, dvec, mask, obj, sc);
+    });
   }
 }
 
@@ -387,9 +397,10 @@ void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, co
     });
     return;
   }
-  const int grid = forward_grid(X.rows, group);
-  TB_GROUP_DISPATCH(group, launch_pdl(csr_dv_kernel<GG, false>, dim3(grid), dim3(kBlock), 0, s, X,
-                                      0, p, dvec, mask, a));
+  TB_GROUP_DISPATCH(group, {
+    auto k = csr_dv_kernel<GG, false>;
+    launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, p, dvec, mask, a);
+  });
 }
 
 int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s) {
