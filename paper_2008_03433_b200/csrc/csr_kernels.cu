@@ -224,8 +224,8 @@ __global__ void permute_kernel(const int32_t* perm, const int32_t* rowid, const 
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const int32_t k = perm[i];
-    ridx[i] = rowid[k];
-    cval[i] = val[k];
+    if (ridx) ridx[i] = rowid[k];
+    if (cval) cval[i] = val[k];
   }
 }
 
@@ -403,7 +403,12 @@ void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, co
   });
 }
 
-int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s) {
+// Structure of the CSC copy: a stable radix sort of the column indices (row
+// order kept inside a column), the row ids and the column pointers.  Needs
+// only X.ptr / X.idx, so the values can still be in flight on another stream;
+// *perm (nnz entries, freed by build_csc_values) maps CSC slots to CSR entries.
+int build_csc_structure(const CsrView& X, int32_t* cptr, int32_t* ridx, int32_t** perm,
+                        cudaStream_t s) {
   const long long nnz = X.nnz;
   int32_t *rowid = nullptr, *perm_in = nullptr, *perm_out = nullptr, *keys_out = nullptr;
   void* temp = nullptr;
@@ -411,6 +416,7 @@ int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cuda
   int end_bit = 1;
   while (end_bit < 31 && (1LL << end_bit) < X.cols) ++end_bit;
   cudaError_t e = cudaSuccess;
+  *perm = nullptr;
   if (nnz > 0) {
     e = cudaMallocAsync(&rowid, nnz * sizeof(int32_t), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&perm_in, nnz * sizeof(int32_t), s);
@@ -427,7 +433,7 @@ int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cuda
                                           (int)nnz, 0, end_bit, s);
     }
     if (e == cudaSuccess) {
-      permute_kernel<<<grid_for(nnz), 256, 0, s>>>(perm_out, rowid, X.val, ridx, cval, nnz);
+      permute_kernel<<<grid_for(nnz), 256, 0, s>>>(perm_out, rowid, nullptr, ridx, nullptr, nnz);
       col_ptr_kernel<<<grid_for(X.cols + 1), 256, 0, s>>>(keys_out, nnz, cptr, X.cols);
     }
   } else {
@@ -435,10 +441,22 @@ int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cuda
   }
   if (rowid) cudaFreeAsync(rowid, s);
   if (perm_in) cudaFreeAsync(perm_in, s);
-  if (perm_out) cudaFreeAsync(perm_out, s);
   if (keys_out) cudaFreeAsync(keys_out, s);
   if (temp) cudaFreeAsync(temp, s);
   if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess)
+    *perm = perm_out;
+  else if (perm_out)
+    cudaFreeAsync(perm_out, s);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+// Values of the CSC copy: cval[i] = val[perm[i]]; frees perm.
+int build_csc_values(int32_t* perm, const double* val, double* cval, int64_t nnz, cudaStream_t s) {
+  if (nnz > 0 && perm)
+    permute_kernel<<<grid_for(nnz), 256, 0, s>>>(perm, nullptr, val, nullptr, cval, nnz);
+  if (perm) cudaFreeAsync(perm, s);
+  const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
 

@@ -288,6 +288,32 @@ void Engine::common_alloc() {
   use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !(ng && ng[0] == '1');
 }
 
+// H2D of a buffer on a private stream ordered after everything issued on
+// `main` so far (allocations included); wait() makes `main` wait for it.
+struct ValueUpload {
+  cudaStream_t main, side = nullptr;
+  cudaEvent_t ev = nullptr;
+  explicit ValueUpload(cudaStream_t m) : main(m) {}
+  void start(void* dst, const void* src, size_t bytes) {
+    cuda_check(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(ev, main), "event record");
+    cuda_check(cudaStreamWaitEvent(side, ev, 0), "stream wait");
+    upload(dst, src, bytes, side);
+    cuda_check(cudaEventRecord(ev, side), "event record");
+  }
+  void wait() {
+    if (side) cuda_check(cudaStreamWaitEvent(main, ev, 0), "stream wait");
+  }
+  ~ValueUpload() {
+    if (side) {
+      cudaStreamWaitEvent(main, ev, 0);  // never leave the copy unordered
+      cudaStreamDestroy(side);
+    }
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+
 std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, const int64_t* ro,
                                            const int32_t* ci, const double* vals, const double* y,
                                            double C, const tron_gpu_options& opt) {
@@ -340,13 +366,10 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       ro64.alloc(l + 1);
       upload(ro64.p, ro, (l + 1) * sizeof(int64_t), s);
       narrow_offsets(ro64.p, e->rptr_.p, (int64_t)(l + 1), s);
-      if (nnz > 0) {
-        upload(e->cidx_.p, ci, nnz * sizeof(int32_t), s);
-        upload(e->rval_.p, vals, nnz * sizeof(double), s);
-      }
+      if (nnz > 0) upload(e->cidx_.p, ci, nnz * sizeof(int32_t), s);
       if (l > 0) upload(e->y_.p, y, l * sizeof(double), s);
     }
-    tr.mark("matrix alloc + H2D issue");
+    tr.mark("structure alloc + H2D issue");
     // O(nnz) column checks and the labels on the device; the host re-checks
     // the first offending row to raise the reference's exact error
     e->screen(e->rptr_.p, e->cidx_.p, (int64_t)l, (int64_t)n,
@@ -357,20 +380,33 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     if (!(C > 0.0)) raise(TRON_ERR_DIMENSION, "problem: C must be positive");  // loss.cpp:30
     tr.mark("device validation");
     e->X_ = CsrView{(int64_t)l, (int64_t)n, nnz, e->rptr_.p, e->cidx_.p, e->rval_.p};
-    const int rc = build_csc(e->X_, e->cptr_.p, e->ridx_.p, e->cval_.p, s);
-    if (rc != 0) cuda_check((cudaError_t)rc, "build_csc");
+    int32_t* perm = nullptr;
+    const int rc = build_csc_structure(e->X_, e->cptr_.p, e->ridx_.p, &perm, s);
+    if (rc != 0) cuda_check((cudaError_t)rc, "build_csc_structure");
+    // The values (2/3 of the bytes) go up on a second stream while the device
+    // sorts the structure and builds the segmented plan; only the value
+    // permutation waits for them.
+    ValueUpload vup(s);
+    if (nnz > 0) vup.start(e->rval_.p, vals, nnz * sizeof(double));
     if (nnz_pad > nnz) {
       cuda_check(cudaMemsetAsync(e->ridx_.p + nnz, 0, (nnz_pad - nnz) * sizeof(int32_t), s), "pad");
       cuda_check(cudaMemsetAsync(e->cval_.p + nnz, 0, (nnz_pad - nnz) * sizeof(double), s), "pad");
     }
     e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
-    tr.mark("device CSC build");
+    auto finish_values = [&] {
+      vup.wait();
+      const int vrc = build_csc_values(perm, e->rval_.p, e->cval_.p, nnz, s);
+      perm = nullptr;
+      if (vrc != 0) cuda_check((cudaError_t)vrc, "build_csc_values");
+    };
+    tr.mark("device CSC structure");
     // TRON_B200_SEG_STREAM=1: the TMA-streamed segmented kernels (seg_stream.cu).
     // Measured slower than the chunk-plan kernels on N1/R1/K1 (gather-bound, see
     // DESIGN.md §9), so the chunk-plan kernels are the default.
     const char* ss = std::getenv("TRON_B200_SEG_STREAM");
     e->use_stream_ = ss && ss[0] == '1';
     if (e->use_stream_) {
+      finish_values();
       // streamed layouts of both orientations, built on the device
       e->build_stream(e->xs_, e->rptr_.p, (int64_t)l, nnz, e->cidx_.p, e->rval_.p);
       e->build_stream(e->xts_, e->cptr_.p, (int64_t)n, nnz, e->ridx_.p, e->cval_.p);
@@ -393,6 +429,8 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
       tr.mark("segmented plan");
+      finish_values();
+      tr.mark("values H2D + CSC values");
     }
     e->group_ = choose_group((int64_t)l, nnz);
     // The persistent cooperative CG (cg_fused), opt-in (TRON_B200_FUSED_CG=1,

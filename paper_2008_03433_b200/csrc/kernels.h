@@ -156,7 +156,9 @@ void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squar
 
 // Device CSC construction from device CSR (stable in row order).
 // Returns 0 on success; temp storage allocated internally.
-int build_csc(const CsrView& X, int32_t* cptr, int32_t* ridx, double* cval, cudaStream_t s);
+int build_csc_structure(const CsrView& X, int32_t* cptr, int32_t* ridx, int32_t** perm,
+                        cudaStream_t s);
+int build_csc_values(int32_t* perm, const double* val, double* cval, int64_t nnz, cudaStream_t s);
 // Input screening: first_bad2[0] = first row whose columns are not strictly
 // ascending within [0, n) (ptr may be null: no matrix check), first_bad2[1] =
 // first label not in {-1, +1}; ~0 when none.  Offsets must already be valid.
