@@ -393,6 +393,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       cuda_check(cudaMemsetAsync(e->cval_.p + nnz, 0, (nnz_pad - nnz) * sizeof(double), s), "pad");
     }
     e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
+    e->group_ = choose_group((int64_t)l, nnz);
     auto finish_values = [&] {
       vup.wait();
       const int vrc = build_csc_values(perm, e->rval_.p, e->cval_.p, nnz, s);
@@ -429,16 +430,25 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
       tr.mark("segmented plan");
-      finish_values();
-      tr.mark("values H2D + CSC values");
     }
-    e->group_ = choose_group((int64_t)l, nnz);
     // The persistent cooperative CG (cg_fused), opt-in (TRON_B200_FUSED_CG=1,
     // any n above the single-block engine): measured 47 us per R1 CG iteration
     // against 40 us for the kernel-per-phase graph.
     const char* fc = std::getenv("TRON_B200_FUSED_CG");
     e->fused_engine_ = !e->use_stream_ && !e->comm_.active() && !e->small_engine_ && fc &&
                        fc[0] == '1';
+    if (!e->use_stream_) {
+      // The CG graphs of both slots (no preconditioner) are captured and
+      // instantiated while the values are still crossing PCIe: a recipe of
+      // fixed buffers, independent of their contents.
+      if (e->use_graphs_ && nnz > 0 && n > 0) {
+        e->build_graph(0, false);
+        e->build_graph(1, false);
+        tr.mark("CG graphs");
+      }
+      finish_values();
+      tr.mark("values H2D + CSC values");
+    }
     cuda_check(cudaStreamSynchronize(s), "csc build");
     cuda_check(cudaGetLastError(), "csc build");
     return e;
