@@ -76,14 +76,14 @@ __device__ __forceinline__ void grid_sums(double (&x)[K], double* parts, int& bu
     for (int k = 0; k < K; ++k) P[blockIdx.x * 4 + k] = x[k];
   }
   grid.sync();
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double t = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(P + b * 4 + k);
-      t = warp_allsum(t);
-      if (threadIdx.x == 0) red[k] = t;
-    }
+  static_assert(BLOCK >= 32 * K, "one warp per component");
+  if (threadIdx.x < 32 * K) {  // warp k adds component k; loads unrolled ahead of the adds
+    const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double t = 0.0;
+#pragma unroll 8
+    for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(P + b * 4 + k);
+    t = warp_allsum(t);
+    if (lane == 0) red[k] = t;
   }
   __syncthreads();
 #pragma unroll
