@@ -106,6 +106,30 @@ def test_synth_r1_full_size(ref):
     assert counts(r.trace) == counts(t_ref)
 
 
+def test_synth_n1_full_size_evaluator(ref):
+    """news20-shaped SYNTH-v1 (configs[1], the bench's default) at full size:
+    f, gradient, Hv and the preconditioner diagonal against the reference
+    evaluator on the same inputs -- the staged segmented CSC product, its
+    empty-column list and the fix-ups of Zipf-hot columns spanning hundreds of
+    chunks, the vectorised row products."""
+    p = synth.make_shape("N1")
+    n = p.X.cols
+    w = synth.testgen_random_vector(41, n, 0.01)
+    v = synth.testgen_random_vector(42, n, 1.0)
+    want = ref.logistic(p, w, v)
+    with make_evaluator(p, LR, plan()) as ev:
+        f = ev.eval_candidate(w)
+        ev.commit()
+        g, hv, M = ev.gradient(), ev.hessian_vec(v), ev.precond_diagonal()
+    assert rel_err(f, want["f"]) <= 1e-13
+    assert rel_err(g, want["g"]) <= 1e-12
+    assert rel_err(hv, want["hv"]) <= 1e-12
+    assert rel_err(M, want["M"]) <= 1e-12
+    cols_used = np.zeros(n, bool)
+    cols_used[p.X.col_indices] = True
+    assert np.array_equal(hv[~cols_used], v[~cols_used])  # empty columns: v + C*0
+
+
 def test_synth_p1_reduced_rows_active_set(ref):
     """proteomics-shaped dense L2-SVM (configs[2]) at 2e5 rows: active set + predictions."""
     p = synth.synth_dense(1, 200_000, 40)
