@@ -37,6 +37,8 @@ __device__ __forceinline__ void set_cond(Cond c, int v) {
   if (c.on) cudaGraphSetConditional((cudaGraphConditionalHandle)c.h, v ? 1u : 0u);
 }
 
+// (uses are unrolled by four: a thread keeps four iterations' loads in
+// flight; the per-thread summation order is unchanged)
 #define GRID_STRIDE(j, n)                                                       \
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < (n); \
        j += (long long)gridDim.x * blockDim.x)
@@ -48,6 +50,7 @@ __global__ void __launch_bounds__(kBlock) axpy_dot_kernel(long long n, const dou
   pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double acc = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, n) {
     const double v = d ? w[j] + d[j] : w[j];  // axpy_inplace(1.0, d, w_cand), tron.cpp:176-177
     wc[j] = v;
@@ -67,6 +70,7 @@ __global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const d
   pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double acc = 0.0, bad = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, n) {
     const double v = g[j];
     acc += v * v;
@@ -91,6 +95,7 @@ __global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const d
 __global__ void epilogue_kernel(long long n, const double* raw, EpiView E, double* out) {
   pdl_wait();
   pdl_trigger();
+#pragma unroll 4
   GRID_STRIDE(j, n) {
     const double s = raw ? raw[j] : 0.0;
     out[j] = E.kind == EPI_VEC ? E.base[j] + E.scale * s
@@ -110,6 +115,7 @@ __global__ void __launch_bounds__(kBlock) cg_init_kernel(CgVectors v, CgState* s
   pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double rz = 0.0, rr = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, v.n) {
     v.d[j] = 0.0;
     const double r = -v.g[j];
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(kBlock) cg_php_kernel(CgVectors v, CgState* st
   pdl_trigger();
   __shared__ double sh[kBlock / kWarp + 1];
   double acc = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, v.n) acc += v.p[j] * v.hp[j];
   const double b = block_sum<kBlock>(acc, sh, true);
   if (threadIdx.x == 0) sc.partials[blockIdx.x] = b;
@@ -184,6 +191,7 @@ __global__ void __launch_bounds__(kBlock) cg_update_kernel(CgVectors v, CgState*
   const double* rc = st->rpar ? v.r1 : v.r0;
   double* rn = st->rpar ? v.r0 : v.r1;
   double dd = 0.0, rz = 0.0, rr = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, v.n) {
     const double dj = v.d[j] + alpha * v.p[j];  // tron.cpp:77
     v.d[j] = dj;
@@ -234,12 +242,14 @@ __global__ void __launch_bounds__(kBlock) cg_direction_kernel(CgVectors v, CgSta
   if (!st->boundary) {
     const double beta = st->beta;
     const double* r = st->rpar ? v.r1 : v.r0;
+#pragma unroll 4
     GRID_STRIDE(j, v.n) v.p[j] = zval(r, v.M, j) + beta * v.p[j];  // tron.cpp:96
     return;
   }
   // Boundary: retreat, then solve for tau on ||d + tau p|| = delta (tron.cpp:78-90).
   const double alpha = st->alpha;
   double dp = 0.0, dd = 0.0, pp = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, v.n) {
     const double pj = v.p[j];
     const double dj = v.d[j] + (-alpha) * pj;
@@ -279,6 +289,7 @@ __global__ void __launch_bounds__(kBlock) cg_post_kernel(CgVectors v, CgState* s
   const double tau = st->tau;
   double* r = st->rpar ? v.r1 : v.r0;
   double dg = 0.0, dr = 0.0, dd = 0.0;
+#pragma unroll 4
   GRID_STRIDE(j, v.n) {
     double dj = v.d[j];
     double rj = r[j];
