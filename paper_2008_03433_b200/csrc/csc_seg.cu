@@ -145,7 +145,8 @@ __device__ __forceinline__ void gather_chunk(const UView& U, const EpiView& E, c
 template <bool SQ, int EPI, bool STAGED, bool COH>
 __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const EpiView& E,
                                               double* __restrict__ out, long long t,
-                                              const LaneChunk& cur, int lane, double* ebuf) {
+                                              const LaneChunk& cur, int lane, double* ebuf,
+                                              double& dacc) {
   double w[kSegLaneItems];
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; ++m)  // row_axpy / row_axpy_squared
@@ -199,15 +200,25 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
   const int nend = __shfl_sync(0xffffffffu, incl, 31);
   if (lane < nend) {
     const double v = ebuf[lane];
-    if (lane == 0 && cont_in)
+    if (lane == 0 && cont_in) {
       S.head[t] = v;  // row began in an earlier chunk: finished by the fix-up
-    else
-      out[cur.col[0]] = epi_apply<EPI>(E, cur.bv[0], v);
+    } else {
+      const double o = epi_apply<EPI>(E, cur.bv[0], v);
+      out[cur.col[0]] = o;
+      if (EPI == EPI_VEC && E.dot_parts) dacc += cur.bv[0] * o;
+    }
   }
-  if (lane + 32 < nend) out[cur.col[1]] = epi_apply<EPI>(E, cur.bv[1], ebuf[lane + 32]);
+  if (lane + 32 < nend) {
+    const double o = epi_apply<EPI>(E, cur.bv[1], ebuf[lane + 32]);
+    out[cur.col[1]] = o;
+    if (EPI == EPI_VEC && E.dot_parts) dacc += cur.bv[1] * o;
+  }
   for (int q = lane + 64; q < nend; q += 32) {
     const int j = __ldg(S.nz_col + chunk_rank + q);
-    out[j] = epi_apply<EPI>(E, epi_base<EPI, COH>(E, j), ebuf[q]);
+    const double bj = epi_base<EPI, COH>(E, j);
+    const double o = epi_apply<EPI>(E, bj, ebuf[q]);
+    out[j] = o;
+    if (EPI == EPI_VEC && E.dot_parts) dacc += bj * o;
   }
   if (lane == 0) S.carry[t] = tail;
   __syncwarp();  // the buffer is reused by the warp's next chunk
@@ -248,6 +259,24 @@ __device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, con
     load_chunk(A, S, t, lane, rank_of(t), b0);
     if (t + W < nch) load_chunk(A, S, t + W, lane, rank_of(t + W), b1);
   }
+  double dacc = 0.0;  // this lane's part of sum base_j * out_j (E.dot_parts)
+  // two buffers in ping-pong (unrolled by two: a register copy of a buffer
+  // whose loads are in flight would wait for them).
+  // chunk t: processed; t+W: gathered; t+2W: nonzeros in flight
+  auto seg_walk = [&](long long t) {
+#define TB_SEG_STEP(P, G)                                                      \
+  process_chunk<SQ, EPI, STAGED, COH>(A, S, E, out, t, P, lane, ebuf, dacc);   \
+  if (t + W >= nch) break;                                                     \
+  gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, G);                         \
+  if (t + 2 * W < nch) load_chunk(A, S, t + 2 * W, lane, rank_of(t + 2 * W), P); \
+  t += W;
+    gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, b0);
+    for (;;) {
+      TB_SEG_STEP(b0, b1)
+      TB_SEG_STEP(b1, b0)
+    }
+#undef TB_SEG_STEP
+  };
   if (STAGED) {
     if (UK == U_VEC) {
       bulk_stage_f64(su, U.u, A.cols);  // TMA bulk copy (UBLKCP)
@@ -269,26 +298,19 @@ __device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, con
     for (int m = 0; m < kEmptyItems; ++m) bb[m] = epi_base<EPI, COH>(E, e[m]);
 #pragma unroll
     for (int m = 0; m < kEmptyItems; ++m)
-      if (e[m] >= 0) out[e[m]] = epi_apply<EPI>(E, bb[m], 0.0);
+      if (e[m] >= 0) {
+        const double o = epi_apply<EPI>(E, bb[m], 0.0);
+        out[e[m]] = o;
+        if (EPI == EPI_VEC && E.dot_parts) dacc += bb[m] * o;
+      }
   }
-  if (t >= nch) return;  // warp-uniform
-
-  // two buffers in ping-pong (unrolled by two: a register copy of a buffer
-  // whose loads are in flight would wait for them).
-  // chunk t: processed; t+W: gathered; t+2W: nonzeros in flight
-#define TB_SEG_STEP(P, G)                                                      \
-  process_chunk<SQ, EPI, STAGED, COH>(A, S, E, out, t, P, lane, ebuf);         \
-  if (t + W >= nch) break;                                                     \
-  gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, G);                         \
-  if (t + 2 * W < nch) load_chunk(A, S, t + 2 * W, lane, rank_of(t + 2 * W), P); \
-  t += W;
-  gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, b0);
-  for (;;) {
-    TB_SEG_STEP(b0, b1)
-    TB_SEG_STEP(b1, b0)
+  if (t < nch) seg_walk(t);
+  if (EPI == EPI_VEC && E.dot_parts) {  // warp partial, fixed order
+    dacc = warp_sum(dacc);
+    if (lane == 0) E.dot_parts[gw] = dacc;
   }
-#undef TB_SEG_STEP
 }
+
 
 template <int UK, bool SQ, int EPI, bool STAGED>
 __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2)
@@ -314,14 +336,18 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock, STAGED ? 1 : 2
 constexpr int kFixSerial = 16;
 template <int EPI, bool COH>
 __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
-                                          double* __restrict__ out, long long t, int lane) {
+                                          double* __restrict__ out, long long t, int lane,
+                                          double& dacc) {
   const long long f = t < S.nchunks ? __ldg(S.chunk_first + t) : -1;
   const bool longspan = f >= 0 && t - f > kFixSerial;
   if (f >= 0 && !longspan) {
     double s = COH ? ld_coh(S.carry + f) : S.carry[f];
     for (long long v = f + 1; v < t; ++v) s = s + (COH ? ld_coh(S.carry + v) : S.carry[v]);
     const int j = S.nz_col[S.chunk_rank[t] & 0x7fffffffu];
-    out[j] = epi_apply<EPI>(E, epi_base<EPI, COH>(E, j), s + (COH ? ld_coh(S.head + t) : S.head[t]));
+    const double bj = epi_base<EPI, COH>(E, j);
+    const double o = epi_apply<EPI>(E, bj, s + (COH ? ld_coh(S.head + t) : S.head[t]));
+    out[j] = o;
+    if (EPI == EPI_VEC && E.dot_parts) dacc += bj * o;
   }
   unsigned todo = __ballot_sync(0xffffffffu, longspan);
   while (todo) {
@@ -334,18 +360,33 @@ __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
     s = warp_sum(s);  // valid in lane 0
     if (lane == 0) {
       const int j = S.nz_col[S.chunk_rank[tt] & 0x7fffffffu];
-      out[j] = epi_apply<EPI>(E, epi_base<EPI, COH>(E, j),
-                              s + (COH ? ld_coh(S.head + tt) : S.head[tt]));
+      const double bj = epi_base<EPI, COH>(E, j);
+      const double o = epi_apply<EPI>(E, bj, s + (COH ? ld_coh(S.head + tt) : S.head[tt]));
+      out[j] = o;
+      if (EPI == EPI_VEC && E.dot_parts) dacc += bj * o;
     }
   }
 }
 
 template <int EPI>
 __global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out, long long Wseg) {
   pdl_wait();
   pdl_trigger();
-  fixup_one<EPI, false>(S, E, out, blockIdx.x * (long long)kBlock + threadIdx.x, threadIdx.x & 31);
+  double dacc = 0.0;
+  fixup_one<EPI, false>(S, E, out, blockIdx.x * (long long)kBlock + threadIdx.x, threadIdx.x & 31,
+                        dacc);
+  if (EPI == EPI_VEC && E.dot_parts) {
+    // this CTA's fix-ups, then the last CTA adds every partial in index order:
+    // [0, Wseg) the segmented kernel's warps, then the fix-up CTAs
+    __shared__ double sh[kBlock / kWarp + 1];
+    const double b = block_sum<kBlock>(dacc, sh);
+    if (threadIdx.x == 0) E.dot_parts[Wseg + blockIdx.x] = b;
+    if (last_block_arrive(E.dot_ticket)) {
+      const double tot = reduce_partials<kBlock>(E.dot_parts, (int)(Wseg + gridDim.x), 1, 0, sh);
+      if (threadIdx.x == 0) *E.dot_out = tot;
+    }
+  }
 }
 
 template <int UK, bool SQ, int EPI, bool STAGED>
@@ -372,8 +413,11 @@ void launch_one(const CsrView& A, const SegView& S, const UView& U, const EpiVie
   if (grid > cap) grid = cap;
   launch_pdl(seg_spmv_kernel<UK, SQ, EPI, STAGED>, dim3((int)grid), dim3(BLK), smem, s, A, S, U, E,
              out);
-  const int fgrid = (int)((S.nchunks + kBlock - 1) / kBlock);
-  if (fgrid) launch_pdl(seg_fixup_kernel<EPI>, dim3(fgrid), dim3(kBlock), 0, s, S, E, out);
+  // the fix-up kernel also finishes E.dot_out, so it always runs when asked to
+  int fgrid = (int)((S.nchunks + kBlock - 1) / kBlock);
+  if (E.dot_parts && fgrid == 0) fgrid = 1;
+  const long long Wseg = grid * (BLK / 32);
+  if (fgrid) launch_pdl(seg_fixup_kernel<EPI>, dim3(fgrid), dim3(kBlock), 0, s, S, E, out, Wseg);
 }
 
 template <int UK, bool SQ, int EPI>
@@ -624,8 +668,9 @@ __global__ void __launch_bounds__(kFusedBlock, 2) cg_fused_kernel(FusedCg F) {
     stamp(3);
     grid.sync();
     stamp(4);
+    double fix_dacc = 0.0;
     for (long long b = gw * 32; b < F.S.nchunks; b += W * 32)
-      fixup_one<EPI_VEC, true>(F.S, E, v.hp, b + lane, lane);
+      fixup_one<EPI_VEC, true>(F.S, E, v.hp, b + lane, lane, fix_dacc);
     grid.sync();
     stamp(5);
     // p.Hp (tron.cpp:71-75)
@@ -784,6 +829,11 @@ void cg_fused(const CsrView& X, const CsrView& At, const SegView& S, int group, 
     case 4: launch_fused<4>(F, s); break;
     default: launch_fused<2>(F, s); break;
   }
+}
+
+int64_t seg_dot_slots(int64_t nchunks) {
+  // segmented warps (16 per SM in either variant) + fix-up CTAs
+  return (int64_t)device_sm_count() * 16 + (nchunks + kBlock - 1) / kBlock + 1;
 }
 
 void csc_spmv(const CsrView& At, const SegView& S, const UView& U, bool squared,

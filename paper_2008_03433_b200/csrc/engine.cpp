@@ -429,6 +429,12 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       if (prc != 0) cuda_check((cudaError_t)prc, "seg_plan_device");
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
+      if (e->coop_engine_ && !e->comm_.active()) {  // p.Hp summed by the Hv kernels
+        e->dot_parts_.alloc(seg_dot_slots(nch));
+        e->dot_out_.alloc(1);
+        e->dot_ticket_.alloc(1);
+        cuda_check(cudaMemsetAsync(e->dot_ticket_.p, 0, sizeof(unsigned), s), "memset");
+      }
       tr.mark("segmented plan");
     }
     // The persistent cooperative CG (cg_fused), opt-in (TRON_B200_FUSED_CG=1,
@@ -853,12 +859,21 @@ void Engine::gradient_host(double* g) {
 // ----------------------------------------------------------------------------
 // Hv (loss.cpp:82-92 / :139-174) and preconditioner (loss.cpp:176-188)
 // ----------------------------------------------------------------------------
-void Engine::hv_kernels(const double* v, double* out) {
+bool Engine::hv_dot_available() const {
+  return !dense_ && !use_stream_ && !comm_.active() && dot_parts_.n > 0;
+}
+
+void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   const Slot& S = slot_[cand_ ^ 1];
   EpiView epi;
   epi.kind = EPI_VEC;
   epi.base = v;
   epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+  if (with_dot) {  // v . out, summed as out is emitted (the CG's p.Hp)
+    epi.dot_parts = dot_parts_.p;
+    epi.dot_out = dot_out_.p;
+    epi.dot_ticket = dot_ticket_.p;
+  }
   if (dense_) {
     dense_vector(DA_HV, v, epi, out);
     return;
@@ -1047,8 +1062,9 @@ void Engine::build_graph(int k, bool use_m) {
     cg_cluster_step(v, st_d_, cond, s_);
     count_launch(1);
   } else if (coop_engine_) {
-    hv_kernels(p_.p, hp_.p);
-    cg_coop_step(v, st_d_, coop_parts_.p, cond, s_);
+    const bool dot = hv_dot_available();
+    hv_kernels(p_.p, hp_.p, dot);
+    cg_coop_step(v, st_d_, coop_parts_.p, cond, s_, dot ? dot_out_.p : nullptr);
     count_launch(1);
   } else {
     hv_kernels(p_.p, hp_.p);
@@ -1138,7 +1154,7 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
       cg_cluster_step(v, st_d_, none, s_);
       count_launch(1);
     } else if (coop_engine_) {
-      cg_coop_step(v, st_d_, coop_parts_.p, none, s_);
+      cg_coop_step(v, st_d_, coop_parts_.p, none, s_);  // (the host loop's Hv ran without the dot)
       count_launch(1);
     } else {
       cg_large_php(v, st_d_, sc_, none, s_);

@@ -159,7 +159,7 @@ class Engine {
   bool enqueue_cg(double delta, const tron_config& cfg, CgState* out);
   double candidate_result();
   void adopt_candidate();
-  void hv_kernels(const double* v, double* out);  // enqueue only
+  void hv_kernels(const double* v, double* out, bool with_dot = false);  // enqueue only
   void gather_active();
   int compact(const Slot& S, DevBuf<int32_t>& idx);
   void read_obj();
@@ -230,6 +230,9 @@ class Engine {
   bool small_engine_ = false;  // n <= kSmallCgMaxN: single-block CG step
   bool mid_engine_ = false;    // n <= kClusterCgMaxN: one 8-CTA cluster kernel per CG step
   bool coop_engine_ = false;   // large n: one cooperative kernel per CG step (cg_coop_step)
+  DevBuf<double> dot_parts_, dot_out_;  // p.Hp from the Hv emission (EpiView::dot_*)
+  DevBuf<unsigned> dot_ticket_;
+  bool hv_dot_available() const;
   bool fused_engine_ = false;  // persistent cooperative CG kernel (cg_fused)
   DevBuf<double> coop_parts_;  // CTA partials of both cooperative engines
   void launch_fused_cg(int k, bool use_m);

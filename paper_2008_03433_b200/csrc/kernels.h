@@ -99,6 +99,12 @@ struct EpiView {
   const double* base = nullptr;
   double cbase = 0.0;
   double scale = 1.0;
+  // EPI_VEC only: also sum base_j * out_j over every j (p.Hp when base = p),
+  // per warp into dot_parts, finished in a fixed order into *dot_out by the
+  // fix-up kernel's last CTA.  dot_parts: seg_dot_slots(nchunks) doubles.
+  double* dot_parts = nullptr;
+  double* dot_out = nullptr;
+  unsigned* dot_ticket = nullptr;
 };
 
 constexpr int kCgConverged = 0;  // CgExit, tron.hpp:29
@@ -151,6 +157,7 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
 void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
             double* a, cudaStream_t s);
 // Transposed product over the CSC copy (csc_seg.cu; segmented chunks, atomic-free).
+int64_t seg_dot_slots(int64_t nchunks);
 void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squared,
               const EpiView& epi, double* out, cudaStream_t s);
 
@@ -213,7 +220,9 @@ constexpr int64_t kClusterCgMaxN = 262144;
 // One large-n CG iteration as a single cooperative kernel (vec_kernels.cu);
 // parts: 8 * cg_coop_grid() doubles.  Ends the loop itself (no post kernel).
 int cg_coop_grid();
-void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s);
+// php_in: p.Hp already summed by the Hv kernels (EpiView::dot_out), or null.
+void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s,
+                  const double* php_in = nullptr);
 // Persistent cooperative CG over a sparse problem (csc_seg.cu): every CG
 // iteration of one truncated_cg in a single launch.  parts: 2 * 4 *
 // cg_fused_max_grid() doubles.  The caller runs cg_large_init first.

@@ -686,7 +686,8 @@ constexpr int kCoopBlock = 256;
 namespace cgg = cooperative_groups;
 
 __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, CgState* st,
-                                                                 double* parts, Cond cond) {
+                                                                 double* parts, Cond cond,
+                                                                 const double* php_in) {
   cgg::grid_group grid = cgg::this_grid();
   __shared__ double sh[kCoopBlock / kWarp + 1];
   __shared__ double red[4];
@@ -699,12 +700,18 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
   int buf = 0;
   double* r = rpar ? v.r1 : v.r0;
   double* rn = rpar ? v.r0 : v.r1;
-  // p.Hp (tron.cpp:71-75)
-  double x1[1] = {0.0};
+  // p.Hp (tron.cpp:71-75): summed by the Hv kernels as they emitted hp
+  // (php_in), else a pass over p and hp
+  double php;
+  if (php_in) {
+    php = *php_in;
+  } else {
+    double x1[1] = {0.0};
 #pragma unroll 4
-  for (long long j = gt; j < v.n; j += NT) x1[0] += v.p[j] * v.hp[j];
-  grid_sums<kCoopBlock, 1>(x1, parts, buf, sh, red, grid);
-  const double php = x1[0];
+    for (long long j = gt; j < v.n; j += NT) x1[0] += v.p[j] * v.hp[j];
+    grid_sums<kCoopBlock, 1>(x1, parts, buf, sh, red, grid);
+    php = x1[0];
+  }
   if (!(php > 0.0)) {
     if (lead) {
       st->iters = iters;
@@ -822,7 +829,8 @@ int cg_coop_grid() {
   return g;
 }
 
-void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s) {
+void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s,
+                  const double* php_in) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cg_coop_grid());
   cfg.blockDim = dim3(kCoopBlock);
@@ -832,7 +840,7 @@ void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cud
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, cg_coop_step_kernel, v, st, parts, cond);
+  cudaLaunchKernelEx(&cfg, cg_coop_step_kernel, v, st, parts, cond, php_in);
 }
 
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {
