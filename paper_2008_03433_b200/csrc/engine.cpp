@@ -1258,6 +1258,35 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   }
   double delta = gnorm0;
   const bool speculative = !(loss_ == TRON_LOSS_L2SVM && svm_strategy_ == TRON_SVM_GATHERED);
+  // TRON_B200_TRACE=1: device time of each outer iteration's phases on stderr
+  struct OuterProf {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    cudaEvent_t e[4] = {};
+    std::chrono::steady_clock::time_point h0;
+    void rec(int i) {
+      if (i == 0) h0 = std::chrono::steady_clock::now();
+      cudaEventRecord(e[i], s);
+    }
+    void report(uint64_t it) {
+      float cg = 0, fw = 0, gr = 0;
+      cudaEventElapsedTime(&cg, e[0], e[1]);
+      cudaEventElapsedTime(&fw, e[1], e[2]);
+      cudaEventElapsedTime(&gr, e[2], e[3]);
+      const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+      std::fprintf(stderr, "[tron_b200] outer %llu: cg %.3f fwd %.3f grad %.3f ms (wall %.3f)\n",
+                   (unsigned long long)it, cg, fw, gr, wall);
+    }
+    ~OuterProf() {
+      for (auto& x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } prof;
+  if (const char* tr = std::getenv("TRON_B200_TRACE"); tr && tr[0] == '1') {
+    prof.on = true;
+    prof.s = s_;
+    for (auto& x : prof.e) cudaEventCreate(&x);
+  }
   while (info->n_iterations < cfg.max_outer_iters) {
     // One host round trip per outer iteration: the CG loop, the candidate's
     // margin pass and -- speculatively -- the candidate's gradient are queued
@@ -1265,16 +1294,21 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     // The gradient is adopted only if the step is accepted (the reference's
     // lazy gradient, backend.cpp:165-183; ledger counts adoptions).
     CgState st;
+    if (prof.on) prof.rec(0);
     const bool cg_done = enqueue_cg(delta, cfg, &st);
     double f_cand;
     if (speculative) {
       const int k = cand_ ^ 1;
+      if (prof.on) prof.rec(1);
       f_cand = eval_candidate_dev(d_.p, /*read=*/false);
+      if (prof.on) prof.rec(2);
       gradient_into(slot_[cand_], gspec_.p);
+      if (prof.on) prof.rec(3);
       if (!cg_done)
         cuda_check(cudaMemcpyAsync(st_h_, st_d_, sizeof(CgState), cudaMemcpyDeviceToHost, s_),
                    "D2H");
       read_obj();
+      if (prof.on) prof.report(info->n_iterations);
       if (!cg_done) {
         st = *st_h_;
         launches += 1 + (uint64_t)st.iters * body_kernels_ + (has_post_kernel() ? 1 : 0);
