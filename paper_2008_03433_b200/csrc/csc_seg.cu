@@ -50,6 +50,20 @@ __device__ __forceinline__ void ld4(const int* p, int& a, int& b, int& c, int& d
                : "l"(p));
 }
 
+// Reduction over the emitted values (EpiView::dot_*): dacc gathers
+// base_j * out_j (mode 0) or out_j^2 (mode 1), bad counts non-finite out_j.
+struct DotAcc {
+  double acc = 0.0, bad = 0.0;
+  __device__ __forceinline__ void add(const EpiView& E, double b, double o) {
+    if (E.dot_mode == 0) {
+      acc += b * o;
+    } else {
+      acc += o * o;
+      if (!isfinite(o)) bad = 1.0;
+    }
+  }
+};
+
 // Epilogue out_j = base_j + scale*sum (VEC), cbase + scale*sum (CONST) or
 // sum (RAW); base_j is requested early (epi_base) and applied at emission.
 // COH (persistent CG kernel): the vector is written inside the same kernel by
@@ -146,7 +160,7 @@ template <bool SQ, int EPI, bool STAGED, bool COH>
 __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S, const EpiView& E,
                                               double* __restrict__ out, long long t,
                                               const LaneChunk& cur, int lane, double* ebuf,
-                                              double& dacc) {
+                                              DotAcc& dacc) {
   double w[kSegLaneItems];
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; ++m)  // row_axpy / row_axpy_squared
@@ -205,20 +219,20 @@ __device__ __forceinline__ void process_chunk(const CsrView& A, const SegView& S
     } else {
       const double o = epi_apply<EPI>(E, cur.bv[0], v);
       out[cur.col[0]] = o;
-      if (EPI == EPI_VEC && E.dot_parts) dacc += cur.bv[0] * o;
+      if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, cur.bv[0], o);
     }
   }
   if (lane + 32 < nend) {
     const double o = epi_apply<EPI>(E, cur.bv[1], ebuf[lane + 32]);
     out[cur.col[1]] = o;
-    if (EPI == EPI_VEC && E.dot_parts) dacc += cur.bv[1] * o;
+    if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, cur.bv[1], o);
   }
   for (int q = lane + 64; q < nend; q += 32) {
     const int j = __ldg(S.nz_col + chunk_rank + q);
     const double bj = epi_base<EPI, COH>(E, j);
     const double o = epi_apply<EPI>(E, bj, ebuf[q]);
     out[j] = o;
-    if (EPI == EPI_VEC && E.dot_parts) dacc += bj * o;
+    if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, bj, o);
   }
   if (lane == 0) S.carry[t] = tail;
   __syncwarp();  // the buffer is reused by the warp's next chunk
@@ -259,7 +273,7 @@ __device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, con
     load_chunk(A, S, t, lane, rank_of(t), b0);
     if (t + W < nch) load_chunk(A, S, t + W, lane, rank_of(t + W), b1);
   }
-  double dacc = 0.0;  // this lane's part of sum base_j * out_j (E.dot_parts)
+  DotAcc dacc;  // this lane's part of the emission reduction (E.dot_parts)
   // two buffers in ping-pong (unrolled by two: a register copy of a buffer
   // whose loads are in flight would wait for them).
   // chunk t: processed; t+W: gathered; t+2W: nonzeros in flight
@@ -301,13 +315,16 @@ __device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, con
       if (e[m] >= 0) {
         const double o = epi_apply<EPI>(E, bb[m], 0.0);
         out[e[m]] = o;
-        if (EPI == EPI_VEC && E.dot_parts) dacc += bb[m] * o;
+        if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, bb[m], o);
       }
   }
   if (t < nch) seg_walk(t);
   if (EPI == EPI_VEC && E.dot_parts) {  // warp partial, fixed order
-    dacc = warp_sum(dacc);
-    if (lane == 0) E.dot_parts[gw] = dacc;
+    const double a = warp_sum(dacc.acc), b = warp_sum(dacc.bad);
+    if (lane == 0) {
+      E.dot_parts[2 * gw] = a;
+      E.dot_parts[2 * gw + 1] = b;
+    }
   }
 }
 
@@ -337,7 +354,7 @@ constexpr int kFixSerial = 16;
 template <int EPI, bool COH>
 __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
                                           double* __restrict__ out, long long t, int lane,
-                                          double& dacc) {
+                                          DotAcc& dacc) {
   const long long f = t < S.nchunks ? __ldg(S.chunk_first + t) : -1;
   const bool longspan = f >= 0 && t - f > kFixSerial;
   if (f >= 0 && !longspan) {
@@ -347,7 +364,7 @@ __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
     const double bj = epi_base<EPI, COH>(E, j);
     const double o = epi_apply<EPI>(E, bj, s + (COH ? ld_coh(S.head + t) : S.head[t]));
     out[j] = o;
-    if (EPI == EPI_VEC && E.dot_parts) dacc += bj * o;
+    if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, bj, o);
   }
   unsigned todo = __ballot_sync(0xffffffffu, longspan);
   while (todo) {
@@ -363,7 +380,7 @@ __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
       const double bj = epi_base<EPI, COH>(E, j);
       const double o = epi_apply<EPI>(E, bj, s + (COH ? ld_coh(S.head + tt) : S.head[tt]));
       out[j] = o;
-      if (EPI == EPI_VEC && E.dot_parts) dacc += bj * o;
+      if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, bj, o);
     }
   }
 }
@@ -373,18 +390,31 @@ __global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
                                                           double* __restrict__ out, long long Wseg) {
   pdl_wait();
   pdl_trigger();
-  double dacc = 0.0;
+  DotAcc dacc;
   fixup_one<EPI, false>(S, E, out, blockIdx.x * (long long)kBlock + threadIdx.x, threadIdx.x & 31,
                         dacc);
   if (EPI == EPI_VEC && E.dot_parts) {
     // this CTA's fix-ups, then the last CTA adds every partial in index order:
     // [0, Wseg) the segmented kernel's warps, then the fix-up CTAs
     __shared__ double sh[kBlock / kWarp + 1];
-    const double b = block_sum<kBlock>(dacc, sh);
-    if (threadIdx.x == 0) E.dot_parts[Wseg + blockIdx.x] = b;
+    const double a = block_sum<kBlock>(dacc.acc, sh);
+    const double b = block_sum<kBlock>(dacc.bad, sh);
+    if (threadIdx.x == 0) {
+      E.dot_parts[2 * (Wseg + blockIdx.x)] = a;
+      E.dot_parts[2 * (Wseg + blockIdx.x) + 1] = b;
+    }
     if (last_block_arrive(E.dot_ticket)) {
-      const double tot = reduce_partials<kBlock>(E.dot_parts, (int)(Wseg + gridDim.x), 1, 0, sh);
-      if (threadIdx.x == 0) *E.dot_out = tot;
+      const int cnt = (int)(Wseg + gridDim.x);
+      const double tot = reduce_partials<kBlock>(E.dot_parts, cnt, 2, 0, sh);
+      const double nb = reduce_partials<kBlock>(E.dot_parts, cnt, 2, 1, sh);
+      if (threadIdx.x == 0) {
+        if (E.dot_mode == 0) {
+          *E.dot_out = tot;
+        } else {
+          E.dot_obj->gnorm = sqrt(tot);
+          E.dot_obj->grad_nonfinite = nb > 0.0;
+        }
+      }
     }
   }
 }
@@ -668,7 +698,7 @@ __global__ void __launch_bounds__(kFusedBlock, 2) cg_fused_kernel(FusedCg F) {
     stamp(3);
     grid.sync();
     stamp(4);
-    double fix_dacc = 0.0;
+    DotAcc fix_dacc;
     for (long long b = gw * 32; b < F.S.nchunks; b += W * 32)
       fixup_one<EPI_VEC, true>(F.S, E, v.hp, b + lane, lane, fix_dacc);
     grid.sync();
@@ -832,8 +862,8 @@ void cg_fused(const CsrView& X, const CsrView& At, const SegView& S, int group, 
 }
 
 int64_t seg_dot_slots(int64_t nchunks) {
-  // segmented warps (16 per SM in either variant) + fix-up CTAs
-  return (int64_t)device_sm_count() * 16 + (nchunks + kBlock - 1) / kBlock + 1;
+  // doubles: 2 per slot; segmented warps (16 per SM in either variant) + fix-up CTAs
+  return 2 * ((int64_t)device_sm_count() * 16 + (nchunks + kBlock - 1) / kBlock + 1);
 }
 
 void csc_spmv(const CsrView& At, const SegView& S, const UView& U, bool squared,

@@ -429,7 +429,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       if (prc != 0) cuda_check((cudaError_t)prc, "seg_plan_device");
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
-      if (e->coop_engine_ && !e->comm_.active()) {  // p.Hp summed by the Hv kernels
+      if (!e->comm_.active()) {  // p.Hp / ||g|| summed by the transposed kernels
         e->dot_parts_.alloc(seg_dot_slots(nch));
         e->dot_out_.alloc(1);
         e->dot_ticket_.alloc(1);
@@ -778,6 +778,14 @@ void Engine::gradient_into(const Slot& S, double* out) {
       u.mask = S.mask.p;
       u.z = S.z.p;
       u.y = y_.p;
+    }
+    if (hv_dot_available()) {  // ||g|| and the finiteness check from the emission
+      epi.dot_parts = dot_parts_.p;
+      epi.dot_ticket = dot_ticket_.p;
+      epi.dot_mode = 1;
+      epi.dot_obj = obj_d_;
+      transposed_raw_or_epi(u, false, epi, out);
+      return;
     }
     transposed_raw_or_epi(u, false, epi, out);
   }

@@ -99,12 +99,17 @@ struct EpiView {
   const double* base = nullptr;
   double cbase = 0.0;
   double scale = 1.0;
-  // EPI_VEC only: also sum base_j * out_j over every j (p.Hp when base = p),
-  // per warp into dot_parts, finished in a fixed order into *dot_out by the
-  // fix-up kernel's last CTA.  dot_parts: seg_dot_slots(nchunks) doubles.
+  // EPI_VEC only: also reduce over every emitted out_j, per warp into
+  // dot_parts (2 doubles per slot; seg_dot_slots(nchunks) doubles), finished in
+  // a fixed order by the fix-up kernel's last CTA:
+  //   dot_mode 0: sum base_j * out_j -> *dot_out (p.Hp when base = p);
+  //   dot_mode 1: sum out_j^2 and any non-finite out_j -> dot_obj->gnorm,
+  //               dot_obj->grad_nonfinite (the gradient's norm check).
   double* dot_parts = nullptr;
   double* dot_out = nullptr;
   unsigned* dot_ticket = nullptr;
+  int dot_mode = 0;
+  struct ObjScalars* dot_obj = nullptr;
 };
 
 constexpr int kCgConverged = 0;  // CgExit, tron.hpp:29
