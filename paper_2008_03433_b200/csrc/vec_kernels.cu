@@ -698,8 +698,15 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
   const int rpar = st->rpar;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   int buf = 0;
-  double* r = rpar ? v.r1 : v.r0;
-  double* rn = rpar ? v.r0 : v.r1;
+  // distinct buffers: restrict lets the unrolled passes issue the next
+  // iterations' loads ahead of this iteration's stores
+  double* __restrict__ r = rpar ? v.r1 : v.r0;
+  double* __restrict__ rn = rpar ? v.r0 : v.r1;
+  double* __restrict__ vd = v.d;
+  double* __restrict__ vp = v.p;
+  const double* __restrict__ vhp = v.hp;
+  const double* __restrict__ vM = v.M;
+  const double* __restrict__ vg = v.g;
   // p.Hp (tron.cpp:71-75): summed by the Hv kernels as they emitted hp
   // (php_in), else a pass over p and hp
   double php;
@@ -708,7 +715,7 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
   } else {
     double x1[1] = {0.0};
 #pragma unroll 4
-    for (long long j = gt; j < v.n; j += NT) x1[0] += v.p[j] * v.hp[j];
+    for (long long j = gt; j < v.n; j += NT) x1[0] += vp[j] * vhp[j];
     grid_sums<kCoopBlock, 1>(x1, parts, buf, sh, red, grid);
     php = x1[0];
   }
@@ -727,12 +734,12 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
   double x2[3] = {0.0, 0.0, 0.0};
 #pragma unroll 4
   for (long long j = gt; j < v.n; j += NT) {
-    const double dj = v.d[j] + alpha * v.p[j];
-    v.d[j] = dj;
+    const double dj = vd[j] + alpha * vp[j];
+    vd[j] = dj;
     x2[0] += dj * dj;
-    const double rj = r[j] + (-alpha) * v.hp[j];
+    const double rj = r[j] + (-alpha) * vhp[j];
     rn[j] = rj;
-    const double z = v.M ? rj / v.M[j] : rj;
+    const double z = vM ? rj / vM[j] : rj;
     x2[1] += rj * z;
     x2[2] += rj * rj;
   }
@@ -742,9 +749,9 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
     double x3[3] = {0.0, 0.0, 0.0};
   #pragma unroll 4
   for (long long j = gt; j < v.n; j += NT) {
-      const double pj = v.p[j];
-      const double dj = v.d[j] + (-alpha) * pj;
-      v.d[j] = dj;
+      const double pj = vp[j];
+      const double dj = vd[j] + (-alpha) * pj;
+      vd[j] = dj;
       x3[0] += dj * pj;
       x3[1] += dj * dj;
       x3[2] += pj * pj;
@@ -756,11 +763,11 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
     double x4[3] = {0.0, 0.0, 0.0};  // q(d) and ||d|| of the final step (tron.cpp:99-106)
   #pragma unroll 4
   for (long long j = gt; j < v.n; j += NT) {
-      const double dj = v.d[j] + tau * v.p[j];
-      const double rj = r[j] + (-tau) * v.hp[j];
-      v.d[j] = dj;
+      const double dj = vd[j] + tau * vp[j];
+      const double rj = r[j] + (-tau) * vhp[j];
+      vd[j] = dj;
       r[j] = rj;
-      x4[0] += dj * v.g[j];
+      x4[0] += dj * vg[j];
       x4[1] += dj * rj;
       x4[2] += dj * dj;
     }
@@ -782,15 +789,15 @@ __global__ void __launch_bounds__(kCoopBlock) cg_coop_step_kernel(CgVectors v, C
   const double rz = x2[1], rnorm = sqrt(x2[2]);
   const double beta = rz / rz_old;
 #pragma unroll 4
-  for (long long j = gt; j < v.n; j += NT) v.p[j] = zval(rn, v.M, j) + beta * v.p[j];  // tron.cpp:96
+  for (long long j = gt; j < v.n; j += NT) vp[j] = (vM ? rn[j] / vM[j] : rn[j]) + beta * vp[j];  // tron.cpp:96
   const int cont = (iters < max_iters) && !(rnorm <= stop);
   if (!cont) {
     // exit classification, q(d) = (d.g - d.r)/2, ||d|| (tron.cpp:97-106)
     double x6[3] = {0.0, 0.0, 0.0};
   #pragma unroll 4
   for (long long j = gt; j < v.n; j += NT) {
-      const double dj = v.d[j];
-      x6[0] += dj * v.g[j];
+      const double dj = vd[j];
+      x6[0] += dj * vg[j];
       x6[1] += dj * rn[j];
       x6[2] += dj * dj;
     }
