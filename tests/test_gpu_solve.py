@@ -130,6 +130,26 @@ def test_synth_n1_full_size_evaluator(ref):
     assert np.array_equal(hv[~cols_used], v[~cols_used])  # empty columns: v + C*0
 
 
+@pytest.mark.parametrize("loss,precond", [(0, False), (1, False), (1, True)])
+def test_large_n_sparse_solve_cooperative_engine(ref, loss, precond):
+    """n > 262144 runs the cooperative CG step (one grid kernel per
+    iteration, p.Hp from the Hv emission) and the emission-fused gradient
+    norm: sparse LR and sparse L2-SVM (indirect strategy), with and without
+    the preconditioner, against the reference solver."""
+    # At eps = 0.01 this problem's sparse SVM trajectory is sensitive: CG counts
+    # of 12/13/14 in the first outer iteration, from different FP64 summation
+    # orders alone, give w 3e-4 .. 1e-2 apart with objectives 2e-7 apart.  So
+    # both solvers run to eps = 1e-6 here and must meet at the same optimum.
+    p = synth.synth_sparse(11, 6000, 300_000, 30)
+    cfg = TrustRegionConfig(eps=1e-6, use_preconditioner=precond)
+    w_ref, t_ref = ref.solve(p, loss, cfg, backend=1, workers=8)
+    kind = LR if loss == 0 else SVM
+    r = solve(p, kind, cfg, plan(svm_strategy=SvmStrategy.Indirect) if loss else plan())
+    assert r.converged and t_ref["converged"]
+    assert rel_err(r.objective, t_ref["objective"]) <= 1e-10
+    assert rel_err(r.w, w_ref) <= 1e-5
+
+
 def test_synth_p1_reduced_rows_active_set(ref):
     """proteomics-shaped dense L2-SVM (configs[2]) at 2e5 rows: active set + predictions."""
     p = synth.synth_dense(1, 200_000, 40)
