@@ -150,6 +150,22 @@ def test_large_n_sparse_solve_cooperative_engine(ref, loss, precond):
     assert rel_err(r.w, w_ref) <= 1e-5
 
 
+@pytest.mark.parametrize("nccl_graph", ["0", "1"])
+def test_large_n_sharded_path_single_rank_nccl(ref, monkeypatch, nccl_graph):
+    """The row-sharded path (one NCCL rank) on the cooperative CG engine:
+    allreduced raw products, then the epilogue, with the CG loop host-driven
+    or captured in the graph together with the allreduces."""
+    monkeypatch.setenv("TRON_B200_FORCE_NCCL", "1")
+    monkeypatch.setenv("TRON_B200_NCCL_GRAPH", nccl_graph)
+    p = synth.synth_sparse(12, 6000, 300_000, 30)
+    cfg = TrustRegionConfig(eps=1e-6)
+    w_ref, t_ref = ref.solve(p, 0, cfg, backend=1, workers=8)
+    r = solve(p, LR, cfg, plan())
+    assert r.converged and t_ref["converged"]
+    assert rel_err(r.objective, t_ref["objective"]) <= 1e-10
+    assert rel_err(r.w, w_ref) <= 1e-5
+
+
 def test_synth_p1_reduced_rows_active_set(ref):
     """proteomics-shaped dense L2-SVM (configs[2]) at 2e5 rows: active set + predictions."""
     p = synth.synth_dense(1, 200_000, 40)
