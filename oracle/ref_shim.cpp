@@ -249,6 +249,119 @@ size_t ref_testgen_random_index_set(uint64_t seed, size_t l, double fraction, in
   return s.size();
 }
 
+// ---- SYNTH-v1, generated with the reference's own
+// testgen::Rng (testgen.hpp:14-36) so the reference arm of bench.py never
+// maps the product library.  Independent of paper_2008_03433_b200/csrc/synth.cpp;
+// tests/test_synth.py checks the two bit for bit.
+// Sparse: k distinct Zipf(s) columns per row (rejection of duplicates), sorted,
+// values 1e-3 + U[0,1), unit-L2 rows; then labels from a random separator.
+int ref_synth_sparse(uint64_t seed, size_t l, size_t n, size_t k, double s, double flip,
+                     int64_t* ro, int32_t* ci, double* vals, double* y) {
+  if (n == 0 || k > n) return OR_ERR_DIMENSION;
+  testgen::Rng rng(seed);
+  std::vector<double> cdf;
+  if (s != 0.0) {
+    cdf.resize(n);
+    double acc = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+      acc += std::pow(static_cast<double>(j + 1), -s);
+      cdf[j] = acc;
+    }
+    const double total = cdf[n - 1];
+    for (auto& c : cdf) c /= total;
+  }
+  std::vector<int32_t> row;
+  ro[0] = 0;
+  for (size_t i = 0; i < l; ++i) {
+    row.clear();
+    while (row.size() < k) {
+      size_t c;
+      if (s != 0.0) {
+        c = static_cast<size_t>(std::lower_bound(cdf.begin(), cdf.end(), rng.next_unit()) -
+                                cdf.begin());
+        if (c >= n) c = n - 1;
+      } else {
+        c = static_cast<size_t>(rng.next_u64() % n);
+      }
+      if (std::find(row.begin(), row.end(), static_cast<int32_t>(c)) == row.end())
+        row.push_back(static_cast<int32_t>(c));
+    }
+    std::sort(row.begin(), row.end());
+    double ss = 0.0;
+    for (size_t t = 0; t < k; ++t) {
+      const double v = 1e-3 + rng.next_unit();
+      ci[i * k + t] = row[t];
+      vals[i * k + t] = v;
+      ss += v * v;
+    }
+    const double inv = 1.0 / std::sqrt(ss);
+    for (size_t t = 0; t < k; ++t) vals[i * k + t] = vals[i * k + t] * inv;
+    ro[i + 1] = static_cast<int64_t>((i + 1) * k);
+  }
+  std::vector<double> ws(n);
+  for (auto& v : ws) v = rng.next_in(-1.0, 1.0);
+  for (size_t i = 0; i < l; ++i) {
+    double score = 0.0;
+    for (int64_t t = ro[i]; t < ro[i + 1]; ++t) score += vals[t] * ws[ci[t]];
+    double label = score >= 0.0 ? 1.0 : -1.0;
+    if (rng.next_unit() < flip) label = -label;
+    y[i] = label;
+  }
+  return OR_OK;
+}
+
+// Dense: row-major l x n, column scales over `decades` decades, common factor
+// rho.  Row i consumes draws [i(n+1), (i+1)(n+1)) of the stream; splitmix64
+// is a counter generator (state after m draws = seed + m*golden), so row
+// ranges are generated on several threads with the sequential stream's bits.
+int ref_synth_dense(uint64_t seed, size_t l, size_t n, double decades, double rho, double flip,
+                    double* values, double* y) {
+  if (n < 2) return OR_ERR_DIMENSION;
+  constexpr uint64_t golden = 0x9e3779b97f4a7c15ull;
+  std::vector<double> sc(n);
+  for (size_t j = 0; j < n; ++j)
+    sc[j] = std::pow(10.0, -decades / 2 + decades * static_cast<double>(j) /
+                                              static_cast<double>(n - 1));
+  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      const size_t b = l * t / nt, e = l * (t + 1) / nt;
+      testgen::Rng r(seed + static_cast<uint64_t>(b) * (n + 1) * golden);
+      for (size_t i = b; i < e; ++i) {
+        const double g = 2 * r.next_unit() - 1;
+        double* row = values + i * n;
+        for (size_t j = 0; j < n; ++j) row[j] = sc[j] * (rho * g + (1 - rho) * (2 * r.next_unit() - 1));
+      }
+    });
+  for (auto& th : pool) th.join();
+  testgen::Rng rng(seed + static_cast<uint64_t>(l) * (n + 1) * golden);
+  std::vector<double> ws(n);
+  for (auto& v : ws) v = rng.next_in(-1.0, 1.0);
+  for (size_t i = 0; i < l; ++i) {
+    const double* row = values + i * n;
+    double score = 0.0;
+    for (size_t j = 0; j < n; ++j) score += row[j] * ws[j];
+    double label = score >= 0.0 ? 1.0 : -1.0;
+    if (rng.next_unit() < flip) label = -label;
+    y[i] = label;
+  }
+  return OR_OK;
+}
+
+// predict (model.cpp:88-117) with the reference's own code: labels of `data`
+// under weights w; returns the number of correct labels.
+size_t ref_predict(int layout, size_t l, size_t n, const int64_t* ro, const int32_t* ci,
+                   const double* vals, const double* y, const double* w, double* labels) {
+  tron::Problem p = make_problem(layout, l, n, ro, ci, vals, y, 1.0);
+  tron::Model m;
+  m.n = n;
+  m.w.assign(w, w + n);
+  auto out = tron::predict(m, p);
+  std::memcpy(labels, out.labels.data(), l * sizeof(double));
+  return out.correct;
+}
+
 // The drop-in boundary exercised literally: the
 // REFERENCE's own tron::solve(LossEvaluator&) (tron.cpp:127-217) driving a
 // LossEvaluator whose every method forwards to the B200 C ABI

@@ -61,8 +61,12 @@ int guarded(F&& fn) {
   }
 }
 
-#define NEED_CTX(ctx) \
-  if (!(ctx) || !(ctx)->engine) return fail(TRON_ERR_ARGUMENT, "null context")
+// Every context entry point runs on the context's device (the current device
+// is per host thread; another context may have changed it) and restores the
+// caller's current device on return.
+#define NEED_CTX(ctx)                                                              \
+  if (!(ctx) || !(ctx)->engine) return fail(TRON_ERR_ARGUMENT, "null context");    \
+  tb::DeviceGuard device_guard_((ctx)->engine->device())
 
 // LossEvaluator over the engine, used by the host-CG parity mode so that
 // the reference control flow (solver.cpp) drives the device kernels.
@@ -242,6 +246,7 @@ int tron_gpu_create_csr(int loss, uint64_t l, uint64_t n, const int64_t* row_off
     tron_gpu_options o;
     tron_gpu_default_options(&o);
     if (opt) o = *opt;
+    tb::DeviceGuard restore(-1);  // creation selects o.device; the caller's device comes back
     auto ctx = std::make_unique<tron_gpu_ctx>();
     ctx->engine = tb::Engine::create_csr(loss, l, n, row_offsets, col_indices, values, y, C, o);
     *out = ctx.release();
@@ -257,13 +262,21 @@ int tron_gpu_create_dense(int loss, uint64_t l, uint64_t n, const double* row_ma
     tron_gpu_options o;
     tron_gpu_default_options(&o);
     if (opt) o = *opt;
+    tb::DeviceGuard restore(-1);  // creation selects o.device; the caller's device comes back
     auto ctx = std::make_unique<tron_gpu_ctx>();
     ctx->engine = tb::Engine::create_dense(loss, l, n, row_major, y, C, o);
     *out = ctx.release();
   });
 }
 
-void tron_gpu_destroy(tron_gpu_ctx* ctx) { delete ctx; }
+void tron_gpu_destroy(tron_gpu_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->engine) {
+    tb::DeviceGuard device_guard_(ctx->engine->device());
+    ctx->engine.reset();
+  }
+  delete ctx;
+}
 
 int tron_gpu_dimension(tron_gpu_ctx* ctx, uint64_t* n) {
   NEED_CTX(ctx);

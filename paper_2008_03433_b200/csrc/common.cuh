@@ -219,6 +219,13 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 bool pdl_enabled();  // TRON_B200_PDL=0 turns the launch attribute off
 
+// A failed launch raises TRON_ERR_CUDA (engine.cpp) instead of leaving the
+// device scalars the host reads next at their previous values.
+[[noreturn]] void launch_failed(cudaError_t e, const char* what);
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes for `func` on the
+// CURRENT device (the attribute is per device); idempotent, thread-safe.
+void ensure_max_dynamic_smem(const void* func, int bytes);
+
 // <<<>>> with the programmatic-stream-serialization attribute (when enabled).
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -233,11 +240,15 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) launch_failed(e, "cudaLaunchKernelEx");
 }
 
-#define TB_LAUNCH_CHECK() \
-  do {                    \
+// After a <<<>>> launch: raise on a launch-configuration error.
+#define TB_LAUNCH_CHECK()                                            \
+  do {                                                               \
+    const cudaError_t tb_e_ = cudaPeekAtLastError();                 \
+    if (tb_e_ != cudaSuccess) ::tb::launch_failed(tb_e_, "launch");  \
   } while (0)
 
 }  // namespace tb

@@ -427,12 +427,7 @@ void launch_one(const CsrView& A, const SegView& S, const UView& U, const EpiVie
   long long cap = device_sm_count();
   if (STAGED) {
     smem = (size_t)A.cols * sizeof(double);
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-      cudaFuncSetAttribute(seg_spmv_kernel<UK, SQ, EPI, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageMaxBytes);
-      configured = true;
-    }
+    ensure_max_dynamic_smem((const void*)seg_spmv_kernel<UK, SQ, EPI, true>, (int)kStageMaxBytes);
   } else {
     cap *= 2;  // persistent: 2 blocks of 8 warps per SM (register-limited)
   }
@@ -577,7 +572,7 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uin
     if (nchunks > 0)
       plan_chunk_rank_kernel<<<pgrid(nchunks), 256, 0, s>>>(cptr, n, colrank, nchunks, chunk_rank,
                                                             chunk_first);
-  }
+    }
   long long counts[2] = {0, 0};
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(counts, cnt, sizeof(counts), cudaMemcpyDeviceToHost, s);
@@ -594,271 +589,6 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uin
   P->nz_col = nz_col;
   P->empty_col = empty_col;
   return e == cudaSuccess ? 0 : (int)e;
-}
-
-// ---------------------------------------------------------------------------
-// Persistent CG (tron.cpp:37-108) for sparse problems: one cooperative launch
-// runs every CG iteration -- a = D(Xp) over the CSR, hp = p + scale X^T a over
-// the CSC (the segmented body above), the fix-ups and the CG vector step --
-// with grid barriers instead of kernel boundaries.  What a CG iteration costs
-// on L2-resident problems (R1) is the latency of its phases, not bytes.
-// Scalars are reduced per CTA, then every CTA sums all CTA partials in the
-// same fixed order, so all CTAs hold identical alpha / beta / norms and take
-// the same branches.  The per-entry arithmetic is cg_cluster_step_kernel's.
-// ---------------------------------------------------------------------------
-namespace {
-
-namespace cgrp = cooperative_groups;
-constexpr int kFusedBlock = 256;
-#ifndef TB_FUSED_PROF
-#define TB_FUSED_PROF 0
-#endif
-#ifndef TB_FUSED_NG
-#define TB_FUSED_NG 2  // groups of four per lane in flight (16 warps per SM here, not 64)
-#endif
-
-struct FusedCg {
-  CsrView X, At;
-  SegView S;
-  CgVectors v;
-  const double* dvec;   // LR: D
-  const uint8_t* mask;  // SVM on CSR: active set
-  double* a;            // l-length: D (X p)
-  double scale;         // C (LR) or 2C (SVM)
-  double* parts;        // [2][grid][4] CTA partials
-  CgState* st;
-};
-
-template <int K>
-__device__ __forceinline__ void fused_sums(double (&x)[K], double* parts, int& buf, double* sh,
-                                           double* red, cgrp::grid_group& grid) {
-  grid_sums<kFusedBlock, K>(x, parts, buf, sh, red, grid);
-}
-
-template <int G>
-__global__ void __launch_bounds__(kFusedBlock, 2) cg_fused_kernel(FusedCg F) {
-  cgrp::grid_group grid = cgrp::this_grid();
-  __shared__ double ebuf_all[kFusedBlock / kWarp][kSegChunk];
-  __shared__ double sh[kFusedBlock / kWarp + 1];
-  __shared__ double red[4];
-  const int lane = threadIdx.x & 31;
-  const long long W = ((long long)gridDim.x * kFusedBlock) >> 5;
-  const long long gw = (blockIdx.x * (long long)kFusedBlock + threadIdx.x) >> 5;
-  const long long gt = blockIdx.x * (long long)kFusedBlock + threadIdx.x;
-  const long long NT = (long long)gridDim.x * kFusedBlock;
-  CgState* st = F.st;
-  const CgVectors v = F.v;
-  if (!st->cont) return;  // the init kernel ended the loop (uniform)
-  double rz_old = st->rz;
-  const double delta = st->delta, stop = st->stop;
-  long long iters = st->iters;
-  const long long max_iters = st->max_iters;
-  int rpar = st->rpar;
-  int buf = 0;
-  UView U;
-  U.kind = U_VEC;
-  U.u = F.a;
-  EpiView E;
-  E.kind = EPI_VEC;
-  E.base = v.p;
-  E.scale = F.scale;
-  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  constexpr int RPW = kWarp / G;
-  const int sub = lane % G;
-#if TB_FUSED_PROF
-  unsigned long long tp[8];
-  auto stamp = [&](int i) {
-    unsigned long long x;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x));
-    tp[i] = x;
-  };
-#else
-  auto stamp = [](int) {};
-#endif
-  for (;;) {
-    ++iters;
-    stamp(0);
-    // a = D (X p) (loss.cpp:86-89; csr_dv_kernel)
-    for (long long r0 = gw * RPW; r0 < F.X.rows; r0 += W * RPW) {
-      const long long row = r0 + lane / G;
-      bool active = row < F.X.rows;
-      if (active && F.mask) active = F.mask[row] != 0;
-      double s = 0.0;
-      if (active) s = row_dot_vec<G, true, TB_FUSED_NG>(F.X, row, sub, v.p);
-      s = group_sum<G>(s);
-      if (sub == 0 && row < F.X.rows) F.a[row] = F.mask ? (active ? s : 0.0) : s * F.dvec[row];
-    }
-    stamp(1);
-    grid.sync();
-    stamp(2);
-    // hp = p + scale X^T a, then the rows split across chunks
-    seg_body<U_VEC, false, EPI_VEC, false, true, kFusedBlock>(F.At, F.S, U, E, v.hp, nullptr,
-                                                              ebuf_all[threadIdx.x >> 5], gw, W,
-                                                              lane);
-    stamp(3);
-    grid.sync();
-    stamp(4);
-    DotAcc fix_dacc;
-    for (long long b = gw * 32; b < F.S.nchunks; b += W * 32)
-      fixup_one<EPI_VEC, true>(F.S, E, v.hp, b + lane, lane, fix_dacc);
-    grid.sync();
-    stamp(5);
-    // p.Hp (tron.cpp:71-75)
-    double* r = rpar ? v.r1 : v.r0;
-    double x1[1] = {0.0};
-    for (long long j = gt; j < v.n; j += NT) x1[0] += ld_coh(v.p + j) * ld_coh(v.hp + j);
-    fused_sums<1>(x1, F.parts, buf, sh, red, grid);
-    const double php = x1[0];
-    if (!(php > 0.0)) {
-      if (lead) {
-        st->iters = iters;
-        st->php = php;
-        st->fail = 1;
-        st->cont = 0;
-      }
-      return;
-    }
-    const double alpha = rz_old / php;
-    // d += alpha p, ||d|| (tron.cpp:76-78), and speculatively r -= alpha Hp,
-    // z = M^-1 r (tron.cpp:91-95) into the other parity buffer, so one
-    // barrier serves both (on the boundary exit rn is simply not used)
-    double* rn = rpar ? v.r0 : v.r1;
-    double x2[3] = {0.0, 0.0, 0.0};
-    for (long long j = gt; j < v.n; j += NT) {
-      const double dj = v.d[j] + alpha * v.p[j];
-      v.d[j] = dj;
-      x2[0] += dj * dj;
-      const double rj = r[j] + (-alpha) * ld_coh(v.hp + j);
-      rn[j] = rj;
-      const double z = v.M ? rj / v.M[j] : rj;
-      x2[1] += rj * z;
-      x2[2] += rj * rj;
-    }
-    fused_sums<3>(x2, F.parts, buf, sh, red, grid);
-    if (sqrt(x2[0]) > delta) {
-      // boundary: retreat, then tau on ||d + tau p|| = delta (tron.cpp:78-90)
-      double x3[3] = {0.0, 0.0, 0.0};
-      for (long long j = gt; j < v.n; j += NT) {
-        const double pj = v.p[j];
-        const double dj = v.d[j] + (-alpha) * pj;
-        v.d[j] = dj;
-        x3[0] += dj * pj;
-        x3[1] += dj * dj;
-        x3[2] += pj * pj;
-      }
-      fused_sums<3>(x3, F.parts, buf, sh, red, grid);
-      const double dp = x3[0], dd = x3[1], pp = x3[2];
-      const double rad = sqrt(dp * dp + pp * (delta * delta - dd));
-      const double tau = dp >= 0.0 ? (delta * delta - dd) / (dp + rad) : (rad - dp) / pp;
-      double x4[3] = {0.0, 0.0, 0.0};  // q(d) and ||d|| of the final step (tron.cpp:99-106)
-      for (long long j = gt; j < v.n; j += NT) {
-        const double dj = v.d[j] + tau * v.p[j];
-        const double rj = r[j] + (-tau) * ld_coh(v.hp + j);
-        v.d[j] = dj;
-        r[j] = rj;
-        x4[0] += dj * v.g[j];
-        x4[1] += dj * rj;
-        x4[2] += dj * dj;
-      }
-      fused_sums<3>(x4, F.parts, buf, sh, red, grid);
-      if (lead) {
-        st->iters = iters;
-        st->php = php;
-        st->alpha = alpha;
-        st->tau = tau;
-        st->boundary = 1;
-        st->exit_kind = kCgBoundary;
-        st->q = 0.5 * (x4[0] - x4[1]);
-        st->dnorm = sqrt(x4[2]);
-        st->cont = 0;
-      }
-      return;
-    }
-    const double rz = x2[1], rnorm = sqrt(x2[2]);
-    stamp(6);
-    const double beta = rz / rz_old;
-    for (long long j = gt; j < v.n; j += NT)
-      v.p[j] = (v.M ? rn[j] / v.M[j] : rn[j]) + beta * v.p[j];  // tron.cpp:96
-    const int cont = (iters < max_iters) && !(rnorm <= stop);
-    if (!cont) {
-      // exit classification, q(d) = (d.g - d.r)/2, ||d|| (tron.cpp:97-106)
-      double x6[3] = {0.0, 0.0, 0.0};
-      for (long long j = gt; j < v.n; j += NT) {
-        const double dj = v.d[j];
-        x6[0] += dj * v.g[j];
-        x6[1] += dj * rn[j];
-        x6[2] += dj * dj;
-      }
-      fused_sums<3>(x6, F.parts, buf, sh, red, grid);
-      if (lead) {
-        st->exit_kind = (iters >= max_iters && rnorm > stop) ? kCgMaxIters : kCgConverged;
-        st->q = 0.5 * (x6[0] - x6[1]);
-        st->dnorm = sqrt(x6[2]);
-      }
-    }
-    if (lead) {
-      st->iters = iters;
-      st->php = php;
-      st->alpha = alpha;
-      st->beta = beta;
-      st->rz = rz;
-      st->rpar = rpar ^ 1;
-      st->rnorm = rnorm;
-      st->cont = cont;
-    }
-    if (!cont) return;
-    rz_old = rz;
-    rpar ^= 1;
-    grid.sync();  // p complete before the next row phase gathers it
-#if TB_FUSED_PROF
-    stamp(7);
-    if (lead && iters == 3)
-      printf("fused phases us: rows %.2f sync %.2f seg %.2f sync+fix+sync %.2f cg2sums %.2f p+sync %.2f\n",
-             (tp[1] - tp[0]) * 1e-3, (tp[2] - tp[1]) * 1e-3, (tp[3] - tp[2]) * 1e-3,
-             (tp[5] - tp[3]) * 1e-3, (tp[6] - tp[5]) * 1e-3, (tp[7] - tp[6]) * 1e-3);
-#endif
-  }
-}
-
-template <int G>
-int fused_grid() {
-  static int g = [] {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel<G>, kFusedBlock, 0);
-    return per_sm * device_sm_count();
-  }();
-  return g;
-}
-
-template <int G>
-void launch_fused(const FusedCg& F, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)fused_grid<G>());
-  cfg.blockDim = dim3(kFusedBlock);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, cg_fused_kernel<G>, F);
-}
-
-}  // namespace
-
-int cg_fused_max_grid() { return 2 * device_sm_count(); }
-
-void cg_fused(const CsrView& X, const CsrView& At, const SegView& S, int group, const CgVectors& v,
-              const double* dvec, const uint8_t* mask, double* a, double scale, double* parts,
-              CgState* st, cudaStream_t s) {
-  FusedCg F{X, At, S, v, dvec, mask, a, scale, parts, st};
-  switch (group) {
-    case 32: launch_fused<32>(F, s); break;
-    case 16: launch_fused<16>(F, s); break;
-    case 8: launch_fused<8>(F, s); break;
-    case 4: launch_fused<4>(F, s); break;
-    default: launch_fused<2>(F, s); break;
-  }
 }
 
 int64_t seg_dot_slots(int64_t nchunks) {

@@ -327,7 +327,7 @@ int choose_group(int64_t rows, int64_t nnz) {
 
 template <class K>
 static void set_smem(K kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotMax * 8);
+  ensure_max_dynamic_smem((const void*)kernel, kHotMax * 8);
 }
 
 // Opt-in (TRON_B200_STAGE=1): measured slower on N1 (occupancy drops to one
@@ -353,16 +353,14 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
     if (loss == kLossLogistic) {
       TB_GROUP_DISPATCH(group, {
         auto k = csr_forward_kernel<GG, kLossLogistic, true>;
-        static bool once = (set_smem(k), true);
-        (void)once;
+        set_smem(k);
         launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, z, zhat, dvec, mask,
                    obj, sc);
       });
     } else {
       TB_GROUP_DISPATCH(group, {
         auto k = csr_forward_kernel<GG, kLossSvm, true>;
-        static bool once = (set_smem(k), true);
-        (void)once;
+        set_smem(k);
         launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, z, zhat, dvec, mask,
                    obj, sc);
       });
@@ -390,8 +388,7 @@ void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, co
     const int hot = (int)(X.cols < kHotMax ? X.cols : kHotMax);
     TB_GROUP_DISPATCH(group, {
       auto k = csr_dv_kernel<GG, true>;
-      static bool once = (set_smem(k), true);
-      (void)once;
+      set_smem(k);
       launch_pdl(k, dim3(device_sm_count()), dim3(kStagedBlock), (size_t)hot * 8, s, X, hot, p, dvec,
                  mask, a);
     });
@@ -466,10 +463,12 @@ void screen_inputs(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t
   if (ptr && rows > 0)
     csr_screen_kernel<<<grid_for(rows * 32), 256, 0, s>>>(ptr, idx, rows, n, first_bad2);
   if (l > 0) labels_screen_kernel<<<grid_for(l), 256, 0, s>>>(y, l, first_bad2 + 1);
+  TB_LAUNCH_CHECK();
 }
 
 void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s) {
   narrow_kernel<<<grid_for(count), 256, 0, s>>>(in, out, count);
+  TB_LAUNCH_CHECK();
 }
 
 }  // namespace tb

@@ -263,11 +263,8 @@ void launch_pass(const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
   const size_t red = (size_t)(T / kWarp) * NMAX * 8;
   if (smem < red) smem = red;
   auto k = dense_pass_kernel<NMAX, T, MODE, LOSS>;
-  static size_t configured = 0;  // per instantiation; the attribute must not exceed
-  if (smem > configured) {       // opt-in max minus the kernel's static shared memory
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
+  // (the attribute must not exceed the opt-in max minus the static shared memory)
+  ensure_max_dynamic_smem((const void*)k, (int)smem);
   const int grid = dense_grid(a.l, a.n);
   launch_pdl(k, dim3(grid), dim3(T + kWarp), smem, s, m, a, ns);
 }
@@ -528,6 +525,7 @@ void dense_transpose_chunk(const double* rm, int64_t rows, int64_t n, double* X,
                            int64_t row0, cudaStream_t s) {
   dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((n + 31) / 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(rm, rows, (int)n, X, ld, row0);
+  TB_LAUNCH_CHECK();
 }
 
 void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, long long* count_out,
@@ -538,8 +536,11 @@ void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, lo
     return;
   }
   count_kernel<<<nb, kBlock, 0, s>>>(l, mask, tmp);
+  TB_LAUNCH_CHECK();
   scan_kernel<<<1, 1024, 0, s>>>(tmp, nb, count_out);
+  TB_LAUNCH_CHECK();
   scatter_kernel<<<nb, kBlock, 0, s>>>(l, mask, tmp, idx);
+  TB_LAUNCH_CHECK();
 }
 
 void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int32_t* idx,
@@ -548,6 +549,7 @@ void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int3
   if (g > (long long)device_sm_count() * 16) g = (long long)device_sm_count() * 16;
   if (g < 1) g = 1;
   gather_kernel<<<(int)g, 256, 0, s>>>(nI, (int)n, X, ld, idx, Xg, ldg);
+  TB_LAUNCH_CHECK();
 }
 
 }  // namespace tb

@@ -12,6 +12,8 @@
 #include <atomic>
 #include <chrono>
 #include <future>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -27,6 +29,24 @@ void cuda_check(cudaError_t e, const char* what) {
   cudaGetLastError();  // clear sticky-less errors
   const int st = (e == cudaErrorMemoryAllocation) ? TRON_ERR_OOM : TRON_ERR_CUDA;
   raise(st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+[[noreturn]] void launch_failed(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  raise(TRON_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ensure_max_dynamic_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{func, dev}];
+  if (have >= bytes) return;
+  cuda_check(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+             "cudaFuncSetAttribute(max dynamic shared memory)");
+  have = bytes;
 }
 
 // ----------------------------------------------------------------------------
@@ -270,14 +290,12 @@ void Engine::common_alloc() {
   if (!dense_) a_.alloc(ll);
   if (dense_) parts_.alloc((size_t)dense_grid(l_, n_) * nn);
   small_engine_ = dense_ || n_ <= kSmallCgMaxN;
-  // large n: one cooperative kernel per CG iteration (TRON_B200_COOP_CG=0: the
-  // three-kernel php / update / direction sequence)
-  const char* co = std::getenv("TRON_B200_COOP_CG");
-  coop_parts_.alloc((size_t)8 * std::max(cg_coop_grid(), cg_fused_max_grid()));
-  // TRON_B200_CLUSTER_CG=0: the three-kernel large-n CG step for mid-size n too
+  coop_parts_.alloc((size_t)8 * cg_coop_grid());
+  // mid-size n: one 8-CTA cluster kernel per CG iteration; larger n (or
+  // TRON_B200_CLUSTER_CG=0): one cooperative grid kernel per iteration
   const char* cc = std::getenv("TRON_B200_CLUSTER_CG");
   mid_engine_ = !small_engine_ && n_ <= kClusterCgMaxN && !(cc && cc[0] == '0');
-  coop_engine_ = !small_engine_ && !mid_engine_ && !(co && co[0] == '0');
+  coop_engine_ = !small_engine_ && !mid_engine_;
   // TRON_B200_NO_GRAPH=1 runs the CG loop host-driven (per-kernel profiling:
   // ncu cannot profile kernel nodes of graphs with conditional nodes).
   const char* ng = std::getenv("TRON_B200_NO_GRAPH");
@@ -401,18 +419,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       if (vrc != 0) cuda_check((cudaError_t)vrc, "build_csc_values");
     };
     tr.mark("device CSC structure");
-    // TRON_B200_SEG_STREAM=1: the TMA-streamed segmented kernels (seg_stream.cu).
-    // Measured slower than the chunk-plan kernels on N1/R1/K1 (gather-bound, see
-    // DESIGN.md §9), so the chunk-plan kernels are the default.
-    const char* ss = std::getenv("TRON_B200_SEG_STREAM");
-    e->use_stream_ = ss && ss[0] == '1';
-    if (e->use_stream_) {
-      finish_values();
-      // streamed layouts of both orientations, built on the device
-      e->build_stream(e->xs_, e->rptr_.p, (int64_t)l, nnz, e->cidx_.p, e->rval_.p);
-      e->build_stream(e->xts_, e->cptr_.p, (int64_t)n, nnz, e->ridx_.p, e->cval_.p);
-      tr.mark("streamed layouts");
-    } else {
+    {
       // one-time structure analysis of the CSC copy, on the device (csc_seg.cu)
       const int64_t nch = (nnz + kSegChunk - 1) / kSegChunk;
       e->chunk_rank_.alloc(std::max<int64_t>(nch, 1));
@@ -437,24 +444,16 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       }
       tr.mark("segmented plan");
     }
-    // The persistent cooperative CG (cg_fused), opt-in (TRON_B200_FUSED_CG=1,
-    // any n above the single-block engine): measured 47 us per R1 CG iteration
-    // against 40 us for the kernel-per-phase graph.
-    const char* fc = std::getenv("TRON_B200_FUSED_CG");
-    e->fused_engine_ = !e->use_stream_ && !e->comm_.active() && !e->small_engine_ && fc &&
-                       fc[0] == '1';
-    if (!e->use_stream_) {
-      // The CG graphs of both slots (no preconditioner) are captured and
-      // instantiated while the values are still crossing PCIe: a recipe of
-      // fixed buffers, independent of their contents.
-      if (e->use_graphs_ && nnz > 0 && n > 0) {
-        e->build_graph(0, false);
-        e->build_graph(1, false);
-        tr.mark("CG graphs");
-      }
-      finish_values();
-      tr.mark("values H2D + CSC values");
+    // The CG graphs of both slots (no preconditioner) are captured and
+    // instantiated while the values are still crossing PCIe: a recipe of
+    // fixed buffers, independent of their contents.
+    if (e->use_graphs_ && nnz > 0 && n > 0) {
+      e->build_graph(0, false);
+      e->build_graph(1, false);
+      tr.mark("CG graphs");
     }
+    finish_values();
+    tr.mark("values H2D + CSC values");
     cuda_check(cudaStreamSynchronize(s), "csc build");
     cuda_check(cudaGetLastError(), "csc build");
     return e;
@@ -584,40 +583,10 @@ void Engine::screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_
   if (h[0] != ~0ull || h[1] != ~0ull) report((uint64_t)h[0], (uint64_t)h[1]);
 }
 
-void Engine::build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64_t nnz,
-                          const int32_t* idx, const double* val) {
-  SegStreamSizes z;
-  seg_stream_sizes(nseg, nnz, &z);
-  B.rec.alloc(std::max<int64_t>(z.rec_bytes, 16));
-  B.off.alloc(z.ntiles + 1);
-  B.nempty.alloc(1);
-  B.empty_seg.alloc(std::max<int64_t>(nseg, 1));
-  B.cta_tail.alloc(kMaxPartialBlocks);
-  B.cta_flags.alloc(kMaxPartialBlocks);
-  B.cta_tag.alloc(kMaxPartialBlocks);
-  B.misc.alloc(2);
-  StreamView& v = B.view;
-  v.nseg = nseg;
-  v.nnz = nnz;
-  v.ntiles = z.ntiles;
-  v.rec = B.rec.p;
-  v.tile_off = B.off.p;
-  v.empty_seg = B.empty_seg.p;
-  v.nempty = B.nempty.p;
-  v.cta_tail = B.cta_tail.p;
-  v.cta_flags = B.cta_flags.p;
-  v.cta_tag = B.cta_tag.p;
-  v.epoch = B.misc.p;
-  v.ticket = B.misc.p + 1;
-  const int rc = seg_stream_build(ptr, nseg, nnz, idx, val, v, s_);
-  if (rc != 0) cuda_check((cudaError_t)rc, "seg_stream_build");
-}
-
 uint64_t Engine::memory_bytes() const {
   uint64_t b = rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
                cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes() + lastbits_.bytes() +
                chunk_rank_.bytes() + empty_col_.bytes() + chunk_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
-  b += xs_.bytes() + xts_.bytes();
   for (const auto& S : slot_)
     b += S.w.bytes() + S.z.bytes() + S.zhat.bytes() + S.dvec.bytes() + S.mask.bytes() +
          S.gparts.bytes();
@@ -627,15 +596,19 @@ uint64_t Engine::memory_bytes() const {
 
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(s_), "synchronize"); }
 
+// The scalars are only trusted after a clean launch record: a failed launch
+// would leave them at their previous values.
 void Engine::read_obj() {
   cuda_check(cudaMemcpyAsync(obj_h_, obj_d_, sizeof(ObjScalars), cudaMemcpyDeviceToHost, s_),
              "D2H");
   cuda_check(cudaStreamSynchronize(s_), "sync");
+  cuda_check(cudaGetLastError(), "kernel launch");
 }
 
 void Engine::read_cg(CgState* out) {
   cuda_check(cudaMemcpyAsync(st_h_, st_d_, sizeof(CgState), cudaMemcpyDeviceToHost, s_), "D2H");
   cuda_check(cudaStreamSynchronize(s_), "sync");
+  cuda_check(cudaGetLastError(), "kernel launch");
   *out = *st_h_;
 }
 
@@ -647,9 +620,6 @@ void Engine::forward(Slot& S) {
   if (dense_) {
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
                   S.gparts.p, obj_d_, sc_, s_);
-  } else if (use_stream_) {
-    stream_forward(xs_.view, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_,
-                   sc_, s_);
   } else {
     csr_forward(X_, group_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_,
                 s_);
@@ -704,11 +674,8 @@ double Engine::eval_candidate_host(const double* w) {
 // ----------------------------------------------------------------------------
 void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out) {
   auto product = [&](const EpiView& E, double* dst) {
-    if (use_stream_)
-      stream_transposed(xts_.view, u, squared, E, dst, s_);
-    else
-      csc_spmv(Xt_, plan_, u, squared, E, dst, s_);
-    count_launch(use_stream_ ? 1 : 2);
+    csc_spmv(Xt_, plan_, u, squared, E, dst, s_);
+    count_launch(2);
   };
   if (!comm_.active()) {
     product(epi, out);
@@ -868,7 +835,8 @@ void Engine::gradient_host(double* g) {
 // Hv (loss.cpp:82-92 / :139-174) and preconditioner (loss.cpp:176-188)
 // ----------------------------------------------------------------------------
 bool Engine::hv_dot_available() const {
-  return !dense_ && !use_stream_ && !comm_.active() && dot_parts_.n > 0;
+  // (nnz == 0: csc_spmv takes the epilogue-only shortcut, which sums nothing)
+  return !dense_ && !comm_.active() && dot_parts_.n > 0 && plan_.nchunks > 0;
 }
 
 void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
@@ -888,10 +856,7 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   }
   const double* dv = loss_ == TRON_LOSS_LOGISTIC ? S.dvec.p : nullptr;
   const uint8_t* mk = loss_ == TRON_LOSS_LOGISTIC ? nullptr : S.mask.p;
-  if (use_stream_)
-    stream_dv(xs_.view, v, dv, mk, a_.p, s_);
-  else
-    csr_dv(X_, group_, v, dv, mk, a_.p, s_);
+  csr_dv(X_, group_, v, dv, mk, a_.p, s_);
   count_launch(1);
   UView u;
   u.kind = U_VEC;
@@ -985,29 +950,7 @@ void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint
 // ----------------------------------------------------------------------------
 // device-resident truncated CG (tron.cpp:37-108)
 // ----------------------------------------------------------------------------
-void Engine::launch_fused_cg(int k, bool use_m) {
-  CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
-  const Slot& S = slot_[k];
-  const bool lr = loss_ == TRON_LOSS_LOGISTIC;
-  Cond none;
-  cg_large_init(v, st_d_, sc_, none, s_);
-  cg_fused(X_, Xt_, plan_, group_, v, lr ? S.dvec.p : nullptr, lr ? nullptr : S.mask.p, a_.p,
-           lr ? C_ : 2.0 * C_, coop_parts_.p, st_d_, s_);
-}
-
 void Engine::build_graph(int k, bool use_m) {
-  if (fused_engine_) {  // init + one persistent kernel: no device-side loop node
-    cudaGraph_t graph;
-    cuda_check(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal), "begin capture");
-    launch_fused_cg(k, use_m);
-    cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
-    cudaGraphExec_t exec;
-    cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-    graph_[k][use_m] = graph;
-    graph_exec_[k][use_m] = exec;
-    body_kernels_ = 0;
-    return;
-  }
   // Captured against committed slot k; CG vectors are fixed buffers.
   cudaGraph_t graph;
   cuda_check(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
@@ -1044,7 +987,6 @@ void Engine::build_graph(int k, bool use_m) {
   cuda_check(cudaStreamUpdateCaptureDependencies(s_, &cond_node, 1,
                                                  cudaStreamSetCaptureDependencies),
              "update deps");
-  if (has_post_kernel()) cg_large_post(v, st_d_, sc_, s_);
   cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
 
   cudaGraph_t body = cp.conditional.phGraph_out[0];
@@ -1069,17 +1011,11 @@ void Engine::build_graph(int k, bool use_m) {
     hv_kernels(p_.p, hp_.p);
     cg_cluster_step(v, st_d_, cond, s_);
     count_launch(1);
-  } else if (coop_engine_) {
+  } else {
     const bool dot = hv_dot_available();
     hv_kernels(p_.p, hp_.p, dot);
     cg_coop_step(v, st_d_, coop_parts_.p, cond, s_, dot ? dot_out_.p : nullptr);
     count_launch(1);
-  } else {
-    hv_kernels(p_.p, hp_.p);
-    cg_large_php(v, st_d_, sc_, cond, s_);
-    cg_large_update(v, st_d_, sc_, cond, s_);
-    cg_large_direction(v, st_d_, sc_, cond, s_);
-    count_launch(3);
   }
   body_kernels_ = launches - before;
   cuda_check(cudaStreamEndCapture(s_, &body), "end body capture");
@@ -1136,13 +1072,7 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     if (!graph_exec_[k][use_m]) build_graph(k, use_m);
     cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
     read_cg(out);
-    launches += 1 + (uint64_t)out->iters * body_kernels_ + (has_post_kernel() ? 1 : 0);
-    return;
-  }
-  if (fused_engine_) {
-    launch_fused_cg(k, use_m);
-    count_launch(2);
-    read_cg(out);
+    launches += 1 + (uint64_t)out->iters * body_kernels_;
     return;
   }
   // host-driven loop (multi-GPU: NCCL between phases)
@@ -1161,20 +1091,10 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     } else if (mid_engine_) {
       cg_cluster_step(v, st_d_, none, s_);
       count_launch(1);
-    } else if (coop_engine_) {
+    } else {
       cg_coop_step(v, st_d_, coop_parts_.p, none, s_);  // (the host loop's Hv ran without the dot)
       count_launch(1);
-    } else {
-      cg_large_php(v, st_d_, sc_, none, s_);
-      cg_large_update(v, st_d_, sc_, none, s_);
-      cg_large_direction(v, st_d_, sc_, none, s_);
-      count_launch(3);
     }
-    read_cg(out);
-  }
-  if (has_post_kernel()) {
-    cg_large_post(v, st_d_, sc_, s_);
-    count_launch(1);
     read_cg(out);
   }
 }
@@ -1221,6 +1141,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   cuda_check(cudaEventCreate(&ev0), "event");
   cuda_check(cudaEventCreate(&ev1), "event");
   cuda_check(cudaEventRecord(ev0, s_), "event record");
+  bool write_w = true;
   auto finish = [&](int status) {
     cudaEventRecord(ev1, s_);
     cudaEventSynchronize(ev1);
@@ -1229,7 +1150,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     info->device_ms = ms;
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    if (w_out) download(w_out, slot_[cand_ ^ 1].w.p, n_ * 8, s_);
+    if (w_out && write_w) download(w_out, slot_[cand_ ^ 1].w.p, n_ * 8, s_);
     info->status = status;
     info->hessian_products = hv_count;
     (void)launches0;
@@ -1244,7 +1165,9 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   double f = eval_candidate_dev(nullptr);
   info->objective_evaluations = 1;
   if (!std::isfinite(f)) {
-    // w_out must reflect the starting point like the reference's result.w
+    // nothing was committed: like the reference (which throws before any
+    // result exists), w_out is left untouched
+    write_w = false;
     finish(TRON_ERR_NUMERICAL);
     raise(TRON_ERR_NUMERICAL, "objective is not finite at the starting point");
   }
@@ -1319,7 +1242,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
       if (prof.on) prof.report(info->n_iterations);
       if (!cg_done) {
         st = *st_h_;
-        launches += 1 + (uint64_t)st.iters * body_kernels_ + (has_post_kernel() ? 1 : 0);
+        launches += 1 + (uint64_t)st.iters * body_kernels_;
       }
       f_cand = candidate_result();
       (void)k;
@@ -1428,12 +1351,7 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
     epi.kind = EPI_VEC;
     epi.base = vtmp_.p;
     epi.scale = C_;
-    out->transposed_ms = time_it([&] {
-      if (use_stream_)
-        stream_transposed(xts_.view, u, false, epi, otmp_.p, s_);
-      else
-        csc_spmv(Xt_, plan_, u, false, epi, otmp_.p, s_);
-    });
+    out->transposed_ms = time_it([&] { csc_spmv(Xt_, plan_, u, false, epi, otmp_.p, s_); });
     out->forward_ms = time_it([&] { forward(slot_[cand_]); });
   } else {
     const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;

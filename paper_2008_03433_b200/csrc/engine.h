@@ -51,6 +51,30 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// Makes `device` current for the guard's lifetime (device < 0: leaves it
+// as is), then restores the caller's current device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+      return;
+    }
+    if (device < 0) return;
+    if (prev == device) {
+      prev = -1;
+      return;
+    }
+    cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // Owns the context stream; declared first in Engine so it is destroyed after
 // every DevBuf member has queued its free on it.
 struct StreamOwner {
@@ -81,20 +105,6 @@ class Comm {
 };
 int nccl_unique_id(void* out128);
 
-// Device buffers of one streamed segmented layout (seg_stream.cu).
-struct StreamBufs {
-  DevBuf<unsigned char> rec;
-  DevBuf<long long> off, nempty;
-  DevBuf<double> cta_tail;
-  DevBuf<int32_t> cta_flags, empty_seg;
-  DevBuf<unsigned> cta_tag, misc;
-  StreamView view{};
-  uint64_t bytes() const {
-    return rec.bytes() + off.bytes() + nempty.bytes() + cta_tail.bytes() + cta_flags.bytes() +
-           empty_seg.bytes() + cta_tag.bytes() + misc.bytes();
-  }
-};
-
 struct KernelTimes {
   double hv_ms = 0, transposed_ms = 0, forward_ms = 0, grad_ms = 0;
 };
@@ -111,6 +121,7 @@ class Engine {
 
   int64_t dimension() const { return n_; }
   int loss() const { return loss_; }
+  int device() const { return device_; }
   bool dense() const { return dense_; }
 
   // LossEvaluator surface (host vectors).
@@ -167,8 +178,6 @@ class Engine {
   void build_graph(int slot, bool use_m);
   template <class Report>
   void screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n, Report report);
-  void build_stream(StreamBufs& B, const int32_t* ptr, int64_t nseg, int64_t nnz,
-                    const int32_t* idx, const double* val);
   void count_launch(uint64_t k) { launches += k; }
 
   int loss_ = 0;
@@ -189,8 +198,6 @@ class Engine {
   DevBuf<int32_t> empty_col_, chunk_first_, nz_col_;
   DevBuf<double> head_, carry_;
   CsrView X_{}, Xt_{};
-  StreamBufs xs_, xts_;     // streamed CSR (rows) and CSC (columns) layouts
-  bool use_stream_ = false;  // TRON_B200_SEG_STREAM=1: the streamed segmented kernels
   SegView plan_{};
   int group_ = 4;
   // dense column-major
@@ -229,17 +236,11 @@ class Engine {
   uint64_t body_kernels_ = 0;
   bool small_engine_ = false;  // n <= kSmallCgMaxN: single-block CG step
   bool mid_engine_ = false;    // n <= kClusterCgMaxN: one 8-CTA cluster kernel per CG step
-  bool coop_engine_ = false;   // large n: one cooperative kernel per CG step (cg_coop_step)
+  bool coop_engine_ = false;   // otherwise: one cooperative kernel per CG step (cg_coop_step)
   DevBuf<double> dot_parts_, dot_out_;  // p.Hp from the Hv emission (EpiView::dot_*)
   DevBuf<unsigned> dot_ticket_;
   bool hv_dot_available() const;
-  bool fused_engine_ = false;  // persistent cooperative CG kernel (cg_fused)
-  DevBuf<double> coop_parts_;  // CTA partials of both cooperative engines
-  void launch_fused_cg(int k, bool use_m);
-  // kernels after the loop body: cg_large_post, or the persistent kernel itself
-  bool has_post_kernel() const {
-    return fused_engine_ || (!small_engine_ && !mid_engine_ && !coop_engine_);
-  }
+  DevBuf<double> coop_parts_;  // CTA partials of the cooperative CG step
   bool use_graphs_ = true;
 };
 

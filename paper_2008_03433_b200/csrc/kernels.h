@@ -51,33 +51,6 @@ int seg_plan_device(const int32_t* ptr, int64_t rows, int64_t nnz, SegView* P,
                     uint32_t* chunk_rank, int32_t* chunk_first, uint32_t* lastbits, int32_t* nz_col,
                     int32_t* empty_col, cudaStream_t s);
 
-// Streamed segmented layout of a compressed matrix (seg_stream.cu): 2048-
-// entry tiles of eight 256-entry pieces, lane-interleaved, with per-lane
-// segment-end bytes, per-tile end ranks and the non-empty segment table,
-// plus the per-CTA records that join segments crossing CTA ranges.
-constexpr int kStreamTilePieces = 8;
-struct StreamView {
-  int64_t nseg = 0, nnz = 0, ntiles = 0;
-  unsigned char* rec = nullptr;       // tile records (see seg_stream.cu)
-  const long long* tile_off = nullptr;  // [ntiles + 1] byte offset of each record
-  const int32_t* empty_seg = nullptr; // [nseg] the empty segments (first *nempty entries)
-  long long* nempty = nullptr;        // device count of empty segments
-  // per-CTA records joining segments that cross CTA ranges
-  double* cta_tail = nullptr;         // [kMaxPartialBlocks] partial open at the CTA's range end
-  int32_t* cta_flags = nullptr;       // bit0: a segment ends in the range
-  unsigned* cta_tag = nullptr;        // launch tag of the record (release/acquire)
-  unsigned* epoch = nullptr;          // launch counter (device-side: CUDA-graph replay safe)
-  unsigned* ticket = nullptr;         // last-CTA ticket
-};
-struct SegStreamSizes {
-  int64_t ntiles = 0, rec_bytes = 0;
-};
-size_t seg_stream_sizes(int64_t nseg, int64_t nnz, SegStreamSizes* z);
-// Builds the layout from segment-ordered device arrays (ptr[nseg+1], idx, val).
-int seg_stream_build(const int32_t* ptr, int64_t nseg, int64_t nnz, const int32_t* idx,
-                     const double* val, const StreamView& A, cudaStream_t s);
-int seg_stream_grid(int64_t ntiles);
-
 // Per-source-row weight u_i used by the transposed product sum_i u_i x_ij.
 enum UKind : int {
   U_VEC = 0,        // u[i]
@@ -179,15 +152,6 @@ void screen_inputs(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t
 // Row-offset narrowing int64 -> int32 (device).
 void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s);
 
-// Streamed versions (seg_stream.cu) of csr_forward / csr_dv / csc_spmv.
-void stream_forward(const StreamView& A, int loss, const double* w, const double* y, double C,
-                    double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
-                    Scratch sc, cudaStream_t s);
-void stream_dv(const StreamView& A, const double* p, const double* dvec, const uint8_t* mask,
-               double* a, cudaStream_t s);
-void stream_transposed(const StreamView& At, const UView& U, bool squared, const EpiView& E,
-                       double* out, cudaStream_t s);
-
 // ---- vector kernels (vec_kernels.cu) -----------------------------------------
 // wc = w + d (d may be null: wc = w); obj->ww = wc.wc
 void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjScalars* obj,
@@ -198,7 +162,7 @@ void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cud
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
 void l2_read_flush(const double* buf, int64_t n, cudaStream_t s);
 
-// Large-n CG engine (one kernel per phase; conditional handle optional).
+// CG initialisation for the mid/large-n engines (d = 0, r = -g, p = M^-1 r).
 struct CgVectors {
   int64_t n;
   const double* g;
@@ -211,13 +175,6 @@ struct CgVectors {
 };
 void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
                    cudaStream_t s);
-void cg_large_php(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
-                  cudaStream_t s);
-void cg_large_update(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
-                     cudaStream_t s);
-void cg_large_direction(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
-                        cudaStream_t s);
-void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s);
 
 // Mid-n CG engine (kSmallCgMaxN < n <= kClusterCgMaxN): one kernel per iteration
 // on a cluster of 8 CTAs (vector phases + scalars; the exit's q(d), ||d|| included).
@@ -228,13 +185,6 @@ int cg_coop_grid();
 // php_in: p.Hp already summed by the Hv kernels (EpiView::dot_out), or null.
 void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cudaStream_t s,
                   const double* php_in = nullptr);
-// Persistent cooperative CG over a sparse problem (csc_seg.cu): every CG
-// iteration of one truncated_cg in a single launch.  parts: 2 * 4 *
-// cg_fused_max_grid() doubles.  The caller runs cg_large_init first.
-int cg_fused_max_grid();
-void cg_fused(const CsrView& X, const CsrView& At, const SegView& S, int group, const CgVectors& v,
-              const double* dvec, const uint8_t* mask, double* a, double scale, double* parts,
-              CgState* st, cudaStream_t s);
 void cg_cluster_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
 
 // Small-n CG engine (n <= kSmallCgMaxN): one single-block kernel per

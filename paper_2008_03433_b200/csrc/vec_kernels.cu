@@ -155,179 +155,6 @@ __global__ void __launch_bounds__(kBlock) cg_init_kernel(CgVectors v, CgState* s
   }
 }
 
-__global__ void __launch_bounds__(kBlock) cg_php_kernel(CgVectors v, CgState* st, Scratch sc,
-                                                       Cond cond) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double sh[kBlock / kWarp + 1];
-  double acc = 0.0;
-#pragma unroll 4
-  GRID_STRIDE(j, v.n) acc += v.p[j] * v.hp[j];
-  const double b = block_sum<kBlock>(acc, sh, true);
-  if (threadIdx.x == 0) sc.partials[blockIdx.x] = b;
-  if (last_block_arrive(sc.tickets + T_CG_PHP)) {
-    const double php = reduce_partials<kBlock>(sc.partials, gridDim.x, 1, 0, sh);
-    if (threadIdx.x == 0) {
-      st->iters += 1;
-      st->php = php;
-      if (!(php > 0.0)) {  // tron.cpp:72-75 non-positive curvature
-        st->fail = 1;
-        st->cont = 0;
-        set_cond(cond, 0);
-      } else {
-        st->alpha = st->rz / php;
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kBlock) cg_update_kernel(CgVectors v, CgState* st, Scratch sc,
-                                                          Cond cond) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double sh[kBlock / kWarp + 1];
-  if (st->fail) return;  // uniform across the grid
-  const double alpha = st->alpha;
-  const double* rc = st->rpar ? v.r1 : v.r0;
-  double* rn = st->rpar ? v.r0 : v.r1;
-  double dd = 0.0, rz = 0.0, rr = 0.0;
-#pragma unroll 4
-  GRID_STRIDE(j, v.n) {
-    const double dj = v.d[j] + alpha * v.p[j];  // tron.cpp:77
-    v.d[j] = dj;
-    dd += dj * dj;
-    const double r = rc[j] + (-alpha) * v.hp[j];  // tron.cpp:91 (speculative)
-    rn[j] = r;
-    const double z = v.M ? r / v.M[j] : r;
-    rz += r * z;
-    rr += r * r;
-  }
-  const double a = block_sum<kBlock>(dd, sh, true);
-  const double b = block_sum<kBlock>(rz, sh, true);
-  const double c = block_sum<kBlock>(rr, sh, true);
-  if (threadIdx.x == 0) {
-    sc.partials[3 * blockIdx.x] = a;
-    sc.partials[3 * blockIdx.x + 1] = b;
-    sc.partials[3 * blockIdx.x + 2] = c;
-  }
-  if (last_block_arrive(sc.tickets + T_CG_UPD)) {
-    const double tdd = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 0, sh);
-    const double trz = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 1, sh);
-    const double trr = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 2, sh);
-    if (threadIdx.x == 0) {
-      if (sqrt(tdd) > st->delta) {  // tron.cpp:78
-        st->boundary = 1;
-        st->cont = 0;
-        set_cond(cond, 0);
-      } else {
-        st->beta = trz / st->rz;  // tron.cpp:93-95
-        st->rz = trz;
-        st->rpar ^= 1;
-        st->rnorm = sqrt(trr);
-        st->exit_kind = kCgMaxIters;
-        const int cont = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
-        st->cont = cont;
-        set_cond(cond, cont);
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kBlock) cg_direction_kernel(CgVectors v, CgState* st,
-                                                             Scratch sc, Cond cond) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double sh[kBlock / kWarp + 1];
-  if (st->fail) return;
-  if (!st->boundary) {
-    const double beta = st->beta;
-    const double* r = st->rpar ? v.r1 : v.r0;
-#pragma unroll 4
-    GRID_STRIDE(j, v.n) v.p[j] = zval(r, v.M, j) + beta * v.p[j];  // tron.cpp:96
-    return;
-  }
-  // Boundary: retreat, then solve for tau on ||d + tau p|| = delta (tron.cpp:78-90).
-  const double alpha = st->alpha;
-  double dp = 0.0, dd = 0.0, pp = 0.0;
-#pragma unroll 4
-  GRID_STRIDE(j, v.n) {
-    const double pj = v.p[j];
-    const double dj = v.d[j] + (-alpha) * pj;
-    v.d[j] = dj;
-    dp += dj * pj;
-    dd += dj * dj;
-    pp += pj * pj;
-  }
-  const double a = block_sum<kBlock>(dp, sh, true);
-  const double b = block_sum<kBlock>(dd, sh, true);
-  const double c = block_sum<kBlock>(pp, sh, true);
-  if (threadIdx.x == 0) {
-    sc.partials[3 * blockIdx.x] = a;
-    sc.partials[3 * blockIdx.x + 1] = b;
-    sc.partials[3 * blockIdx.x + 2] = c;
-  }
-  if (last_block_arrive(sc.tickets + T_CG_P)) {
-    const double tdp = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 0, sh);
-    const double tdd = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 1, sh);
-    const double tpp = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 2, sh);
-    if (threadIdx.x == 0) {
-      const double delta = st->delta;
-      const double rad = sqrt(tdp * tdp + tpp * (delta * delta - tdd));
-      st->tau = tdp >= 0.0 ? (delta * delta - tdd) / (tdp + rad) : (rad - tdp) / tpp;
-      st->exit_kind = kCgBoundary;
-      st->cont = 0;
-      set_cond(cond, 0);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kBlock) cg_post_kernel(CgVectors v, CgState* st, Scratch sc) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double sh[kBlock / kWarp + 1];
-  const bool boundary = st->boundary && !st->fail;
-  const double tau = st->tau;
-  double* r = st->rpar ? v.r1 : v.r0;
-  double dg = 0.0, dr = 0.0, dd = 0.0;
-#pragma unroll 4
-  GRID_STRIDE(j, v.n) {
-    double dj = v.d[j];
-    double rj = r[j];
-    if (boundary) {
-      dj = dj + tau * v.p[j];          // tron.cpp:86
-      rj = rj + (-tau) * v.hp[j];      // tron.cpp:87
-      v.d[j] = dj;
-      r[j] = rj;
-    }
-    dg += dj * v.g[j];
-    dr += dj * rj;
-    dd += dj * dj;
-  }
-  const double a = block_sum<kBlock>(dg, sh, true);
-  const double b = block_sum<kBlock>(dr, sh, true);
-  const double c = block_sum<kBlock>(dd, sh, true);
-  if (threadIdx.x == 0) {
-    sc.partials[3 * blockIdx.x] = a;
-    sc.partials[3 * blockIdx.x + 1] = b;
-    sc.partials[3 * blockIdx.x + 2] = c;
-  }
-  if (last_block_arrive(sc.tickets + T_CG_POST)) {
-    const double tdg = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 0, sh);
-    const double tdr = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 1, sh);
-    const double tdd = reduce_partials<kBlock>(sc.partials, gridDim.x, 3, 2, sh);
-    if (threadIdx.x == 0) {
-      // tron.cpp:99-103 exit classification
-      if (st->iters >= st->max_iters && st->exit_kind != kCgBoundary &&
-          st->rnorm > st->stop)
-        st->exit_kind = kCgMaxIters;
-      else if (st->exit_kind != kCgBoundary)
-        st->exit_kind = kCgConverged;
-      st->q = 0.5 * (tdg - tdr);  // tron.cpp:106
-      st->dnorm = sqrt(tdd);
-    }
-  }
-}
-
 // ---------------- mid-n CG: one cluster of 8 CTAs per iteration ----------------
 // For n up to kClusterCgMaxN the CG vector work of an iteration (tron.cpp:70-97:
 // p.Hp, alpha, d, the boundary test and tau, r, z, beta, p) is one kernel on a
@@ -847,7 +674,8 @@ void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cud
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, cg_coop_step_kernel, v, st, parts, cond, php_in);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, cg_coop_step_kernel, v, st, parts, cond, php_in);
+  if (e != cudaSuccess) launch_failed(e, "cg_coop_step (cooperative launch)");
 }
 
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {
@@ -860,18 +688,6 @@ void cg_cluster_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s)
 
 void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
   launch_pdl(cg_init_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
-}
-void cg_large_php(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  launch_pdl(cg_php_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
-}
-void cg_large_update(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  launch_pdl(cg_update_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
-}
-void cg_large_direction(const CgVectors& v, CgState* st, Scratch sc, Cond cond, cudaStream_t s) {
-  launch_pdl(cg_direction_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc, cond);
-}
-void cg_large_post(const CgVectors& v, CgState* st, Scratch sc, cudaStream_t s) {
-  launch_pdl(cg_post_kernel, dim3(vec_grid(v.n)), dim3(kBlock), 0, s, v, st, sc);
 }
 
 void cg_small_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s) {
@@ -909,6 +725,7 @@ __global__ void read_flush_kernel(const double2* __restrict__ p, long long n2, d
 void l2_read_flush(const double* buf, int64_t n, cudaStream_t s) {
   read_flush_kernel<<<device_sm_count() * 4, 512, 0, s>>>((const double2*)buf, n / 2,
                                                            const_cast<double*>(buf));
+  TB_LAUNCH_CHECK();
 }
 
 }  // namespace tb

@@ -251,21 +251,15 @@ def test_device_cg_matches_host_cg(port, case, precond):
             assert np.linalg.norm(dev.d) <= delta * (1 + 1e-12)
 
 
-# the CG engines on the same mid-size problem: the persistent cooperative
-# kernel (opt-in; in a graph and host-launched), single cluster kernel per step
+# the CG engines on the same mid-size problem: single cluster kernel per step
 # (default for 4096 < n <= 262144), the cooperative large-n step (default above),
-# the three-kernel large-n step, and the host-driven loop (no graph), each
-# against the host restatement
-@pytest.mark.parametrize("engine", ["fused", "fused_nograph", "cluster", "coop", "large", "nograph"])
+# and the host-driven loop (no graph), each against the host restatement
+@pytest.mark.parametrize("engine", ["cluster", "coop", "nograph"])
 @pytest.mark.parametrize("precond", [False, True])
 def test_cg_engines_match_host_cg(port, monkeypatch, engine, precond):
-    if engine.startswith("fused"):
-        monkeypatch.setenv("TRON_B200_FUSED_CG", "1")
-    if engine in ("coop", "large"):
+    if engine == "coop":
         monkeypatch.setenv("TRON_B200_CLUSTER_CG", "0")
-    if engine == "large":
-        monkeypatch.setenv("TRON_B200_COOP_CG", "0")
-    if engine in ("nograph", "fused_nograph"):
+    if engine == "nograph":
         monkeypatch.setenv("TRON_B200_NO_GRAPH", "1")
     p = synth.synth_sparse(9, 2000, 5000, 37)  # n = 5000 > kSmallCgMaxN
     w = synth.testgen_random_vector(3007, p.X.cols, 0.3)  # the state of fixture case 7 above
@@ -363,52 +357,3 @@ def test_gathered_csr_rejected():
     p = synth.testgen_sparse_problem(1, 20, 10, 1.0, 0.3)
     with pytest.raises(StrategyPreconditionError):
         gpu(p, SVM, svm_strategy=SvmStrategy.Gathered)
-
-
-# ---------------------------------------------------------------- streamed segmented kernels
-# (seg_stream.cu, opt-in with TRON_B200_SEG_STREAM=1): same parity bar, plus
-# a problem large enough to span many CTA ranges, long columns crossing
-# tiles and CTA ranges, empty rows/columns, and bit-reproducibility.
-
-@pytest.fixture
-def stream_env(monkeypatch):
-    monkeypatch.setenv("TRON_B200_SEG_STREAM", "1")
-
-
-def _stream_cases():
-    big = synth.synth_sparse(11, 30000, 200000, 40)  # ~590 tiles: every CTA range used
-    # empty rows and columns: drop every 7th row's entries
-    src = synth.testgen_sparse_problem(21, 900, 3000, 0.01, 0.1)
-    return [("synth", synth.synth_sparse(9, 2000, 5000, 37)), ("big", big), ("sparse_empty", src)]
-
-
-@pytest.mark.parametrize("case", range(3))
-@pytest.mark.parametrize("loss", [LR, SVM])
-def test_stream_kernels_parity(port, stream_env, case, loss):
-    name, p = _stream_cases()[case]
-    n = p.X.cols
-    w = synth.testgen_random_vector(3000 + case, n, 0.3)
-    v = synth.testgen_random_vector(4000 + case, n, 1.0)
-    want = port.logistic(p, w, v) if loss == LR else port.svm(p, w, v)
-    with gpu(p, loss) as ev:
-        assert rel_err(ev.eval_candidate(w), want["f"]) <= 1e-13, name
-        s = ev.candidate_state()
-        assert rel_err(s.z, want["z"]) <= 1e-14
-        if loss == SVM:
-            assert np.array_equal(s.active, want["active"])
-        ev.commit()
-        assert rel_err(ev.gradient(), want["g"]) <= 1e-12, name
-        hv = ev.hessian_vec(v)
-        assert rel_err(hv, want["hv"]) <= 1e-12, name
-        assert np.array_equal(ev.hessian_vec(v), hv), "repeated launches must be bit-identical"
-        assert rel_err(ev.precond_diagonal(), want["M"]) <= 1e-12, name
-
-
-def test_stream_kernels_solve(ref, stream_env):
-    p = synth.synth_sparse(1, 20242, 47236, 74)  # R1 shape
-    cfg = TrustRegionConfig(eps=0.01)
-    got = solve(p, LR, cfg, ExecutionPlan.gpu())
-    w_ref, t_ref = ref.solve(p, 0, cfg)
-    assert rel_err(got.objective, t_ref["objective"]) <= 1e-9
-    assert rel_err(got.w, w_ref) <= 1e-6
-    assert [it.cg_iters for it in got.trace.iterations] == [it["cg_iters"] for it in t_ref["iterations"]]
