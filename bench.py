@@ -3,20 +3,28 @@
 
 A *step* is one complete TRON solve to eps (tron::solve, tron.cpp:127-217)
 of the workload below, from w0 = 0, with the problem already resident in
-HBM.  Default workload: BASELINE.json configs[1], the synthetic news20-shaped
-sparse logistic regression (SYNTH-v1 N1: 19,996 x 1,355,191, 455 nnz/row,
-C = 1, eps = 0.01, FP64).
+HBM; ``value`` is the host wall time of that solve call (the boundary of
+cli.cpp:215-218: the call returns with w on the host).  Default workload:
+BASELINE.json configs[2], the largest single-GPU configuration -- the
+synthetic proteomics-shaped L2-SVM (SYNTH-v1 P1: 2.3e7 x 40 dense, C = 1,
+eps = 0.01, FP64).  R1/N1 (sparse LR) and K1/Q1 (the 1/2/4/8-GPU configs)
+are selectable with --workload.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload N1|R1|P1|K1]
-  python bench.py --impl reference ...   # the reference CPU solver (oracle/_ref)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload P1|R1|N1|K1|Q1]
+  python bench.py --impl reference ...   # the reference CPU solver (oracle/_ref only)
 
-For N > 1 (torchrun) the rows are sharded contiguously across ranks and the
-per-call partial vectors are summed with NCCL (the north star's row-sharded
-layout); time is the max over ranks.
+For N > 1 the rows are sharded contiguously across ranks and the per-call
+partial vectors are summed with NCCL (the north star's row-sharded layout);
+time is the max over ranks.  Without torchrun, ``--gpus N`` (N > 1) re-launches
+itself under torch.distributed.run.
+
+The reference arm never maps the product library: its inputs come from the
+SYNTH-v1 generator inside oracle/_ref (the reference's own testgen::Rng).
 """
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -29,6 +37,40 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TRON train time to eps (s)"
 UNIT = "s"
+SEED = 1
+TEST_SEED = 2  # held-out rows for the prediction parity check
+
+# SYNTH-v1 shapes (BASELINE.json configs).  Kept here so the
+# reference arm does not import the product package (tests check it equals
+# paper_2008_03433_b200.synth.SHAPES).
+SHAPES = {
+    "R1": dict(kind="sparse", l=20242, n=47236, k=74, loss="logistic",
+               desc="rcv1-shaped sparse LR 20,242x47,236, 74 nnz/row"),
+    "N1": dict(kind="sparse", l=19996, n=1355191, k=455, loss="logistic",
+               desc="news20-shaped sparse LR 19,996x1,355,191, 455 nnz/row"),
+    "P1": dict(kind="dense", l=23_000_000, n=40, loss="l2svm",
+               desc="proteomics-shaped dense L2-SVM 2.3e7x40"),
+    "K1": dict(kind="sparse", l=8_400_000, n=20_000_000, k=36, loss="logistic",
+               desc="kdd2010-shaped sparse LR 8.4e6x2.0e7, 36 nnz/row"),
+    "Q1": dict(kind="dense", l=215_000_000, n=40, loss="l2svm",
+               desc="quarter-billion dense L2-SVM 2.15e8x40"),
+}
+# Full reference solves that fit the bounded CPU sample (<= ~30 s on 16 cores).
+FULL_SOLVE_SAMPLE = {"R1", "N1", "P1"}
+PARITY_FILES = {"K1": "profiles/parity_K1.json", "Q1": "profiles/parity_Q1.json"}
+
+
+def workload_config(name, eps, rows=None):
+    """The config dict both arms print (identical by construction)."""
+    s = SHAPES[name]
+    l = rows if rows is not None else s["l"]
+    nnz = l * (s["k"] if s["kind"] == "sparse" else s["n"])
+    return {"workload": name, "shape": s["desc"] + (f", first {l} rows" if rows is not None else ""),
+            "l": l, "n": s["n"], "nnz": nnz, "C": 1.0,
+            "eps": eps, "loss": "Logistic" if s["loss"] == "logistic" else "L2Svm", "w0": "zeros",
+            "generator": f"SYNTH-v1 seed {SEED}",
+            "l2": ("inputs larger than L2 (126 MB) and a 256 MiB read-based L2 eviction before every "
+                   "step" if (nnz * 12 > 126e6) else "256 MiB read-based L2 eviction before every step")}
 
 
 def load_peaks():
@@ -38,6 +80,29 @@ def load_peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def host_description():
+    model, mem_gb = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem_gb = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "usable_cores": cpu_cores(), "mem_gb": mem_gb}
 
 
 class ClockSampler:
@@ -63,7 +128,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.25)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -89,15 +154,133 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def workload_problem(name, rows=None):
+# ---------------------------------------------------------------------------- oracle-side data
+
+class _Matrix:  # the attributes pyoracle reads (FeatureMatrix-like)
+    def __init__(self, layout, rows, cols, values, row_offsets=None, col_indices=None):
+        self.layout, self.rows, self.cols = layout, rows, cols
+        self.values, self.row_offsets, self.col_indices = values, row_offsets, col_indices
+
+    def stored(self):
+        return self.values.size
+
+
+class _Problem:
+    def __init__(self, X, y, C=1.0):
+        self.X, self.y, self.C = X, y, C
+
+
+def oracle_problem(ref, name, seed=SEED, rows=None):
+    """SYNTH-v1 problem generated inside oracle/_ref (no product library)."""
+    s = SHAPES[name]
+    l = rows if rows is not None else s["l"]
+    if s["kind"] == "sparse":
+        ro, ci, vals, y = ref.synth_sparse(seed, l, s["n"], s["k"])
+        return _Problem(_Matrix("csr", l, s["n"], vals, ro, ci), y)
+    vals, y = ref.synth_dense(seed, l, s["n"])
+    return _Problem(_Matrix("dense", l, s["n"], vals), y)
+
+
+def ref_loss(name):
+    return 0 if SHAPES[name]["loss"] == "logistic" else 1
+
+
+def ref_cfg(eps):
+    from pyoracle import make_config
+    return make_config(None, eps=eps)
+
+
+def counts_of(trace_iters):
+    return {"outer": len(trace_iters), "accepted": sum(1 for r in trace_iters if r["accepted"]),
+            "cg_iters": [int(r["cg_iters"]) for r in trace_iters]}
+
+
+def modelled_reference_solve(ref, p, name, threads):
+    """K1/Q1: a full reference solve takes 9-10 minutes (K1) or needs ~140 GB
+    of host RAM (Q1), so a step is the reference evaluator's measured per-call
+    cost (fun, grad, Hv at w = 0; Q1 on its first 2.3e7 rows, scaled by rows)
+    times the call counts of the measured full reference solve recorded in
+    profiles/parity_<W>.json."""
+    rec = json.load(open(os.path.join(ROOT, PARITY_FILES[name])))
+    rc = rec["reference"]
+    n_fun, n_grad, n_hv = 1 + rc["outer"], 1 + rc["accepted"], sum(rc["cg_iters"])
+    p_s, scale = p, 1.0
+    if name == "Q1":
+        rows = 23_000_000
+        X = p.X
+        p_s = _Problem(_Matrix("dense", rows, X.cols, X.values[: rows * X.cols]), p.y[:rows])
+        scale = X.rows / rows
+    t = ref.time_calls(p_s, ref_loss(name), threads, reps=1)
+    v = scale * (n_fun * t["fun_ms"] + n_grad * t["grad_ms"] + n_hv * t["hv_ms"]) / 1e3
+    return v, (f"per-call model: reference evaluator ExecutionPlan::parallel({threads}) fun "
+               f"{t['fun_ms']:.1f} ms, grad {t['grad_ms']:.1f} ms, Hv {t['hv_ms']:.1f} ms at w=0"
+               + (f" on the first {23_000_000} rows x{scale:.3f}" if scale != 1.0 else "")
+               + f", x the measured reference solve's calls ({n_fun} fun, {n_grad} grad, {n_hv} Hv; "
+               f"{PARITY_FILES[name]})")
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    """The reference's own CPU solver (proj/src, compiled in place into
+    oracle/_ref) through its public tron::solve, ExecutionPlan::parallel(T)."""
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import REF_PATH, Reference, have_reference
+    if not have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": f"{REF_PATH} not built"}))
+        return 0
+    ref = Reference()
+    threads = min(cpu_cores(), 64)  # the reference splits work into 64 tasks (parallel.hpp:24)
+    p = oracle_problem(ref, args.workload, rows=args.rows)
+    cfg = ref_cfg(args.eps)
+    loss = ref_loss(args.workload)
+    extra = {}
+    if args.workload in FULL_SOLVE_SAMPLE or args.rows is not None:
+        for _ in range(args.warmup):
+            ref.solve(p, loss, cfg, backend=Reference.PAR, workers=threads)
+        times, t_obj = [], None
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            w, t_obj = ref.solve(p, loss, cfg, backend=Reference.PAR, workers=threads)
+            times.append(time.perf_counter() - t0)
+        v = float(np.mean(times))
+        sample = f"full {args.workload} solve x{args.steps} (mean; min {min(times):.4f} s)"
+        extra = {"objective": t_obj["objective"], "hessian_products": sum(counts_of(t_obj["iterations"])["cg_iters"]),
+                 "outer_iterations": len(t_obj["iterations"]), "wall_min_s": min(times)}
+    else:
+        vs = []
+        for _ in range(args.warmup + args.steps):
+            v, sample = modelled_reference_solve(ref, p, args.workload, threads)
+            vs.append(v)
+        v = float(np.mean(vs[args.warmup:]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (SYNTH-v1 seed {SEED}, generated inside oracle/_ref)",
+        "config": workload_config(args.workload, args.eps, args.rows),
+        "backend": f"ExecutionPlan::parallel({threads}) on the host CPU",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                         "host": host_description()},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    line.update(extra)
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------- B200 arm helpers
+
+def product_problem(name, seed=SEED, rows=None):
     from paper_2008_03433_b200 import LossKind, synth
-    s = synth.SHAPES[name]
-    p = synth.make_shape(name, seed=1, rows=rows)
-    loss = LossKind.Logistic if s["loss"] == "logistic" else LossKind.L2Svm
-    return p, loss, s
+    s = SHAPES[name]
+    p = synth.make_shape(name, seed=seed, rows=rows)
+    return p, (LossKind.Logistic if s["loss"] == "logistic" else LossKind.L2Svm)
 
 
-def algorithmic_bytes(p, loss, active_frac=1.0):
+def algorithmic_bytes(p):
     """SURVEY.md §8(d) algorithmic bytes per call (FP64 values, int32 indices)."""
     X = p.X
     l, n = X.rows, X.cols
@@ -137,130 +320,109 @@ def pin_problem(p, torch):
 
 
 def read_traffic(workload):
-    path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        d = json.load(open(path))
-        return d.get(workload)
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(workload)
     except Exception:
         return None
 
 
-def cpu_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
-
-
-# ---------------------------------------------------------------------------- reference arm
-
-def run_reference(args, rank, world):
-    """The reference's own CPU solver (proj/src, compiled in place into oracle/_ref)."""
-    if rank != 0:
-        return 0
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from pyoracle import REF_PATH, Reference, have_reference
-    if not have_reference():
-        print(json.dumps({"impl": "reference", "unavailable": f"{REF_PATH} not built"}))
-        return 0
-    if args.workload not in FULL_SOLVE_SAMPLE:
-        print(json.dumps({"impl": "reference", "unavailable":
-                          f"a full reference solve of {args.workload} takes 10+ minutes on the host; the b200 "
-                          "line's cpu_baseline carries the reference's per-call model instead"}))
-        return 0
-    from paper_2008_03433_b200 import TrustRegionConfig
-    p, loss, s = workload_problem(args.workload)
-    ref = Reference()
-    threads = min(cpu_cores(), 64)  # the reference splits work into 64 tasks (parallel.hpp:24)
-    cfg = TrustRegionConfig(eps=args.eps)
-    oloss = 0 if loss.name == "Logistic" else 1
-    for _ in range(args.warmup):
-        ref.solve(p, oloss, cfg, backend=Reference.PAR, workers=threads)
-    times = []
-    t_obj = None
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        w, t = ref.solve(p, oloss, cfg, backend=Reference.PAR, workers=threads)
-        times.append(time.perf_counter() - t0)
-        t_obj = t
-    v = float(np.mean(times))
-    hv = sum(r["cg_iters"] for r in t_obj["iterations"])
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SYNTH-v1, seed 1)",
-        "config": {"workload": args.workload, "shape": s["desc"], "C": 1.0, "eps": args.eps,
-                   "backend": f"ExecutionPlan::parallel({threads})"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full {args.workload} solve x{args.steps} (min {min(times):.3f} s)"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "objective": t_obj["objective"], "hessian_products": hv,
-        "outer_iterations": len(t_obj["iterations"]),
-    }
-    print(json.dumps(line))
-    return 0
-
-
-# Workloads whose full reference solve fits the bounded CPU sample (<= ~30 s
-# on the box's 16 cores); the others are timed per call (see cpu_baseline).
-FULL_SOLVE_SAMPLE = {"R1", "N1", "P1"}
-PER_CALL_ROWS = {"Q1": 23_000_000}  # Q1: per-call costs on its first 2.3e7 rows, scaled by rows
-
-
-def solve_call_counts(res):
-    """fun / grad / Hv calls of a solve (tron.cpp:127-217 from the trace)."""
-    it = res.trace.iterations if hasattr(res, "trace") else res["iterations"]
-    acc = sum(1 for r in it if (r.accepted if hasattr(r, "accepted") else r["accepted"]))
-    hv = sum((r.cg_iters if hasattr(r, "cg_iters") else r["cg_iters"]) for r in it)
-    return 1 + len(it), 1 + acc, hv
-
-
-def cpu_baseline(args, p_full, loss, cfg, res):
-    """The reference CPU solver (oracle/_ref) on this host's cores, bounded.
-
-    R1/N1/P1: full solves (min of up to 3 within ~20 s), with parity of the
-    GPU result against it.  K1/Q1 (a full reference solve takes 10+ min):
-    the reference evaluator's per-call cost (fun, grad, Hv at w = 0, the
-    first outer iteration's state) times the solve's call counts; Q1's calls
-    are timed on its first 2.3e7 rows and scaled by rows (dense: cost is
-    linear in rows)."""
+def cpu_baseline(args, p_full, res, ev, loss, cfg, plan):
+    """The reference CPU solver (oracle/_ref) on this host's cores, bounded,
+    plus the parity of the GPU result against it (north-star gate)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import Reference, have_reference
     if not have_reference():
         return None
     ref = Reference()
     threads = min(cpu_cores(), 64)  # the reference splits work into 64 tasks (parallel.hpp:24)
-    oloss = 0 if loss.name == "Logistic" else 1
-    if args.workload in FULL_SOLVE_SAMPLE:
-        ts = []
-        t_begin = time.perf_counter()
-        while len(ts) < 3 and (time.perf_counter() - t_begin) < 20.0:
-            t0 = time.perf_counter()
-            w_ref, t_ref = ref.solve(p_full, oloss, cfg, backend=Reference.PAR, workers=threads)
-            ts.append(time.perf_counter() - t0)
-        rel_f = abs(res.objective - t_ref["objective"]) / abs(t_ref["objective"])
-        rel_w = float(np.linalg.norm(res.w - w_ref) / np.linalg.norm(w_ref))
-        return {"value": float(min(ts)), "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{len(ts)} full {args.workload} solves (min), ExecutionPlan::parallel({threads})",
-                "parity": {"rel_objective": rel_f, "rel_w": rel_w,
-                           "outer": [len(res.trace.iterations), len(t_ref["iterations"])],
-                           "hv": [res.hessian_products, sum(r["cg_iters"] for r in t_ref["iterations"])]}}
-    from paper_2008_03433_b200.tron import FeatureMatrix, Problem
-    p_s, scale = p_full, 1.0
-    rows = PER_CALL_ROWS.get(args.workload)
-    if rows is not None and rows < p_full.X.rows:
+    oloss = ref_loss(args.workload)
+    rcfg = ref_cfg(args.eps)
+    out = {"unit": UNIT, "cores": threads, "kind": "reference", "host": host_description()}
+    if args.workload not in FULL_SOLVE_SAMPLE and args.rows is None:
+        v, sample = modelled_reference_solve(ref, p_full, args.workload, threads)
+        out.update(value=v, sample=sample)
+        try:
+            out["parity"] = json.load(open(os.path.join(ROOT, PARITY_FILES[args.workload])))["parity"]
+            out["parity"]["source"] = PARITY_FILES[args.workload] + " (full-size run, same generator)"
+        except Exception:
+            pass
+        return out
+    ts = []
+    t_begin = time.perf_counter()
+    while len(ts) < 3 and (time.perf_counter() - t_begin) < 25.0:
+        t0 = time.perf_counter()
+        w_ref, t_ref = ref.solve(p_full, oloss, rcfg, backend=Reference.PAR, workers=threads)
+        ts.append(time.perf_counter() - t0)
+    out.update(value=float(min(ts)),
+               sample=f"{len(ts)} full {args.workload} solves (min), ExecutionPlan::parallel({threads})")
+    # the 1-core leg: ExecutionPlan::sequential() -- a full solve when the
+    # parallel one is short, else the per-call model on a row sample
+    if ts[0] < 2.0:
+        t0 = time.perf_counter()
+        ref.solve(p_full, oloss, rcfg, backend=Reference.SEQ, workers=1)
+        out["sequential"] = {"value": time.perf_counter() - t0, "cores": 1,
+                             "sample": f"1 full {args.workload} solve, ExecutionPlan::sequential()"}
+    elif p_full.X.layout == "dense":
+        from paper_2008_03433_b200.tron import FeatureMatrix, Problem
         X = p_full.X
-        p_s = Problem(FeatureMatrix("dense", rows, X.cols, X.values[: rows * X.cols]), p_full.y[:rows], p_full.C)
-        scale = X.rows / rows
-    t = ref.time_calls(p_s, oloss, threads, reps=1)
-    n_fun, n_grad, n_hv = solve_call_counts(res)
-    v = scale * (n_fun * t["fun_ms"] + n_grad * t["grad_ms"] + n_hv * t["hv_ms"]) / 1e3
-    what = f"first {rows} rows, x{scale:.3f} by rows" if scale != 1.0 else "full problem"
-    return {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": (f"per-call model: reference evaluator (ExecutionPlan::parallel({threads})) "
-                       f"fun {t['fun_ms']:.1f} ms, grad {t['grad_ms']:.1f} ms, Hv {t['hv_ms']:.1f} ms "
-                       f"at w=0 on the {what}, x the solve's calls ({n_fun} fun, {n_grad} grad, {n_hv} Hv)"),
-            "per_call_ms": {k: float(x) for k, x in t.items()}}
+        rows = X.rows // 10
+        p_s = Problem(FeatureMatrix("dense", rows, X.cols, X.values[: rows * X.cols]), p_full.y[:rows], 1.0)
+        t = ref.time_calls(p_s, oloss, 1, reps=1, backend=Reference.SEQ)
+        c = counts_of(t_ref["iterations"])
+        n_fun, n_grad, n_hv = 1 + c["outer"], 1 + c["accepted"], sum(c["cg_iters"])
+        out["sequential"] = {"value": 10 * (n_fun * t["fun_ms"] + n_grad * t["grad_ms"] + n_hv * t["hv_ms"]) / 1e3,
+                             "cores": 1,
+                             "sample": (f"per-call model: ExecutionPlan::sequential() fun {t['fun_ms']:.0f} ms, "
+                                        f"grad {t['grad_ms']:.0f} ms, Hv {t['hv_ms']:.0f} ms at w=0 on the first "
+                                        f"{rows} rows x10, x the reference solve's calls")}
+    # ---- parity (BASELINE.json north star): objective and w within 1e-6,
+    # counts within +-1, SVM active sets and test predictions identical
+    it_gpu = [{"accepted": r.accepted, "cg_iters": r.cg_iters} for r in res.trace.iterations]
+    cg, cr = counts_of(it_gpu), counts_of(t_ref["iterations"])
+    rel_f = abs(res.objective - t_ref["objective"]) / abs(t_ref["objective"])
+    rel_w = float(np.linalg.norm(res.w - w_ref) / np.linalg.norm(w_ref))
+    par = {"rel_objective": rel_f, "rel_w": rel_w, "outer": [cg["outer"], cr["outer"]],
+           "accepted": [cg["accepted"], cr["accepted"]], "cg_iters": [cg["cg_iters"], cr["cg_iters"]],
+           "hv": [sum(cg["cg_iters"]), sum(cr["cg_iters"])]}
+    par["gate_pass"] = bool(rel_f <= 1e-6 and rel_w <= 1e-6 and abs(cg["outer"] - cr["outer"]) <= 1
+                            and all(abs(a - b) <= 1 for a, b in zip(cg["cg_iters"], cr["cg_iters"]))
+                            and len(cg["cg_iters"]) == len(cr["cg_iters"]))
+    if oloss == 1:  # SVM active set I = {i : 1 - y_i z_i > 0} at each solver's final w
+        act_gpu = ev.committed_state().active
+        act_ref = ref.svm(p_full, w_ref, np.zeros(p_full.X.cols))["active"]
+        par["active_set_identical"] = bool(np.array_equal(act_gpu, act_ref))
+        par["active_set_sizes"] = [int(act_gpu.size), int(act_ref.size)]
+        par["active_set_symmetric_difference"] = int(np.setxor1d(act_gpu, act_ref).size)
+        ev.eval_candidate(w_ref)  # the GPU margin pass at the reference's w: bit-exact rows
+        par["active_set_identical_at_reference_w"] = bool(np.array_equal(ev.candidate_state().active, act_ref))
+    # predictions (model.cpp:88-117) on held-out SYNTH-v1 rows (seed 2)
+    from paper_2008_03433_b200 import make_evaluator
+    test_rows = min(p_full.X.rows, 2_000_000)
+    p_test, _ = product_problem(args.workload, seed=TEST_SEED, rows=test_rows)
+    with make_evaluator(p_test, loss, plan) as evt:
+        lab_gpu, correct_gpu = evt.predict(res.w)
+        lab_gpu_at_ref, _ = evt.predict(w_ref)
+    Xt = p_test.X
+    Xt.y = p_test.y
+    lab_ref, correct_ref = ref.predict(Xt, w_ref)
+    par["predictions_identical"] = bool(np.array_equal(lab_gpu, lab_ref))
+    par["predictions_differing"] = int(np.sum(lab_gpu != lab_ref))
+    par["predictions_identical_at_reference_w"] = bool(np.array_equal(lab_gpu_at_ref, lab_ref))
+    par["test_rows"] = test_rows
+    par["test_accuracy"] = [correct_gpu / test_rows, correct_ref / test_rows]
+    out["parity"] = par
+    return out
+
+
+def spawn_ranks(args):
+    """--gpus N without torchrun: re-launch under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------- B200 arm
@@ -271,34 +433,38 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="N1", choices=["R1", "N1", "P1", "K1", "Q1"])
+    ap.add_argument("--workload", default="P1", choices=list(SHAPES))
     ap.add_argument("--eps", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--rows", type=int, default=None,
+                    help="first ROWS rows of the workload only (tests; the config says so)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
 
     if args.impl == "reference":
-        rc = run_reference(args, rank, world)
-        if dist is not None:
-            dist.barrier()
-            dist.destroy_process_group()
-        return rc
+        return run_reference(args, rank, world)
 
     import ctypes
+
+    import torch
+    import torch.distributed as dist_mod
 
     from paper_2008_03433_b200 import ExecutionPlan, TrustRegionConfig, make_evaluator
     from paper_2008_03433_b200 import _lib
     from paper_2008_03433_b200.sharding import shard
 
-    p_full, loss, s = workload_problem(args.workload)
+    dist = None
+    if world > 1:
+        dist = dist_mod
+        dist.init_process_group("gloo")
+
+    p_full, loss = product_problem(args.workload, rows=args.rows)
     p, row_begin = shard(p_full, rank, world) if world > 1 else (p_full, 0)
     plan = ExecutionPlan.gpu(device=local_rank)
     if world > 1:
@@ -314,108 +480,115 @@ def main():
         plan.row_begin, plan.global_rows = row_begin, p_full.X.rows
     cfg = TrustRegionConfig(eps=args.eps)
 
-    import torch
     torch.cuda.set_device(local_rank)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    ev = make_evaluator(p, loss, plan)
-    for _ in range(args.warmup):
-        ev.solve(cfg)
+    def evict_l2():  # read-based: leaves nothing dirty to write back inside the step
+        if flush is not None:
+            flush.view(torch.int64).sum()
+        torch.cuda.synchronize()
 
     def barrier():
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
 
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    ev = make_evaluator(p, loss, plan)
+    for _ in range(args.warmup):
+        ev.solve(cfg)
+
     launches0 = ev.launch_count()
-    step_ms, wall, res = [], [], None
+    wall, dev_ms, res = [], [], None
     sampler = ClockSampler(local_rank)
     barrier()
     with sampler:
         for _ in range(args.steps):
-            if flush is not None:  # inputs > L2 anyway for N1/K1/P1; flush for R1-sized cases
-                flush.fill_(1)
-                torch.cuda.synchronize()
+            evict_l2()
             t0 = time.perf_counter()
-            res = ev.solve(cfg)
+            res = ev.solve(cfg)  # returns with w in host memory
             wall.append(time.perf_counter() - t0)
-            step_ms.append(res.device_ms)
+            dev_ms.append(res.device_ms)
     barrier()
     launches = ev.launch_count() - launches0
-    t_step = float(np.mean(step_ms)) / 1e3  # CUDA-event time per solve on this rank
-    if dist is not None:
-        t = torch.tensor([t_step], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t[0])
+    t_step = max_over_ranks(float(np.mean(wall)))
+    t_dev = max_over_ranks(float(np.mean(dev_ms)) / 1e3)
 
     # ---- kernel-level roofline (dominant kernel: the Hessian-vector product)
     kt = ev.bench_kernels(reps=20, flush_l2=True)
-    ab = algorithmic_bytes(p, loss)
+    ab = algorithmic_bytes(p)
     peak, peak_kind = load_peaks()
-    hv_s = kt["hv_ms"] / 1e3
-    achieved = ab["hv"] / hv_s / 1e9
+    achieved = ab["hv"] / (kt["hv_ms"] / 1e3) / 1e9
     trans_gbs = ab["transposed"] / (kt["transposed_ms"] / 1e3) / 1e9
 
-    # ---- e2e: the public API from pinned host buffers (create = H2D + on-device
-    # CSC build, solve, w D2H), every step; the pinned copies are made untimed
-    p_pin = pin_problem(p, torch) if args.workload != "Q1" else p  # Q1: 68.8 GB stays pageable
-    e2e = []
-    for k in range(max(2, min(args.steps, 5))):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        with make_evaluator(p_pin, loss, plan) as ev2:
-            r2 = ev2.solve(cfg)
-        e2e.append(time.perf_counter() - t0)
-    del p_pin
-    e2e_v = float(np.median(e2e))
-    if dist is not None:
-        t = torch.tensor([e2e_v], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_v = float(t[0])
+    # ---- e2e through the public API, every step: make_evaluator from the
+    # caller's PAGEABLE numpy arrays (H2D + on-device CSC build / transpose),
+    # solve, w to host, destroy.  The pinned-input variant is an extra key.
+    def e2e_time(prob, reps):
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with make_evaluator(prob, loss, plan) as ev2:
+                ev2.solve(cfg)
+            ts.append(time.perf_counter() - t0)
+        return max_over_ranks(float(np.median(ts)))
+
+    reps = max(2, min(args.steps, 5))
+    e2e_v = e2e_time(p, reps)
+    e2e_pin = None
+    if args.workload != "Q1":  # Q1's 68.8 GB is not duplicated into pinned memory
+        p_pin = pin_problem(p, torch)
+        e2e_pin = e2e_time(p_pin, reps)
+        del p_pin
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(args, p_full, res, ev, loss, cfg, plan)
 
     if rank != 0:
         ev.close()
-        if dist is not None:
-            dist.barrier()
-            dist.destroy_process_group()
+        barrier()
+        dist.destroy_process_group()
         return 0
 
-    # ---- CPU baseline: the reference solver on this host, bounded sample
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(args, p_full, loss, cfg, res)
-
-    nnz = p_full.X.stored()
     line = {
         "metric": METRIC, "value": t_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SYNTH-v1 generator, seed 1; SURVEY.md §8(d))",
-        "config": {"workload": args.workload, "shape": s["desc"], "l": p_full.X.rows, "n": p_full.X.cols,
-                   "nnz": nnz, "C": 1.0, "eps": args.eps, "loss": loss.name,
-                   "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
-                   "l2": "256 MiB flush before every step" if flush is not None else "no flush",
-                   "timing": "CUDA events on the solver stream around each solve, mean over steps"},
+        "data": f"synthetic (SYNTH-v1 generator, seed {SEED}; SURVEY.md §8(d))",
+        "config": workload_config(args.workload, args.eps, args.rows),
+        "parallelism": f"row-sharded x{world} (NCCL allreduce of partials)" if world > 1 else "1 GPU",
+        "timing": ("value: host wall time of each solve call (returns with w on the host), mean over "
+                   "steps, max over ranks; device_s: CUDA-event time of the same solves"),
+        "device_s": t_dev, "wall_s_min": max_over_ranks(float(np.min(wall))) if world > 1 else float(np.min(wall)),
         "objective": res.objective, "converged": res.converged,
         "outer_iterations": len(res.trace.iterations), "hessian_products": res.hessian_products,
         "hv_per_s": res.hessian_products / t_step if t_step > 0 else None,
-        "wall_ms_per_step": float(np.mean(wall)) * 1e3,
         "roofline": {"bound": "hbm",
                      "kernel": ("Hessian-vector product (CSR D*Xv + CSC segmented X^T u)" if p.X.layout == "csr"
                                 else "Hessian-vector product (dense tall-skinny TMA pass, one read of X)"),
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_source": f"{peak_kind} (copy read+write GB/s; frac is 'of {peak_kind}')",
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs: copy read+write GB/s)",
                      "traffic": read_traffic(args.workload),
                      "algorithmic_bytes_per_launch": ab["hv"], "avg_launch_ms": kt["hv_ms"],
                      "launch_timing": "CUDA events around each Hv launch on the solver stream, 256 MiB "
-                                      "L2 flush before each, mean of 20, same process after the timed solves",
+                                      "read-based L2 eviction before each, mean of 20, after the timed solves",
                      "hv_share_of_step": res.hessian_products * kt["hv_ms"] / (t_step * 1e3) if t_step > 0 else None,
                      "transposed_only_gbs": trans_gbs, "kernel_ms": kt},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes(p),
                 "d2h_bytes_per_step": int(8 * p.X.cols + 64),
-                "what": ("make_evaluator from " + ("pageable (staged)" if args.workload == "Q1" else "pinned")
-                         + " host arrays (H2D + device CSC build / transpose) + solve + w to host + destroy, via the C ABI")},
+                "what": ("make_evaluator from the caller's pageable numpy arrays (H2D + on-device CSC build / "
+                         "transpose) + solve + w to host + destroy, through the C ABI; median of "
+                         f"{reps}"),
+                "pinned_inputs_value": e2e_pin},
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
         "device_memory_bytes": ev.memory_bytes(),
@@ -423,7 +596,7 @@ def main():
     print(json.dumps(line))
     ev.close()
     if dist is not None:
-        dist.barrier()
+        barrier()
         dist.destroy_process_group()
     return 0
 

@@ -148,6 +148,14 @@ int tron_gpu_truncated_cg(tron_gpu_ctx *ctx, double delta, const tron_config *cf
 int tron_gpu_solve(tron_gpu_ctx *ctx, const tron_config *cfg, const double *w0, double *w_out,
                    tron_solve_info *info, tron_iteration *trace, uint64_t trace_cap);
 
+/* predict(Model, Problem) (model.cpp:88-117) over this context's rows:
+ * labels[i] = sign(x_i . w), ties to +1 (labels nullable, l entries);
+ * *correct (nullable) = number of labels equal to y_i.  w has dimension()
+ * entries.  Each row is summed sequentially in storage order without FMA,
+ * the reference's rounding, so the labels match the reference's for the
+ * same w.  To score a test set, create a context on the test rows. */
+int tron_gpu_predict(tron_gpu_ctx *ctx, const double *w, double *labels, uint64_t *correct);
+
 int tron_gpu_ledger(tron_gpu_ctx *ctx, tron_ledger *out);
 int tron_gpu_reset_ledger(tron_gpu_ctx *ctx);
 
@@ -155,7 +163,8 @@ int tron_gpu_reset_ledger(tron_gpu_ctx *ctx);
  * context's stream) over `reps` launches on the committed state of
  * out_ms[0] whole Hv product, [1] the transposed product alone (CSC merge
  * SpMV, or the dense tall-skinny accumulation), [2] the forward margin
- * pass, [3] the gradient.  flush_l2 writes 256 MiB between launches. */
+ * pass, [3] the gradient.  flush_l2 evicts the L2 between launches by
+ * reading a 256 MiB buffer (nothing dirty is left to write back). */
 int tron_gpu_bench_kernels(tron_gpu_ctx *ctx, int reps, int flush_l2, double out_ms[4]);
 /* Device bytes held by the context (matrix copies + vectors). */
 int tron_gpu_memory_bytes(tron_gpu_ctx *ctx, uint64_t *bytes);

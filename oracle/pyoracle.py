@@ -222,7 +222,7 @@ class Reference:
                                 POINTER(or_config), c_int, ctypes.c_uint, PD, PD,
                                 POINTER(or_solve_info), POINTER(or_iteration), c_size_t]
         L.ref_time_calls.argtypes = [c_int, c_size_t, c_size_t, PI64, PI32, PD, PD, c_double, c_int,
-                                     ctypes.c_uint, c_int, PD]
+                                     c_int, ctypes.c_uint, c_int, PD]
         L.ref_logistic_fused_pass.restype = c_double
         L.ref_logistic_fused_pass.argtypes = [c_int, c_size_t, c_size_t, PI64, PI32, PD, PD,
                                               c_double, PD, PD, PD, PD, PD]
@@ -243,6 +243,12 @@ class Reference:
         L.ref_testgen_random_vector.argtypes = [c_uint64, c_size_t, c_double, PD]
         L.ref_testgen_random_index_set.restype = c_size_t
         L.ref_testgen_random_index_set.argtypes = [c_uint64, c_size_t, c_double, PI64]
+        L.ref_synth_sparse.argtypes = [c_uint64, c_size_t, c_size_t, c_size_t, c_double, c_double,
+                                       PI64, PI32, PD, PD]
+        L.ref_synth_dense.argtypes = [c_uint64, c_size_t, c_size_t, c_double, c_double, c_double,
+                                      PD, PD]
+        L.ref_predict.restype = c_size_t
+        L.ref_predict.argtypes = [c_int, c_size_t, c_size_t, PI64, PI32, PD, PD, PD, PD]
 
     def _args(self, problem):
         lay, l, n, ro, ci, vals = _matrix_args(problem.X)
@@ -311,11 +317,12 @@ class Reference:
         L.ref_parsed_free(h)
         return "ok", (ro, ci, vals, y, c.value)
 
-    def time_calls(self, problem, loss, workers, reps=1):
-        """Per-call ms of the reference evaluator (fun, grad, Hv) at w = 0, parallel(workers)."""
+    def time_calls(self, problem, loss, workers, reps=1, backend=1):
+        """Per-call ms of the reference evaluator (fun, grad, Hv) at w = 0 under
+        ExecutionPlan::parallel(workers) (backend 1) or ::sequential() (backend 0)."""
         args, keep = self._args(problem)
         out = np.zeros(3)
-        st = self.lib.ref_time_calls(*args, loss, workers, reps, _p(out))
+        st = self.lib.ref_time_calls(*args, loss, backend, workers, reps, _p(out))
         if st != 0:
             raise RuntimeError(f"ref_time_calls failed ({st})")
         return dict(fun_ms=out[0], grad_ms=out[1], hv_ms=out[2])
@@ -343,6 +350,33 @@ class Reference:
         g, hv, m = np.empty(n), np.empty(n), np.empty(n)
         self.lib.ref_svm_grad_hv(*args, _p(w), _p(v), _p(g), _p(hv), _p(m))
         return dict(f=f, z=z, active=act[:na.value].copy(), g=g, hv=hv, M=m)
+
+    def predict(self, X, w):
+        """The reference's predict (model.cpp:88-117): (labels, correct) of the
+        rows of X (a FeatureMatrix-like object) under w; y optional via X.y."""
+        lay, l, n, ro, ci, vals = _matrix_args(X)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        y = getattr(X, "y", None)
+        y = np.ascontiguousarray(y, dtype=np.float64) if y is not None else np.zeros(l)
+        labels = np.empty(l)
+        c = self.lib.ref_predict(lay, l, n, _p(ro, PI64), _p(ci, PI32), _p(vals), _p(y), _p(w), _p(labels))
+        return labels, int(c)
+
+    # SYNTH-v1 (SURVEY.md §8(d)) with the reference's testgen::Rng
+    def synth_sparse(self, seed, l, n, k, s=1.0, flip=0.1):
+        ro, ci = np.empty(l + 1, dtype=np.int64), np.empty(l * k, dtype=np.int32)
+        vals, y = np.empty(l * k), np.empty(l)
+        st = self.lib.ref_synth_sparse(seed, l, n, k, s, flip, _p(ro, PI64), _p(ci, PI32), _p(vals), _p(y))
+        if st != 0:
+            raise ValueError("ref_synth_sparse: bad shape")
+        return ro, ci, vals, y
+
+    def synth_dense(self, seed, l, n=40, decades=2.0, rho=0.0, flip=0.1):
+        vals, y = np.empty(l * n), np.empty(l)
+        st = self.lib.ref_synth_dense(seed, l, n, decades, rho, flip, _p(vals), _p(y))
+        if st != 0:
+            raise ValueError("ref_synth_dense: bad shape")
+        return vals, y
 
     # fixture generators
     def dense_problem(self, seed, l, n, flip=0.1):

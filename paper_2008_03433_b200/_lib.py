@@ -87,6 +87,7 @@ SIGNATURES = [
                                       PD]),
     ("tron_gpu_solve", c_int, [c_void_p, POINTER(tron_config), PD, PD, POINTER(tron_solve_info),
                                POINTER(tron_iteration), c_uint64]),
+    ("tron_gpu_predict", c_int, [c_void_p, PD, PD, PU64]),
     ("tron_gpu_ledger", c_int, [c_void_p, POINTER(tron_ledger)]),
     ("tron_gpu_reset_ledger", c_int, [c_void_p]),
     ("tron_gpu_bench_kernels", c_int, [c_void_p, c_int, c_int, PD]),

@@ -379,6 +379,15 @@ int tron_gpu_solve(tron_gpu_ctx* ctx, const tron_config* cfg, const double* w0, 
   return st;
 }
 
+int tron_gpu_predict(tron_gpu_ctx* ctx, const double* w, double* labels, uint64_t* correct) {
+  NEED_CTX(ctx);
+  if (!w && ctx->engine->dimension() > 0) return fail(TRON_ERR_ARGUMENT, "null weights");
+  return guarded([&] {
+    const uint64_t c = ctx->engine->predict(w, labels);
+    if (correct) *correct = c;
+  });
+}
+
 int tron_gpu_ledger(tron_gpu_ctx* ctx, tron_ledger* out) {
   NEED_CTX(ctx);
   *out = ctx->engine->ledger;

@@ -1312,6 +1312,29 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
 }
 
 // ----------------------------------------------------------------------------
+// predict (model.cpp:88-117)
+// ----------------------------------------------------------------------------
+uint64_t Engine::predict(const double* w, double* labels) {
+  AllocScope scope(s_);
+  DevBuf<double> lab;
+  lab.alloc(l_ > 0 ? l_ : 1);
+  DevBuf<unsigned long long> correct;
+  correct.alloc(1);
+  if (n_ > 0) upload(vtmp_.p, w, n_ * sizeof(double), s_);
+  if (dense_)
+    predict_dense(l_, n_, ld_, Xc_.p, vtmp_.p, y_.p, lab.p, correct.p, s_);
+  else
+    predict_csr(X_, vtmp_.p, y_.p, lab.p, correct.p, s_);
+  count_launch(1);
+  unsigned long long c = 0;
+  cuda_check(cudaMemcpyAsync(&c, correct.p, sizeof(c), cudaMemcpyDeviceToHost, s_), "D2H");
+  if (labels && l_ > 0) download(labels, lab.p, l_ * sizeof(double), s_);
+  synchronize();
+  cuda_check(cudaGetLastError(), "predict");
+  return c;
+}
+
+// ----------------------------------------------------------------------------
 // per-kernel timing for the roofline figures of bench.py
 // ----------------------------------------------------------------------------
 void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {

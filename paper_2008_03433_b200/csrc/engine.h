@@ -137,6 +137,8 @@ class Engine {
   void solve_device(const tron_config& cfg, const double* w0, double* w_out, tron_solve_info* info,
                     tron_iteration* trace, uint64_t cap);
   void bench_kernels(int reps, bool flush_l2, KernelTimes* out);
+  // predict (model.cpp:88-117) of this context's rows under host weights w.
+  uint64_t predict(const double* w, double* labels);
 
   tron_ledger ledger{};
   uint64_t launches = 0;

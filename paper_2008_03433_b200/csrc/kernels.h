@@ -152,6 +152,14 @@ void screen_inputs(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t
 // Row-offset narrowing int64 -> int32 (device).
 void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t s);
 
+// ---- predict (predict.cu; model.cpp:88-117) ---------------------------------
+// labels[i] = sign(x_i . w) (ties +1), rows summed sequentially in storage
+// order (bit-exact with the reference); *correct (device) = #{labels == y}.
+void predict_csr(const CsrView& X, const double* w, const double* y, double* labels,
+                 unsigned long long* correct, cudaStream_t s);
+void predict_dense(int64_t l, int64_t n, int64_t ld, const double* X, const double* w,
+                   const double* y, double* labels, unsigned long long* correct, cudaStream_t s);
+
 // ---- vector kernels (vec_kernels.cu) -----------------------------------------
 // wc = w + d (d may be null: wc = w); obj->ww = wc.wc
 void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjScalars* obj,

@@ -451,6 +451,18 @@ class GpuEvaluator:
         return SolveResult(w, trace, info.objective, bool(info.converged), int(info.hessian_products),
                            float(info.device_ms))
 
+    def predict(self, w):
+        """predict(Model, Problem) (model.cpp:88-117) on this evaluator's rows:
+        (labels, correct) with labels = sign(x_i . w), ties to +1."""
+        w = _f64(w)
+        if w.size != self.n:
+            raise DimensionError(f"predict: w has length {w.size}, expected {self.n}")
+        labels = np.empty(self.l)
+        correct = ctypes.c_uint64()
+        _raise(lib.tron_gpu_predict(self._h, _ptr(w, ctypes.c_double), _ptr(labels, ctypes.c_double),
+                                    ctypes.byref(correct)))
+        return labels, int(correct.value)
+
     # -- plumbing
     def ledger(self) -> TransferLedger:
         lg = _lib.tron_ledger()

@@ -328,3 +328,27 @@ def test_reference_solver_drives_the_gpu_evaluator(ref, case):
     assert rel_err(t_gpu["objective"], t_ref["objective"]) <= 1e-9
     assert rel_err(w_gpu, w_ref) <= 1e-6
     assert [it["cg_iters"] for it in t_gpu["iterations"]] == [it["cg_iters"] for it in t_ref["iterations"]]
+
+
+# predict (model.cpp:88-117) on the device against the reference's own predict:
+# at the same w the labels are bit-identical (sequential row sums, no FMA), and
+# each solver's own model labels a held-out set identically.
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_predict_matches_reference(ref, kind):
+    if kind == "dense":
+        p, pt, loss, oloss = synth.synth_dense(1, 200_000, 40), synth.synth_dense(2, 100_000, 40), SVM, 1
+    else:
+        p, pt = synth.synth_sparse(1, 20242, 47236, 74), synth.synth_sparse(2, 10000, 47236, 74)
+        loss, oloss = LR, 0
+    cfg = TrustRegionConfig(eps=0.01)
+    res = solve(p, loss, cfg, plan())
+    w_ref, _ = ref.solve(p, oloss, cfg)
+    Xt = pt.X
+    Xt.y = pt.y
+    with make_evaluator(pt, loss, plan()) as ev:
+        lab_ref_w, c_ref_w = ev.predict(w_ref)
+        lab_gpu, _ = ev.predict(res.w)
+    lab_ref, c_ref = ref.predict(Xt, w_ref)
+    assert np.array_equal(lab_ref_w, lab_ref) and c_ref_w == c_ref
+    assert np.array_equal(lab_gpu, lab_ref)
+    assert set(np.unique(lab_gpu)) <= {-1.0, 1.0}

@@ -96,3 +96,44 @@ def test_synth_dense_matches_sequential_stream(seed, l, n):
     rows, y = py_dense(seed, l, n)
     assert np.array_equal(p.X.values, np.array([v for r in rows for _, v in r]))
     assert np.array_equal(p.y, np.array(y))
+
+
+# The reference arm of bench.py generates SYNTH-v1 inside oracle/_ref
+# (ref_shim.cpp, the reference's own testgen::Rng) so it never maps the product
+# library; both generators must produce the same bits.
+@pytest.mark.parametrize("seed,l,n,k", [(1, 300, 5000, 17), (4, 64, 200, 200), (7, 500, 40000, 3)])
+def test_reference_side_synth_sparse_matches_product(ref, seed, l, n, k):
+    from paper_2008_03433_b200 import synth
+    p = synth.synth_sparse(seed, l, n, k)
+    ro, ci, vals, y = ref.synth_sparse(seed, l, n, k)
+    assert np.array_equal(ro, p.X.row_offsets)
+    assert np.array_equal(ci, p.X.col_indices)
+    assert np.array_equal(vals.view(np.uint64), p.X.values.view(np.uint64))
+    assert np.array_equal(y, p.y)
+
+
+@pytest.mark.parametrize("seed,l,n", [(1, 40000, 40), (3, 777, 7), (9, 5, 64)])
+def test_reference_side_synth_dense_matches_product(ref, seed, l, n):
+    from paper_2008_03433_b200 import synth
+    p = synth.synth_dense(seed, l, n)
+    vals, y = ref.synth_dense(seed, l, n)
+    assert np.array_equal(vals.view(np.uint64), p.X.values.view(np.uint64))
+    assert np.array_equal(y, p.y)
+
+
+def test_reference_predict_matches_sign_of_sequential_dot(ref):
+    from paper_2008_03433_b200 import synth
+    p = synth.synth_dense(2, 3000, 40)
+    w = synth.testgen_random_vector(5, 40, 1.0)
+    X = p.X
+    X.y = p.y
+    labels, correct = ref.predict(X, w)
+    Xd = X.values.reshape(3000, 40)
+    want = np.empty(3000)
+    for i in range(3000):
+        s = 0.0
+        for j in range(40):
+            s += Xd[i, j] * w[j]
+        want[i] = -1.0 if s < 0.0 else 1.0
+    assert np.array_equal(labels, want)
+    assert correct == int(np.sum(want == p.y))
