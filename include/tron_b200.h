@@ -41,7 +41,13 @@ typedef enum {
 } tron_status;
 
 typedef enum { TRON_LOSS_LOGISTIC = 0, TRON_LOSS_L2SVM = 1 } tron_loss; /* loss.hpp:11 */
-typedef enum { TRON_SVM_GATHERED = 0, TRON_SVM_INDIRECT = 1 } tron_svm_strategy; /* loss.hpp:16 */
+/* SvmStrategy (loss.hpp:16).  GATHERED copies the active rows X_I at every
+ * commit (gather_rows, linalg.cpp:197-229; dense panel or CSR rows plus their
+ * CSC copy) after the reference's budget check (backend.cpp:255-261: over
+ * budget -> TRON_ERR_BUDGET); INDIRECT masks the full matrix.  AUTO (no
+ * reference counterpart) gathers only when X_I holds at most half of X and
+ * fits the budget, else runs INDIRECT -- the results agree either way. */
+typedef enum { TRON_SVM_GATHERED = 0, TRON_SVM_INDIRECT = 1, TRON_SVM_AUTO = 2 } tron_svm_strategy;
 typedef enum { TRON_CG_CONVERGED = 0, TRON_CG_BOUNDARY = 1, TRON_CG_MAXITERS = 2 } tron_cg_exit;
 /* Solve modes: DEVICE keeps CG and every n-vector on the GPU (only scalars
  * reach the host); HOST_CG runs the reference control flow on the host and

@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("TRON_B200_LIB") or os.path.join(HERE, "libtron_b200.s
 OK, ERR_DIMENSION, ERR_BOUNDS, ERR_STRATEGY, ERR_BUDGET, ERR_NUMERICAL, ERR_LOGIC, ERR_CUDA, \
     ERR_NCCL, ERR_OOM, ERR_ARGUMENT, ERR_PARSE, ERR_UNSUPPORTED_LABEL = range(13)
 LOSS_LOGISTIC, LOSS_L2SVM = 0, 1
-SVM_GATHERED, SVM_INDIRECT = 0, 1
+SVM_GATHERED, SVM_INDIRECT, SVM_AUTO = 0, 1, 2
 SOLVE_DEVICE, SOLVE_HOST_CG = 0, 1
 
 

@@ -7,6 +7,7 @@
 //  * build_csc: the device-built CSC copy (stable in row order) that
 //    csc_seg.cu streams for every X^T u.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <cstdlib>
 
@@ -183,7 +184,8 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
       // loss.cpp:86-89: a0_i *= dvec_i; svm indirect skips inactive rows.
-      a[row] = mask ? (active ? s : 0.0) : s * dvec[row];
+      // (no mask and no dvec: the gathered rows X_I, every row active)
+      a[row] = mask ? (active ? s : 0.0) : (dvec ? s * dvec[row] : s);
     }
   }
 }
@@ -446,6 +448,57 @@ int build_csc_structure(const CsrView& X, int32_t* cptr, int32_t* ridx, int32_t*
   else if (perm_out)
     cudaFreeAsync(perm_out, s);
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// gather_rows on a CSR (linalg.cpp:197-229): X_I = rows idx[0..nI) of X, in
+// order.  Offsets: row lengths then an exclusive scan; entries: one warp per
+// gathered row copies its indices and values (coalesced).
+namespace {
+__global__ void gather_len_kernel(CsrView X, const int32_t* __restrict__ idx, long long nI,
+                                  int32_t* __restrict__ gptr) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k <= nI;
+       k += (long long)gridDim.x * blockDim.x)
+    gptr[k] = k < nI ? X.ptr[idx[k] + 1] - X.ptr[idx[k]] : 0;
+}
+__global__ void gather_rows_kernel(CsrView X, const int32_t* __restrict__ idx, long long nI,
+                                   const int32_t* __restrict__ gptr, int32_t* __restrict__ gidx,
+                                   double* __restrict__ gval) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long k = w0; k < nI; k += nw) {
+    const int src = X.ptr[idx[k]], len = X.ptr[idx[k] + 1] - src, dst = gptr[k];
+    for (int t = lane; t < len; t += 32) {
+      gidx[dst + t] = X.idx[src + t];
+      gval[dst + t] = X.val[src + t];
+    }
+  }
+}
+}  // namespace
+
+int csr_gather_offsets(const CsrView& X, const int32_t* idx, int64_t nI, int32_t* gptr,
+                       long long* nnz_out, cudaStream_t s) {
+  gather_len_kernel<<<grid_for(nI + 1), 256, 0, s>>>(X, idx, nI, gptr);
+  size_t temp_bytes = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, gptr, gptr, (int)(nI + 1), s);
+  void* temp = nullptr;
+  if (e == cudaSuccess) e = cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, s);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, gptr, gptr, (int)(nI + 1), s);
+  if (temp) cudaFreeAsync(temp, s);
+  int32_t last = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last, gptr + nI, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  *nnz_out = last;
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+void csr_gather_rows(const CsrView& X, const int32_t* idx, int64_t nI, const int32_t* gptr,
+                     int32_t* gidx, double* gval, cudaStream_t s) {
+  if (nI == 0) return;
+  gather_rows_kernel<<<grid_for(nI * 32), 256, 0, s>>>(X, idx, nI, gptr, gidx, gval);
+  TB_LAUNCH_CHECK();
 }
 
 // Values of the CSC copy: cval[i] = val[perm[i]]; frees perm.

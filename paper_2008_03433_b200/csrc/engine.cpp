@@ -238,7 +238,8 @@ struct PhaseTrace {
 void check_options(int loss, const tron_gpu_options& opt) {
   if (loss != TRON_LOSS_LOGISTIC && loss != TRON_LOSS_L2SVM)
     raise(TRON_ERR_ARGUMENT, "unknown loss kind");
-  if (opt.svm_strategy != TRON_SVM_GATHERED && opt.svm_strategy != TRON_SVM_INDIRECT)
+  if (opt.svm_strategy != TRON_SVM_GATHERED && opt.svm_strategy != TRON_SVM_INDIRECT &&
+      opt.svm_strategy != TRON_SVM_AUTO)
     raise(TRON_ERR_DIMENSION, "plan: unknown svm strategy");
   if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world)
     raise(TRON_ERR_ARGUMENT, "invalid rank/world");
@@ -347,10 +348,6 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     raise(TRON_ERR_DIMENSION,
           "csr shard exceeds int32 indexing (nnz, rows, cols < 2^31 per GPU); shard across more "
           "GPUs");
-  if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
-    raise(TRON_ERR_STRATEGY,
-          "gathered L2-SVM strategy needs dense features on the GPU backend; use Indirect "
-          "(masked CSR/CSC traversal)");
   try {
     std::unique_ptr<Engine> e(new Engine());
     e->loss_ = loss;
@@ -411,6 +408,11 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       cuda_check(cudaMemsetAsync(e->cval_.p + nnz, 0, (nnz_pad - nnz) * sizeof(double), s), "pad");
     }
     e->Xt_ = CsrView{(int64_t)n, (int64_t)l, nnz, e->cptr_.p, e->ridx_.p, e->cval_.p};
+    if (loss == TRON_LOSS_L2SVM && opt.svm_strategy != TRON_SVM_INDIRECT) {
+      e->idx_.alloc(l > 0 ? l : 1);
+      e->idx_tmp_.alloc((l + 1023) / 1024 + 2);
+      e->count_.alloc(1);
+    }
     e->group_ = choose_group((int64_t)l, nnz);
     auto finish_values = [&] {
       vup.wait();
@@ -477,8 +479,6 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   if (!y || (l * n > 0 && !row_major)) raise(TRON_ERR_ARGUMENT, "null problem array");
   if (n > (uint64_t)kDenseMaxN) {
     // Wide dense problems run through the sparse kernels (explicit entries).
-    if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
-      raise(TRON_ERR_STRATEGY, "gathered L2-SVM strategy supports n <= 64 dense features on GPU");
     std::vector<int64_t> ro(l + 1);
     std::vector<int32_t> ci(l * n);
     for (uint64_t i = 0; i <= l; ++i) ro[i] = (int64_t)(i * n);
@@ -584,7 +584,9 @@ void Engine::screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_
 }
 
 uint64_t Engine::memory_bytes() const {
-  uint64_t b = rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
+  uint64_t b = grptr_.bytes() + gcidx_.bytes() + grval_.bytes() + gcptr_.bytes() + gridx_.bytes() +
+               gcval_.bytes();
+  b += rptr_.bytes() + cidx_.bytes() + rval_.bytes() + cptr_.bytes() + ridx_.bytes() +
                cval_.bytes() + Xc_.bytes() + Xg_.bytes() + y_.bytes() + lastbits_.bytes() +
                chunk_rank_.bytes() + empty_col_.bytes() + chunk_first_.bytes() + nz_col_.bytes() + head_.bytes() + carry_.bytes();
   for (const auto& S : slot_)
@@ -672,9 +674,12 @@ double Engine::eval_candidate_host(const double* w) {
 // ----------------------------------------------------------------------------
 // transposed products: X^T u with epilogue, world-aware
 // ----------------------------------------------------------------------------
-void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out) {
+void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out,
+                                   const CsrView* At, const SegView* plan) {
+  const CsrView& T = At ? *At : Xt_;
+  const SegView& P = plan ? *plan : plan_;
   auto product = [&](const EpiView& E, double* dst) {
-    csc_spmv(Xt_, plan_, u, squared, E, dst, s_);
+    csc_spmv(T, P, u, squared, E, dst, s_);
     count_launch(2);
   };
   if (!comm_.active()) {
@@ -769,30 +774,106 @@ int Engine::compact(const Slot& S, DevBuf<int32_t>& idx) {
   return (int)cnt;
 }
 
+namespace {
+std::string budget_message(uint64_t projected, uint64_t budget) {  // error.hpp:54-62
+  return "gathered submatrix would need " + std::to_string(projected) + " bytes, exceeding the " +
+         std::to_string(budget) +
+         "-byte budget; use the mix backend (MixedActiveSet), which answers Hessian products by "
+         "index-indirect traversal instead";
+}
+// TRON_SVM_AUTO gathers when the active rows hold at most this share of X:
+// a gather costs about 3 passes over X_I (CSR: the copy plus the CSC sort),
+// and each of the ~8 Hessian products of a commit then reads X_I instead of
+// X -- it pays below ~2/3 (CSR) to ~3/4 (dense); half is the safe side.
+constexpr double kAutoGatherShare = 0.5;
+}  // namespace
+
+// SvmEvaluator::commit's Gathered branch (backend.cpp:255-265): the budget
+// check on projected_gather_bytes (backend.cpp:47-54), then gather_rows.
+// TRON_SVM_AUTO applies the cost model above instead of raising.
 void Engine::gather_active() {
   AllocScope scope(s_);
   const Slot& S = slot_[cand_ ^ 1];
-  const uint64_t projected = (uint64_t)S.nact * (uint64_t)n_ * sizeof(double);
-  if (projected > budget_) {
-    raise(TRON_ERR_BUDGET, "gathered submatrix would need " + std::to_string(projected) +
-                               " bytes, exceeding the " + std::to_string(budget_) +
-                               "-byte budget; use the mix backend (MixedActiveSet), which "
-                               "answers Hessian products by index-indirect traversal instead");
-  }
-  const int nI = compact(S, idx_);
-  const int64_t ldg = dense_ld(nI);
-  if ((size_t)ldg * n_ > Xg_.n) Xg_.alloc((size_t)std::max<int64_t>(ldg, kDenseTile) * n_);
-  if (nI > 0) {
+  const bool auto_mode = svm_strategy_ == TRON_SVM_AUTO;
+  if (dense_) {
+    const uint64_t projected = (uint64_t)S.nact * (uint64_t)n_ * sizeof(double);
+    if (auto_mode) {
+      if (projected > budget_ || (double)S.nact > kAutoGatherShare * (double)l_) return;
+    } else if (projected > budget_) {
+      raise(TRON_ERR_BUDGET, budget_message(projected, budget_));
+    }
+    const int nI = compact(S, idx_);
+    if (nI == 0) return;  // nothing active: the masked pass answers Hv = v exactly
+    const int64_t ldg = dense_ld(nI);
+    if ((size_t)ldg * n_ > Xg_.n) Xg_.alloc((size_t)std::max<int64_t>(ldg, kDenseTile) * n_);
     dense_gather(nI, n_, Xc_.p, ld_, idx_.p, Xg_.p, ldg, s_);
     count_launch(1);
+    if (dense_make_map(&gmap_, Xg_.p, ldg, nI, n_) != 0)
+      raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gathered panel");
+    nI_ = nI;
+    ldg_ = ldg;
+    gathered_valid_ = true;
+    ledger.gathered_submatrix_bytes =
+        std::max<uint64_t>(ledger.gathered_submatrix_bytes, (uint64_t)nI * n_ * sizeof(double));
+  } else {
+    const int nI = compact(S, idx_);
+    grptr_.alloc((size_t)nI + 1);
+    long long nnzI = 0;
+    const int rc = csr_gather_offsets(X_, idx_.p, nI, grptr_.p, &nnzI, s_);
+    if (rc != 0) cuda_check((cudaError_t)rc, "csr_gather_offsets");
+    count_launch(1);
+    const uint64_t projected = (uint64_t)nnzI * (sizeof(double) + sizeof(int32_t)) +
+                               ((uint64_t)nI + 1) * sizeof(int64_t);
+    if (auto_mode) {
+      if (projected > budget_ || (double)nnzI > kAutoGatherShare * (double)X_.nnz) return;
+    } else if (projected > budget_) {
+      raise(TRON_ERR_BUDGET, budget_message(projected, budget_));
+    }
+    build_gathered_csr(nI, nnzI);
+    ledger.gathered_submatrix_bytes = std::max<uint64_t>(ledger.gathered_submatrix_bytes, projected);
   }
-  if (dense_make_map(&gmap_, Xg_.p, ldg, nI, n_) != 0)
-    raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gathered panel");
-  nI_ = nI;
-  ldg_ = ldg;
-  gathered_valid_ = true;
-  ledger.gathered_submatrix_bytes =
-      std::max<uint64_t>(ledger.gathered_submatrix_bytes, (uint64_t)nI * n_ * sizeof(double));
+  ++gathered_epoch_;
+}
+
+// X_I (rows idx_[0..nI), offsets already in grptr_) plus its CSC copy and
+// segmented plan, built on the device like the full matrix's at creation.
+void Engine::build_gathered_csr(int nI, long long nnzI) {
+  gcidx_.alloc((size_t)nnzI + 4);  // + 4: the row kernels read aligned groups of four
+  grval_.alloc((size_t)nnzI + 4);
+  cuda_check(cudaMemsetAsync(gcidx_.p + nnzI, 0, 4 * sizeof(int32_t), s_), "pad");
+  cuda_check(cudaMemsetAsync(grval_.p + nnzI, 0, 4 * sizeof(double), s_), "pad");
+  csr_gather_rows(X_, idx_.p, nI, grptr_.p, gcidx_.p, grval_.p, s_);
+  count_launch(1);
+  Xg_csr_ = CsrView{(int64_t)nI, n_, (int64_t)nnzI, grptr_.p, gcidx_.p, grval_.p};
+  const int64_t nnz_pad = (nnzI + kSegChunk - 1) / kSegChunk * kSegChunk;
+  gcptr_.alloc((size_t)n_ + 1);
+  gridx_.alloc((size_t)std::max<int64_t>(nnz_pad, 1));
+  gcval_.alloc((size_t)std::max<int64_t>(nnz_pad, 1));
+  int32_t* perm = nullptr;
+  int rc = build_csc_structure(Xg_csr_, gcptr_.p, gridx_.p, &perm, s_);
+  if (rc != 0) cuda_check((cudaError_t)rc, "build_csc_structure (gathered)");
+  if (nnz_pad > nnzI) {
+    cuda_check(cudaMemsetAsync(gridx_.p + nnzI, 0, (nnz_pad - nnzI) * sizeof(int32_t), s_), "pad");
+    cuda_check(cudaMemsetAsync(gcval_.p + nnzI, 0, (nnz_pad - nnzI) * sizeof(double), s_), "pad");
+  }
+  rc = build_csc_values(perm, grval_.p, gcval_.p, nnzI, s_);
+  if (rc != 0) cuda_check((cudaError_t)rc, "build_csc_values (gathered)");
+  Xgt_ = CsrView{n_, (int64_t)nI, (int64_t)nnzI, gcptr_.p, gridx_.p, gcval_.p};
+  const int64_t nch = (nnzI + kSegChunk - 1) / kSegChunk;
+  const int64_t slots = std::max<int64_t>(nch, 1);
+  gchunk_rank_.alloc(slots);
+  glastbits_.alloc(nch * (kSegChunk / 32) + 2);
+  gnz_col_.alloc((size_t)n_ + 1);
+  gempty_col_.alloc((size_t)std::max<int64_t>(n_, 1));
+  gchunk_first_.alloc(slots);
+  ghead_.alloc(slots);
+  gcarry_.alloc(slots);
+  rc = seg_plan_device(gcptr_.p, n_, nnzI, &gplan_, gchunk_rank_.p, gchunk_first_.p, glastbits_.p,
+                       gnz_col_.p, gempty_col_.p, s_);
+  if (rc != 0) cuda_check((cudaError_t)rc, "seg_plan_device (gathered)");
+  gplan_.head = ghead_.p;
+  gplan_.carry = gcarry_.p;
+  gathered_csr_valid_ = true;
 }
 
 void Engine::commit(double* gnorm) {
@@ -802,7 +883,8 @@ void Engine::commit(double* gnorm) {
   committed_valid_ = true;
   precond_valid_ = false;
   gathered_valid_ = false;
-  if (loss_ == TRON_LOSS_L2SVM && svm_strategy_ == TRON_SVM_GATHERED) gather_active();
+  gathered_csr_valid_ = false;
+  if (loss_ == TRON_LOSS_L2SVM && svm_strategy_ != TRON_SVM_INDIRECT) gather_active();
   gradient_dev();
   read_obj();
   gnorm_ = obj_h_->gnorm;
@@ -819,6 +901,7 @@ void Engine::adopt_candidate() {
   committed_valid_ = true;
   precond_valid_ = false;
   gathered_valid_ = false;
+  gathered_csr_valid_ = false;
   if (n_ > 0)
     cuda_check(cudaMemcpyAsync(g_.p, gspec_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_),
                "D2D");
@@ -836,7 +919,8 @@ void Engine::gradient_host(double* g) {
 // ----------------------------------------------------------------------------
 bool Engine::hv_dot_available() const {
   // (nnz == 0: csc_spmv takes the epilogue-only shortcut, which sums nothing)
-  return !dense_ && !comm_.active() && dot_parts_.n > 0 && plan_.nchunks > 0;
+  const SegView& P = gathered_csr_valid_ ? gplan_ : plan_;
+  return !dense_ && !comm_.active() && dot_parts_.n > 0 && P.nchunks > 0;
 }
 
 void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
@@ -854,13 +938,19 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
     dense_vector(DA_HV, v, epi, out);
     return;
   }
+  UView u;
+  u.kind = U_VEC;
+  u.u = a_.p;
+  if (gathered_csr_valid_) {  // Gathered L2-SVM: every row of X_I is active
+    csr_dv(Xg_csr_, group_, v, nullptr, nullptr, a_.p, s_);
+    count_launch(1);
+    transposed_raw_or_epi(u, false, epi, out, &Xgt_, &gplan_);
+    return;
+  }
   const double* dv = loss_ == TRON_LOSS_LOGISTIC ? S.dvec.p : nullptr;
   const uint8_t* mk = loss_ == TRON_LOSS_LOGISTIC ? nullptr : S.mask.p;
   csr_dv(X_, group_, v, dv, mk, a_.p, s_);
   count_launch(1);
-  UView u;
-  u.kind = U_VEC;
-  u.u = a_.p;
   transposed_raw_or_epi(u, false, epi, out);
 }
 
@@ -998,9 +1088,14 @@ void Engine::build_graph(int k, bool use_m) {
     if (dense_) {
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
-      dense_accum(DA_HV, l_, n_, ld_, Xc_.p, xmap_, loss, p_.p, S.dvec.p, S.mask.p, parts_.p, s_);
-      cg_small_step(v, parts_.p, dense_grid(l_, n_), loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_,
-                    st_d_, cond, s_);
+      const double scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+      if (gathered_valid_) {  // Gathered L2-SVM: the compact panel X_I, every row active
+        dense_accum(DA_HV, nI_, n_, ldg_, Xg_.p, gmap_, kLossSvm, p_.p, nullptr, nullptr, parts_.p, s_);
+        cg_small_step(v, parts_.p, dense_grid(nI_, n_), scale, st_d_, cond, s_);
+      } else {
+        dense_accum(DA_HV, l_, n_, ld_, Xc_.p, xmap_, loss, p_.p, S.dvec.p, S.mask.p, parts_.p, s_);
+        cg_small_step(v, parts_.p, dense_grid(l_, n_), scale, st_d_, cond, s_);
+      }
       count_launch(2);
     } else {
       hv_kernels(p_.p, hp_.p);
@@ -1026,6 +1121,20 @@ void Engine::build_graph(int k, bool use_m) {
   cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
   graph_[k][use_m] = graph;
   graph_exec_[k][use_m] = exec;
+  graph_epoch_[k][use_m] = gathered_epoch_;
+}
+
+// The CG graph of committed slot k, (re)built when it was captured for the
+// gathered rows of an earlier commit.
+void Engine::launch_cg_graph(int k, bool use_m) {
+  if (graph_exec_[k][use_m] && graph_epoch_[k][use_m] != gathered_epoch_) {
+    cudaGraphExecDestroy(graph_exec_[k][use_m]);
+    cudaGraphDestroy(graph_[k][use_m]);
+    graph_exec_[k][use_m] = nullptr;
+    graph_[k][use_m] = nullptr;
+  }
+  if (!graph_exec_[k][use_m]) build_graph(k, use_m);
+  cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
 }
 
 // Graph path: enqueues the CG loop and returns without waiting (false); the
@@ -1047,9 +1156,7 @@ bool Engine::enqueue_cg(double delta, const tron_config& cfg, CgState* out) {
   init.use_m = use_m;
   *st_h_ = init;
   cuda_check(cudaMemcpyAsync(st_d_, st_h_, sizeof(CgState), cudaMemcpyHostToDevice, s_), "H2D");
-  const int k = cand_ ^ 1;
-  if (!graph_exec_[k][use_m]) build_graph(k, use_m);
-  cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
+  launch_cg_graph(cand_ ^ 1, use_m);
   return false;
 }
 
@@ -1069,8 +1176,7 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
   const int k = cand_ ^ 1;
   CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
   if (use_graphs_) {
-    if (!graph_exec_[k][use_m]) build_graph(k, use_m);
-    cuda_check(cudaGraphLaunch(graph_exec_[k][use_m], s_), "graph launch");
+    launch_cg_graph(k, use_m);
     read_cg(out);
     launches += 1 + (uint64_t)out->iters * body_kernels_;
     return;
@@ -1188,7 +1294,8 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     return;
   }
   double delta = gnorm0;
-  const bool speculative = !(loss_ == TRON_LOSS_L2SVM && svm_strategy_ == TRON_SVM_GATHERED);
+  // Gathered / Auto L2-SVM gather X_I at commit, before the CG that uses it
+  const bool speculative = !(loss_ == TRON_LOSS_L2SVM && svm_strategy_ != TRON_SVM_INDIRECT);
   // TRON_B200_TRACE=1: device time of each outer iteration's phases on stderr
   struct OuterProf {
     bool on = false;

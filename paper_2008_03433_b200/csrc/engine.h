@@ -165,7 +165,8 @@ class Engine {
   void common_alloc();
   void forward(Slot& S);
   void gradient_dev();
-  void transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out);
+  void transposed_raw_or_epi(const UView& u, bool squared, const EpiView& epi, double* out,
+                             const CsrView* At = nullptr, const SegView* plan = nullptr);
   void dense_vector(int kind, const double* v, const EpiView& epi, double* out,
                     const Slot* grad_slot = nullptr);
   void gradient_into(const Slot& S, double* out);
@@ -174,10 +175,12 @@ class Engine {
   void adopt_candidate();
   void hv_kernels(const double* v, double* out, bool with_dot = false);  // enqueue only
   void gather_active();
+  void build_gathered_csr(int nI, long long nnzI);
   int compact(const Slot& S, DevBuf<int32_t>& idx);
   void read_obj();
   void read_cg(CgState* out);
   void build_graph(int slot, bool use_m);
+  void launch_cg_graph(int slot, bool use_m);
   template <class Report>
   void screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n, Report report);
   void count_launch(uint64_t k) { launches += k; }
@@ -210,6 +213,19 @@ class Engine {
   DevBuf<double> Xg_;  // gathered panel X_{I,:} (Gathered strategy)
   int64_t ldg_ = 0, nI_ = 0;
   bool gathered_valid_ = false;
+  // gathered CSR rows X_I (Gathered L2-SVM on sparse features, linalg.cpp:197-229)
+  // and their CSC copy + segmented plan, rebuilt at every commit
+  DevBuf<int32_t> grptr_, gcidx_, gcptr_, gridx_;
+  DevBuf<double> grval_, gcval_;
+  DevBuf<uint32_t> glastbits_, gchunk_rank_;
+  DevBuf<int32_t> gempty_col_, gchunk_first_, gnz_col_;
+  DevBuf<double> ghead_, gcarry_;
+  CsrView Xg_csr_{}, Xgt_{};
+  SegView gplan_{};
+  bool gathered_csr_valid_ = false;
+  // graphs capture the gathered views of the commit they were built for
+  uint64_t gathered_epoch_ = 0;
+  uint64_t graph_epoch_[2][2] = {{0, 0}, {0, 0}};
   DevBuf<int32_t> idx_, idx_tmp_;
   DevBuf<long long> count_;
 

@@ -131,7 +131,8 @@ int choose_group(int64_t rows, int64_t nnz);
 void csr_forward(const CsrView& X, int group, int loss, const double* w, const double* y, double C,
                  double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
                  Scratch sc, cudaStream_t s);
-// a_i = (x_i . p) * dvec_i  (or mask_i ? x_i . p : 0 when mask given)
+// a_i = (x_i . p) * dvec_i  (or mask_i ? x_i . p : 0 when mask given; x_i . p
+// when neither is given)
 void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
             double* a, cudaStream_t s);
 // Transposed product over the CSC copy (csc_seg.cu; segmented chunks, atomic-free).
@@ -144,6 +145,12 @@ void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squar
 int build_csc_structure(const CsrView& X, int32_t* cptr, int32_t* ridx, int32_t** perm,
                         cudaStream_t s);
 int build_csc_values(int32_t* perm, const double* val, double* cval, int64_t nnz, cudaStream_t s);
+// gather_rows on a CSR (linalg.cpp:197-229): gptr[nI+1] offsets of the rows
+// idx[0..nI) (synchronizes s; *nnz_out = their entry count), then the entries.
+int csr_gather_offsets(const CsrView& X, const int32_t* idx, int64_t nI, int32_t* gptr,
+                       long long* nnz_out, cudaStream_t s);
+void csr_gather_rows(const CsrView& X, const int32_t* idx, int64_t nI, const int32_t* gptr,
+                     int32_t* gidx, double* gval, cudaStream_t s);
 // Input screening: first_bad2[0] = first row whose columns are not strictly
 // ascending within [0, n) (ptr may be null: no matrix check), first_bad2[1] =
 // first label not in {-1, +1}; ~0 when none.  Offsets must already be valid.

@@ -92,6 +92,7 @@ class LossKind(enum.Enum):
 class SvmStrategy(enum.Enum):
     Gathered = _lib.SVM_GATHERED
     Indirect = _lib.SVM_INDIRECT
+    Auto = _lib.SVM_AUTO  # B200 cost model: gather only when X_I <= half of X
 
 
 class CgExit(enum.IntEnum):

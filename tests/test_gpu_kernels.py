@@ -353,7 +353,41 @@ def test_gathered_equals_indirect(port):
         assert rel_err(a, b) <= 1e-12
 
 
-def test_gathered_csr_rejected():
-    p = synth.testgen_sparse_problem(1, 20, 10, 1.0, 0.3)
-    with pytest.raises(StrategyPreconditionError):
-        gpu(p, SVM, svm_strategy=SvmStrategy.Gathered)
+# Gathered L2-SVM on CSR features (gather_rows' CSR branch, linalg.cpp:212-228):
+# X_I and its CSC copy are rebuilt at every commit; Hv over them equals the
+# masked traversal and the reference evaluator, and the budget check uses the
+# reference's projected_gather_bytes (backend.cpp:47-54).
+@pytest.mark.parametrize("strategy", [SvmStrategy.Gathered, SvmStrategy.Auto])
+def test_gathered_csr_equals_indirect_and_reference(port, strategy):
+    p = synth.synth_sparse(5, 3000, 8000, 40)
+    n = p.X.cols
+    w = synth.testgen_random_vector(61, n, 2.0)
+    want = port.svm(p, w, None)
+    outs = {}
+    for strat in (strategy, SvmStrategy.Indirect):
+        with gpu(p, SVM, svm_strategy=strat) as ev:
+            ev.eval_candidate(w)
+            ev.commit()
+            assert rel_err(ev.gradient(), want["g"]) <= 1e-12
+            vs = [synth.testgen_random_vector(300 + k, n) for k in range(4)]
+            outs[strat] = [ev.hessian_vec(v) for v in vs]
+            if strat == SvmStrategy.Gathered:
+                nnz_I = int(sum(p.X.row_offsets[i + 1] - p.X.row_offsets[i] for i in want["active"]))
+                assert ev.ledger().gathered_submatrix_bytes == nnz_I * 12 + (want["active"].size + 1) * 8
+    for k, (a, b) in enumerate(zip(outs[strategy], outs[SvmStrategy.Indirect])):
+        ref_hv = port.svm(p, w, synth.testgen_random_vector(300 + k, n))["hv"]
+        assert rel_err(a, b) <= 1e-13 and rel_err(a, ref_hv) <= 1e-12
+
+
+def test_gathered_csr_budget_names_mix():
+    p = synth.synth_sparse(5, 3000, 8000, 40)
+    with gpu(p, SVM, svm_strategy=SvmStrategy.Gathered, gathered_budget_bytes=1 << 16) as ev:
+        ev.eval_candidate(np.zeros(p.X.cols))
+        with pytest.raises(BudgetExceededError) as e:
+            ev.commit()
+        assert "MixedActiveSet" in str(e.value)
+    # Auto never raises: over budget it stays on the masked traversal
+    with gpu(p, SVM, svm_strategy=SvmStrategy.Auto, gathered_budget_bytes=1 << 16) as ev:
+        ev.eval_candidate(np.zeros(p.X.cols))
+        ev.commit()
+        assert ev.ledger().gathered_submatrix_bytes == 0

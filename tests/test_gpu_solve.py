@@ -264,6 +264,23 @@ def test_gathered_vs_indirect_solve():  # test_backend.cpp:245-257
     assert pg.ledger.gathered_submatrix_bytes > 0
 
 
+@pytest.mark.parametrize("strategy", [SvmStrategy.Gathered, SvmStrategy.Auto])
+@pytest.mark.parametrize("mode", ["device", "host_cg"])
+def test_gathered_csr_solve_matches_reference(ref, strategy, mode):
+    # sparse L2-SVM, Gathered on CSR: the device CG runs over X_I (graph rebuilt
+    # per commit); same optimum and counts as Indirect and the reference
+    p = synth.synth_sparse(3, 20000, 30000, 30)
+    cfg = TrustRegionConfig(eps=1e-3)
+    pg = plan(svm_strategy=strategy, solve_mode=mode)
+    a = solve(p, SVM, cfg, pg)
+    b = solve(p, SVM, cfg, plan(svm_strategy=SvmStrategy.Indirect, solve_mode=mode))
+    w_ref, t_ref = ref.solve(p, 1, cfg)
+    assert_parity(a, w_ref, t_ref, X=p.X)
+    assert rel_err(a.w, b.w) <= 1e-8  # X_I vs masked X: different FP64 summation orders
+    if strategy == SvmStrategy.Gathered:
+        assert pg.ledger.gathered_submatrix_bytes > 0
+
+
 def test_host_cg_ledger_schedule():  # test_backend.cpp:152-184 (staged semantics)
     p = synth.testgen_dense_problem_scaled(117, 80, 8, 1000.0, 20.0)
     pl = plan(solve_mode="host_cg")
