@@ -101,6 +101,12 @@ typedef struct {
   int32_t rank, world;          /* world > 1 => NCCL allreduce of partials */
   const void *nccl_unique_id;   /* 128-byte ncclUniqueId when world > 1 */
   uint64_t row_begin, global_rows;
+  /* Dense L2-SVM only (n <= 48, one GPU, Indirect): run every reduction in the
+   * reference's order -- 64 sequential blocks + the pairwise tree
+   * (parallel.hpp:14-34), serial n-length dots -- so the solve is bit-for-bit
+   * the reference's (objective, w, counts, active set).  Default 0: the
+   * parallel fixed-order reductions (parity within the north-star tolerance). */
+  int32_t reference_order;
 } tron_gpu_options;
 
 typedef struct tron_gpu_ctx tron_gpu_ctx;

@@ -56,7 +56,8 @@ class tron_ledger(ctypes.Structure):
 class tron_gpu_options(ctypes.Structure):
     _fields_ = [("device", c_int32), ("svm_strategy", c_int32),
                 ("gathered_budget_bytes", c_uint64), ("rank", c_int32), ("world", c_int32),
-                ("nccl_unique_id", c_void_p), ("row_begin", c_uint64), ("global_rows", c_uint64)]
+                ("nccl_unique_id", c_void_p), ("row_begin", c_uint64), ("global_rows", c_uint64),
+                ("reference_order", c_int32)]
 
 
 PD = POINTER(c_double)

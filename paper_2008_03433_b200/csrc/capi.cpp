@@ -168,6 +168,7 @@ void tron_gpu_default_options(tron_gpu_options* o) {
   o->nccl_unique_id = nullptr;
   o->row_begin = 0;
   o->global_rows = 0;
+  o->reference_order = 0;
 }
 
 const char* tron_gpu_last_error(void) { return g_last_error.c_str(); }

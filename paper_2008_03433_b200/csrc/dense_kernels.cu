@@ -437,6 +437,11 @@ __global__ void gather_kernel(long long nI, int n, const double* __restrict__ X,
 int64_t dense_ld(int64_t l) { return (l + kDenseTile - 1) / kDenseTile * kDenseTile; }
 
 int dense_make_map(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, int64_t n) {
+  return dense_make_map_box(map, X, ld, rows, n, dense_tile_rows(n));
+}
+
+int dense_make_map_box(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, int64_t n,
+                       int box_rows) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -454,7 +459,7 @@ int dense_make_map(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, 
   if (rows < 1) rows = 1;
   const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)(n > 0 ? n : 1)};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)dense_tile_rows(n), (cuuint32_t)(n > 0 ? n : 1)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)(n > 0 ? n : 1)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -487,14 +487,25 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     return create_csr(loss, l, n, ro.data(), ci.data(), row_major, y, C, opt);
   }
   if (l >= (uint64_t{1} << 31)) raise(TRON_ERR_DIMENSION, "dense shard exceeds 2^31 rows per GPU");
+  if (opt.reference_order) {
+    if (loss != TRON_LOSS_L2SVM || n > (uint64_t)kRoMaxN || opt.world > 1)
+      raise(TRON_ERR_ARGUMENT,
+            "reference_order needs a dense L2-SVM with n <= 48 features on one GPU");
+    if (opt.svm_strategy == TRON_SVM_GATHERED)
+      raise(TRON_ERR_STRATEGY,
+            "reference_order runs the Indirect traversal (the reference's Gathered route is "
+            "bitwise equal to it, loss.cpp:160-162); use Indirect");
+  }
   std::unique_ptr<Engine> e(new Engine());
+  e->ro_ = opt.reference_order != 0;
+  const int svm_strategy = e->ro_ ? (int)TRON_SVM_INDIRECT : opt.svm_strategy;
   e->loss_ = loss;
   e->dense_ = true;
   e->l_ = (int64_t)l;
   e->n_ = (int64_t)n;
   e->C_ = C;
   e->device_ = opt.device;
-  e->svm_strategy_ = opt.svm_strategy;
+  e->svm_strategy_ = svm_strategy;
   e->budget_ = opt.gathered_budget_bytes;
   e->row_begin_ = opt.row_begin;
   e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
@@ -553,6 +564,21 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     e->idx_.alloc(l > 0 ? l : 1);
     e->idx_tmp_.alloc((l + 1023) / 1024 + 2);
     e->count_.alloc(1);
+  }
+  if (e->ro_) {
+    AllocScope scope(e->s_);
+    if (dense_make_map_box(&e->xmap128_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n, 128) != 0)
+      raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the dense matrix (128-row boxes)");
+    for (auto& S : e->slot_) {
+      S.idx.alloc(l > 0 ? l : 1);
+      S.cnt.alloc(1);
+      cuda_check(cudaMemsetAsync(S.cnt.p, 0, sizeof(long long), e->s_), "memset");
+    }
+    e->ro_parts_.alloc((size_t)64 * std::max<uint64_t>(n, 1));
+    e->ro_hparts_.alloc(64);
+    e->ro_tickets_.alloc(2);
+    cuda_check(cudaMemsetAsync(e->ro_tickets_.p, 0, 2 * sizeof(unsigned), e->s_), "memset");
+    cuda_check(cudaStreamSynchronize(e->s_), "reference-order buffers");
   }
   cuda_check(cudaGetLastError(), "dense create");
   return e;
@@ -622,6 +648,11 @@ void Engine::forward(Slot& S) {
   if (dense_) {
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
                   S.gparts.p, obj_d_, sc_, s_);
+    if (ro_) {  // I of this slot, then f in the reference's order (loss.cpp:114-119)
+      compact_mask(l_, S.mask.p, S.idx.p, idx_tmp_.p, S.cnt.p, s_);
+      ro_hinge(l_, n_, S.z.p, y_.p, S.w.p, C_, ro_hparts_.p, ro_tickets_.p, obj_d_, s_);
+      count_launch(4);
+    }
   } else {
     csr_forward(X_, group_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_,
                 s_);
@@ -738,6 +769,10 @@ void Engine::gradient_into(const Slot& S, double* out) {
   epi.kind = EPI_VEC;
   epi.base = S.w.p;
   epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+  if (ro_) {  // masked_matvec_transpose in the reference's order, norm2(g) serial
+    ro_accum_slot(RO_GRAD, S, nullptr, epi, out);
+    return;
+  }
   if (dense_) {
     dense_vector(-1, nullptr, epi, out, &S);  // partials from the fused margin pass
   } else {
@@ -917,6 +952,12 @@ void Engine::gradient_host(double* g) {
 // ----------------------------------------------------------------------------
 // Hv (loss.cpp:82-92 / :139-174) and preconditioner (loss.cpp:176-188)
 // ----------------------------------------------------------------------------
+void Engine::ro_accum_slot(int mode, const Slot& S, const double* v, const EpiView& epi, double* out) {
+  ro_accum(mode, l_, n_, xmap128_, S.cnt.p, S.idx.p, S.mask.p, v, S.z.p, y_.p, ro_parts_.p,
+           ro_tickets_.p + 1, epi, out, obj_d_, s_);
+  count_launch(1);
+}
+
 bool Engine::hv_dot_available() const {
   // (nnz == 0: csc_spmv takes the epilogue-only shortcut, which sums nothing)
   const SegView& P = gathered_csr_valid_ ? gplan_ : plan_;
@@ -933,6 +974,10 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
     epi.dot_parts = dot_parts_.p;
     epi.dot_out = dot_out_.p;
     epi.dot_ticket = dot_ticket_.p;
+  }
+  if (ro_) {
+    ro_accum_slot(RO_HV, S, v, epi, out);
+    return;
   }
   if (dense_) {
     dense_vector(DA_HV, v, epi, out);
@@ -975,7 +1020,9 @@ void Engine::ensure_precond() {
   epi.kind = EPI_CONST;
   epi.cbase = 1.0;
   epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
-  if (dense_) {
+  if (ro_) {
+    ro_accum_slot(RO_PRECOND, S, nullptr, epi, M_.p);
+  } else if (dense_) {
     dense_vector(DA_PRECOND, nullptr, epi, M_.p);
   } else {
     UView u;
@@ -1058,7 +1105,9 @@ void Engine::build_graph(int k, bool use_m) {
   cuda_check(cudaStreamBeginCaptureToGraph(s_, graph, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal),
              "begin capture");
-  if (small_engine_)
+  if (ro_)
+    ro_cg_init(v, st_d_, cond, s_);
+  else if (small_engine_)
     cg_small_init(v, st_d_, cond, s_);
   else
     cg_large_init(v, st_d_, sc_, cond, s_);
@@ -1084,7 +1133,11 @@ void Engine::build_graph(int k, bool use_m) {
                                            cudaStreamCaptureModeThreadLocal),
              "begin body capture");
   const uint64_t before = launches;
-  if (small_engine_) {
+  if (ro_) {
+    hv_kernels(p_.p, hp_.p);
+    ro_cg_step(v, st_d_, cond, s_);
+    count_launch(1);
+  } else if (small_engine_) {
     if (dense_) {
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
@@ -1183,7 +1236,9 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
   }
   // host-driven loop (multi-GPU: NCCL between phases)
   Cond none;
-  if (small_engine_)
+  if (ro_)
+    ro_cg_init(v, st_d_, none, s_);
+  else if (small_engine_)
     cg_small_init(v, st_d_, none, s_);
   else
     cg_large_init(v, st_d_, sc_, none, s_);
@@ -1191,7 +1246,10 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
   read_cg(out);
   while (out->cont) {
     hv_kernels(p_.p, hp_.p);
-    if (small_engine_) {
+    if (ro_) {
+      ro_cg_step(v, st_d_, none, s_);
+      count_launch(1);
+    } else if (small_engine_) {
       cg_small_step(v, nullptr, 0, 0.0, st_d_, none, s_);
       count_launch(1);
     } else if (mid_engine_) {

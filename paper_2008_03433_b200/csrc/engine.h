@@ -158,6 +158,8 @@ class Engine {
     DevBuf<double> w, z, zhat, dvec;
     DevBuf<uint8_t> mask;
     DevBuf<double> gparts;  // dense: gradient partials from this slot's margin pass
+    DevBuf<int32_t> idx;    // reference order: this slot's active set I (ascending)
+    DevBuf<long long> cnt;  // ... and |I| (device)
     double f = 0.0;
     long long nact = 0;
     bool valid = false;
@@ -226,6 +228,12 @@ class Engine {
   // graphs capture the gathered views of the commit they were built for
   uint64_t gathered_epoch_ = 0;
   uint64_t graph_epoch_[2][2] = {{0, 0}, {0, 0}};
+  // reference-order reductions (dense L2-SVM, refexact.cu)
+  bool ro_ = false;
+  alignas(64) CUtensorMap xmap128_{};
+  DevBuf<double> ro_parts_, ro_hparts_;
+  DevBuf<unsigned> ro_tickets_;
+  void ro_accum_slot(int mode, const Slot& S, const double* v, const EpiView& epi, double* out);
   DevBuf<int32_t> idx_, idx_tmp_;
   DevBuf<long long> count_;
 

@@ -254,4 +254,25 @@ void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, lo
 void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int32_t* idx,
                   double* Xg, int64_t ldg, cudaStream_t s);
 
+// ---- reference-order reductions for the dense L2-SVM (refexact.cu) --------
+// Bit-for-bit the reference's arithmetic: 64 sequential block sums + the
+// pairwise tree (parallel.hpp:14-34), serial n-length dots.  n <= kRoMaxN.
+constexpr int64_t kRoMaxN = 48;
+enum RoMode : int { RO_HV = 0, RO_GRAD = 1, RO_PRECOND = 2 };
+// out = epi(sum over I of c_i x_i) with c = x_i.v (HV), z_i - y_i (GRAD), or
+// the squares (PRECOND); GRAD also sets obj->gnorm (serial) and grad_nonfinite.
+// xmap128: TMA map of X with 128-row boxes; partials >= 64*n doubles.
+void ro_accum(int mode, int64_t l, int64_t n, const CUtensorMap& xmap128, const long long* count,
+              const int32_t* idx, const uint8_t* mask, const double* v, const double* z,
+              const double* y, double* partials, unsigned* ticket, const EpiView& epi, double* out,
+              ObjScalars* obj, cudaStream_t s);
+// obj->f = 0.5*dot(w,w) + C*reduce_sum(max(1 - y z, 0)^2), obj->ww; partials >= 64.
+void ro_hinge(int64_t l, int64_t n, const double* z, const double* y, const double* w, double C,
+              double* partials, unsigned* ticket, ObjScalars* obj, cudaStream_t s);
+void ro_cg_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
+void ro_cg_step(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
+// dense_make_map with `box_rows`-row boxes.
+int dense_make_map_box(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, int64_t n,
+                       int box_rows);
+
 }  // namespace tb

@@ -203,12 +203,16 @@ class ExecutionPlan:
     nccl_unique_id: Optional[bytes] = None
     row_begin: int = 0
     global_rows: int = 0
+    # dense L2-SVM: every reduction in the reference's order (bit-for-bit results)
+    reference_order: bool = False
 
     @staticmethod
     def gpu(device: int = 0, svm_strategy: SvmStrategy = SvmStrategy.Indirect,
-            gathered_budget_bytes: int = 2 << 30, solve_mode: str = "device") -> "ExecutionPlan":
+            gathered_budget_bytes: int = 2 << 30, solve_mode: str = "device",
+            reference_order: bool = False) -> "ExecutionPlan":
         return ExecutionPlan(device=device, svm_strategy=svm_strategy,
-                             gathered_budget_bytes=gathered_budget_bytes, solve_mode=solve_mode)
+                             gathered_budget_bytes=gathered_budget_bytes, solve_mode=solve_mode,
+                             reference_order=reference_order)
 
     def to_c(self):
         o = _lib.tron_gpu_options()
@@ -218,6 +222,7 @@ class ExecutionPlan:
         o.gathered_budget_bytes = self.gathered_budget_bytes
         o.rank, o.world = self.rank, self.world
         o.row_begin, o.global_rows = self.row_begin, self.global_rows
+        o.reference_order = int(bool(self.reference_order))
         keep = None
         if self.nccl_unique_id is not None:
             keep = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)

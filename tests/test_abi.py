@@ -43,7 +43,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.tron_config) == 8 * 10 + 8
     assert ctypes.sizeof(_lib.tron_iteration) == 4 * 8 + 8 + 8
     assert ctypes.sizeof(_lib.tron_ledger) == 7 * 8
-    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8
+    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8  # + int32 + pad
 
 
 def test_defaults_mirror_reference():
