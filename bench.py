@@ -202,7 +202,7 @@ def modelled_reference_solve(ref, p, name, threads):
     times the call counts of the measured full reference solve recorded in
     profiles/parity_<W>.json."""
     rec = json.load(open(os.path.join(ROOT, PARITY_FILES[name])))
-    rc = rec["reference"]
+    rc = rec["reference"]  # scripts/parity_run.py format
     n_fun, n_grad, n_hv = 1 + rc["outer"], 1 + rc["accepted"], sum(rc["cg_iters"])
     p_s, scale = p, 1.0
     if name == "Q1":
@@ -410,6 +410,27 @@ def cpu_baseline(args, p_full, res, ev, loss, cfg, plan):
     par["predictions_identical_at_reference_w"] = bool(np.array_equal(lab_gpu_at_ref, lab_ref))
     par["test_rows"] = test_rows
     par["test_accuracy"] = [correct_gpu / test_rows, correct_ref / test_rows]
+    if oloss == 1 and p_full.X.layout == "dense" and p_full.X.cols <= 48:
+        # the bit-for-bit mode: every reduction in the reference's order (refexact.cu)
+        from paper_2008_03433_b200 import ExecutionPlan
+        with make_evaluator(p_full, loss, ExecutionPlan.gpu(device=plan.device, reference_order=True)) as evr:
+            evr.solve(cfg)  # warm (graph instantiation)
+            t0 = time.perf_counter()
+            r3 = evr.solve(cfg)
+            t_ro = time.perf_counter() - t0
+            act_ro = evr.committed_state().active
+        lab_ro, _ = ref.predict(Xt, r3.w)
+        c3 = counts_of([{"accepted": r.accepted, "cg_iters": r.cg_iters} for r in r3.trace.iterations])
+        par["reference_order"] = {
+            "what": "same solve with ExecutionPlan.gpu(reference_order=True): the reference's 64-block "
+                    "chains + pairwise tree and serial n-dots (refexact.cu)",
+            "solve_s": t_ro,
+            "w_bitwise_identical": bool(np.array_equal(r3.w.view(np.uint64), w_ref.view(np.uint64))),
+            "objective_bitwise_identical": bool(r3.objective == t_ref["objective"]),
+            "counts_identical": c3 == cr,
+            "active_set_identical": bool(np.array_equal(act_ro, act_ref)),
+            "predictions_identical": bool(np.array_equal(lab_ro, lab_ref)),
+        }
     out["parity"] = par
     return out
 

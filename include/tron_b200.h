@@ -107,6 +107,13 @@ typedef struct {
    * the reference's (objective, w, counts, active set).  Default 0: the
    * parallel fixed-order reductions (parity within the north-star tolerance). */
   int32_t reference_order;
+  /* Host data plane for the row-sharded layout (world > 1) in place of NCCL:
+   * host_allreduce(user, buf, count) must sum buf[0..count) (host memory)
+   * over the ranks, in place, with the same result on every rank (e.g. an
+   * MPI / gloo allreduce).  The per-call partials are staged through pinned
+   * host memory and the CG loop runs host-driven.  NULL: NCCL. */
+  void (*host_allreduce)(void *user, double *buf, uint64_t count);
+  void *host_allreduce_user;
 } tron_gpu_options;
 
 typedef struct tron_gpu_ctx tron_gpu_ctx;
@@ -140,6 +147,9 @@ int tron_gpu_commit(tron_gpu_ctx *ctx, double *gnorm);
 int tron_gpu_gradient(tron_gpu_ctx *ctx, double *g);
 /* LossEvaluator::hessian_vec (tron.hpp:121; backend.cpp:185-198/279-290). */
 int tron_gpu_hessian_vec(tron_gpu_ctx *ctx, const double *v, double *out);
+/* quadratic_model(g, hv, d) (tron.hpp:83; tron.cpp:31-35) with g the committed
+ * gradient and hv this context's Hessian: *q = g.d + 0.5 d.(H d). */
+int tron_gpu_quadratic_model(tron_gpu_ctx *ctx, const double *d, double *q);
 /* LossEvaluator::precond_diagonal (tron.hpp:124; backend.cpp:200-214/292-306). */
 int tron_gpu_precond_diagonal(tron_gpu_ctx *ctx, double *m);
 

@@ -8,5 +8,5 @@ from .tron import (  # noqa: F401
     ExecutionPlan, FeatureMatrix, GpuEvaluator, IterationRecord, LogicError, LossKind,
     NumericalFailureError, Problem, SolveResult, SolverTrace, StrategyPreconditionError,
     SvmStrategy, TransferLedger, TrustRegionConfig, device_count, make_evaluator, solve,
-    trust_region_update)
+    quadratic_model, trust_region_update)
 from ._lib import LIB_PATH  # noqa: F401

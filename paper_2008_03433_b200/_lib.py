@@ -57,7 +57,12 @@ class tron_gpu_options(ctypes.Structure):
     _fields_ = [("device", c_int32), ("svm_strategy", c_int32),
                 ("gathered_budget_bytes", c_uint64), ("rank", c_int32), ("world", c_int32),
                 ("nccl_unique_id", c_void_p), ("row_begin", c_uint64), ("global_rows", c_uint64),
-                ("reference_order", c_int32)]
+                ("reference_order", c_int32), ("host_allreduce", c_void_p),
+                ("host_allreduce_user", c_void_p)]
+
+
+# void (*)(void* user, double* buf, uint64_t count): a host allreduce (sum, in place)
+HOST_ALLREDUCE = ctypes.CFUNCTYPE(None, c_void_p, POINTER(c_double), c_uint64)
 
 
 PD = POINTER(c_double)
@@ -82,6 +87,7 @@ SIGNATURES = [
     ("tron_gpu_gradient", c_int, [c_void_p, PD]),
     ("tron_gpu_hessian_vec", c_int, [c_void_p, PD, PD]),
     ("tron_gpu_precond_diagonal", c_int, [c_void_p, PD]),
+    ("tron_gpu_quadratic_model", c_int, [c_void_p, PD, PD]),
     ("tron_gpu_state_lr", c_int, [c_void_p, c_int, PD, PD, PD]),
     ("tron_gpu_state_svm", c_int, [c_void_p, c_int, PD, PI64, c_uint64, PU64]),
     ("tron_gpu_truncated_cg", c_int, [c_void_p, c_double, POINTER(tron_config), PD, PI32, PU64,

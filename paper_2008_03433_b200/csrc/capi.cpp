@@ -169,6 +169,8 @@ void tron_gpu_default_options(tron_gpu_options* o) {
   o->row_begin = 0;
   o->global_rows = 0;
   o->reference_order = 0;
+  o->host_allreduce = nullptr;
+  o->host_allreduce_user = nullptr;
 }
 
 const char* tron_gpu_last_error(void) { return g_last_error.c_str(); }
@@ -306,6 +308,14 @@ int tron_gpu_gradient(tron_gpu_ctx* ctx, double* g) {
 int tron_gpu_hessian_vec(tron_gpu_ctx* ctx, const double* v, double* out) {
   NEED_CTX(ctx);
   return guarded([&] { ctx->engine->hessian_vec_host(v, out); });
+}
+
+int tron_gpu_quadratic_model(tron_gpu_ctx* ctx, const double* d, double* q) {
+  NEED_CTX(ctx);
+  return guarded([&] {
+    const double v = ctx->engine->quadratic_model_host(d);
+    if (q) *q = v;
+  });
 }
 
 int tron_gpu_precond_diagonal(tron_gpu_ctx* ctx, double* m) {

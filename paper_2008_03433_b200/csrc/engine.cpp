@@ -94,23 +94,29 @@ int nccl_unique_id(void* out128) {
   return TRON_OK;
 }
 
-void Comm::init(int rank_, int world_, const void* unique_id, int device) {
-  rank = rank_;
-  world = world_;
+void Comm::init(const tron_gpu_options& opt) {
+  rank = opt.rank;
+  world = opt.world;
+  if (opt.host_allreduce && world > 1) {  // caller's host collective
+    host_fn_ = opt.host_allreduce;
+    host_user_ = opt.host_allreduce_user;
+    return;
+  }
   // TRON_B200_FORCE_NCCL=1 runs a single-rank problem through the sharded code
   // path with a real one-rank NCCL communicator (tests the multi-GPU plumbing
   // on one GPU: partials, allreduce on the stream, host-driven CG).
   const char* fe = std::getenv("TRON_B200_FORCE_NCCL");
   forced = world == 1 && fe && fe[0] == '1';
   if (world <= 1 && !forced) return;
-  if (!unique_id && world > 1) raise(TRON_ERR_ARGUMENT, "world > 1 requires an nccl_unique_id");
+  if (!opt.nccl_unique_id && world > 1)
+    raise(TRON_ERR_ARGUMENT, "world > 1 requires an nccl_unique_id or a host_allreduce");
   if (!g_nccl.load()) raise(TRON_ERR_NCCL, "libnccl.so.2 not loadable");
   ncclUniqueId id;
-  if (unique_id)
-    std::memcpy(&id, unique_id, sizeof(id));
+  if (opt.nccl_unique_id)
+    std::memcpy(&id, opt.nccl_unique_id, sizeof(id));
   else
     nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
-  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaSetDevice(opt.device), "cudaSetDevice");
   ncclComm_t c;
   nccl_check(g_nccl.CommInitRank(&c, world, id, rank), "ncclCommInitRank");
   comm_ = c;
@@ -118,10 +124,25 @@ void Comm::init(int rank_, int world_, const void* unique_id, int device) {
 
 Comm::~Comm() {
   if (comm_ && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)comm_);
+  if (stage_) tron_host_free(stage_);
 }
 
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
   if (!active() || count == 0) return;
+  if (host_fn_) {
+    if (stage_n_ < count) {
+      if (stage_) tron_host_free(stage_);
+      stage_ = static_cast<double*>(tron_host_alloc(count * sizeof(double)));
+      if (!stage_) raise(TRON_ERR_OOM, "pinned staging buffer for the host allreduce");
+      stage_n_ = count;
+    }
+    cuda_check(cudaMemcpyAsync(stage_, buf, count * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "host allreduce sync");
+    host_fn_(host_user_, stage_, (uint64_t)count);
+    cuda_check(cudaMemcpyAsync(buf, stage_, count * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    // the next host allreduce overwrites stage_ only after this copy (it syncs s first)
+    return;
+  }
   nccl_check(g_nccl.AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)comm_, s),
              "ncclAllReduce");
 }
@@ -262,6 +283,8 @@ void Engine::common_alloc() {
   st_buf_.alloc(1);
   obj_d_ = obj_buf_.p;
   st_d_ = st_buf_.p;
+  ss_buf_.alloc(1);
+  ss_h_ = static_cast<SolveState*>(pinned_block_get());
   cuda_check(cudaMemsetAsync(obj_d_, 0, sizeof(ObjScalars), s_), "memset");
   cuda_check(cudaMemsetAsync(st_d_, 0, sizeof(CgState), s_), "memset");
   static_assert(sizeof(ObjScalars) <= 256 && sizeof(CgState) <= 256, "pinned block size");
@@ -304,7 +327,7 @@ void Engine::common_alloc() {
   // rank's CG state is identical, so every rank runs the same number of
   // allreduces); TRON_B200_NCCL_GRAPH=0 selects the host-driven CG loop.
   const char* cg = std::getenv("TRON_B200_NCCL_GRAPH");
-  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !(ng && ng[0] == '1');
+  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !comm_.host() && !(ng && ng[0] == '1');
 }
 
 // H2D of a buffer on a private stream ordered after everything issued on
@@ -359,7 +382,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     e->svm_strategy_ = opt.svm_strategy;
     e->budget_ = opt.gathered_budget_bytes;
     e->row_begin_ = opt.row_begin;
-    e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
+    e->comm_.init(opt);
     e->common_alloc();
     cudaStream_t s = e->s_;
     tr.s = s;
@@ -438,7 +461,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       if (prc != 0) cuda_check((cudaError_t)prc, "seg_plan_device");
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
-      if (!e->comm_.active()) {  // p.Hp / ||g|| summed by the transposed kernels
+      {  // p.Hp / ||g|| summed as the transposed product (or its epilogue) emits
         e->dot_parts_.alloc(seg_dot_slots(nch));
         e->dot_out_.alloc(1);
         e->dot_ticket_.alloc(1);
@@ -450,9 +473,13 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     // instantiated while the values are still crossing PCIe: a recipe of
     // fixed buffers, independent of their contents.
     if (e->use_graphs_ && nnz > 0 && n > 0) {
-      e->build_graph(0, false);
-      e->build_graph(1, false);
-      tr.mark("CG graphs");
+      if (e->device_loop_ok()) {
+        e->build_solve_graph(false);
+      } else {
+        e->build_graph(0, false);
+        e->build_graph(1, false);
+      }
+      tr.mark("solve / CG graphs");
     }
     finish_values();
     tr.mark("values H2D + CSC values");
@@ -508,7 +535,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->svm_strategy_ = svm_strategy;
   e->budget_ = opt.gathered_budget_bytes;
   e->row_begin_ = opt.row_begin;
-  e->comm_.init(opt.rank, opt.world, opt.nccl_unique_id, opt.device);
+  e->comm_.init(opt);
   e->ld_ = dense_ld((int64_t)l);
   // labels are checked on the worker pool while the matrix streams in
   try {
@@ -591,8 +618,13 @@ Engine::~Engine() {
       if (graph_exec_[a][b]) cudaGraphExecDestroy(graph_exec_[a][b]);
       if (graph_[a][b]) cudaGraphDestroy(graph_[a][b]);
     }
+  for (int b = 0; b < 2; ++b) {
+    if (solve_exec_[b]) cudaGraphExecDestroy(solve_exec_[b]);
+    if (solve_graph_[b]) cudaGraphDestroy(solve_graph_[b]);
+  }
   pinned_block_put(obj_h_);
   pinned_block_put(st_h_);
+  pinned_block_put(ss_h_);
   // DevBuf members queue their frees on s_; stream_owner_ then syncs + destroys it
 }
 
@@ -959,9 +991,9 @@ void Engine::ro_accum_slot(int mode, const Slot& S, const double* v, const EpiVi
 }
 
 bool Engine::hv_dot_available() const {
-  // (nnz == 0: csc_spmv takes the epilogue-only shortcut, which sums nothing)
-  const SegView& P = gathered_csr_valid_ ? gplan_ : plan_;
-  return !dense_ && !comm_.active() && dot_parts_.n > 0 && P.nchunks > 0;
+  // sharded or nnz == 0: the vector epilogue after the allreduce (or the
+  // epilogue-only shortcut) does the reduction instead of the segmented kernels
+  return !dense_ && dot_parts_.n > 0;
 }
 
 void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
@@ -1012,10 +1044,33 @@ void Engine::hessian_vec_host(const double* v, double* out) {
   ledger.concealed_vector_returns++;
 }
 
+// quadratic_model (tron.cpp:31-35) at the committed iterate: q(d) = g.d + 0.5 d.Hd
+// with g the committed gradient -- one Hv and one fused pair of dots.
+double Engine::quadratic_model_host(const double* d) {
+  if (!committed_valid_) raise(TRON_ERR_LOGIC, "quadratic_model() before the first commit()");
+  AllocScope scope(s_);
+  DevBuf<double> dots;
+  dots.alloc(2);
+  if (n_ > 0) upload(vtmp_.p, d, n_ * sizeof(double), s_);
+  hv_kernels(vtmp_.p, otmp_.p);
+  vec_dot2(n_, g_.p, vtmp_.p, vtmp_.p, otmp_.p, dots.p, sc_, s_);
+  count_launch(1);
+  double h[2] = {0.0, 0.0};
+  if (n_ > 0) cuda_check(cudaMemcpyAsync(h, dots.p, sizeof(h), cudaMemcpyDeviceToHost, s_), "D2H");
+  synchronize();
+  cuda_check(cudaGetLastError(), "quadratic_model");
+  return h[0] + 0.5 * h[1];
+}
+
 void Engine::ensure_precond() {
   if (!committed_valid_) raise(TRON_ERR_LOGIC, "precond_diagonal() before the first commit()");
   if (precond_valid_) return;
-  const Slot& S = slot_[cand_ ^ 1];
+  precond_kernels(slot_[cand_ ^ 1]);
+  precond_valid_ = true;
+}
+
+// M = 1 + C s sum_i d_i X_ij^2 of slot S into M_ (loss.cpp:176-188).
+void Engine::precond_kernels(const Slot& S) {
   EpiView epi;
   epi.kind = EPI_CONST;
   epi.cbase = 1.0;
@@ -1023,7 +1078,10 @@ void Engine::ensure_precond() {
   if (ro_) {
     ro_accum_slot(RO_PRECOND, S, nullptr, epi, M_.p);
   } else if (dense_) {
+    const int saved = cand_;
+    cand_ = (int)(&S - slot_) ^ 1;  // dense_vector reads the committed slot_[cand_ ^ 1]
     dense_vector(DA_PRECOND, nullptr, epi, M_.p);
+    cand_ = saved;
   } else {
     UView u;
     if (loss_ == TRON_LOSS_LOGISTIC) {
@@ -1035,7 +1093,6 @@ void Engine::ensure_precond() {
     }
     transposed_raw_or_epi(u, true, epi, M_.p);
   }
-  precond_valid_ = true;
 }
 
 void Engine::precond_host(double* m) {
@@ -1087,58 +1144,28 @@ void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint
 // ----------------------------------------------------------------------------
 // device-resident truncated CG (tron.cpp:37-108)
 // ----------------------------------------------------------------------------
-void Engine::build_graph(int k, bool use_m) {
-  // Captured against committed slot k; CG vectors are fixed buffers.
-  cudaGraph_t graph;
-  cuda_check(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
-  cudaGraphConditionalHandle handle;
-  cuda_check(cudaGraphConditionalHandleCreate(&handle, graph, 0, 0), "conditional handle");
-  Cond cond;
-  cond.h = (unsigned long long)handle;
-  cond.on = 1;
-  CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
-
-  const int saved_cand = cand_;
-  cand_ = k ^ 1;  // so that slot_[cand_^1] == committed slot k during capture
-  const uint64_t saved_launches = launches;
-
-  cuda_check(cudaStreamBeginCaptureToGraph(s_, graph, nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeThreadLocal),
-             "begin capture");
+// CG initialisation (d = 0, r = -g, p = M^-1 r) into the current capture.
+void Engine::capture_cg_init(const CgVectors& v, Cond cond) {
   if (ro_)
     ro_cg_init(v, st_d_, cond, s_);
   else if (small_engine_)
     cg_small_init(v, st_d_, cond, s_);
   else
     cg_large_init(v, st_d_, sc_, cond, s_);
-  cudaStreamCaptureStatus cs;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t ndeps = 0;
-  cudaGraph_t capg = nullptr;
-  cuda_check(cudaStreamGetCaptureInfo(s_, &cs, nullptr, &capg, &deps, &ndeps), "capture info");
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = handle;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t cond_node;
-  cuda_check(cudaGraphAddNode(&cond_node, capg, deps, ndeps, &cp), "add conditional node");
-  cuda_check(cudaStreamUpdateCaptureDependencies(s_, &cond_node, 1,
-                                                 cudaStreamSetCaptureDependencies),
-             "update deps");
-  cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
+  count_launch(1);
+}
 
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  cuda_check(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeThreadLocal),
-             "begin body capture");
-  const uint64_t before = launches;
+// One CG iteration with slot k committed (Hv of p, then the step kernel that
+// sets `cond`) into the current capture.
+void Engine::capture_cg_body(int k, const CgVectors& v, Cond cond) {
+  const int saved_cand = cand_;
+  cand_ = k ^ 1;  // so that slot_[cand_^1] == committed slot k
   if (ro_) {
     hv_kernels(p_.p, hp_.p);
     ro_cg_step(v, st_d_, cond, s_);
     count_launch(1);
   } else if (small_engine_) {
-    if (dense_) {
+    if (dense_ && !comm_.active()) {  // sharded: hv_kernels allreduces the partials
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
       const double scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
@@ -1165,10 +1192,66 @@ void Engine::build_graph(int k, bool use_m) {
     cg_coop_step(v, st_d_, coop_parts_.p, cond, s_, dot ? dot_out_.p : nullptr);
     count_launch(1);
   }
+  cand_ = saved_cand;
+}
+
+namespace {
+// Adds a conditional node of `type` after the current capture's dependencies
+// and makes it the capture's only dependency; returns its body graph.
+cudaGraph_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle handle,
+                            cudaGraphConditionalNodeType type) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t capg = nullptr;
+  cuda_check(cudaStreamGetCaptureInfo(s, &cs, nullptr, &capg, &deps, &ndeps), "capture info");
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = type;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  cuda_check(cudaGraphAddNode(&node, capg, deps, ndeps, &cp), "add conditional node");
+  cuda_check(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies),
+             "update deps");
+  return cp.conditional.phGraph_out[0];
+}
+
+Cond make_cond(cudaGraph_t g, unsigned dflt, unsigned flags) {
+  cudaGraphConditionalHandle h;
+  cuda_check(cudaGraphConditionalHandleCreate(&h, g, dflt, flags), "conditional handle");
+  Cond c;
+  c.h = (unsigned long long)h;
+  c.on = 1;
+  return c;
+}
+
+void begin_capture(cudaStream_t s, cudaGraph_t g) {
+  cuda_check(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal),
+             "begin capture");
+}
+}  // namespace
+
+void Engine::build_graph(int k, bool use_m) {
+  // Captured against committed slot k; CG vectors are fixed buffers.
+  cudaGraph_t graph;
+  cuda_check(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
+  const Cond cond = make_cond(graph, 0, 0);
+  CgVectors v{n_, g_.p, use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
+  const uint64_t saved_launches = launches;
+
+  begin_capture(s_, graph);
+  capture_cg_init(v, cond);
+  cudaGraph_t body = add_conditional(s_, (cudaGraphConditionalHandle)cond.h, cudaGraphCondTypeWhile);
+  cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
+
+  begin_capture(s_, body);
+  const uint64_t before = launches;
+  capture_cg_body(k, v, cond);
   body_kernels_ = launches - before;
   cuda_check(cudaStreamEndCapture(s_, &body), "end body capture");
   launches = saved_launches;
-  cand_ = saved_cand;
 
   cudaGraphExec_t exec;
   cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
@@ -1234,31 +1317,13 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
     launches += 1 + (uint64_t)out->iters * body_kernels_;
     return;
   }
-  // host-driven loop (multi-GPU: NCCL between phases)
+  // host-driven loop (host data plane, or TRON_B200_NO_GRAPH / NCCL_GRAPH=0):
+  // the graph's kernels, launched one iteration at a time
   Cond none;
-  if (ro_)
-    ro_cg_init(v, st_d_, none, s_);
-  else if (small_engine_)
-    cg_small_init(v, st_d_, none, s_);
-  else
-    cg_large_init(v, st_d_, sc_, none, s_);
-  count_launch(1);
+  capture_cg_init(v, none);
   read_cg(out);
   while (out->cont) {
-    hv_kernels(p_.p, hp_.p);
-    if (ro_) {
-      ro_cg_step(v, st_d_, none, s_);
-      count_launch(1);
-    } else if (small_engine_) {
-      cg_small_step(v, nullptr, 0, 0.0, st_d_, none, s_);
-      count_launch(1);
-    } else if (mid_engine_) {
-      cg_cluster_step(v, st_d_, none, s_);
-      count_launch(1);
-    } else {
-      cg_coop_step(v, st_d_, coop_parts_.p, none, s_);  // (the host loop's Hv ran without the dot)
-      count_launch(1);
-    }
+    capture_cg_body(k, v, none);
     read_cg(out);
   }
 }
@@ -1326,7 +1391,15 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     else
       cuda_check(cudaMemsetAsync(C0.w.p, 0, n_ * 8, s_), "memset");
   }
-  double f = eval_candidate_dev(nullptr);
+  const char* trace_env = std::getenv("TRON_B200_TRACE");
+  const bool device_loop = device_loop_ok() && !(trace_env && trace_env[0] == '1');
+  // device loop: the starting point's margin pass and gradient in one round trip
+  double f = eval_candidate_dev(nullptr, /*read=*/!device_loop);
+  if (device_loop) {
+    gradient_into(slot_[cand_], gbuf(cand_));  // adopted below unless f is not finite
+    read_obj();
+    f = candidate_result();
+  }
   info->objective_evaluations = 1;
   if (!std::isfinite(f)) {
     // nothing was committed: like the reference (which throws before any
@@ -1335,7 +1408,21 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     finish(TRON_ERR_NUMERICAL);
     raise(TRON_ERR_NUMERICAL, "objective is not finite at the starting point");
   }
-  commit(nullptr);
+  if (device_loop) {
+    cand_ ^= 1;
+    slot_[cand_].valid = false;
+    committed_valid_ = true;
+    precond_valid_ = false;
+    gathered_valid_ = false;
+    gathered_csr_valid_ = false;
+    gnorm_ = obj_h_->gnorm;
+    ledger.gradient_materializations++;
+    if (cand_ == 0)  // the committed slot is 1: g_ must hold its gradient for the API
+      cuda_check(cudaMemcpyAsync(g_.p, gspec_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_),
+                 "D2D");
+  } else {
+    commit(nullptr);
+  }
   info->gradient_materializations = 1;
   if (obj_h_->grad_nonfinite) {
     finish(TRON_ERR_NUMERICAL);
@@ -1348,6 +1435,18 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   info->objective = f;
   if (gnorm <= cfg.eps * gnorm0) {
     info->converged = 1;
+    finish(TRON_OK);
+    return;
+  }
+  if (device_loop) {
+    int status = TRON_OK;
+    std::string what;
+    solve_device_loop(cfg, f, info, trace, cap, &status, &what);
+    hv_count = info->hessian_products;
+    if (status != TRON_OK) {
+      finish(status);
+      raise(status, what);
+    }
     finish(TRON_OK);
     return;
   }
@@ -1474,6 +1573,156 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     }
   }
   finish(TRON_OK);
+}
+
+// ----------------------------------------------------------------------------
+// device-resident outer loop (tron.cpp:127-217 as one graph; trloop.cu)
+// ----------------------------------------------------------------------------
+bool Engine::device_loop_ok() const {
+  const char* e = std::getenv("TRON_B200_DEVICE_LOOP");  // 0: host-driven outer loop
+  const bool on = !(e && e[0] == '0');
+  // Gathered / Auto L2-SVM re-gather X_I on the host at every commit
+  return on && use_graphs_ && n_ > 0 &&
+         !(loss_ == TRON_LOSS_L2SVM && svm_strategy_ != TRON_SVM_INDIRECT);
+}
+
+// WHILE(outer) { dispatch; IF(committed == 0) body(0); IF(committed == 1) body(1) }
+// with body(k) = [M of slot k] prep, CG init, WHILE(cg){Hv, step}, w_cand = w_k + d,
+// margin pass and speculative gradient of slot k^1, tr_update.
+void Engine::build_solve_graph(bool use_m) {
+  const uint64_t saved_launches = launches;
+  cudaGraph_t top;
+  cuda_check(cudaGraphCreate(&top, 0), "cudaGraphCreate");
+  const Cond outer = make_cond(top, 1, cudaGraphCondAssignDefault);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = (cudaGraphConditionalHandle)outer.h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  cuda_check(cudaGraphAddNode(&wnode, top, nullptr, 0, &cp), "add outer while node");
+  cudaGraph_t B = cp.conditional.phGraph_out[0];
+  const Cond K[2] = {make_cond(B, 0, 0), make_cond(B, 0, 0)};
+  SolveState* ss = ss_buf_.p;
+  begin_capture(s_, B);
+  tr_dispatch(ss, K[0], K[1], s_);
+  cudaGraph_t I[2];
+  I[0] = add_conditional(s_, (cudaGraphConditionalHandle)K[0].h, cudaGraphCondTypeIf);
+  I[1] = add_conditional(s_, (cudaGraphConditionalHandle)K[1].h, cudaGraphCondTypeIf);
+  cuda_check(cudaStreamEndCapture(s_, &B), "end capture");
+  for (int k = 0; k < 2; ++k) {
+    CgVectors v{n_, gbuf(k), use_m ? M_.p : nullptr, d_.p, r0_.p, r1_.p, p_.p, hp_.p};
+    const Cond ck = make_cond(I[k], 0, 0);
+    begin_capture(s_, I[k]);
+    uint64_t before = launches;
+    if (use_m) precond_kernels(slot_[k]);  // recomputed per iteration: same bits as cached
+    tr_prep(ss, st_d_, s_);
+    count_launch(1);
+    capture_cg_init(v, ck);
+    cudaGraph_t W = add_conditional(s_, (cudaGraphConditionalHandle)ck.h, cudaGraphCondTypeWhile);
+    const int saved = cand_;
+    cand_ = k ^ 1;
+    eval_candidate_dev(d_.p, /*read=*/false);  // slot k^1: w_k + d, margin pass
+    gradient_into(slot_[k ^ 1], gbuf(k ^ 1));  // speculative gradient
+    cand_ = saved;
+    tr_update(ss, st_d_, obj_d_, k, outer, K[k ^ 1], s_);
+    count_launch(1);
+    outer_kernels_ = launches - before;
+    cuda_check(cudaStreamEndCapture(s_, &I[k]), "end capture");
+    begin_capture(s_, W);
+    before = launches;
+    capture_cg_body(k, v, ck);
+    body_kernels_ = launches - before;
+    cuda_check(cudaStreamEndCapture(s_, &W), "end capture");
+  }
+  launches = saved_launches;
+  cudaGraphExec_t exec;
+  cuda_check(cudaGraphInstantiate(&exec, top, 0), "solve graph instantiate");
+  solve_graph_[use_m] = top;
+  solve_exec_[use_m] = exec;
+}
+
+// The outer loop after the initial commit: one H2D of the solver scalars, one
+// graph launch, one D2H of the scalars and the iteration records.
+void Engine::solve_device_loop(const tron_config& cfg, double f, tron_solve_info* info,
+                               tron_iteration* trace, uint64_t cap, int* status, std::string* what) {
+  static_assert(sizeof(TrRecord) == sizeof(tron_iteration), "TrRecord mirrors tron_iteration");
+  static_assert(sizeof(SolveState) <= 256, "pinned block size");
+  AllocScope scope(s_);
+  const bool use_m = cfg.use_preconditioner != 0;
+  constexpr uint64_t kInlineRecords = 64;  // read back together with the scalars
+  const uint64_t want = std::max<uint64_t>(std::min<uint64_t>(cap, cfg.max_outer_iters), 1);
+  if (trace_buf_.n < want) trace_buf_.alloc(std::max<uint64_t>(want, kInlineRecords));
+  if (!solve_exec_[use_m]) build_solve_graph(use_m);
+  SolveState& S = *ss_h_;
+  std::memset(&S, 0, sizeof(S));
+  uint64_t max_cg = cfg.max_cg_iters;
+  if (max_cg == 0) max_cg = (uint64_t)n_ < 1000 ? (uint64_t)n_ : 1000;  // tron.cpp:40-41
+  S.cfg = TrConfig{cfg.eps, cfg.sigma0, cfg.eta1, cfg.eta2, cfg.gamma1, cfg.gamma2, cfg.gamma3,
+                   cfg.cg_tol, C_, (long long)cfg.max_outer_iters, (long long)max_cg,
+                   use_m ? 1 : 0, comm_.active() ? 1 : 0};
+  S.f = f;
+  S.delta = gnorm_;  // tron.cpp:159
+  S.gnorm = gnorm_;
+  S.gnorm0 = gnorm_;
+  S.committed = cand_ ^ 1;
+  S.cont = cfg.max_outer_iters > 0;
+  S.trace = trace_buf_.p;
+  S.cap = (long long)trace_buf_.n;
+  info->hessian_products = 0;
+  if (S.cont) {
+    cuda_check(cudaMemcpyAsync(ss_buf_.p, &S, sizeof(S), cudaMemcpyHostToDevice, s_), "H2D");
+    cuda_check(cudaGraphLaunch(solve_exec_[use_m], s_), "solve graph launch");
+    cuda_check(cudaMemcpyAsync(&S, ss_buf_.p, sizeof(S), cudaMemcpyDeviceToHost, s_), "D2H");
+    const uint64_t inline_n = std::min<uint64_t>(std::min<uint64_t>(cap, kInlineRecords), trace_buf_.n);
+    if (trace && inline_n)
+      cuda_check(cudaMemcpyAsync(trace, trace_buf_.p, inline_n * sizeof(TrRecord), cudaMemcpyDeviceToHost,
+                                 s_),
+                 "D2H");
+    synchronize();
+    cuda_check(cudaGetLastError(), "solve graph");
+    const uint64_t nrec = std::min<uint64_t>((uint64_t)S.n_iter, cap);
+    if (trace && nrec > inline_n) {
+      cuda_check(cudaMemcpyAsync(trace + inline_n, trace_buf_.p + inline_n,
+                                 (nrec - inline_n) * sizeof(TrRecord), cudaMemcpyDeviceToHost, s_),
+                 "D2H");
+      synchronize();
+    }
+  }
+  // the committed slot and its gradient (g[k] -> g_ for gradient())
+  cand_ = S.committed ^ 1;
+  slot_[cand_].valid = false;
+  slot_[cand_ ^ 1].f = S.f;
+  committed_valid_ = true;
+  precond_valid_ = false;
+  if (S.committed == 1)
+    cuda_check(cudaMemcpyAsync(g_.p, gspec_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_), "D2D");
+  gnorm_ = S.gnorm;
+  info->n_iterations = (uint64_t)S.n_iter;
+  info->accepted_steps = (uint64_t)S.accepted;
+  info->objective_evaluations += (uint64_t)S.obj_evals;
+  info->gradient_materializations += (uint64_t)S.grad_mats;
+  info->objective = S.f;
+  info->converged = S.converged;
+  info->hessian_products = (uint64_t)S.hv_count;
+  ledger.margin_passes += (uint64_t)S.obj_evals;
+  ledger.scalar_returns += (uint64_t)S.obj_evals;
+  ledger.gradient_materializations += (uint64_t)S.grad_mats;
+  if (loss_ == TRON_LOSS_L2SVM)
+    ledger.index_set_bytes = std::max<uint64_t>(ledger.index_set_bytes, (uint64_t)S.max_nact * 8);
+  launches += 1 + (uint64_t)(S.obj_evals + (S.status == kTrFailCg)) * (outer_kernels_ + 1) +
+              (uint64_t)S.hv_count * body_kernels_;
+  *status = TRON_OK;
+  if (S.status == kTrFailCg) {
+    *status = TRON_ERR_NUMERICAL;
+    *what = "conjugate gradients met non-positive curvature (" + std::to_string(S.fail_php) + ")";
+  } else if (S.status == kTrFailObjective) {
+    *status = TRON_ERR_NUMERICAL;
+    *what = "objective is not finite at a candidate step";
+  } else if (S.status == kTrFailGradient) {
+    *status = TRON_ERR_NUMERICAL;
+    *what = "gradient is not finite after an accepted step";
+  }
 }
 
 // ----------------------------------------------------------------------------

@@ -91,17 +91,26 @@ struct StreamOwner {
 };
 
 // Lazily-loaded NCCL (libnccl.so.2) for the row-sharded multi-GPU layout.
+// Or, when the caller supplies tron_gpu_options::host_allreduce, a host data
+// plane: the partials are staged through pinned memory and summed by the
+// caller's collective (MPI, gloo, ...); such a context is never captured
+// into graphs (the CG loop runs host-driven).
 class Comm {
  public:
   int rank = 0, world = 1;
-  void init(int rank, int world, const void* unique_id, int device);
+  void init(const tron_gpu_options& opt);
   ~Comm();
   void allreduce_sum(double* buf, size_t count, cudaStream_t s);
   bool active() const { return world > 1 || forced; }
+  bool host() const { return host_fn_ != nullptr && world > 1; }
   bool forced = false;  // one-rank communicator forced on (TRON_B200_FORCE_NCCL=1)
 
  private:
   void* comm_ = nullptr;
+  void (*host_fn_)(void*, double*, uint64_t) = nullptr;
+  void* host_user_ = nullptr;
+  double* stage_ = nullptr;  // pinned (tron_host_alloc pool)
+  size_t stage_n_ = 0;
 };
 int nccl_unique_id(void* out128);
 
@@ -130,6 +139,7 @@ class Engine {
   void gradient_host(double* g);
   void hessian_vec_host(const double* v, double* out);
   void precond_host(double* m);
+  double quadratic_model_host(const double* d);
   void state_lr(int which, double* z, double* zhat, double* dvec);
   void state_svm(int which, double* z, int64_t* active, uint64_t cap, uint64_t* n_active);
   void truncated_cg(double delta, const tron_config& cfg, double* d, int32_t* exit_kind,
@@ -183,6 +193,16 @@ class Engine {
   void read_cg(CgState* out);
   void build_graph(int slot, bool use_m);
   void launch_cg_graph(int slot, bool use_m);
+  // CG pieces captured into the current stream capture (committed slot k)
+  void capture_cg_init(const CgVectors& v, Cond cond);
+  void capture_cg_body(int k, const CgVectors& v, Cond cond);
+  void precond_kernels(const Slot& S);
+  // device-resident outer loop (trloop.cu): one graph per use_m
+  bool device_loop_ok() const;
+  void build_solve_graph(bool use_m);
+  void solve_device_loop(const tron_config& cfg, double f, tron_solve_info* info,
+                         tron_iteration* trace, uint64_t cap, int* status, std::string* what);
+  double* gbuf(int k) { return k == 0 ? g_.p : gspec_.p; }
   template <class Report>
   void screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_t n, Report report);
   void count_launch(uint64_t k) { launches += k; }
@@ -268,6 +288,14 @@ class Engine {
   bool hv_dot_available() const;
   DevBuf<double> coop_parts_;  // CTA partials of the cooperative CG step
   bool use_graphs_ = true;
+  // device-resident outer loop
+  cudaGraphExec_t solve_exec_[2] = {nullptr, nullptr};
+  cudaGraph_t solve_graph_[2] = {nullptr, nullptr};
+  uint64_t solve_epoch_[2] = {0, 0};
+  uint64_t outer_kernels_ = 0;  // kernels per outer iteration outside the CG body
+  DevBuf<SolveState> ss_buf_;
+  SolveState* ss_h_ = nullptr;  // pinned
+  DevBuf<TrRecord> trace_buf_;
 };
 
 }  // namespace tb

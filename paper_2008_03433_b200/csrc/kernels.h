@@ -120,7 +120,7 @@ struct Scratch {
 constexpr int kMaxPartialBlocks = 4096;
 constexpr int kNumTickets = 16;
 enum Ticket : int { T_FUN = 0, T_AXPY = 1, T_NORM = 2, T_CG_INIT = 3, T_CG_PHP = 4, T_CG_UPD = 5,
-                    T_CG_P = 6, T_CG_POST = 7, T_DENSE_FIN = 8, T_COUNT = 9 };
+                    T_CG_P = 6, T_CG_POST = 7, T_DENSE_FIN = 8, T_COUNT = 9, T_DOT2 = 10 };
 
 int device_sm_count();
 
@@ -173,6 +173,9 @@ void vec_axpy_dot(int64_t n, const double* w, const double* d, double* wc, ObjSc
                   Scratch sc, cudaStream_t s);
 // obj->gnorm = ||g||, obj->grad_nonfinite
 void vec_norm_check(int64_t n, const double* g, ObjScalars* obj, Scratch sc, cudaStream_t s);
+// out2[0] = a.b, out2[1] = c.d (fixed-order two-stage sums)
+void vec_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d,
+              double* out2, Scratch sc, cudaStream_t s);
 // out = base + scale*raw  (after an allreduce of raw partials; raw == nullptr => 0)
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
 void l2_read_flush(const double* buf, int64_t n, cudaStream_t s);
@@ -209,6 +212,36 @@ constexpr int64_t kSmallCgMaxN = 4096;
 void cg_small_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s);
 void cg_small_step(const CgVectors& v, const double* partials, int nparts, double scale,
                    CgState* st, Cond cond, cudaStream_t s);
+
+// ---- device-resident outer trust-region loop (trloop.cu) --------------------
+// TrustRegionConfig (tron.hpp:13-27) as the device reads it.
+struct TrConfig {
+  double eps, sigma0, eta1, eta2, gamma1, gamma2, gamma3, cg_tol, C;
+  long long max_outer, max_cg;
+  int use_m, sharded;  // sharded: f = 0.5 ww + C * (allreduced loss sum)
+};
+// IterationRecord (tron.hpp:38-48); the layout of tron_iteration.
+struct TrRecord {
+  double f_candidate, gradient_norm, delta, sigma;
+  int accepted, cg_exit;
+  long long cg_iters;
+};
+enum TrStatus : int { kTrOk = 0, kTrFailCg = 1, kTrFailObjective = 2, kTrFailGradient = 3 };
+// The solver's scalars (tron.cpp:127-217 locals + SolverTrace counters).
+struct SolveState {
+  TrConfig cfg;
+  double f, delta, gnorm, gnorm0, fail_php;
+  long long n_iter, accepted, obj_evals, grad_mats, hv_count, max_nact;
+  int committed;  // slot of the committed iterate
+  int status;     // TrStatus
+  int converged, cont;
+  TrRecord* trace;  // device records [cap]
+  long long cap;
+};
+void tr_dispatch(const SolveState* S, Cond k0, Cond k1, cudaStream_t s);
+void tr_prep(const SolveState* S, CgState* st, cudaStream_t s);
+void tr_update(SolveState* S, const CgState* cg, const ObjScalars* obj, int k, Cond outer,
+               Cond other, cudaStream_t s);
 
 // ---- dense column-major kernels (dense_kernels.cu), n <= 64 -----------------
 // X is column-major with ld = dense_ld(l) rows (a multiple of kDenseTile,

@@ -92,14 +92,77 @@ __global__ void __launch_bounds__(kBlock) norm_check_kernel(long long n, const d
   }
 }
 
-__global__ void epilogue_kernel(long long n, const double* raw, EpiView E, double* out) {
+__global__ void __launch_bounds__(kBlock) dot2_kernel(long long n, const double* a, const double* b,
+                                                     const double* c, const double* d, double* out2,
+                                                     Scratch sc) {
   pdl_wait();
   pdl_trigger();
+  __shared__ double sh[kBlock / kWarp + 1];
+  double x = 0.0, y = 0.0;
+#pragma unroll 4
+  GRID_STRIDE(j, n) {
+    x += a[j] * b[j];
+    y += c[j] * d[j];
+  }
+  const double bx = block_sum<kBlock>(x, sh, true);
+  const double by = block_sum<kBlock>(y, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[2 * blockIdx.x] = bx;
+    sc.partials[2 * blockIdx.x + 1] = by;
+  }
+  if (last_block_arrive(sc.tickets + T_DOT2)) {
+    const double tx = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 0, sh);
+    const double ty = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      out2[0] = tx;
+      out2[1] = ty;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) epilogue_kernel(long long n, const double* raw, EpiView E,
+                                                         double* out) {
+  pdl_wait();
+  pdl_trigger();
+  // EPI_VEC with dot_parts: the emission's reduction (EpiView::dot_*), as the
+  // segmented kernels do it unsharded -- so p.Hp and ||g|| survive sharding
+  // (raw is the allreduced sum: every rank reduces the same bits)
+  const bool dot = E.kind == EPI_VEC && E.dot_parts != nullptr;
+  double acc = 0.0, bad = 0.0;
 #pragma unroll 4
   GRID_STRIDE(j, n) {
     const double s = raw ? raw[j] : 0.0;
-    out[j] = E.kind == EPI_VEC ? E.base[j] + E.scale * s
-                               : (E.kind == EPI_CONST ? E.cbase + E.scale * s : s);
+    const double o = E.kind == EPI_VEC ? E.base[j] + E.scale * s
+                                       : (E.kind == EPI_CONST ? E.cbase + E.scale * s : s);
+    out[j] = o;
+    if (dot) {
+      if (E.dot_mode == 0) {
+        acc += E.base[j] * o;
+      } else {
+        acc += o * o;
+        if (!isfinite(o)) bad = 1.0;
+      }
+    }
+  }
+  if (!dot) return;
+  __shared__ double sh[kBlock / kWarp + 1];
+  const double b = block_sum<kBlock>(acc, sh, true);
+  const double bb = block_sum<kBlock>(bad, sh, true);
+  if (threadIdx.x == 0) {
+    E.dot_parts[2 * blockIdx.x] = b;
+    E.dot_parts[2 * blockIdx.x + 1] = bb;
+  }
+  if (last_block_arrive(E.dot_ticket)) {
+    const double tot = reduce_partials<kBlock>(E.dot_parts, gridDim.x, 2, 0, sh);
+    const double nb = reduce_partials<kBlock>(E.dot_parts, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      if (E.dot_mode == 0) {
+        *E.dot_out = tot;
+      } else {
+        E.dot_obj->gnorm = sqrt(tot);
+        E.dot_obj->grad_nonfinite = nb > 0.0;
+      }
+    }
   }
 }
 
@@ -676,6 +739,11 @@ void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cud
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, cg_coop_step_kernel, v, st, parts, cond, php_in);
   if (e != cudaSuccess) launch_failed(e, "cg_coop_step (cooperative launch)");
+}
+
+void vec_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d,
+              double* out2, Scratch sc, cudaStream_t s) {
+  launch_pdl(dot2_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, a, b, c, d, out2, sc);
 }
 
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s) {

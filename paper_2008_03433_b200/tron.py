@@ -14,7 +14,7 @@ from __future__ import annotations
 import ctypes
 import enum
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import Callable, List, Optional
 
 import numpy as np
 
@@ -205,6 +205,9 @@ class ExecutionPlan:
     global_rows: int = 0
     # dense L2-SVM: every reduction in the reference's order (bit-for-bit results)
     reference_order: bool = False
+    # host data plane instead of NCCL (world > 1): fn(buf: np.ndarray) sums buf
+    # over the ranks in place (e.g. a gloo / MPI allreduce)
+    host_allreduce: Optional[Callable[[np.ndarray], None]] = None
 
     @staticmethod
     def gpu(device: int = 0, svm_strategy: SvmStrategy = SvmStrategy.Indirect,
@@ -223,10 +226,20 @@ class ExecutionPlan:
         o.rank, o.world = self.rank, self.world
         o.row_begin, o.global_rows = self.row_begin, self.global_rows
         o.reference_order = int(bool(self.reference_order))
-        keep = None
+        keep = []
         if self.nccl_unique_id is not None:
-            keep = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)
-            o.nccl_unique_id = ctypes.cast(keep, ctypes.c_void_p)
+            uid = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)
+            o.nccl_unique_id = ctypes.cast(uid, ctypes.c_void_p)
+            keep.append(uid)
+        if self.host_allreduce is not None:
+            fn = self.host_allreduce
+
+            def trampoline(_user, buf, count):
+                fn(np.ctypeslib.as_array(buf, shape=(count,)))
+
+            cb = _lib.HOST_ALLREDUCE(trampoline)
+            o.host_allreduce = ctypes.cast(cb, ctypes.c_void_p)
+            keep.append(cb)
         return o, keep
 
 
@@ -392,6 +405,16 @@ class GpuEvaluator:
         self._sync_ledger()
         return out
 
+    def quadratic_model(self, d) -> float:
+        """quadratic_model(g, hv, d) (tron.cpp:31-35) at the committed iterate, on the
+        device: g.d + 0.5 d.Hd with g = gradient() and this evaluator's Hessian."""
+        d = _f64(d)
+        if d.size != self.n:
+            raise DimensionError(f"quadratic_model: direction has length {d.size}, expected {self.n}")
+        q = ctypes.c_double()
+        _raise(lib.tron_gpu_quadratic_model(self._h, _ptr(d, ctypes.c_double), ctypes.byref(q)))
+        return q.value
+
     def precond_diagonal(self) -> np.ndarray:
         out = np.empty(self.n)
         _raise(lib.tron_gpu_precond_diagonal(self._h, _ptr(out, ctypes.c_double)))
@@ -507,6 +530,22 @@ def solve(problem: Problem, loss: LossKind, cfg: TrustRegionConfig, plan: Execut
     cfg.validate()
     with make_evaluator(problem, loss, plan) as ev:
         return ev.solve(cfg, warm_start)
+
+
+def quadratic_model(g, hv, d) -> float:
+    """quadratic_model (tron.hpp:83, tron.cpp:31-35): g.d + 0.5 d.(hv(d)), with the
+    reference's serial left-to-right dots.  hv is any Hessian apply, e.g. a
+    GpuEvaluator's hessian_vec (the device-side variant is
+    GpuEvaluator.quadratic_model)."""
+    g, d = _f64(g), _f64(d)
+    hd = _f64(hv(d))
+    gd = 0.0
+    for a, b in zip(g.tolist(), d.tolist()):
+        gd += a * b
+    dh = 0.0
+    for a, b in zip(d.tolist(), hd.tolist()):
+        dh += a * b
+    return gd + 0.5 * dh
 
 
 def trust_region_update(sigma, delta, step_norm, cfg: TrustRegionConfig):

@@ -43,7 +43,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.tron_config) == 8 * 10 + 8
     assert ctypes.sizeof(_lib.tron_iteration) == 4 * 8 + 8 + 8
     assert ctypes.sizeof(_lib.tron_ledger) == 7 * 8
-    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8  # + int32 + pad
+    # ... reference_order (int32 + pad), host_allreduce and its user pointer
+    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 8
 
 
 def test_defaults_mirror_reference():
@@ -88,3 +89,12 @@ def test_validation_happens_before_device_use():
                                     np.array([5], np.int32)), np.array([1.0]), 1.0)
     with pytest.raises(BoundsError):
         make_evaluator(bad_col, LossKind.Logistic, ExecutionPlan.gpu())
+
+
+def test_quadratic_model_kats():  # test_tron.cpp:44-51 on the host mirror
+    from paper_2008_03433_b200 import quadratic_model
+    hv = lambda d: np.asarray(d, dtype=np.float64).copy()  # identity Hessian
+    assert quadratic_model([1.0, 0.0], hv, [0.0, 0.0]) == 0.0
+    assert quadratic_model([1.0, 0.0], hv, [-1.0, 0.0]) == -0.5
+    g, d = np.array([3.0, -4.0]), np.array([-3.0, 4.0])
+    assert abs(quadratic_model(g, hv, d) - (-g @ g / 2.0)) <= 1e-15 * (g @ g / 2.0)

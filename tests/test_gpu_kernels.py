@@ -391,3 +391,30 @@ def test_gathered_csr_budget_names_mix():
         ev.eval_candidate(np.zeros(p.X.cols))
         ev.commit()
         assert ev.ledger().gathered_submatrix_bytes == 0
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_device_quadratic_model(port, case):
+    """tron_gpu_quadratic_model (tron.cpp:31-35) at the committed iterate against
+    the oracle's g.d + 0.5 d.Hd; and the CG's residual identity (tron.cpp:106):
+    the CG result's model value is q(d) of its own step."""
+    from paper_2008_03433_b200 import quadratic_model
+    probs = [(synth.synth_sparse(3, 800, 20000, 30), LossKind.Logistic, 0),
+             (synth.synth_dense(2, 3000, 40), LossKind.L2Svm, 1),
+             (synth.synth_sparse(6, 700, 5000, 25), LossKind.L2Svm, 1)]
+    p, loss, ol = probs[case]
+    n = p.X.cols
+    w = synth.testgen_random_vector(11, n, 0.05)
+    d = synth.testgen_random_vector(12, n, 1.0)
+    with make_evaluator(p, loss, ExecutionPlan.gpu()) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        q = ev.quadratic_model(d)
+        q_host = quadratic_model(ev.gradient(), ev.hessian_vec, d)
+        cg = ev.truncated_cg(np.linalg.norm(ev.gradient()), TrustRegionConfig(eps=0.01))
+        q_step = ev.quadratic_model(cg.d)
+    want = port.logistic(p, w, d) if ol == 0 else port.svm(p, w, d)
+    q_ref = float(want["g"] @ d + 0.5 * d @ want["hv"])
+    assert abs(q - q_ref) <= 1e-11 * abs(q_ref)
+    assert abs(q - q_host) <= 1e-12 * abs(q_ref)
+    assert abs(q_step - cg.model_value) <= 1e-9 * abs(cg.model_value)
