@@ -215,6 +215,17 @@ int tron_parsed_sizes(const tron_parsed *p, uint64_t *rows, uint64_t *cols, uint
 int tron_parsed_copy(const tron_parsed *p, int64_t *row_offsets, int32_t *col_indices,
                      double *values, double *y);
 void tron_parsed_free(tron_parsed *p);
+/* load_dense (io.hpp:31, io.cpp:164-197): "label v1 ... vn" per line, exactly n
+ * values, the reference's error messages; the result is dense (row-major values,
+ * l*n of them; tron_parsed_copy ignores row_offsets / col_indices) and feeds
+ * tron_gpu_create_dense. */
+int tron_load_dense(const char *text, uint64_t len, uint64_t n, tron_parsed **out);
+int tron_load_dense_file(const char *path, uint64_t n, tron_parsed **out);
+int tron_parsed_layout(const tron_parsed *p, int32_t *dense);
+/* Binary cache ("TRONBIN1"): a parsed problem written once and read back at
+ * storage speed. */
+int tron_parsed_save_binary(const tron_parsed *p, const char *path);
+int tron_load_binary(const char *path, tron_parsed **out);
 uint64_t tron_gpu_last_error_line(void);
 
 /* ---- deterministic synthetic inputs (host-side tooling) ---- */

@@ -317,6 +317,27 @@ class Reference:
         L.ref_parsed_free(h)
         return "ok", (ro, ci, vals, y, c.value)
 
+    def load_dense(self, text: bytes, n: int):
+        """The reference's load_dense (io.cpp:164-197) on an in-memory text:
+        ('ok', (values, y)) or (kind, (message, line))."""
+        L = self.lib
+        self.parse_libsvm(b"")  # binds the parsed_* helpers
+        L.ref_load_dense.argtypes = [ctypes.c_char_p, c_size_t, c_size_t, ctypes.POINTER(ctypes.c_void_p),
+                                     ctypes.c_char_p, c_size_t, POINTER(c_size_t)]
+        h = ctypes.c_void_p()
+        msg = ctypes.create_string_buffer(512)
+        line = c_size_t()
+        rc = L.ref_load_dense(text, len(text), n, ctypes.byref(h), msg, 512, ctypes.byref(line))
+        if rc != 0:
+            return {1: "parse", 2: "label"}.get(rc, "other"), (msg.value.decode(), line.value)
+        r, c, z = c_size_t(), c_size_t(), c_size_t()
+        L.ref_parsed_sizes(h, ctypes.byref(r), ctypes.byref(c), ctypes.byref(z))
+        vals = np.empty(z.value)
+        y = np.empty(r.value)
+        L.ref_parsed_copy(h, None, None, _p(vals), _p(y))
+        L.ref_parsed_free(h)
+        return "ok", (vals, y)
+
     def time_calls(self, problem, loss, workers, reps=1, backend=1):
         """Per-call ms of the reference evaluator (fun, grad, Hv) at w = 0 under
         ExecutionPlan::parallel(workers) (backend 1) or ::sequential() (backend 0)."""

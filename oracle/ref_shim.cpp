@@ -500,6 +500,31 @@ int ref_parse_libsvm(const char* text, size_t len, size_t n_override, void** out
   }
 }
 
+// load_dense (io.cpp:164-197) on an in-memory text; same return codes.
+int ref_load_dense(const char* text, size_t len, size_t n, void** out, char* msg, size_t msglen,
+                   size_t* line) {
+  *out = nullptr;
+  if (msglen) msg[0] = 0;
+  *line = 0;
+  try {
+    std::istringstream in(std::string(text, len));
+    auto* p = new tron::Problem(tron::load_dense(in, n));
+    *out = p;
+    return 0;
+  } catch (const tron::UnsupportedLabelError& e) {
+    std::snprintf(msg, msglen, "%s", e.what());
+    *line = e.line();
+    return 2;
+  } catch (const tron::ParseError& e) {
+    std::snprintf(msg, msglen, "%s", e.what());
+    *line = e.line();
+    return 1;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, msglen, "%s", e.what());
+    return 3;
+  }
+}
+
 void ref_parsed_sizes(const void* h, size_t* rows, size_t* cols, size_t* nnz) {
   const auto* p = static_cast<const tron::Problem*>(h);
   *rows = p->X.rows();
@@ -512,8 +537,8 @@ void ref_parsed_copy(const void* h, int64_t* ro, int32_t* ci, double* vals, doub
   auto o = p->X.row_offsets();
   auto c = p->X.col_indices();
   auto v = p->X.values();
-  std::memcpy(ro, o.data(), o.size() * sizeof(int64_t));
-  std::memcpy(ci, c.data(), c.size() * sizeof(int32_t));
+  if (ro) std::memcpy(ro, o.data(), o.size() * sizeof(int64_t));
+  if (ci) std::memcpy(ci, c.data(), c.size() * sizeof(int32_t));
   std::memcpy(vals, v.data(), v.size() * sizeof(double));
   std::memcpy(y, p->y.data(), p->y.size() * sizeof(double));
 }

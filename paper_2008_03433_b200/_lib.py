@@ -119,6 +119,11 @@ SIGNATURES = [
                                   ctypes.POINTER(c_uint64)]),
     ("tron_parsed_copy", c_int, [ctypes.c_void_p, PI64, PI32, PD, PD]),
     ("tron_parsed_free", None, [ctypes.c_void_p]),
+    ("tron_load_dense", c_int, [c_char_p, c_uint64, c_uint64, POINTER(c_void_p)]),
+    ("tron_load_dense_file", c_int, [c_char_p, c_uint64, POINTER(c_void_p)]),
+    ("tron_parsed_layout", c_int, [c_void_p, PI32]),
+    ("tron_parsed_save_binary", c_int, [c_void_p, c_char_p]),
+    ("tron_load_binary", c_int, [c_char_p, POINTER(c_void_p)]),
     ("tron_gpu_last_error_line", c_uint64, []),
     ("tron_host_alloc", c_void_p, [c_uint64]),
     ("tron_host_free", None, [c_void_p]),

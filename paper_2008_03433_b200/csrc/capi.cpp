@@ -215,6 +215,47 @@ int tron_parsed_copy(const tron_parsed* p, int64_t* row_offsets, int32_t* col_in
   return TRON_OK;
 }
 
+int tron_load_dense(const char* text, uint64_t len, uint64_t n, tron_parsed** out) {
+  if (!out || (!text && len > 0)) return fail(TRON_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<tron_parsed>();
+    h->p = tb::load_dense_buffer(text ? text : "", len, n);
+    *out = h.release();
+  });
+}
+
+int tron_load_dense_file(const char* path, uint64_t n, tron_parsed** out) {
+  if (!out || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<tron_parsed>();
+    h->p = tb::load_dense_file(path, n);
+    *out = h.release();
+  });
+}
+
+int tron_parsed_layout(const tron_parsed* p, int32_t* dense) {
+  if (!p) return fail(TRON_ERR_ARGUMENT, "null parse handle");
+  if (dense) *dense = p->p.dense ? 1 : 0;
+  return TRON_OK;
+}
+
+int tron_parsed_save_binary(const tron_parsed* p, const char* path) {
+  if (!p || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
+  return guarded([&] { tb::save_binary(p->p, path); });
+}
+
+int tron_load_binary(const char* path, tron_parsed** out) {
+  if (!out || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<tron_parsed>();
+    h->p = tb::load_binary(path);
+    *out = h.release();
+  });
+}
+
 void tron_parsed_free(tron_parsed* p) { delete p; }
 
 void* tron_host_alloc(uint64_t bytes) {

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <charconv>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -151,6 +152,119 @@ bool parse_line(const char* ptr, const char* end, Part& P) {
   return true;
 }
 
+// load_dense's per-line rules (io.cpp:171-192): a label, then exactly n values.
+bool parse_dense_line(const char* ptr, const char* end, uint64_t n, Part& P) {
+  if (ptr < end && end[-1] == '\r') --end;
+  ptr = skip_ws(ptr, end);
+  if (ptr == end) return true;  // blank line
+  double raw;
+  if (!parse_double(ptr, end, "label", &raw, &P.err)) return false;
+  double label;  // map_label, io.cpp:40-45
+  if (raw == 1.0)
+    label = 1.0;
+  else if (raw == -1.0 || raw == 0.0)
+    label = -1.0;
+  else {
+    P.err = {2, "label " + std::to_string(raw) + " not in {-1, 0, +1}", 0};
+    return false;
+  }
+  P.y.push_back(label);
+  uint64_t fields = 0;
+  for (;;) {
+    ptr = skip_ws(ptr, end);
+    if (ptr == end) break;
+    if (fields == n) {
+      P.err = {1, "more than " + std::to_string(n) + " values", 0};
+      return false;
+    }
+    double v;
+    if (!parse_double(ptr, end, "feature value", &v, &P.err)) return false;
+    P.vals.push_back(v);
+    ++fields;
+  }
+  if (fields != n) {
+    P.err = {1, "expected " + std::to_string(n) + " values, got " + std::to_string(fields), 0};
+    return false;
+  }
+  return true;
+}
+
+template <class LineFn>
+void parse_part_with(Part& P, LineFn line_fn) {
+  const char* p = P.begin;
+  while (p < P.end) {
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', P.end - p));
+    const char* le = nl ? nl : P.end;
+    ++P.lines;
+    if (!line_fn(p, le, P)) {
+      P.err.local_line = P.lines;
+      return;
+    }
+    p = nl ? nl + 1 : P.end;
+  }
+}
+
+// Line-boundary ranges of the text, ~4 MB or more each, one or more per worker.
+std::vector<Part> split_parts(const char* data, uint64_t len) {
+  const size_t want = std::max<size_t>(1, std::min<size_t>((size_t)host_workers() * 4,
+                                                           (size_t)(len >> 22) + 1));
+  std::vector<const char*> cut{data};
+  for (size_t k = 1; k < want; ++k) {
+    const char* p = data + len * k / want;
+    if (p <= cut.back()) continue;
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', data + len - p));
+    if (!nl) break;
+    if (nl + 1 > cut.back() && nl + 1 < data + len) cut.push_back(nl + 1);
+  }
+  cut.push_back(data + len);
+  std::vector<Part> parts(cut.size() - 1);
+  for (size_t k = 0; k + 1 < cut.size(); ++k) {
+    parts[k].begin = cut[k];
+    parts[k].end = cut[k + 1];
+  }
+  return parts;
+}
+
+// The first error in file order (the lines of earlier ranges are all valid).
+void raise_first_error(const std::vector<Part>& parts) {
+  uint64_t line_base = 0;
+  for (const Part& P : parts) {
+    if (P.err.kind) {
+      const uint64_t line = line_base + P.err.local_line;
+      throw ParseFailure(P.err.kind == 2 ? TRON_ERR_UNSUPPORTED_LABEL : TRON_ERR_PARSE,
+                         "line " + std::to_string(line) + ": " + P.err.what, line);
+    }
+    line_base += P.lines;
+  }
+}
+
+template <class Fn>
+auto with_mapped_file(const char* path, Fn fn) {
+  const int fd = ::open(path, O_RDONLY);
+  if (fd < 0) throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot open ") + path, 0);
+  struct stat st;
+  if (::fstat(fd, &st) != 0) {
+    ::close(fd);
+    throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot stat ") + path, 0);
+  }
+  const size_t len = (size_t)st.st_size;
+  if (len == 0) {
+    ::close(fd);
+    return fn("", (uint64_t)0);
+  }
+  void* map = ::mmap(nullptr, len, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd, 0);
+  ::close(fd);
+  if (map == MAP_FAILED) throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot map ") + path, 0);
+  try {
+    auto out = fn(static_cast<const char*>(map), (uint64_t)len);
+    ::munmap(map, len);
+    return out;
+  } catch (...) {
+    ::munmap(map, len);
+    throw;
+  }
+}
+
 void parse_part(Part& P) {
   const char* p = P.begin;
   while (p < P.end) {
@@ -168,37 +282,12 @@ void parse_part(Part& P) {
 }  // namespace
 
 ParsedProblem parse_libsvm_buffer(const char* data, uint64_t len, uint64_t n_override) {
-  // ranges at line boundaries, ~4 MB or more each
-  const size_t want = std::max<size_t>(1, std::min<size_t>((size_t)host_workers() * 4,
-                                                           (size_t)(len >> 22) + 1));
-  std::vector<const char*> cut{data};
-  for (size_t k = 1; k < want; ++k) {
-    const char* p = data + len * k / want;
-    if (p <= cut.back()) continue;
-    const char* nl = static_cast<const char*>(std::memchr(p, '\n', data + len - p));
-    if (!nl) break;
-    if (nl + 1 > cut.back() && nl + 1 < data + len) cut.push_back(nl + 1);
-  }
-  cut.push_back(data + len);
-  const size_t np = cut.size() - 1;
-  std::vector<Part> parts(np);
-  for (size_t k = 0; k < np; ++k) {
-    parts[k].begin = cut[k];
-    parts[k].end = cut[k + 1];
-  }
+  std::vector<Part> parts = split_parts(data, len);
+  const size_t np = parts.size();
   parallel_for(np, 1, [&](size_t b, size_t e) {
     for (size_t k = b; k < e; ++k) parse_part(parts[k]);
   });
-  // the first error in file order (lines of earlier ranges are all valid)
-  uint64_t line_base = 0;
-  for (const Part& P : parts) {
-    if (P.err.kind) {
-      const uint64_t line = line_base + P.err.local_line;
-      throw ParseFailure(P.err.kind == 2 ? TRON_ERR_UNSUPPORTED_LABEL : TRON_ERR_PARSE,
-                         "line " + std::to_string(line) + ": " + P.err.what, line);
-    }
-    line_base += P.lines;
-  }
+  raise_first_error(parts);
   ParsedProblem out;
   uint64_t rows = 0, nnz = 0, max_index = 0;
   std::vector<uint64_t> row0(np + 1, 0), nz0(np + 1, 0);
@@ -240,29 +329,111 @@ ParsedProblem parse_libsvm_buffer(const char* data, uint64_t len, uint64_t n_ove
 }
 
 ParsedProblem parse_libsvm_file(const char* path, uint64_t n_override) {
-  const int fd = ::open(path, O_RDONLY);
-  if (fd < 0) throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot open ") + path, 0);
-  struct stat st;
-  if (::fstat(fd, &st) != 0) {
-    ::close(fd);
-    throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot stat ") + path, 0);
+  return with_mapped_file(path, [&](const char* d, uint64_t len) {
+    return parse_libsvm_buffer(d, len, n_override);
+  });
+}
+
+ParsedProblem load_dense_buffer(const char* data, uint64_t len, uint64_t n) {
+  std::vector<Part> parts = split_parts(data, len);
+  const size_t np = parts.size();
+  parallel_for(np, 1, [&](size_t b, size_t e) {
+    for (size_t k = b; k < e; ++k)
+      parse_part_with(parts[k], [n](const char* a, const char* z, Part& P) {
+        return parse_dense_line(a, z, n, P);
+      });
+  });
+  raise_first_error(parts);
+  ParsedProblem out;
+  out.dense = true;
+  out.cols = n;
+  std::vector<uint64_t> row0(np + 1, 0);
+  for (size_t k = 0; k < np; ++k) row0[k + 1] = row0[k] + parts[k].y.size();
+  const uint64_t rows = row0[np];
+  out.row_offsets.clear();
+  out.values.resize(rows * n);
+  out.y.resize(rows);
+  parallel_for(np, 1, [&](size_t b, size_t e) {
+    for (size_t k = b; k < e; ++k) {
+      const Part& P = parts[k];
+      std::memcpy(out.values.data() + row0[k] * n, P.vals.data(), P.vals.size() * sizeof(double));
+      std::memcpy(out.y.data() + row0[k], P.y.data(), P.y.size() * sizeof(double));
+    }
+  });
+  return out;
+}
+
+ParsedProblem load_dense_file(const char* path, uint64_t n) {
+  return with_mapped_file(path, [&](const char* d, uint64_t len) { return load_dense_buffer(d, len, n); });
+}
+
+// ---- binary cache ---------------------------------------------------------
+namespace {
+constexpr char kMagic[8] = {'T', 'R', 'O', 'N', 'B', 'I', 'N', '1'};
+struct BinHeader {
+  char magic[8];
+  uint64_t layout;  // 0 CSR, 1 dense
+  uint64_t rows, cols, nnz;
+};
+}  // namespace
+
+void save_binary(const ParsedProblem& p, const char* path) {
+  BinHeader h;
+  std::memcpy(h.magic, kMagic, sizeof(kMagic));
+  h.layout = p.dense ? 1 : 0;
+  h.rows = p.y.size();
+  h.cols = p.cols;
+  h.nnz = p.values.size();
+  const std::string tmp = std::string(path) + ".tmp";
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot create ") + tmp, 0);
+  auto put = [&](const void* d, size_t bytes) {
+    if (bytes && std::fwrite(d, 1, bytes, f) != bytes) {
+      std::fclose(f);
+      std::remove(tmp.c_str());
+      throw ParseFailure(TRON_ERR_ARGUMENT, std::string("short write to ") + tmp, 0);
+    }
+  };
+  put(&h, sizeof(h));
+  if (!p.dense) {
+    put(p.row_offsets.data(), p.row_offsets.size() * sizeof(int64_t));
+    put(p.col_indices.data(), p.col_indices.size() * sizeof(int32_t));
   }
-  const size_t len = (size_t)st.st_size;
-  if (len == 0) {
-    ::close(fd);
-    return parse_libsvm_buffer("", 0, n_override);
-  }
-  void* map = ::mmap(nullptr, len, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd, 0);
-  ::close(fd);
-  if (map == MAP_FAILED) throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot map ") + path, 0);
-  try {
-    ParsedProblem p = parse_libsvm_buffer(static_cast<const char*>(map), len, n_override);
-    ::munmap(map, len);
+  put(p.values.data(), p.values.size() * sizeof(double));
+  put(p.y.data(), p.y.size() * sizeof(double));
+  if (std::fclose(f) != 0 || std::rename(tmp.c_str(), path) != 0)
+    throw ParseFailure(TRON_ERR_ARGUMENT, std::string("cannot write ") + path, 0);
+}
+
+ParsedProblem load_binary(const char* path) {
+  return with_mapped_file(path, [&](const char* d, uint64_t len) {
+    BinHeader h;
+    if (len < sizeof(h)) throw ParseFailure(TRON_ERR_PARSE, std::string(path) + ": not a TRONBIN1 file", 0);
+    std::memcpy(&h, d, sizeof(h));
+    if (std::memcmp(h.magic, kMagic, sizeof(kMagic)) != 0 || h.layout > 1)
+      throw ParseFailure(TRON_ERR_PARSE, std::string(path) + ": not a TRONBIN1 file", 0);
+    ParsedProblem p;
+    p.dense = h.layout == 1;
+    p.cols = h.cols;
+    const uint64_t want = sizeof(h) + (p.dense ? 0 : (h.rows + 1) * 8 + h.nnz * 4) + h.nnz * 8 + h.rows * 8;
+    if (len != want || (p.dense && h.nnz != h.rows * h.cols))
+      throw ParseFailure(TRON_ERR_PARSE, std::string(path) + ": truncated or inconsistent TRONBIN1 file", 0);
+    const char* q = d + sizeof(h);
+    auto take = [&](auto& v, uint64_t count) {
+      v.resize(count);
+      std::memcpy(v.data(), q, count * sizeof(v[0]));
+      q += count * sizeof(v[0]);
+    };
+    if (!p.dense) {
+      take(p.row_offsets, h.rows + 1);
+      take(p.col_indices, h.nnz);
+    } else {
+      p.row_offsets.clear();
+    }
+    take(p.values, h.nnz);
+    take(p.y, h.rows);
     return p;
-  } catch (...) {
-    ::munmap(map, len);
-    throw;
-  }
+  });
 }
 
 }  // namespace tb

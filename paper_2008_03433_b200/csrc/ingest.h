@@ -11,6 +11,7 @@
 namespace tb {
 
 struct ParsedProblem {
+  bool dense = false;  // dense: values row-major rows x cols, no offsets / indices
   std::vector<int64_t> row_offsets{0};
   std::vector<int32_t> col_indices;
   std::vector<double> values, y;
@@ -27,5 +28,13 @@ struct ParseFailure : std::runtime_error {
 
 ParsedProblem parse_libsvm_buffer(const char* data, uint64_t len, uint64_t n_override);
 ParsedProblem parse_libsvm_file(const char* path, uint64_t n_override);
+// load_dense (io.cpp:164-197): "label v1 ... vn" per line, exactly n values.
+ParsedProblem load_dense_buffer(const char* data, uint64_t len, uint64_t n);
+ParsedProblem load_dense_file(const char* path, uint64_t n);
+// Binary cache of a parsed problem (little-endian; "TRONBIN1" header, the
+// layout, rows, cols, nnz, then the arrays): written once, read back at
+// storage speed instead of re-parsing text.
+void save_binary(const ParsedProblem& p, const char* path);
+ParsedProblem load_binary(const char* path);
 
 }  // namespace tb

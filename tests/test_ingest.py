@@ -108,3 +108,93 @@ def test_parse_file_matches_bytes(tmp_path, big_text):
     f.write_bytes(big_text)
     a, b = io.parse_libsvm(str(f)), io.parse_libsvm(big_text)
     assert np.array_equal(a.X.values, b.X.values) and np.array_equal(a.X.row_offsets, b.X.row_offsets)
+
+
+# ---- load_dense (io.cpp:164-197) ---------------------------------------------
+
+def dense_both(ref, text, n):
+    try:
+        p = io.load_dense(text, n)
+        mine = ("ok", p)
+    except io.UnsupportedLabelError as e:
+        mine = ("label", (str(e), e.line))
+    except io.ParseError as e:
+        mine = ("parse", (str(e), e.line))
+    theirs = ref.load_dense(text, n)
+    assert mine[0] == theirs[0], (mine, theirs)
+    if mine[0] != "ok":
+        assert mine[1] == theirs[1]
+        return mine
+    vals, y = theirs[1]
+    p = mine[1]
+    assert p.X.layout == "dense" and p.X.cols == n and p.X.rows == y.size
+    assert np.array_equal(p.X.values.view(np.uint64), vals.view(np.uint64))
+    assert np.array_equal(p.y, y)
+    return mine
+
+
+@pytest.mark.parametrize("text,n", [
+    (b"+1 1 2\n-1 3 4\n", 2),
+    (b"0 1e-3 -2.5\r\n\n  \t\n1\t7 8\n", 2),      # CRLF, blank lines, tabs, label 0
+    (b"1 1.7976931348623157e308 -0.0\n", 2),      # extremes, no final newline below
+    (b"-1 0 0 0", 3),
+    (b"", 4),                                      # empty input: 0 x 4
+    (b"1 1 2 3\n", 2),                             # more than n values
+    (b"1 1\n", 2),                                 # fewer
+    (b"1 1 2\n-1 3 x\n", 2),                       # bad value, line 2
+    (b"1 1 2\n2 3 4\n", 2),                        # unsupported label
+    (b"1 1e999 2\n", 2),                           # out of range
+    (b"1x 1 2\n", 2),                              # label glued to garbage
+    (b"1 +3 4\n", 2),                              # '+' on a value
+])
+def test_load_dense_matches_reference(ref, text, n):
+    dense_both(ref, text, n)
+
+
+def test_load_dense_multi_range_and_late_error(ref):
+    p = synth.synth_dense(3, 60000, 12)
+    rows = p.X.values.reshape(-1, 12)
+    lines = [(b"+1 " if y > 0 else b"-1 ") + b" ".join(repr(float(v)).encode() for v in r)
+             for r, y in zip(rows, p.y)]
+    text = b"\n".join(lines) + b"\n"
+    kind, q = dense_both(ref, text, 12)
+    assert np.array_equal(q.X.values, p.X.values) and np.array_equal(q.y, p.y)
+    bad = b"\n".join(lines[:50000] + [lines[50000] + b" 9"] + lines[50001:]) + b"\n"
+    kind, (msg, line) = dense_both(ref, bad, 12)
+    assert kind == "parse" and line == 50001
+
+
+# ---- binary cache --------------------------------------------------------------
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_binary_cache_roundtrip(tmp_path, dense):
+    p = synth.synth_dense(2, 3000, 9) if dense else synth.synth_sparse(4, 3000, 7000, 15)
+    path = tmp_path / "x.tronbin"
+    io.save_binary(p, path)
+    q = io.load_binary(path)
+    assert q.X.layout == p.X.layout and (q.X.rows, q.X.cols) == (p.X.rows, p.X.cols)
+    assert np.array_equal(q.X.values.view(np.uint64), p.X.values.view(np.uint64))
+    assert np.array_equal(q.y, p.y)
+    if not dense:
+        assert np.array_equal(q.X.row_offsets, p.X.row_offsets)
+        assert np.array_equal(q.X.col_indices, p.X.col_indices)
+    (tmp_path / "bad.tronbin").write_bytes(b"TRONBIN1" + b"\0" * 10)
+    with pytest.raises(io.ParseError):
+        io.load_binary(tmp_path / "bad.tronbin")
+
+
+def test_load_cached_writes_then_reuses(tmp_path, big_text):
+    src = tmp_path / "data.svm"
+    src.write_bytes(big_text)
+    a = io.load_cached(src)
+    cache = tmp_path / "data.svm.tronbin"
+    assert cache.exists()
+    b = io.load_cached(src)  # from the cache
+    for p in (a, b):
+        q = io.parse_libsvm(big_text)
+        assert np.array_equal(p.X.values, q.X.values) and np.array_equal(p.X.col_indices, q.X.col_indices)
+        assert np.array_equal(p.X.row_offsets, q.X.row_offsets) and p.X.cols == q.X.cols
+    d = tmp_path / "d.txt"
+    d.write_bytes(b"1 1 2\n-1 3 4\n")
+    p = io.load_cached(d, n=2, dense=True)
+    assert p.X.layout == "dense" and np.array_equal(io.load_cached(d, n=2, dense=True).X.values, [1, 2, 3, 4])
