@@ -114,6 +114,18 @@ typedef struct {
    * host memory and the CG loop runs host-driven.  NULL: NCCL. */
   void (*host_allreduce)(void *user, double *buf, uint64_t count);
   void *host_allreduce_user;
+  /* Dense problems larger than device memory (the
+   * reference's mix-backend remedy, backend.cpp:256-261): X stays in the
+   * caller's host array -- which must then outlive the context, as the
+   * reference's evaluators hold the Problem by reference (backend.hpp:123) --
+   * and every pass streams it over PCIe in blocks of stream_block_rows rows
+   * (0: about 256 MB per block), double-buffered against the kernels; the
+   * array is page-locked in place (cudaHostRegister) while the context lives.
+   * out_of_core: 0 = when X does not fit in free device memory, 1 = always,
+   * -1 = never.  Indirect L2-SVM traversal (Gathered raises
+   * TRON_ERR_STRATEGY), one GPU, host-driven CG loop. */
+  int32_t out_of_core;
+  uint64_t stream_block_rows;
 } tron_gpu_options;
 
 typedef struct tron_gpu_ctx tron_gpu_ctx;

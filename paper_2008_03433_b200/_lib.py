@@ -58,7 +58,8 @@ class tron_gpu_options(ctypes.Structure):
                 ("gathered_budget_bytes", c_uint64), ("rank", c_int32), ("world", c_int32),
                 ("nccl_unique_id", c_void_p), ("row_begin", c_uint64), ("global_rows", c_uint64),
                 ("reference_order", c_int32), ("host_allreduce", c_void_p),
-                ("host_allreduce_user", c_void_p)]
+                ("host_allreduce_user", c_void_p), ("out_of_core", c_int32),
+                ("stream_block_rows", c_uint64)]
 
 
 # void (*)(void* user, double* buf, uint64_t count): a host allreduce (sum, in place)

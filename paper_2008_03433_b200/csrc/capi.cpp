@@ -171,12 +171,15 @@ void tron_gpu_default_options(tron_gpu_options* o) {
   o->reference_order = 0;
   o->host_allreduce = nullptr;
   o->host_allreduce_user = nullptr;
+  o->out_of_core = 0;
+  o->stream_block_rows = 0;
 }
 
 const char* tron_gpu_last_error(void) { return g_last_error.c_str(); }
 uint64_t tron_gpu_last_error_line(void) { return g_last_error_line; }
 
 int tron_parse_libsvm(const char* text, uint64_t len, uint64_t n_override, tron_parsed** out) {
+  tb::NvtxRange nvtx_range("tron_parse_libsvm");
   if (!out || (!text && len > 0)) return fail(TRON_ERR_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
@@ -187,6 +190,7 @@ int tron_parse_libsvm(const char* text, uint64_t len, uint64_t n_override, tron_
 }
 
 int tron_parse_libsvm_file(const char* path, uint64_t n_override, tron_parsed** out) {
+  tb::NvtxRange nvtx_range("tron_parse_libsvm_file");
   if (!out || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
@@ -216,6 +220,7 @@ int tron_parsed_copy(const tron_parsed* p, int64_t* row_offsets, int32_t* col_in
 }
 
 int tron_load_dense(const char* text, uint64_t len, uint64_t n, tron_parsed** out) {
+  tb::NvtxRange nvtx_range("tron_load_dense");
   if (!out || (!text && len > 0)) return fail(TRON_ERR_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
@@ -226,6 +231,7 @@ int tron_load_dense(const char* text, uint64_t len, uint64_t n, tron_parsed** ou
 }
 
 int tron_load_dense_file(const char* path, uint64_t n, tron_parsed** out) {
+  tb::NvtxRange nvtx_range("tron_load_dense_file");
   if (!out || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
@@ -247,6 +253,7 @@ int tron_parsed_save_binary(const tron_parsed* p, const char* path) {
 }
 
 int tron_load_binary(const char* path, tron_parsed** out) {
+  tb::NvtxRange nvtx_range("tron_load_binary");
   if (!out || !path) return fail(TRON_ERR_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
@@ -284,6 +291,7 @@ int tron_gpu_device_count(int* count) {
 int tron_gpu_create_csr(int loss, uint64_t l, uint64_t n, const int64_t* row_offsets,
                         const int32_t* col_indices, const double* values, const double* y,
                         double C, const tron_gpu_options* opt, tron_gpu_ctx** out) {
+  tb::NvtxRange nvtx_range("tron_gpu_create_csr");
   if (!out) return fail(TRON_ERR_ARGUMENT, "null output handle");
   *out = nullptr;
   return guarded([&] {
@@ -300,6 +308,7 @@ int tron_gpu_create_csr(int loss, uint64_t l, uint64_t n, const int64_t* row_off
 int tron_gpu_create_dense(int loss, uint64_t l, uint64_t n, const double* row_major,
                           const double* y, double C, const tron_gpu_options* opt,
                           tron_gpu_ctx** out) {
+  tb::NvtxRange nvtx_range("tron_gpu_create_dense");
   if (!out) return fail(TRON_ERR_ARGUMENT, "null output handle");
   *out = nullptr;
   return guarded([&] {
@@ -329,11 +338,13 @@ int tron_gpu_dimension(tron_gpu_ctx* ctx, uint64_t* n) {
 }
 
 int tron_gpu_eval_candidate(tron_gpu_ctx* ctx, const double* w, double* f) {
+  tb::NvtxRange nvtx_range("tron_gpu_eval_candidate");
   NEED_CTX(ctx);
   return guarded([&] { *f = ctx->engine->eval_candidate_host(w); });
 }
 
 int tron_gpu_commit(tron_gpu_ctx* ctx, double* gnorm) {
+  tb::NvtxRange nvtx_range("tron_gpu_commit");
   NEED_CTX(ctx);
   return guarded([&] { ctx->engine->commit(gnorm); });
 }
@@ -347,11 +358,13 @@ int tron_gpu_gradient(tron_gpu_ctx* ctx, double* g) {
 }
 
 int tron_gpu_hessian_vec(tron_gpu_ctx* ctx, const double* v, double* out) {
+  tb::NvtxRange nvtx_range("tron_gpu_hessian_vec");
   NEED_CTX(ctx);
   return guarded([&] { ctx->engine->hessian_vec_host(v, out); });
 }
 
 int tron_gpu_quadratic_model(tron_gpu_ctx* ctx, const double* d, double* q) {
+  tb::NvtxRange nvtx_range("tron_gpu_quadratic_model");
   NEED_CTX(ctx);
   return guarded([&] {
     const double v = ctx->engine->quadratic_model_host(d);
@@ -360,6 +373,7 @@ int tron_gpu_quadratic_model(tron_gpu_ctx* ctx, const double* d, double* q) {
 }
 
 int tron_gpu_precond_diagonal(tron_gpu_ctx* ctx, double* m) {
+  tb::NvtxRange nvtx_range("tron_gpu_precond_diagonal");
   NEED_CTX(ctx);
   return guarded([&] {
     ctx->engine->precond_host(m);
@@ -380,6 +394,7 @@ int tron_gpu_state_svm(tron_gpu_ctx* ctx, int which, double* z, int64_t* active,
 
 int tron_gpu_truncated_cg(tron_gpu_ctx* ctx, double delta, const tron_config* cfg, double* d,
                           int32_t* exit_kind, uint64_t* iters, double* model_value) {
+  tb::NvtxRange nvtx_range("tron_gpu_truncated_cg");
   NEED_CTX(ctx);
   return guarded([&] {
     tron_config c;
@@ -391,6 +406,7 @@ int tron_gpu_truncated_cg(tron_gpu_ctx* ctx, double delta, const tron_config* cf
 
 int tron_gpu_solve(tron_gpu_ctx* ctx, const tron_config* cfg, const double* w0, double* w_out,
                    tron_solve_info* info, tron_iteration* trace, uint64_t trace_cap) {
+  tb::NvtxRange nvtx_range("tron_gpu_solve");
   NEED_CTX(ctx);
   if (!info) return fail(TRON_ERR_ARGUMENT, "null info");
   tron_config c;
@@ -432,6 +448,7 @@ int tron_gpu_solve(tron_gpu_ctx* ctx, const tron_config* cfg, const double* w0, 
 }
 
 int tron_gpu_predict(tron_gpu_ctx* ctx, const double* w, double* labels, uint64_t* correct) {
+  tb::NvtxRange nvtx_range("tron_gpu_predict");
   NEED_CTX(ctx);
   if (!w && ctx->engine->dimension() > 0) return fail(TRON_ERR_ARGUMENT, "null weights");
   return guarded([&] {

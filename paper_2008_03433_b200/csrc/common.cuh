@@ -48,6 +48,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh, bool broadcast
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_sum(v);
   if (lane == 0) sh[wid] = v;
+  __syncwarp();  // reconverge the warp before the block barrier
   __syncthreads();
   if (wid == 0) {
     double t = lane < NW ? sh[lane] : 0.0;

@@ -246,6 +246,7 @@ struct PhaseTrace {
     if (on) std::fprintf(stderr, "[tron_b200] %s\n", what);
   }
   void mark(const char* phase) {
+    nvtxMarkA(phase);
     if (!on) return;
     if (s) cudaStreamSynchronize(s);
     const auto now = std::chrono::steady_clock::now();
@@ -306,13 +307,20 @@ void Engine::common_alloc() {
       S.mask.alloc(ll);
       if (dense_) cuda_check(cudaMemsetAsync(S.mask.p, 0, S.mask.bytes(), s_), "memset");
     }
-    if (dense_) S.gparts.alloc((size_t)dense_grid(l_, n_) * nn);
+    if (dense_) {
+      S.gparts.alloc((size_t)dense_nparts() * nn);
+      // streamed blocks: the slots a short last block leaves unused stay zero
+      if (ooc_) cuda_check(cudaMemsetAsync(S.gparts.p, 0, S.gparts.bytes(), s_), "memset");
+    }
   }
   for (DevBuf<double>* b : {&g_, &gspec_, &M_, &d_, &r0_, &r1_, &p_, &hp_, &vtmp_, &otmp_})
     b->alloc(nn);
   if (comm_.active()) raw_.alloc(nn);
   if (!dense_) a_.alloc(ll);
-  if (dense_) parts_.alloc((size_t)dense_grid(l_, n_) * nn);
+  if (dense_) {
+    parts_.alloc((size_t)dense_nparts() * nn);
+    if (ooc_) cuda_check(cudaMemsetAsync(parts_.p, 0, parts_.bytes(), s_), "memset");
+  }
   small_engine_ = dense_ || n_ <= kSmallCgMaxN;
   coop_parts_.alloc((size_t)8 * cg_coop_grid());
   // mid-size n: one 8-CTA cluster kernel per CG iteration; larger n (or
@@ -327,7 +335,8 @@ void Engine::common_alloc() {
   // rank's CG state is identical, so every rank runs the same number of
   // allreduces); TRON_B200_NCCL_GRAPH=0 selects the host-driven CG loop.
   const char* cg = std::getenv("TRON_B200_NCCL_GRAPH");
-  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !comm_.host() && !(ng && ng[0] == '1');
+  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !comm_.host() && !ooc_ &&
+                !(ng && ng[0] == '1');
 }
 
 // H2D of a buffer on a private stream ordered after everything issued on
@@ -537,12 +546,49 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->row_begin_ = opt.row_begin;
   e->comm_.init(opt);
   e->ld_ = dense_ld((int64_t)l);
+  {  // out-of-core streaming when X does not fit (or when asked to)
+    // (no usable device: decided as in-memory; creation then reports the
+    // device error after the input checks, below)
+    size_t free_b = 0, total_b = 0;
+    const bool have = cudaSetDevice(opt.device) == cudaSuccess &&
+                      cudaMemGetInfo(&free_b, &total_b) == cudaSuccess;
+    if (!have) cudaGetLastError();
+    const double xbytes = 8.0 * (double)e->ld_ * (double)n;
+    const double state = (double)e->ld_ * (loss == TRON_LOSS_LOGISTIC ? 56.0 : 26.0);
+    const bool want = opt.out_of_core > 0 ||
+                      (opt.out_of_core == 0 && have &&
+                       xbytes + state + double(2ull << 30) > (double)free_b);
+    if (want && l > 0 && n > 0) {
+      if (opt.world > 1) raise(TRON_ERR_ARGUMENT, "out-of-core streaming runs on one GPU");
+      if (opt.reference_order) raise(TRON_ERR_ARGUMENT, "reference_order needs X in device memory");
+      if (loss == TRON_LOSS_L2SVM && opt.svm_strategy == TRON_SVM_GATHERED)
+        raise(TRON_ERR_STRATEGY,
+              "the gathered submatrix needs X in device memory; out-of-core streaming answers "
+              "Hessian products by index-indirect traversal (the mix backend's route)");
+      e->ooc_ = true;
+      e->svm_strategy_ = TRON_SVM_INDIRECT;
+      int64_t b = opt.stream_block_rows > 0
+                      ? (int64_t)opt.stream_block_rows
+                      : std::max<int64_t>(kDenseTile, (int64_t{256} << 20) / (int64_t)(8 * n));
+      b = std::min<int64_t>(dense_ld(b), e->ld_);
+      e->blk_ = b;
+      e->nblk_ = ((int64_t)l + b - 1) / b;
+      e->Xhost_ = row_major;
+    }
+  }
   // labels are checked on the worker pool while the matrix streams in
   try {
     e->common_alloc();
     cudaStream_t s = e->s_;
     tr.s = s;
     tr.mark("context + state alloc");
+    if (e->ooc_) {
+      e->y_.alloc((size_t)std::max<int64_t>(e->ld_, 1));
+      cuda_check(cudaMemsetAsync(e->y_.p, 0, e->y_.bytes(), s), "memset");
+      upload(e->y_.p, y, l * sizeof(double), s);
+      e->ooc_setup();
+      tr.mark("out-of-core windows + host registration");
+    } else {
     e->Xc_.alloc((size_t)std::max<int64_t>(e->ld_, 1) * (n > 0 ? n : 1));
     e->y_.alloc((size_t)std::max<int64_t>(e->ld_, 1));
     cuda_check(cudaMemsetAsync(e->y_.p, 0, e->y_.bytes(), s), "memset");
@@ -576,6 +622,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       cudaEventDestroy(ev[1]);
     }
     tr.mark("matrix alloc + H2D + transpose");
+    }
     e->screen(nullptr, nullptr, 0, (int64_t)n, [&](uint64_t, uint64_t bad_label) {
       if (bad_label != UINT64_MAX) validate_labels_C(l, y, C);  // raises the exact error
     });
@@ -585,7 +632,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     if (err.status == TRON_ERR_CUDA || err.status == TRON_ERR_OOM) validate_labels_C(l, y, C);
     throw;
   }
-  if (dense_make_map(&e->xmap_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n) != 0)
+  if (!e->ooc_ && dense_make_map(&e->xmap_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n) != 0)
     raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for the dense matrix");
   if (loss == TRON_LOSS_L2SVM) {
     e->idx_.alloc(l > 0 ? l : 1);
@@ -613,6 +660,13 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
 
 Engine::~Engine() {
   if (s_) cudaStreamSynchronize(s_);
+  if (cs_) {
+    cudaStreamSynchronize(cs_);
+    cudaStreamDestroy(cs_);
+  }
+  for (cudaEvent_t ev : {ev_copied_[0], ev_copied_[1], ev_free_[0], ev_free_[1]})
+    if (ev) cudaEventDestroy(ev);
+  if (host_registered_) cudaHostUnregister(const_cast<double*>(Xhost_));
   for (int a = 0; a < 2; ++a)
     for (int b = 0; b < 2; ++b) {
       if (graph_exec_[a][b]) cudaGraphExecDestroy(graph_exec_[a][b]);
@@ -673,11 +727,88 @@ void Engine::read_cg(CgState* out) {
 }
 
 // ----------------------------------------------------------------------------
+// out-of-core dense streaming
+// ----------------------------------------------------------------------------
+int Engine::dense_nparts() const {
+  return ooc_ ? (int)(nblk_ * dense_grid(blk_, n_)) : dense_grid(l_, n_);
+}
+
+// Two device windows (column-major, ld = blk_) and two row-major staging
+// buffers; the caller's array is page-locked in place so every block is one
+// DMA (cudaHostRegister; if that fails the pageable staging path is used).
+void Engine::ooc_setup() {
+  for (int k = 0; k < 2; ++k) {
+    win_[k].alloc((size_t)blk_ * n_);
+    stage_[k].alloc((size_t)blk_ * n_);
+    cuda_check(cudaMemsetAsync(win_[k].p, 0, win_[k].bytes(), s_), "memset");
+    if (dense_make_map(&winmap_[k], win_[k].p, blk_, blk_, n_) != 0)
+      raise(TRON_ERR_CUDA, "cuTensorMapEncodeTiled failed for a streaming window");
+    cuda_check(cudaEventCreateWithFlags(&ev_copied_[k], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_free_[k], cudaEventDisableTiming), "event");
+  }
+  cuda_check(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking), "stream");
+  blk_red_.alloc((size_t)2 * nblk_);
+  const char* pin = std::getenv("TRON_B200_OOC_PIN");  // 0: staged copies (tests the pageable path)
+  if (!is_pinned(Xhost_) && !(pin && pin[0] == '0')) {
+    const cudaError_t e = cudaHostRegister(const_cast<double*>(Xhost_), (size_t)l_ * n_ * sizeof(double),
+                                           cudaHostRegisterReadOnly);
+    if (e == cudaSuccess)
+      host_registered_ = true;
+    else
+      cudaGetLastError();  // staged copies instead
+  }
+}
+
+// Runs on_block(b, row0, rows, window, map) for every block, the H2D of block
+// b+1 on cs_ overlapping the kernels of block b on s_.  A window is reused
+// only after the kernels that read it (ev_free_), and the rows of a short
+// last block past its end are zeroed (the tiled passes read whole tiles).
+template <class F>
+void Engine::ooc_pass(F&& on_block) {
+  for (int64_t b = 0; b < nblk_; ++b) {
+    const int k = (int)(b & 1);
+    const int64_t r0 = b * blk_;
+    const int64_t rows = std::min<int64_t>(blk_, l_ - r0);
+    if (ev_free_used_[k]) cuda_check(cudaStreamWaitEvent(cs_, ev_free_[k], 0), "wait");
+    upload(stage_[k].p, Xhost_ + (size_t)r0 * n_, (size_t)rows * n_ * sizeof(double), cs_);
+    cuda_check(cudaEventRecord(ev_copied_[k], cs_), "record");
+    cuda_check(cudaStreamWaitEvent(s_, ev_copied_[k], 0), "wait");
+    const int64_t rows_pad = dense_ld(rows);
+    if (rows_pad > rows)
+      cuda_check(cudaMemset2DAsync(win_[k].p + rows, blk_ * sizeof(double), 0,
+                                   (rows_pad - rows) * sizeof(double), n_, s_),
+                 "memset");
+    dense_transpose_chunk(stage_[k].p, rows, n_, win_[k].p, blk_, 0, s_);
+    on_block(b, r0, rows, (const double*)win_[k].p, (const CUtensorMap&)winmap_[k]);
+    count_launch(2);
+    cuda_check(cudaEventRecord(ev_free_[k], s_), "record");
+    ev_free_used_[k] = true;
+  }
+}
+
+namespace {
+template <class T>
+T* off(T* p, int64_t r0) {
+  return p ? p + r0 : nullptr;
+}
+}  // namespace
+
+// ----------------------------------------------------------------------------
 // fun: fused margin pass (loss.cpp:35-58 / :94-122)
 // ----------------------------------------------------------------------------
 void Engine::forward(Slot& S) {
   const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
-  if (dense_) {
+  if (dense_ && ooc_) {
+    const int64_t G = dense_grid(blk_, n_);
+    ooc_pass([&](int64_t b, int64_t r0, int64_t rows, const double* win, const CUtensorMap& map) {
+      dense_forward(rows, n_, blk_, win, map, loss, S.w.p, y_.p + r0, C_, S.z.p + r0, off(S.zhat.p, r0),
+                    off(S.dvec.p, r0), off(S.mask.p, r0), S.gparts.p + b * G * n_, obj_d_, sc_, s_);
+      cuda_check(cudaMemcpyAsync(blk_red_.p + 2 * b, obj_d_->red, 2 * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s_),
+                 "D2D");
+    });
+    obj_combine_blocks(obj_d_, blk_red_.p, nblk_, C_, s_);
+  } else if (dense_) {
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
                   S.gparts.p, obj_d_, sc_, s_);
     if (ro_) {  // I of this slot, then f in the reference's order (loss.cpp:114-119)
@@ -765,10 +896,16 @@ void Engine::dense_vector(int kind, const double* v, const EpiView& epi, double*
   const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
   const bool gathered = kind == DA_HV && gathered_valid_;
   const double* parts = parts_.p;
-  int nparts = dense_grid(gathered ? nI_ : l_, n_);
+  int nparts = gathered ? dense_grid(nI_, n_) : dense_nparts();
   if (kind < 0) {
     parts = S.gparts.p;
-    nparts = dense_grid(l_, n_);
+    nparts = dense_nparts();
+  } else if (ooc_) {
+    const int64_t G = dense_grid(blk_, n_);
+    ooc_pass([&](int64_t b, int64_t r0, int64_t rows, const double* win, const CUtensorMap& map) {
+      dense_accum(kind, rows, n_, blk_, win, map, loss, v, off(S.dvec.p, r0), off(S.mask.p, r0),
+                  parts_.p + b * G * n_, s_);
+    });
   } else if (gathered) {
     dense_accum(DA_HV, nI_, n_, ldg_, Xg_.p, gmap_, kLossSvm, v, nullptr, nullptr, parts_.p, s_);
     count_launch(1);
@@ -1165,7 +1302,7 @@ void Engine::capture_cg_body(int k, const CgVectors& v, Cond cond) {
     ro_cg_step(v, st_d_, cond, s_);
     count_launch(1);
   } else if (small_engine_) {
-    if (dense_ && !comm_.active()) {  // sharded: hv_kernels allreduces the partials
+    if (dense_ && !comm_.active() && !ooc_) {  // sharded / streamed: through hv_kernels
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
       const double scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
@@ -1439,6 +1576,7 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
     return;
   }
   if (device_loop) {
+    NvtxRange nvtx_range("tron.solve.device_loop");
     int status = TRON_OK;
     std::string what;
     solve_device_loop(cfg, f, info, trace, cap, &status, &what);
@@ -1735,13 +1873,26 @@ uint64_t Engine::predict(const double* w, double* labels) {
   DevBuf<unsigned long long> correct;
   correct.alloc(1);
   if (n_ > 0) upload(vtmp_.p, w, n_ * sizeof(double), s_);
-  if (dense_)
-    predict_dense(l_, n_, ld_, Xc_.p, vtmp_.p, y_.p, lab.p, correct.p, s_);
-  else
-    predict_csr(X_, vtmp_.p, y_.p, lab.p, correct.p, s_);
-  count_launch(1);
   unsigned long long c = 0;
-  cuda_check(cudaMemcpyAsync(&c, correct.p, sizeof(c), cudaMemcpyDeviceToHost, s_), "D2H");
+  if (dense_ && ooc_) {
+    DevBuf<unsigned long long> per;
+    per.alloc((size_t)std::max<int64_t>(nblk_, 1));
+    ooc_pass([&](int64_t b, int64_t r0, int64_t rows, const double* win, const CUtensorMap&) {
+      predict_dense(rows, n_, blk_, win, vtmp_.p, y_.p + r0, lab.p + r0, per.p + b, s_);
+    });
+    std::vector<unsigned long long> h((size_t)nblk_);
+    if (nblk_) cuda_check(cudaMemcpyAsync(h.data(), per.p, nblk_ * sizeof(unsigned long long),
+                                          cudaMemcpyDeviceToHost, s_), "D2H");
+    synchronize();
+    for (auto x : h) c += x;
+  } else {
+    if (dense_)
+      predict_dense(l_, n_, ld_, Xc_.p, vtmp_.p, y_.p, lab.p, correct.p, s_);
+    else
+      predict_csr(X_, vtmp_.p, y_.p, lab.p, correct.p, s_);
+    count_launch(1);
+    cuda_check(cudaMemcpyAsync(&c, correct.p, sizeof(c), cudaMemcpyDeviceToHost, s_), "D2H");
+  }
   if (labels && l_ > 0) download(labels, lab.p, l_ * sizeof(double), s_);
   synchronize();
   cuda_check(cudaGetLastError(), "predict");
@@ -1789,6 +1940,9 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
     epi.base = vtmp_.p;
     epi.scale = C_;
     out->transposed_ms = time_it([&] { csc_spmv(Xt_, plan_, u, false, epi, otmp_.p, s_); });
+    out->forward_ms = time_it([&] { forward(slot_[cand_]); });
+  } else if (ooc_) {  // every pass streams X: the Hv is the streamed accumulation
+    out->transposed_ms = out->hv_ms;
     out->forward_ms = time_it([&] { forward(slot_[cand_]); });
   } else {
     const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <memory>
@@ -16,6 +17,15 @@
 #include "tron_b200.h"
 
 namespace tb {
+
+// NVTX range over a scope (header-only NVTX 3: a no-op unless a profiler such
+// as Nsight Systems attaches): every C-ABI entry and the solve's phases.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct StatusError : std::runtime_error {
   int status;
@@ -288,6 +298,23 @@ class Engine {
   bool hv_dot_available() const;
   DevBuf<double> coop_parts_;  // CTA partials of the cooperative CG step
   bool use_graphs_ = true;
+  // out-of-core dense layout: X stays in the caller's
+  // host array (page-locked in place) and every pass streams it in blocks of
+  // blk_ rows through two device windows, copy (cs_) overlapping compute (s_)
+  bool ooc_ = false;
+  const double* Xhost_ = nullptr;
+  bool host_registered_ = false;
+  int64_t blk_ = 0, nblk_ = 0;
+  DevBuf<double> win_[2], stage_[2];
+  alignas(64) CUtensorMap winmap_[2] = {};
+  cudaStream_t cs_ = nullptr;
+  cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_free_[2] = {nullptr, nullptr};
+  bool ev_free_used_[2] = {false, false};
+  DevBuf<double> blk_red_;
+  template <class F>
+  void ooc_pass(F&& on_block);
+  void ooc_setup();
+  int dense_nparts() const;
   // device-resident outer loop
   cudaGraphExec_t solve_exec_[2] = {nullptr, nullptr};
   cudaGraph_t solve_graph_[2] = {nullptr, nullptr};

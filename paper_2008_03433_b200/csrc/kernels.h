@@ -179,6 +179,9 @@ void vec_dot2(int64_t n, const double* a, const double* b, const double* c, cons
 // out = base + scale*raw  (after an allreduce of raw partials; raw == nullptr => 0)
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
 void l2_read_flush(const double* buf, int64_t n, cudaStream_t s);
+// Streamed (out-of-core) margin pass: the per-block loss sums and |I|
+// (red[2b], red[2b+1]) into obj->f = 0.5 ww + C sum, nact, red[0..1]; fixed order.
+void obj_combine_blocks(ObjScalars* obj, const double* red, int64_t nblk, double C, cudaStream_t s);
 
 // CG initialisation for the mid/large-n engines (d = 0, r = -g, p = M^-1 r).
 struct CgVectors {

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kRoThreads, 1)
     mbar_fence_init();
   }
   for (int j = tid; j < 64; j += kRoThreads) s_v[j] = (a.mode == RO_HV && j < n) ? a.v[j] : 0.0;
+  __syncwarp();
   __syncthreads();
 
   if (wid == 0) {

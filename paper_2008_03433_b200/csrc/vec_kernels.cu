@@ -741,6 +741,23 @@ void cg_coop_step(const CgVectors& v, CgState* st, double* parts, Cond cond, cud
   if (e != cudaSuccess) launch_failed(e, "cg_coop_step (cooperative launch)");
 }
 
+__global__ void obj_combine_kernel(ObjScalars* obj, const double* red, long long nblk, double C) {
+  double tot = 0.0, cnt = 0.0;
+  for (long long b = 0; b < nblk; ++b) {
+    tot += red[2 * b];
+    cnt += red[2 * b + 1];
+  }
+  obj->f = 0.5 * obj->ww + C * tot;  // loss.cpp:57 / :119
+  obj->nact = (long long)cnt;
+  obj->red[0] = tot;
+  obj->red[1] = cnt;
+}
+
+void obj_combine_blocks(ObjScalars* obj, const double* red, int64_t nblk, double C, cudaStream_t s) {
+  obj_combine_kernel<<<1, 1, 0, s>>>(obj, red, (long long)nblk, C);
+  TB_LAUNCH_CHECK();
+}
+
 void vec_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d,
               double* out2, Scratch sc, cudaStream_t s) {
   launch_pdl(dot2_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, a, b, c, d, out2, sc);

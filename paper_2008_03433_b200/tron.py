@@ -208,14 +208,20 @@ class ExecutionPlan:
     # host data plane instead of NCCL (world > 1): fn(buf: np.ndarray) sums buf
     # over the ranks in place (e.g. a gloo / MPI allreduce)
     host_allreduce: Optional[Callable[[np.ndarray], None]] = None
+    # dense X larger than device memory: 0 auto, 1 always stream X from host
+    # memory (the caller keeps the Problem alive), -1 never
+    out_of_core: int = 0
+    stream_block_rows: int = 0
 
     @staticmethod
     def gpu(device: int = 0, svm_strategy: SvmStrategy = SvmStrategy.Indirect,
             gathered_budget_bytes: int = 2 << 30, solve_mode: str = "device",
-            reference_order: bool = False) -> "ExecutionPlan":
+            reference_order: bool = False, out_of_core: int = 0,
+            stream_block_rows: int = 0) -> "ExecutionPlan":
         return ExecutionPlan(device=device, svm_strategy=svm_strategy,
                              gathered_budget_bytes=gathered_budget_bytes, solve_mode=solve_mode,
-                             reference_order=reference_order)
+                             reference_order=reference_order, out_of_core=out_of_core,
+                             stream_block_rows=stream_block_rows)
 
     def to_c(self):
         o = _lib.tron_gpu_options()
@@ -226,6 +232,8 @@ class ExecutionPlan:
         o.rank, o.world = self.rank, self.world
         o.row_begin, o.global_rows = self.row_begin, self.global_rows
         o.reference_order = int(bool(self.reference_order))
+        o.out_of_core = int(self.out_of_core)
+        o.stream_block_rows = int(self.stream_block_rows)
         keep = []
         if self.nccl_unique_id is not None:
             uid = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)
@@ -345,7 +353,9 @@ class GpuEvaluator:
                                          _ptr(X.values, ctypes.c_double), _ptr(y, ctypes.c_double),
                                          float(problem.C), ctypes.byref(opts), ctypes.byref(h))
         else:
-            st = lib.tron_gpu_create_dense(loss.value, X.rows, X.cols, _ptr(X.values, ctypes.c_double),
+            # out-of-core contexts stream X from this very array for their lifetime
+            self._x_host = _f64(X.values)
+            st = lib.tron_gpu_create_dense(loss.value, X.rows, X.cols, _ptr(self._x_host, ctypes.c_double),
                                            _ptr(y, ctypes.c_double), float(problem.C),
                                            ctypes.byref(opts), ctypes.byref(h))
         _raise(st)

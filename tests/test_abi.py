@@ -43,8 +43,9 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.tron_config) == 8 * 10 + 8
     assert ctypes.sizeof(_lib.tron_iteration) == 4 * 8 + 8 + 8
     assert ctypes.sizeof(_lib.tron_ledger) == 7 * 8
-    # ... reference_order (int32 + pad), host_allreduce and its user pointer
-    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 8
+    # ... reference_order (int32 + pad), host_allreduce + its user pointer,
+    # out_of_core (int32 + pad), stream_block_rows
+    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8
 
 
 def test_defaults_mirror_reference():

@@ -24,6 +24,10 @@ from conftest import ROOT, rel_err
 
 pytestmark = pytest.mark.gpu
 WORLD = 2
+# solve tolerance per problem: the dense L2-SVM is flat around its optimum at
+# eps = 1e-4 (w moves 1e-5 under a different summation split), so it is solved
+# to 1e-8 where every w meets the 1e-6 gate
+EPS = {"dense-svm": 1e-8}
 
 
 def _free_port():
@@ -78,7 +82,7 @@ def _worker(rank, port, names, q):
                 g = ev.gradient()
                 hv = ev.hessian_vec(v)
                 m = ev.precond_diagonal()
-                res = ev.solve(TrustRegionConfig(eps=1e-4))
+                res = ev.solve(TrustRegionConfig(eps=EPS.get(name, 1e-4)))
                 act = ev.committed_state().active if loss.name == "L2Svm" else None
             out[name] = dict(f=f, g=g, hv=hv, m=m, w=res.w, obj=res.objective,
                              cg=[it.cg_iters for it in res.trace.iterations], act=act,
@@ -119,7 +123,7 @@ def test_two_shards_compose(sharded, ref, name):
         act_w = ev.candidate_state().active if loss.name == "L2Svm" else None
         ev.commit()
         g, hv, m = ev.gradient(), ev.hessian_vec(v), ev.precond_diagonal()
-        res = ev.solve(TrustRegionConfig(eps=1e-4))
+        res = ev.solve(TrustRegionConfig(eps=EPS.get(name, 1e-4)))
         act = ev.committed_state().active if loss.name == "L2Svm" else None
     a, b = sharded[0][name], sharded[1][name]
     for r in (a, b):  # every rank holds the same replicated result
@@ -132,7 +136,7 @@ def test_two_shards_compose(sharded, ref, name):
     assert rel_err(a["obj"], res.objective) <= 1e-10
     assert rel_err(a["w"], res.w) <= 1e-7
     assert all(abs(x - y) <= 1 for x, y in zip(a["cg"], [it.cg_iters for it in res.trace.iterations]))
-    w_ref, t_ref = ref.solve(p, 0 if loss.name == "Logistic" else 1, TrustRegionConfig(eps=1e-4))
+    w_ref, t_ref = ref.solve(p, 0 if loss.name == "Logistic" else 1, TrustRegionConfig(eps=EPS.get(name, 1e-4)))
     assert rel_err(a["obj"], t_ref["objective"]) <= 1e-6 and rel_err(a["w"], w_ref) <= 1e-6
     if act is not None:
         # same w => same margins row by row (sequential row dots): the shards'
