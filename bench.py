@@ -106,26 +106,59 @@ def host_description():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in process
+    through NVML (no nvidia-smi subprocess: forking the benchmark process every
+    sample stalled short solves); nvidia-smi only if NVML is unavailable."""
 
+    # nvmlClocksEventReasons bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown"}
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device=0):
         self.device = device
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reasons)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(device).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self._nvml = (pynvml, h)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return float(sm), float(mx), {name for b, name in self.REASONS.items() if bits & b}
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        r = [x.strip() for x in out.split(",")]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return float(r[0]), float(r[1]), {n for n, v in zip(names, r[3:7]) if v.lower() == "active"}
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self.rows.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
             self._stop.wait(0.25)
@@ -142,16 +175,10 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for name, val in zip(names, r[3:7]):
-                if val.strip().lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        reasons = set().union(*(r[2] for r in self.rows))
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": sorted(reasons),
+                "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------- oracle-side data
@@ -326,7 +353,7 @@ def read_traffic(workload):
         return None
 
 
-def cpu_baseline(args, p_full, res, ev, loss, cfg, plan):
+def cpu_baseline(args, p_full, res, ev, loss, cfg, plan, act_gpu=None):
     """The reference CPU solver (oracle/_ref) on this host's cores, bounded,
     plus the parity of the GPU result against it (north-star gate)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -388,18 +415,22 @@ def cpu_baseline(args, p_full, res, ev, loss, cfg, plan):
                             and all(abs(a - b) <= 1 for a, b in zip(cg["cg_iters"], cr["cg_iters"]))
                             and len(cg["cg_iters"]) == len(cr["cg_iters"]))
     if oloss == 1:  # SVM active set I = {i : 1 - y_i z_i > 0} at each solver's final w
-        act_gpu = ev.committed_state().active
+        sharded = act_gpu is not None  # the ranks' local sets, concatenated in rank order
+        if not sharded:
+            act_gpu = ev.committed_state().active
         act_ref = ref.svm(p_full, w_ref, np.zeros(p_full.X.cols))["active"]
         par["active_set_identical"] = bool(np.array_equal(act_gpu, act_ref))
         par["active_set_sizes"] = [int(act_gpu.size), int(act_ref.size)]
         par["active_set_symmetric_difference"] = int(np.setxor1d(act_gpu, act_ref).size)
-        ev.eval_candidate(w_ref)  # the GPU margin pass at the reference's w: bit-exact rows
-        par["active_set_identical_at_reference_w"] = bool(np.array_equal(ev.candidate_state().active, act_ref))
+        if not sharded:
+            ev.eval_candidate(w_ref)  # the GPU margin pass at the reference's w: bit-exact rows
+            par["active_set_identical_at_reference_w"] = bool(
+                np.array_equal(ev.candidate_state().active, act_ref))
     # predictions (model.cpp:88-117) on held-out SYNTH-v1 rows (seed 2)
-    from paper_2008_03433_b200 import make_evaluator
+    from paper_2008_03433_b200 import ExecutionPlan, make_evaluator
     test_rows = min(p_full.X.rows, 2_000_000)
     p_test, _ = product_problem(args.workload, seed=TEST_SEED, rows=test_rows)
-    with make_evaluator(p_test, loss, plan) as evt:
+    with make_evaluator(p_test, loss, ExecutionPlan.gpu(device=plan.device)) as evt:
         lab_gpu, correct_gpu = evt.predict(res.w)
         lab_gpu_at_ref, _ = evt.predict(w_ref)
     Xt = p_test.X
@@ -412,7 +443,6 @@ def cpu_baseline(args, p_full, res, ev, loss, cfg, plan):
     par["test_accuracy"] = [correct_gpu / test_rows, correct_ref / test_rows]
     if oloss == 1 and p_full.X.layout == "dense" and p_full.X.cols <= 48:
         # the bit-for-bit mode: every reduction in the reference's order (refexact.cu)
-        from paper_2008_03433_b200 import ExecutionPlan
         with make_evaluator(p_full, loss, ExecutionPlan.gpu(device=plan.device, reference_order=True)) as evr:
             evr.solve(cfg)  # warm (graph instantiation)
             t0 = time.perf_counter()
@@ -569,9 +599,21 @@ def main():
         e2e_pin = e2e_time(p_pin, reps)
         del p_pin
 
+    replicas_identical = None
+    if world > 1:  # the replicated w must be bit-identical on every rank
+        import hashlib
+        digests = [None] * world
+        dist.all_gather_object(digests, hashlib.sha1(np.ascontiguousarray(res.w).tobytes()).hexdigest())
+        replicas_identical = len(set(digests)) == 1
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(args, p_full, res, ev, loss, cfg, plan)
+    act_all = None
+    if world > 1 and not args.no_cpu_baseline and SHAPES[args.workload]["loss"] == "l2svm":
+        parts = [None] * world  # every rank's local active set (global row ids)
+        dist.all_gather_object(parts, ev.committed_state().active)
+        act_all = np.concatenate(parts)
+    if rank == 0 and not args.no_cpu_baseline:
+        # (N > 1: rank 0 alone, the other ranks wait at the closing barrier)
+        cpu = cpu_baseline(args, p_full, res, ev, loss, cfg, plan, act_gpu=act_all)
 
     if rank != 0:
         ev.close()
@@ -610,6 +652,7 @@ def main():
                          "transpose) + solve + w to host + destroy, through the C ABI; median of "
                          f"{reps}"),
                 "pinned_inputs_value": e2e_pin},
+        "replica_w_bitwise_identical": replicas_identical,
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
         "device_memory_bytes": ev.memory_bytes(),
