@@ -22,6 +22,7 @@
 //    in one pass.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <cooperative_groups.h>
 
@@ -39,6 +40,24 @@ namespace {
 constexpr int kBlock = 256;  // 8 warps = 8 chunks in flight per block
 constexpr int kEmptyItems = 4;  // empty rows per lane per visit
 
+// TB_LD256: the chunk's nonzeros as 256-bit loads (sm_100: one LDG.256 moves
+// 32 B per lane) marked L2::evict_first, so the once-read X stream does not
+// push the gathered vector out of L2.
+#ifndef TB_LD256
+#define TB_LD256 1  // measured: N1 Hv 91.8 -> 80.6 us, K1 3.63 -> 3.47 ms
+#endif
+__device__ __forceinline__ void ld4d_ef(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+__device__ __forceinline__ void ld8i_ef(const int* p, int (&x)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
+                 "=r"(x[7])
+               : "l"(p));
+}
+#if !TB_LD256
 __device__ __forceinline__ void ld2(const double* p, double& a, double& b) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
                : "=d"(a), "=d"(b)
@@ -49,6 +68,7 @@ __device__ __forceinline__ void ld4(const int* p, int& a, int& b, int& c, int& d
                : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
                : "l"(p));
 }
+#endif
 
 // Reduction over the emitted values (EpiView::dot_*): dacc gathers
 // base_j * out_j (mode 0) or out_j^2 (mode 1), bad counts non-finite out_j.
@@ -122,12 +142,19 @@ struct LaneChunk {
 // so every chunk is read in full without bounds checks.
 __device__ __forceinline__ void load_chunk(const CsrView& A, const SegView& S, long long t, int lane,
                                            unsigned cr, LaneChunk& c) {
-  c.base = t * kSegChunk + lane * kSegLaneItems;  // 16-B aligned
+  c.base = t * kSegChunk + lane * kSegLaneItems;  // 64-B aligned (values), 32-B (indices)
+#if TB_LD256
+  static_assert(kSegLaneItems == 8, "two 256-bit value loads, one index load per lane");
+  ld4d_ef(A.val + c.base, c.v[0], c.v[1], c.v[2], c.v[3]);
+  ld4d_ef(A.val + c.base + 4, c.v[4], c.v[5], c.v[6], c.v[7]);
+  ld8i_ef(A.idx + c.base, c.ix);
+#else
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; m += 2) ld2(A.val + c.base + m, c.v[m], c.v[m + 1]);
 #pragma unroll
   for (int m = 0; m < kSegLaneItems; m += 4)
     ld4(A.idx + c.base + m, c.ix[m], c.ix[m + 1], c.ix[m + 2], c.ix[m + 3]);
+#endif
   // a lane's 8 items never straddle a 32-bit word (base is a multiple of 8)
   c.word = __ldg(S.lastbits + (c.base >> 5));
   c.cr = cr;
@@ -355,7 +382,8 @@ template <int EPI, bool COH>
 __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
                                           double* __restrict__ out, long long t, int lane,
                                           DotAcc& dacc) {
-  const long long f = t < S.nchunks ? __ldg(S.chunk_first + t) : -1;
+  long long f = t < S.nchunks ? __ldg(S.chunk_first + t) : -1;
+  if (f >= 0 && t - f > kFixCta) f = -1;  // a CTA of its own finishes it (seg_fixup_kernel)
   const bool longspan = f >= 0 && t - f > kFixSerial;
   if (f >= 0 && !longspan) {
     double s = COH ? ld_coh(S.carry + f) : S.carry[f];
@@ -373,6 +401,7 @@ __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
     const long long tt = __shfl_sync(0xffffffffu, t, src);
     const long long ff = __shfl_sync(0xffffffffu, f, src);
     double s = 0.0;
+#pragma unroll 4
     for (long long v = ff + lane; v < tt; v += 32) s += COH ? ld_coh(S.carry + v) : S.carry[v];
     s = warp_sum(s);  // valid in lane 0
     if (lane == 0) {
@@ -385,14 +414,35 @@ __device__ __forceinline__ void fixup_one(const SegView& S, const EpiView& E,
   }
 }
 
+// CTAs [0, nreg) take one chunk per thread (fixup_one); CTA nreg + k finishes
+// the k-th long span S.long_fix[k] with all its threads (lane-strided sums,
+// then the block tree: a fixed order, so results stay bit-reproducible).
 template <int EPI>
 __global__ void __launch_bounds__(kBlock) seg_fixup_kernel(SegView S, EpiView E,
-                                                          double* __restrict__ out, long long Wseg) {
+                                                          double* __restrict__ out, long long Wseg,
+                                                          int nreg) {
   pdl_wait();
   pdl_trigger();
   DotAcc dacc;
-  fixup_one<EPI, false>(S, E, out, blockIdx.x * (long long)kBlock + threadIdx.x, threadIdx.x & 31,
-                        dacc);
+  if ((int)blockIdx.x < nreg) {
+    fixup_one<EPI, false>(S, E, out, blockIdx.x * (long long)kBlock + threadIdx.x, threadIdx.x & 31,
+                          dacc);
+  } else {
+    __shared__ double shl[kBlock / kWarp + 1];
+    const long long t = __ldg(S.long_fix + (blockIdx.x - nreg));
+    const long long f = __ldg(S.chunk_first + t);
+    double s = 0.0;
+#pragma unroll 4
+    for (long long v = f + threadIdx.x; v < t; v += kBlock) s += S.carry[v];
+    s = block_sum<kBlock>(s, shl);  // valid in thread 0
+    if (threadIdx.x == 0) {
+      const int j = S.nz_col[S.chunk_rank[t] & 0x7fffffffu];
+      const double bj = epi_base<EPI, false>(E, j);
+      const double o = epi_apply<EPI>(E, bj, s + S.head[t]);
+      out[j] = o;
+      if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, bj, o);
+    }
+  }
   if (EPI == EPI_VEC && E.dot_parts) {
     // this CTA's fix-ups, then the last CTA adds every partial in index order:
     // [0, Wseg) the segmented kernel's warps, then the fix-up CTAs
@@ -439,10 +489,12 @@ void launch_one(const CsrView& A, const SegView& S, const UView& U, const EpiVie
   launch_pdl(seg_spmv_kernel<UK, SQ, EPI, STAGED>, dim3((int)grid), dim3(BLK), smem, s, A, S, U, E,
              out);
   // the fix-up kernel also finishes E.dot_out, so it always runs when asked to
-  int fgrid = (int)((S.nchunks + kBlock - 1) / kBlock);
-  if (E.dot_parts && fgrid == 0) fgrid = 1;
+  int nreg = (int)((S.nchunks + kBlock - 1) / kBlock);
+  if (E.dot_parts && nreg == 0) nreg = 1;
+  const int fgrid = nreg + (int)S.nlong;
   const long long Wseg = grid * (BLK / 32);
-  if (fgrid) launch_pdl(seg_fixup_kernel<EPI>, dim3(fgrid), dim3(kBlock), 0, s, S, E, out, Wseg);
+  if (fgrid)
+    launch_pdl(seg_fixup_kernel<EPI>, dim3(fgrid), dim3(kBlock), 0, s, S, E, out, Wseg, nreg);
 }
 
 template <int UK, bool SQ, int EPI>
@@ -520,6 +572,12 @@ __global__ void plan_chunk_rank_kernel(const int32_t* cptr, long long n, const i
   }
 }
 
+__global__ void plan_long_flags_kernel(const int32_t* first, long long nchunks, uint8_t* flag) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nchunks;
+       t += (long long)gridDim.x * blockDim.x)
+    flag[t] = first[t] >= 0 && t - first[t] > kFixCta;
+}
+
 __global__ void plan_sentinel_kernel(int32_t* nz_col, const int32_t* colrank, long long n) {
   nz_col[colrank[n]] = (int32_t)n;
 }
@@ -534,19 +592,25 @@ int pgrid(long long n) {
 
 int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uint32_t* chunk_rank,
                     int32_t* chunk_first, uint32_t* lastbits, int32_t* nz_col, int32_t* empty_col,
-                    cudaStream_t s) {
+                    int32_t* long_fix, cudaStream_t s) {
   const int64_t nchunks = (nnz + kSegChunk - 1) / kSegChunk;
   const size_t n1 = n > 0 ? n : 1;
   int32_t *nonempty = nullptr, *colrank = nullptr, *ids = nullptr;
   uint8_t* empty = nullptr;
-  long long* cnt = nullptr;  // [0] non-empty rows, [1] empty rows
+  long long* cnt = nullptr;  // [0] non-empty rows, [1] empty rows, [2] long fix-ups
+  uint8_t* lflag = nullptr;
   void* temp = nullptr;
-  size_t tb1 = 0, tb2 = 0, tb3 = 0;
+  size_t tb1 = 0, tb2 = 0, tb3 = 0, tb4 = 0;
+  const int64_t nch1 = nchunks > 0 ? nchunks : 1;
   cudaError_t e = cudaMallocAsync(&nonempty, (n1 + 1) * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaMallocAsync(&colrank, (n1 + 1) * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaMallocAsync(&ids, n1 * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaMallocAsync(&empty, n1, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&cnt, 2 * sizeof(long long), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&cnt, 3 * sizeof(long long), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&lflag, nch1, s);
+  thrust::counting_iterator<int32_t> chunk_ids(0);
+  if (e == cudaSuccess)
+    e = cub::DeviceSelect::Flagged(nullptr, tb4, chunk_ids, lflag, long_fix, cnt + 2, (int)nch1, s);
   if (e == cudaSuccess)
     e = cub::DeviceScan::ExclusiveSum(nullptr, tb1, nonempty, colrank, (int)(n + 1), s);
   if (e == cudaSuccess)
@@ -554,11 +618,11 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uin
   if (e == cudaSuccess)
     e = cub::DeviceSelect::Flagged(nullptr, tb3, ids, empty, empty_col, cnt + 1, (int)n, s);
   if (e == cudaSuccess)
-    e = cudaMallocAsync(&temp, std::max<size_t>(std::max(tb1, std::max(tb2, tb3)), 1), s);
+    e = cudaMallocAsync(&temp, std::max<size_t>(std::max(std::max(tb1, tb4), std::max(tb2, tb3)), 1), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(nonempty, 0, (n1 + 1) * sizeof(int32_t), s);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(lastbits, 0, (size_t)(nchunks * (kSegChunk / 32) + 2) * sizeof(uint32_t), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 2 * sizeof(long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 3 * sizeof(long long), s);
   if (e == cudaSuccess) {
     if (n > 0) plan_cols_kernel<<<pgrid(n), 256, 0, s>>>(cptr, n, lastbits, nonempty, ids, empty);
     e = cub::DeviceScan::ExclusiveSum(temp, tb1, nonempty, colrank, (int)(n + 1), s);
@@ -569,15 +633,18 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uin
     e = cub::DeviceSelect::Flagged(temp, tb3, ids, empty, empty_col, cnt + 1, (int)n, s);
   if (e == cudaSuccess) {
     plan_sentinel_kernel<<<1, 1, 0, s>>>(nz_col, colrank, n);
-    if (nchunks > 0)
+    if (nchunks > 0) {
       plan_chunk_rank_kernel<<<pgrid(nchunks), 256, 0, s>>>(cptr, n, colrank, nchunks, chunk_rank,
                                                             chunk_first);
+      plan_long_flags_kernel<<<pgrid(nchunks), 256, 0, s>>>(chunk_first, nchunks, lflag);
+      e = cub::DeviceSelect::Flagged(temp, tb4, chunk_ids, lflag, long_fix, cnt + 2, (int)nchunks, s);
     }
-  long long counts[2] = {0, 0};
+  }
+  long long counts[3] = {0, 0, 0};
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(counts, cnt, sizeof(counts), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  for (void* p : {(void*)nonempty, (void*)colrank, (void*)ids, (void*)empty, (void*)cnt, temp})
+  for (void* p : {(void*)nonempty, (void*)colrank, (void*)ids, (void*)empty, (void*)cnt, (void*)lflag, temp})
     if (p) cudaFreeAsync(p, s);
   if (e == cudaSuccess) e = cudaGetLastError();
   P->nchunks = nchunks;
@@ -588,12 +655,15 @@ int seg_plan_device(const int32_t* cptr, int64_t n, int64_t nnz, SegView* P, uin
   P->lastbits = lastbits;
   P->nz_col = nz_col;
   P->empty_col = empty_col;
+  P->long_fix = long_fix;
+  P->nlong = counts[2];
   return e == cudaSuccess ? 0 : (int)e;
 }
 
 int64_t seg_dot_slots(int64_t nchunks) {
   // doubles: 2 per slot; segmented warps (16 per SM in either variant) + fix-up CTAs
-  return 2 * ((int64_t)device_sm_count() * 16 + (nchunks + kBlock - 1) / kBlock + 1);
+  return 2 * ((int64_t)device_sm_count() * 16 + (nchunks + kBlock - 1) / kBlock + 1 +
+              seg_long_fix_cap(nchunks));
 }
 
 void csc_spmv(const CsrView& At, const SegView& S, const UView& U, bool squared,

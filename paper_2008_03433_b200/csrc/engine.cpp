@@ -464,9 +464,10 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       e->chunk_first_.alloc(slots);
       e->head_.alloc(slots);
       e->carry_.alloc(slots);
+      e->long_fix_.alloc(seg_long_fix_cap(nch));
       const int prc = seg_plan_device(e->cptr_.p, (int64_t)n, nnz, &e->plan_, e->chunk_rank_.p,
                                       e->chunk_first_.p, e->lastbits_.p, e->nz_col_.p,
-                                      e->empty_col_.p, s);
+                                      e->empty_col_.p, e->long_fix_.p, s);
       if (prc != 0) cuda_check((cudaError_t)prc, "seg_plan_device");
       e->plan_.head = e->head_.p;
       e->plan_.carry = e->carry_.p;
@@ -1072,8 +1073,9 @@ void Engine::build_gathered_csr(int nI, long long nnzI) {
   gchunk_first_.alloc(slots);
   ghead_.alloc(slots);
   gcarry_.alloc(slots);
+  glong_fix_.alloc(seg_long_fix_cap(nch));
   rc = seg_plan_device(gcptr_.p, n_, nnzI, &gplan_, gchunk_rank_.p, gchunk_first_.p, glastbits_.p,
-                       gnz_col_.p, gempty_col_.p, s_);
+                       gnz_col_.p, gempty_col_.p, glong_fix_.p, s_);
   if (rc != 0) cuda_check((cudaError_t)rc, "seg_plan_device (gathered)");
   gplan_.head = ghead_.p;
   gplan_.carry = gcarry_.p;

@@ -232,7 +232,7 @@ class Engine {
   DevBuf<int32_t> rptr_, cidx_, cptr_, ridx_;
   DevBuf<double> rval_, cval_;
   DevBuf<uint32_t> lastbits_, chunk_rank_;
-  DevBuf<int32_t> empty_col_, chunk_first_, nz_col_;
+  DevBuf<int32_t> empty_col_, chunk_first_, nz_col_, long_fix_;
   DevBuf<double> head_, carry_;
   CsrView X_{}, Xt_{};
   SegView plan_{};
@@ -250,7 +250,7 @@ class Engine {
   DevBuf<int32_t> grptr_, gcidx_, gcptr_, gridx_;
   DevBuf<double> grval_, gcval_;
   DevBuf<uint32_t> glastbits_, gchunk_rank_;
-  DevBuf<int32_t> gempty_col_, gchunk_first_, gnz_col_;
+  DevBuf<int32_t> gempty_col_, gchunk_first_, gnz_col_, glong_fix_;
   DevBuf<double> ghead_, gcarry_;
   CsrView Xg_csr_{}, Xgt_{};
   SegView gplan_{};

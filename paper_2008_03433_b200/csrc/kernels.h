@@ -42,14 +42,21 @@ struct SegView {
                                          // ends there (a fix-up), else -1
   double* head = nullptr;   // [nchunks] partial of the row open at the chunk's start, if it ends inside
   double* carry = nullptr;  // [nchunks] partial of the row open at the chunk's end
+  // fix-ups spanning more than kFixCta chunks (Zipf-hot rows: K1's hottest
+  // column covers ~29k chunks), each finished by a whole CTA
+  const int32_t* long_fix = nullptr;  // [nlong] chunk ids, ascending
+  int64_t nlong = 0;
 };
+constexpr int kFixCta = 512;
+// long_fix buffer entries seg_plan_device may write
+inline int64_t seg_long_fix_cap(int64_t nchunks) { return nchunks / kFixCta + 1; }
 // Device-built plan from the compressed-row offsets (ptr, rows+1).  Buffers:
 // chunk_rank[nchunks], chunk_first[nchunks], lastbits[nchunks*8+2],
 // nz_col[rows+1], empty_col[rows]; P's head / carry are left to the caller.
 // Synchronizes s (returns the counts in P).
 int seg_plan_device(const int32_t* ptr, int64_t rows, int64_t nnz, SegView* P,
                     uint32_t* chunk_rank, int32_t* chunk_first, uint32_t* lastbits, int32_t* nz_col,
-                    int32_t* empty_col, cudaStream_t s);
+                    int32_t* empty_col, int32_t* long_fix, cudaStream_t s);
 
 // Per-source-row weight u_i used by the transposed product sum_i u_i x_ij.
 enum UKind : int {

@@ -32,6 +32,15 @@ __device__ __forceinline__ void ldv2d(const double* p, double& a, double& b) {
                : "=d"(a), "=d"(b)
                : "l"(p));
 }
+#ifndef TB_LD256
+#define TB_LD256 1
+#endif
+// four values (32 B, 32-B aligned) as one 256-bit load, L2::evict_first
+__device__ __forceinline__ void ldv4d_ef(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
 // COH: v is written inside the same (persistent) kernel by other CTAs, so it
 // is read through L2 (ld.global.cg), never the non-coherent path.
 template <int G, bool COH, int NG = TB_CSR_NG>
@@ -48,8 +57,12 @@ __device__ __forceinline__ double row_dot_vec(const CsrView& X, long long row, i
       const int k = g0 + 4 * G * q;
       if (k < end) {  // the group is inside the (16-B padded) arrays
         ldv4i(X.idx + k, c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
+#if TB_LD256
+        ldv4d_ef(X.val + k, a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+#else
         ldv2d(X.val + k, a[4 * q], a[4 * q + 1]);
         ldv2d(X.val + k + 2, a[4 * q + 2], a[4 * q + 3]);
+#endif
       } else {
 #pragma unroll
         for (int m = 0; m < 4; ++m) {

@@ -418,3 +418,43 @@ def test_device_quadratic_model(port, case):
     assert abs(q - q_ref) <= 1e-11 * abs(q_ref)
     assert abs(q - q_host) <= 1e-12 * abs(q_ref)
     assert abs(q_step - cg.model_value) <= 1e-9 * abs(cg.model_value)
+
+
+@pytest.mark.parametrize("hot_rows", [140_000, 400_000])
+def test_csc_long_fixup_spans(port, hot_rows):
+    """Columns spanning more than kFixCta = 512 chunks (131k+ entries, like K1's
+    Zipf-hot columns) are finished by a CTA of their own: gradient, Hv (with
+    the fused p.Hp of the solve) and the preconditioner against the oracle,
+    bit-reproducible run to run."""
+    rng = np.random.default_rng(7)
+    l, n = hot_rows, 3000
+    hot = [0, 1, 17]  # three columns present in (almost) every row
+    rows_cols = []
+    for i in range(l):
+        cols = set(hot[:2] if i % 3 else hot)
+        cols.update(rng.integers(18, n, size=3).tolist())
+        rows_cols.append(sorted(cols))
+    ro = np.zeros(l + 1, np.int64)
+    ro[1:] = np.cumsum([len(c) for c in rows_cols])
+    ci = np.concatenate([np.array(c, np.int32) for c in rows_cols])
+    vals = rng.uniform(0.01, 1.0, ci.size)
+    y = np.where(rng.random(l) < 0.5, -1.0, 1.0)
+    p = Problem(FeatureMatrix("csr", l, n, vals, ro, ci), y, 1.0)
+    w = rng.uniform(-0.01, 0.01, n)
+    v = rng.uniform(-1, 1, n)
+    want = port.logistic(p, w, v)
+    outs = []
+    for _ in range(2):
+        with gpu(p, LR) as ev:
+            ev.eval_candidate(w)
+            ev.commit()
+            outs.append((ev.gradient(), ev.hessian_vec(v), ev.precond_diagonal()))
+    g, hv, m = outs[0]
+    assert rel_err(g, want["g"]) <= 1e-12
+    assert rel_err(hv, want["hv"]) <= 1e-12
+    assert rel_err(m, want["M"]) <= 1e-12
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    r = solve(p, LR, TrustRegionConfig(eps=1e-3), ExecutionPlan.gpu())
+    w_ref, t_ref = port.solve(p, 0, TrustRegionConfig(eps=1e-3))
+    assert rel_err(r.objective, t_ref["objective"]) <= 1e-10 and rel_err(r.w, w_ref) <= 1e-7

