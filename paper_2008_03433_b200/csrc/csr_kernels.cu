@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -94,7 +95,7 @@ template <int G, int LOSS, bool STAGED>
 __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
     csr_forward_kernel(CsrView X, int hot, const double* __restrict__ w,
                                                             const double* __restrict__ y, double C,
-                                                            double* __restrict__ z,
+                                                            const double* zin, double* z,
                                                             double* __restrict__ zhat,
                                                             double* __restrict__ dvec,
                                                             uint8_t* __restrict__ mask,
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
       const double yi = y[row];
+      if (zin) s = zin[row] + s;  // earlier column panels
       z[row] = s;
       if (LOSS == kLossLogistic) {
         const double t = yi * s;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
     csr_dv_kernel(CsrView X, int hot, const double* __restrict__ p,
                                                        const double* __restrict__ dvec,
                                                        const uint8_t* __restrict__ mask,
-                                                       double* __restrict__ a) {
+                                                       const double* ain, double* a, int final) {
   pdl_wait();
   pdl_trigger();
   constexpr int BLK = STAGED ? kStagedBlock : kBlock;
@@ -183,9 +185,10 @@ __global__ void __launch_bounds__(STAGED ? kStagedBlock : kBlock)
     }
     s = group_sum<G>(s);
     if (sub == 0 && row < X.rows) {
+      if (ain) s = ain[row] + s;  // earlier column panels
       // loss.cpp:86-89: a0_i *= dvec_i; svm indirect skips inactive rows.
       // (no mask and no dvec: the gathered rows X_I, every row active)
-      a[row] = mask ? (active ? s : 0.0) : (dvec ? s * dvec[row] : s);
+      a[row] = !final ? s : (mask ? (active ? s : 0.0) : (dvec ? s * dvec[row] : s));
     }
   }
 }
@@ -347,8 +350,8 @@ static bool stage_rows(const CsrView& X) {
 
 void csr_forward(const CsrView& X, int group, int loss, const double* w, const double* y, double C,
                  double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
-                 Scratch sc, cudaStream_t s) {
-  if (stage_rows(X)) {
+                 Scratch sc, cudaStream_t s, const double* zin) {
+  if (stage_rows(X) && !zin && !X.rbeg) {
     const int hot = (int)(X.cols < kHotMax ? X.cols : kHotMax);
     const int grid = device_sm_count();
     const size_t smem = (size_t)hot * 8;
@@ -356,15 +359,15 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
       TB_GROUP_DISPATCH(group, {
         auto k = csr_forward_kernel<GG, kLossLogistic, true>;
         set_smem(k);
-        launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, z, zhat, dvec, mask,
-                   obj, sc);
+        launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, zin, z, zhat, dvec,
+                   mask, obj, sc);
       });
     } else {
       TB_GROUP_DISPATCH(group, {
         auto k = csr_forward_kernel<GG, kLossSvm, true>;
         set_smem(k);
-        launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, z, zhat, dvec, mask,
-                   obj, sc);
+        launch_pdl(k, dim3(grid), dim3(kStagedBlock), smem, s, X, hot, w, y, C, zin, z, zhat, dvec,
+                   mask, obj, sc);
       });
     }
     return;
@@ -372,34 +375,101 @@ void csr_forward(const CsrView& X, int group, int loss, const double* w, const d
   if (loss == kLossLogistic) {
     TB_GROUP_DISPATCH(group, {
       auto k = csr_forward_kernel<GG, kLossLogistic, false>;
-      launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, w, y, C, z,
+      launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, w, y, C, zin, z,
                  zhat, dvec, mask, obj, sc);
     });
   } else {
     TB_GROUP_DISPATCH(group, {
       auto k = csr_forward_kernel<GG, kLossSvm, false>;
-      launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, w, y, C, z,
+      launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, w, y, C, zin, z,
                  zhat, dvec, mask, obj, sc);
     });
   }
 }
 
 void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
-            double* a, cudaStream_t s) {
-  if (stage_rows(X)) {
+            double* a, cudaStream_t s, const double* ain, bool final) {
+  const int fin = final ? 1 : 0;
+  if (stage_rows(X) && !ain && final && !X.rbeg) {
     const int hot = (int)(X.cols < kHotMax ? X.cols : kHotMax);
     TB_GROUP_DISPATCH(group, {
       auto k = csr_dv_kernel<GG, true>;
       set_smem(k);
       launch_pdl(k, dim3(device_sm_count()), dim3(kStagedBlock), (size_t)hot * 8, s, X, hot, p, dvec,
-                 mask, a);
+                 mask, ain, a, fin);
     });
     return;
   }
   TB_GROUP_DISPATCH(group, {
     auto k = csr_dv_kernel<GG, false>;
-    launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, p, dvec, mask, a);
+    launch_pdl(k, dim3(forward_grid(k, X.rows, group)), dim3(kBlock), 0, s, X, 0, p, dvec, mask, ain,
+               a, fin);
   });
+}
+
+namespace {
+constexpr int kMaxPanelBounds = 8;
+struct PanelBounds {
+  int32_t bound[kMaxPanelBounds];
+  int32_t* split[kMaxPanelBounds];
+  int n;
+};
+// split[k][i] = lower_bound of bound[k] in row i's (ascending) columns
+__global__ void panel_split_kernel(CsrView X, PanelBounds B) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < X.rows;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int beg = X.ptr[i], end = X.ptr[i + 1];
+    for (int k = 0; k < B.n; ++k) {
+      int lo = beg, hi = end;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (X.idx[mid] < B.bound[k])
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      B.split[k][i] = lo;
+    }
+  }
+}
+}  // namespace
+
+static __global__ void panel_count_kernel(CsrView X, PanelBounds B, unsigned long long* counts) {
+  unsigned long long local[kMaxPanelBounds + 1] = {};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < X.rows;
+       i += (long long)gridDim.x * blockDim.x) {
+    int lo = X.ptr[i];
+    for (int k = 0; k <= B.n; ++k) {
+      const int hi = k < B.n ? B.split[k][i] : X.ptr[i + 1];
+      local[k] += (unsigned long long)(hi - lo);
+      lo = hi;
+    }
+  }
+  for (int k = 0; k <= B.n; ++k) atomicAdd(counts + k, local[k]);
+}
+
+int csr_panel_splits(const CsrView& X, const int32_t* bounds, int nbounds, int32_t* const* split,
+                     unsigned long long* counts, cudaStream_t s) {
+  PanelBounds B{};
+  B.n = nbounds < kMaxPanelBounds ? nbounds : kMaxPanelBounds;
+  for (int k = 0; k < B.n; ++k) {
+    B.bound[k] = bounds[k];
+    B.split[k] = split[k];
+  }
+  unsigned long long* dc = nullptr;
+  cudaError_t e = cudaMallocAsync(&dc, (kMaxPanelBounds + 1) * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dc, 0, (kMaxPanelBounds + 1) * sizeof(unsigned long long), s);
+  if (e == cudaSuccess && X.rows > 0) {
+    const int grid = (int)std::min<long long>((X.rows + 255) / 256, 148LL * 16);
+    panel_split_kernel<<<grid, 256, 0, s>>>(X, B);
+    panel_count_kernel<<<grid, 256, 0, s>>>(X, B, dc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(counts, dc, (B.n + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (dc) cudaFreeAsync(dc, s);
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
 // Structure of the CSC copy: a stable radix sort of the column indices (row

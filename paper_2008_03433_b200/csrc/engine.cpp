@@ -479,6 +479,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
       }
       tr.mark("segmented plan");
     }
+    e->setup_panels();
     // The CG graphs of both slots (no preconditioner) are captured and
     // instantiated while the values are still crossing PCIe: a recipe of
     // fixed buffers, independent of their contents.
@@ -817,6 +818,13 @@ void Engine::forward(Slot& S) {
       ro_hinge(l_, n_, S.z.p, y_.p, S.w.p, C_, ro_hparts_.p, ro_tickets_.p, obj_d_, s_);
       count_launch(4);
     }
+  } else if (!panels_.empty()) {  // raw row sums of the leading panels, then the fused pass
+    const size_t K = panels_.size();
+    for (size_t k = 0; k + 1 < K; ++k)
+      csr_dv(panels_[k], panel_group_[k], S.w.p, nullptr, nullptr, S.z.p, s_, k ? S.z.p : nullptr, false);
+    count_launch(K - 1);
+    csr_forward(panels_[K - 1], panel_group_[K - 1], loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p,
+                S.mask.p, obj_d_, sc_, s_, S.z.p);
   } else {
     csr_forward(X_, group_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_,
                 s_);
@@ -1135,6 +1143,53 @@ bool Engine::hv_dot_available() const {
   return !dense_ && dot_parts_.n > 0;
 }
 
+// Column panels for the row products (csr_dv, csr_forward) when the gathered
+// vector is larger than ~96 MB: measured on K1 (v = 160 MB), half of the
+// gathers missed L2 and doubled the pass's DRAM traffic.  Panel width
+// TRON_B200_PANEL_COLS (0: off).
+void Engine::setup_panels() {
+  panels_.clear();
+  panel_group_.clear();
+  const char* e = std::getenv("TRON_B200_PANEL_COLS");  // explicit: any n (tests, A/B)
+  const int64_t W = e ? std::atoll(e) : (int64_t{6} << 20);
+  if (W <= 0 || X_.nnz == 0) return;
+  if (!e && n_ * (int64_t)sizeof(double) <= (int64_t{96} << 20)) return;
+  const int K = (int)std::min<int64_t>((n_ + W - 1) / W, 8);
+  if (K < 2) return;
+  std::vector<int32_t> bounds;
+  for (int k = 1; k < K; ++k) bounds.push_back((int32_t)(n_ * k / K));
+  int32_t* splits[8] = {};
+  for (int k = 0; k < K - 1; ++k) {
+    psplit_[k].alloc((size_t)l_);
+    splits[k] = psplit_[k].p;
+  }
+  unsigned long long h[8] = {};
+  const int rc = csr_panel_splits(X_, bounds.data(), K - 1, splits, h, s_);
+  if (rc != 0) cuda_check((cudaError_t)rc, "csr_panel_splits");
+  for (int k = 0; k < K; ++k) {
+    CsrView P = X_;
+    P.rbeg = k == 0 ? nullptr : psplit_[k - 1].p;
+    P.rend = k == K - 1 ? nullptr : psplit_[k].p;
+    P.nnz = (int64_t)h[k];
+    panels_.push_back(P);
+    panel_group_.push_back(choose_group(l_, (int64_t)h[k]));
+  }
+}
+
+// a_i = (x_i . v) * dvec_i / mask_i ? x_i . v : 0 (loss.cpp:84-89, :143-160)
+// over the column panels in order, or in one pass.
+void Engine::row_products(const double* v, const double* dvec, const uint8_t* mask, double* a) {
+  if (panels_.empty()) {
+    csr_dv(X_, group_, v, dvec, mask, a, s_);
+    count_launch(1);
+    return;
+  }
+  const size_t K = panels_.size();
+  for (size_t k = 0; k < K; ++k)
+    csr_dv(panels_[k], panel_group_[k], v, dvec, mask, a, s_, k ? a : nullptr, k + 1 == K);
+  count_launch(K);
+}
+
 void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   const Slot& S = slot_[cand_ ^ 1];
   EpiView epi;
@@ -1165,8 +1220,7 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   }
   const double* dv = loss_ == TRON_LOSS_LOGISTIC ? S.dvec.p : nullptr;
   const uint8_t* mk = loss_ == TRON_LOSS_LOGISTIC ? nullptr : S.mask.p;
-  csr_dv(X_, group_, v, dv, mk, a_.p, s_);
-  count_launch(1);
+  row_products(v, dv, mk, a_.p);
   transposed_raw_or_epi(u, false, epi, out);
 }
 

@@ -235,6 +235,14 @@ class Engine {
   DevBuf<int32_t> empty_col_, chunk_first_, nz_col_, long_fix_;
   DevBuf<double> head_, carry_;
   CsrView X_{}, Xt_{};
+  // column panels of X for the row products when v does not fit in L2
+  // (K1: 160 MB): panel k = columns [k W, (k+1) W), row i's part located by
+  // the split arrays; the row sums accumulate panel by panel in a fixed order
+  std::vector<CsrView> panels_;
+  std::vector<int> panel_group_;
+  DevBuf<int32_t> psplit_[7];
+  void setup_panels();
+  void row_products(const double* v, const double* dvec, const uint8_t* mask, double* a);
   SegView plan_{};
   int group_ = 4;
   // dense column-major

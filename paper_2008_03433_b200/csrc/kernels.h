@@ -21,7 +21,16 @@ struct CsrView {
   const int32_t* ptr = nullptr;
   const int32_t* idx = nullptr;
   const double* val = nullptr;
+  // column panel (row products only): row i's entries [rbeg[i], rend[i]) instead
+  // of [ptr[i], ptr[i+1]) -- the part of a column-sorted row inside the panel
+  const int32_t* rbeg = nullptr;
+  const int32_t* rend = nullptr;
 };
+// Column panels of a CSR (row products of X with v too large for L2): split[k]
+// [i] = first entry of row i with column >= bound[k] (k = 0 .. K-2, K <= 8);
+// counts[k] (host) = entries of panel k.  Synchronizes s; 0 or a cudaError_t.
+int csr_panel_splits(const CsrView& X, const int32_t* bounds, int nbounds, int32_t* const* split,
+                     unsigned long long* counts, cudaStream_t s);
 
 // Segmented-chunk plan of a compressed matrix (fixed per structure): the
 // nonzeros are cut into fixed chunks of 32*kSegLaneItems (one warp each);
@@ -135,13 +144,16 @@ int device_sm_count();
 int choose_group(int64_t rows, int64_t nnz);
 // Fused margin pass: z = Xw; LR: zhat, dvec; SVM: mask (+ active count).
 // f = 0.5*ww + C*sum(loss terms) is written to obj->f (obj->ww precomputed).
+// zin (may alias z): the row sums of the earlier column panels, added first.
 void csr_forward(const CsrView& X, int group, int loss, const double* w, const double* y, double C,
                  double* z, double* zhat, double* dvec, uint8_t* mask, ObjScalars* obj,
-                 Scratch sc, cudaStream_t s);
+                 Scratch sc, cudaStream_t s, const double* zin = nullptr);
 // a_i = (x_i . p) * dvec_i  (or mask_i ? x_i . p : 0 when mask given; x_i . p
 // when neither is given)
+// Column panels: ain (may alias a) holds the earlier panels' row sums; only
+// the last panel (final) applies dvec / mask, the others store the raw sum.
 void csr_dv(const CsrView& X, int group, const double* p, const double* dvec, const uint8_t* mask,
-            double* a, cudaStream_t s);
+            double* a, cudaStream_t s, const double* ain = nullptr, bool final = true);
 // Transposed product over the CSC copy (csc_seg.cu; segmented chunks, atomic-free).
 int64_t seg_dot_slots(int64_t nchunks);
 void csc_spmv(const CsrView& At, const SegView& plan, const UView& u, bool squared,

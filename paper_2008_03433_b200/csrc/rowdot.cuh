@@ -46,7 +46,8 @@ __device__ __forceinline__ void ldv4d_ef(const double* p, double& a, double& b, 
 template <int G, bool COH, int NG = TB_CSR_NG>
 __device__ __forceinline__ double row_dot_vec(const CsrView& X, long long row, int sub,
                                               const double* __restrict__ v) {
-  const int beg = X.ptr[row], end = X.ptr[row + 1];
+  const int beg = X.rbeg ? X.rbeg[row] : X.ptr[row];
+  const int end = X.rend ? X.rend[row] : X.ptr[row + 1];
   const int base = beg & ~3;
   double s = 0.0;
   for (int g0 = base + 4 * sub; g0 < end; g0 += 4 * G * NG) {

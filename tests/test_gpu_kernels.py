@@ -458,3 +458,30 @@ def test_csc_long_fixup_spans(port, hot_rows):
     r = solve(p, LR, TrustRegionConfig(eps=1e-3), ExecutionPlan.gpu())
     w_ref, t_ref = port.solve(p, 0, TrustRegionConfig(eps=1e-3))
     assert rel_err(r.objective, t_ref["objective"]) <= 1e-10 and rel_err(r.w, w_ref) <= 1e-7
+
+
+@pytest.mark.parametrize("width", [1000, 4096, 30000])
+def test_column_panels_row_products(port, monkeypatch, width):
+    """Column panels of the row products (TRON_B200_PANEL_COLS; on by default
+    when v exceeds ~96 MB, e.g. K1): fun / grad / Hv of LR and of the sparse
+    L2-SVM against the oracle, and whole solves against the unpaneled ones."""
+    monkeypatch.setenv("TRON_B200_PANEL_COLS", str(width))
+    p = synth.synth_sparse(13, 3000, 40000, 30)
+    n = p.X.cols
+    w = synth.testgen_random_vector(21, n, 0.05)
+    v = synth.testgen_random_vector(22, n, 1.0)
+    for loss, ol in ((LR, 0), (SVM, 1)):
+        want = port.logistic(p, w, v) if ol == 0 else port.svm(p, w, v)
+        with gpu(p, loss) as ev:
+            f = ev.eval_candidate(w)
+            st = ev.candidate_state()
+            ev.commit()
+            g, hv = ev.gradient(), ev.hessian_vec(v)
+            r = ev.solve(TrustRegionConfig(eps=1e-4))
+        assert rel_err(f, want["f"]) <= 1e-13
+        assert rel_err(st.z, want["z"]) <= 1e-13
+        assert rel_err(g, want["g"]) <= 1e-12 and rel_err(hv, want["hv"]) <= 1e-12
+        monkeypatch.setenv("TRON_B200_PANEL_COLS", "0")
+        r0 = solve(p, loss, TrustRegionConfig(eps=1e-4), ExecutionPlan.gpu())
+        monkeypatch.setenv("TRON_B200_PANEL_COLS", str(width))
+        assert rel_err(r.objective, r0.objective) <= 1e-12 and rel_err(r.w, r0.w) <= 1e-8

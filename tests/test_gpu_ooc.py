@@ -15,9 +15,11 @@ from paper_2008_03433_b200.tron import Error
 pytestmark = pytest.mark.gpu
 LR, SVM = LossKind.Logistic, LossKind.L2Svm
 
+# (equal column scales: well-conditioned, so whole solves can be compared at
+# 1e-6 in w; the 2-decade SYNTH scales leave w flat to ~1e-5 at eps = 1e-6)
 CASES = [
-    ("svm", lambda: synth.synth_dense(1, 300_000, 40), SVM, 40_000),
-    ("svm-small-blocks", lambda: synth.synth_dense(7, 50_001, 40), SVM, 256),
+    ("svm", lambda: synth.synth_dense(1, 300_000, 40, decades=0.0), SVM, 40_000),
+    ("svm-small-blocks", lambda: synth.synth_dense(7, 50_001, 40, decades=0.0), SVM, 256),
     ("lr", lambda: synth.testgen_dense_problem(2001, 60_003, 30, 1.0), LR, 7_000),
 ]
 
