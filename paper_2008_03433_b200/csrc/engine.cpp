@@ -554,7 +554,20 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     size_t free_b = 0, total_b = 0;
     const bool have = cudaSetDevice(opt.device) == cudaSuccess &&
                       cudaMemGetInfo(&free_b, &total_b) == cudaSuccess;
-    if (!have) cudaGetLastError();
+    if (!have) {
+      cudaGetLastError();
+    } else {
+      // blocks an earlier context returned to the stream-ordered pool are free
+      // for this one, though the driver still counts them as used
+      cudaMemPool_t pool;
+      cuuint64_t reserved = 0, used = 0;
+      if (cudaDeviceGetDefaultMemPool(&pool, opt.device) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+          reserved > used)
+        free_b += (size_t)(reserved - used);
+      cudaGetLastError();
+    }
     const double xbytes = 8.0 * (double)e->ld_ * (double)n;
     const double state = (double)e->ld_ * (loss == TRON_LOSS_LOGISTIC ? 56.0 : 26.0);
     const bool want = opt.out_of_core > 0 ||
