@@ -1163,10 +1163,13 @@ bool Engine::hv_dot_available() const {
 void Engine::setup_panels() {
   panels_.clear();
   panel_group_.clear();
-  const char* e = std::getenv("TRON_B200_PANEL_COLS");  // explicit: any n (tests, A/B)
-  const int64_t W = e ? std::atoll(e) : (int64_t{6} << 20);
+  // Opt-in: measured on K1 the panels cut the fused margin pass (2.12 -> 1.57 ms
+  // with 10M-column panels: the heavy panel runs in the lean csr_dv kernel) but
+  // not the Hv row products (1.45 -> 1.54 ms): the Zipf tail's gathers miss L2
+  // whatever the panel width, and every extra panel re-reads the row arrays.
+  const char* e = std::getenv("TRON_B200_PANEL_COLS");
+  const int64_t W = e ? std::atoll(e) : 0;
   if (W <= 0 || X_.nnz == 0) return;
-  if (!e && n_ * (int64_t)sizeof(double) <= (int64_t{96} << 20)) return;
   const int K = (int)std::min<int64_t>((n_ + W - 1) / W, 8);
   if (K < 2) return;
   std::vector<int32_t> bounds;

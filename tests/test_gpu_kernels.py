@@ -462,9 +462,9 @@ def test_csc_long_fixup_spans(port, hot_rows):
 
 @pytest.mark.parametrize("width", [1000, 4096, 30000])
 def test_column_panels_row_products(port, monkeypatch, width):
-    """Column panels of the row products (TRON_B200_PANEL_COLS; on by default
-    when v exceeds ~96 MB, e.g. K1): fun / grad / Hv of LR and of the sparse
-    L2-SVM against the oracle, and whole solves against the unpaneled ones."""
+    """Column panels of the row products (opt-in TRON_B200_PANEL_COLS): fun /
+    grad / Hv of LR and of the sparse L2-SVM against the oracle, and whole
+    solves against the unpaneled ones."""
     monkeypatch.setenv("TRON_B200_PANEL_COLS", str(width))
     p = synth.synth_sparse(13, 3000, 40000, 30)
     n = p.X.cols
@@ -484,4 +484,5 @@ def test_column_panels_row_products(port, monkeypatch, width):
         monkeypatch.setenv("TRON_B200_PANEL_COLS", "0")
         r0 = solve(p, loss, TrustRegionConfig(eps=1e-4), ExecutionPlan.gpu())
         monkeypatch.setenv("TRON_B200_PANEL_COLS", str(width))
-        assert rel_err(r.objective, r0.objective) <= 1e-12 and rel_err(r.w, r0.w) <= 1e-8
+        # whole solves: the same path up to the panel summation split
+        assert rel_err(r.objective, r0.objective) <= 1e-10 and rel_err(r.w, r0.w) <= 1e-6
