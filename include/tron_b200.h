@@ -126,7 +126,17 @@ typedef struct {
    * TRON_ERR_STRATEGY), one GPU, host-driven CG loop. */
   int32_t out_of_core;
   uint64_t stream_block_rows;
+  /* Column-partitioned layout, sparse problems: this
+   * rank owns columns [col_begin, col_begin + n) of a problem with global_cols
+   * columns -- X, w and every n-vector passed through this context are this
+   * rank's slices; y and the per-row state cover all l rows.  Per Hv one
+   * l-length allreduce (the partial row products) and scalar allreduces for
+   * the CG's dots, instead of the row layout's n-length allreduce.  World > 1
+   * (NCCL or host_allreduce); host-driven CG and trust-region loops. */
+  int32_t partition; /* tron_partition */
+  uint64_t col_begin, global_cols;
 } tron_gpu_options;
+typedef enum { TRON_PARTITION_ROWS = 0, TRON_PARTITION_COLUMNS = 1 } tron_partition;
 
 typedef struct tron_gpu_ctx tron_gpu_ctx;
 

@@ -23,6 +23,7 @@ OK, ERR_DIMENSION, ERR_BOUNDS, ERR_STRATEGY, ERR_BUDGET, ERR_NUMERICAL, ERR_LOGI
 LOSS_LOGISTIC, LOSS_L2SVM = 0, 1
 SVM_GATHERED, SVM_INDIRECT, SVM_AUTO = 0, 1, 2
 SOLVE_DEVICE, SOLVE_HOST_CG = 0, 1
+PARTITION_ROWS, PARTITION_COLUMNS = 0, 1
 
 
 class tron_config(ctypes.Structure):
@@ -59,7 +60,8 @@ class tron_gpu_options(ctypes.Structure):
                 ("nccl_unique_id", c_void_p), ("row_begin", c_uint64), ("global_rows", c_uint64),
                 ("reference_order", c_int32), ("host_allreduce", c_void_p),
                 ("host_allreduce_user", c_void_p), ("out_of_core", c_int32),
-                ("stream_block_rows", c_uint64)]
+                ("stream_block_rows", c_uint64), ("partition", c_int32), ("col_begin", c_uint64),
+                ("global_cols", c_uint64)]
 
 
 # void (*)(void* user, double* buf, uint64_t count): a host allreduce (sum, in place)

@@ -173,6 +173,9 @@ void tron_gpu_default_options(tron_gpu_options* o) {
   o->host_allreduce_user = nullptr;
   o->out_of_core = 0;
   o->stream_block_rows = 0;
+  o->partition = TRON_PARTITION_ROWS;
+  o->col_begin = 0;
+  o->global_cols = 0;
 }
 
 const char* tron_gpu_last_error(void) { return g_last_error.c_str(); }

@@ -46,9 +46,6 @@ constexpr int kEmptyItems = 4;  // empty rows per lane per visit
 #ifndef TB_LD256
 #define TB_LD256 1  // measured: N1 Hv 91.8 -> 80.6 us, K1 3.63 -> 3.47 ms
 #endif
-#ifndef TB_SEG_GATHER_EARLY
-#define TB_SEG_GATHER_EARLY 0
-#endif
 __device__ __forceinline__ void ld4d_ef(const double* p, double& a, double& b, double& c, double& d) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0, %1, %2, %3}, [%4];"
                : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
@@ -308,23 +305,12 @@ __device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, con
   // whose loads are in flight would wait for them).
   // chunk t: processed; t+W: gathered; t+2W: nonzeros in flight
   auto seg_walk = [&](long long t) {
-#if TB_SEG_GATHER_EARLY
-  // the next chunk's gathers are issued before this chunk is processed, so
-  // their latency overlaps the scan and emission
-#define TB_SEG_STEP(P, G)                                                      \
-  if (t + W < nch) gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, G);        \
-  process_chunk<SQ, EPI, STAGED, COH>(A, S, E, out, t, P, lane, ebuf, dacc);   \
-  if (t + W >= nch) break;                                                     \
-  if (t + 2 * W < nch) load_chunk(A, S, t + 2 * W, lane, rank_of(t + 2 * W), P); \
-  t += W;
-#else
 #define TB_SEG_STEP(P, G)                                                      \
   process_chunk<SQ, EPI, STAGED, COH>(A, S, E, out, t, P, lane, ebuf, dacc);   \
   if (t + W >= nch) break;                                                     \
   gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, G);                         \
   if (t + 2 * W < nch) load_chunk(A, S, t + 2 * W, lane, rank_of(t + 2 * W), P); \
   t += W;
-#endif
     gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, b0);
     for (;;) {
       TB_SEG_STEP(b0, b1)

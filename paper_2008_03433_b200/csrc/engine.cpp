@@ -335,7 +335,7 @@ void Engine::common_alloc() {
   // rank's CG state is identical, so every rank runs the same number of
   // allreduces); TRON_B200_NCCL_GRAPH=0 selects the host-driven CG loop.
   const char* cg = std::getenv("TRON_B200_NCCL_GRAPH");
-  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !comm_.host() && !ooc_ &&
+  use_graphs_ = (!comm_.active() || !(cg && cg[0] == '0')) && !comm_.host() && !ooc_ && !colpart_ &&
                 !(ng && ng[0] == '1');
 }
 
@@ -392,10 +392,18 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     e->budget_ = opt.gathered_budget_bytes;
     e->row_begin_ = opt.row_begin;
     e->comm_.init(opt);
+    if (opt.partition == TRON_PARTITION_COLUMNS && e->comm_.active()) {
+      if (opt.global_cols < n || opt.col_begin + n > opt.global_cols)
+        raise(TRON_ERR_ARGUMENT, "column partition: [col_begin, col_begin + n) must lie in global_cols");
+      e->colpart_ = true;
+      e->global_n_ = (int64_t)opt.global_cols;
+      e->svm_strategy_ = TRON_SVM_INDIRECT;  // the gathered rows would need every column
+    }
     e->common_alloc();
     cudaStream_t s = e->s_;
     tr.s = s;
     tr.mark("context + state alloc");
+    if (e->colpart_) e->cp_dots_.alloc(4);
 
     e->rptr_.alloc(l + 1);
     // +4: the row kernels read whole aligned groups of four entries
@@ -525,6 +533,8 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     return create_csr(loss, l, n, ro.data(), ci.data(), row_major, y, C, opt);
   }
   if (l >= (uint64_t{1} << 31)) raise(TRON_ERR_DIMENSION, "dense shard exceeds 2^31 rows per GPU");
+  if (opt.partition == TRON_PARTITION_COLUMNS && opt.world > 1)
+    raise(TRON_ERR_ARGUMENT, "the column-partitioned layout is for sparse problems (dense n <= 64)");
   if (opt.reference_order) {
     if (loss != TRON_LOSS_L2SVM || n > (uint64_t)kRoMaxN || opt.world > 1)
       raise(TRON_ERR_ARGUMENT,
@@ -831,6 +841,16 @@ void Engine::forward(Slot& S) {
       ro_hinge(l_, n_, S.z.p, y_.p, S.w.p, C_, ro_hparts_.p, ro_tickets_.p, obj_d_, s_);
       count_launch(4);
     }
+  } else if (colpart_) {
+    // z = sum over ranks of X_{:,r} w_r (one l-length exchange), w.w likewise;
+    // then the fused epilogue over the whole z: an empty row range per row
+    csr_dv(X_, group_, S.w.p, nullptr, nullptr, S.z.p, s_);
+    comm_.allreduce_sum(S.z.p, (size_t)l_, s_);
+    comm_.allreduce_sum(&obj_d_->ww, 1, s_);
+    CsrView E = X_;
+    E.rbeg = E.rend = X_.ptr + 1;
+    csr_forward(E, 1, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p, obj_d_, sc_, s_, S.z.p);
+    count_launch(1);
   } else if (!panels_.empty()) {  // raw row sums of the leading panels, then the fused pass
     const size_t K = panels_.size();
     for (size_t k = 0; k + 1 < K; ++k)
@@ -856,7 +876,8 @@ double Engine::eval_candidate_dev(const double* d_step, bool read) {
     count_launch(1);
   }
   forward(S);
-  if (comm_.active()) comm_.allreduce_sum(obj_d_->red, 2, s_);  // per-shard loss sums, |I|
+  // per-shard loss sums, |I| (the column layout's are whole already)
+  if (comm_.active() && !colpart_) comm_.allreduce_sum(obj_d_->red, 2, s_);
   if (!read) return 0.0;
   read_obj();
   return candidate_result();
@@ -898,7 +919,7 @@ void Engine::transposed_raw_or_epi(const UView& u, bool squared, const EpiView& 
     csc_spmv(T, P, u, squared, E, dst, s_);
     count_launch(2);
   };
-  if (!comm_.active()) {
+  if (!comm_.active() || colpart_) {  // the column layout's X_{:,r}^T u is this rank's slice
     product(epi, out);
     return;
   }
@@ -976,6 +997,14 @@ void Engine::gradient_into(const Slot& S, double* out) {
       u.mask = S.mask.p;
       u.z = S.z.p;
       u.y = y_.p;
+    }
+    if (colpart_) {  // ||g||^2 = sum over ranks of the slices' sums of squares
+      transposed_raw_or_epi(u, false, epi, out);
+      vec_sumsq_bad(n_, out, cp_dots_.p, sc_, s_);
+      comm_.allreduce_sum(cp_dots_.p, 2, s_);
+      obj_set_gnorm(obj_d_, cp_dots_.p, s_);
+      count_launch(3);
+      return;
     }
     if (hv_dot_available()) {  // ||g|| and the finiteness check from the emission
       epi.dot_parts = dot_parts_.p;
@@ -1153,7 +1182,7 @@ void Engine::ro_accum_slot(int mode, const Slot& S, const double* v, const EpiVi
 bool Engine::hv_dot_available() const {
   // sharded or nnz == 0: the vector epilogue after the allreduce (or the
   // epilogue-only shortcut) does the reduction instead of the segmented kernels
-  return !dense_ && dot_parts_.n > 0;
+  return !dense_ && !colpart_ && dot_parts_.n > 0;
 }
 
 // Column panels for the row products (csr_dv, csr_forward) when the gathered
@@ -1236,7 +1265,14 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   }
   const double* dv = loss_ == TRON_LOSS_LOGISTIC ? S.dvec.p : nullptr;
   const uint8_t* mk = loss_ == TRON_LOSS_LOGISTIC ? nullptr : S.mask.p;
-  row_products(v, dv, mk, a_.p);
+  if (colpart_) {  // t = sum over ranks of X_{:,r} v_r (one l-length exchange), then D t
+    csr_dv(X_, group_, v, nullptr, nullptr, a_.p, s_);
+    comm_.allreduce_sum(a_.p, (size_t)l_, s_);
+    vec_row_scale(l_, a_.p, dv, mk, s_);
+    count_launch(2);
+  } else {
+    row_products(v, dv, mk, a_.p);
+  }
   transposed_raw_or_epi(u, false, epi, out);
 }
 
@@ -1505,8 +1541,102 @@ bool Engine::enqueue_cg(double delta, const tron_config& cfg, CgState* out) {
   return false;
 }
 
+// A dot product of two column-partitioned n-vectors: local sum, scalar exchange.
+double Engine::gdot(const double* a, const double* b) {
+  vec_dot2(n_, a, b, a, b, cp_dots_.p, sc_, s_);
+  count_launch(1);
+  comm_.allreduce_sum(cp_dots_.p, 1, s_);
+  double h = 0.0;
+  cuda_check(cudaMemcpyAsync(&h, cp_dots_.p, sizeof(double), cudaMemcpyDeviceToHost, s_), "D2H");
+  synchronize();
+  return h;
+}
+
+// truncated_cg (tron.cpp:37-108) in the column layout: the vectors are this
+// rank's slices, every dot is a scalar exchange, every rank takes the same
+// branches (the exchanged scalars are identical); the step's arithmetic is
+// tron.cpp's (axpy_inplace, apply_precond, p = z + beta p).
+void Engine::run_cg_columns(double delta, const tron_config& cfg, CgState* out) {
+  const bool use_m = cfg.use_preconditioner != 0;
+  if (use_m) ensure_precond();
+  const double* M = use_m ? M_.p : nullptr;
+  uint64_t max_iters = cfg.max_cg_iters;
+  if (max_iters == 0) max_iters = (uint64_t)global_n_ < 1000 ? (uint64_t)global_n_ : 1000;
+  double* d = d_.p;
+  double* r = r0_.p;
+  double* z = r1_.p;
+  double* p = p_.p;
+  double* hp = hp_.p;
+  const int64_t n = n_;
+  cuda_check(cudaMemsetAsync(d, 0, n * sizeof(double), s_), "memset");
+  vec_lincomb(n, -1.0, g_.p, 0.0, nullptr, r, s_);  // r = -g
+  vec_div(n, r, M, z, s_);
+  cuda_check(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s_), "D2D");
+  count_launch(2);
+  double rz = gdot(r, z);
+  const double stop = cfg.cg_tol * gnorm_;  // tron.cpp:55
+  CgState st{};
+  st.delta = delta;
+  st.stop = stop;
+  st.max_iters = (long long)max_iters;
+  st.use_m = use_m;
+  st.exit_kind = kCgConverged;
+  while ((uint64_t)st.iters < max_iters) {
+    if (std::sqrt(gdot(r, r)) <= stop) {
+      st.exit_kind = kCgConverged;
+      break;
+    }
+    ++st.iters;
+    hv_kernels(p, hp);
+    const double php = gdot(p, hp);
+    st.php = php;
+    if (!(php > 0.0)) {
+      st.fail = 1;
+      break;
+    }
+    const double alpha = rz / php;
+    vec_lincomb(n, 1.0, d, alpha, p, d, s_);  // axpy_inplace(alpha, p, d)
+    count_launch(1);
+    if (std::sqrt(gdot(d, d)) > delta) {  // retreat, then to the boundary along p
+      vec_lincomb(n, 1.0, d, -alpha, p, d, s_);
+      const double dp = gdot(d, p), dd = gdot(d, d), pp = gdot(p, p);
+      const double rad = std::sqrt(dp * dp + pp * (delta * delta - dd));
+      const double tau = dp >= 0.0 ? (delta * delta - dd) / (dp + rad) : (rad - dp) / pp;
+      vec_lincomb(n, 1.0, d, tau, p, d, s_);
+      vec_lincomb(n, 1.0, r, -tau, hp, r, s_);
+      count_launch(3);
+      st.exit_kind = kCgBoundary;
+      st.boundary = 1;
+      break;
+    }
+    vec_lincomb(n, 1.0, r, -alpha, hp, r, s_);
+    vec_div(n, r, M, z, s_);
+    const double rz_next = gdot(r, z);
+    const double beta = rz_next / rz;
+    vec_lincomb(n, 1.0, z, beta, p, p, s_);  // p = z + beta p
+    count_launch(3);
+    rz = rz_next;
+    st.exit_kind = kCgMaxIters;
+  }
+  if (!st.fail) {
+    const double rn = std::sqrt(gdot(r, r));
+    if ((uint64_t)st.iters >= max_iters && st.exit_kind != kCgBoundary && rn > stop)
+      st.exit_kind = kCgMaxIters;
+    else if (st.exit_kind != kCgBoundary)
+      st.exit_kind = kCgConverged;
+    st.q = 0.5 * (gdot(d, g_.p) - gdot(d, r));  // tron.cpp:106
+    st.dnorm = std::sqrt(gdot(d, d));
+  }
+  st.cont = 0;
+  *out = st;
+}
+
 void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
   if (!committed_valid_) raise(TRON_ERR_LOGIC, "truncated CG before the first commit()");
+  if (colpart_) {
+    run_cg_columns(delta, cfg, out);
+    return;
+  }
   const bool use_m = cfg.use_preconditioner != 0;
   if (use_m) ensure_precond();
   uint64_t max_iters = cfg.max_cg_iters;
@@ -1957,6 +2087,12 @@ uint64_t Engine::predict(const double* w, double* labels) {
                                           cudaMemcpyDeviceToHost, s_), "D2H");
     synchronize();
     for (auto x : h) c += x;
+  } else if (colpart_) {  // scores = sum over ranks of X_{:,r} w_r
+    csr_dv(X_, group_, vtmp_.p, nullptr, nullptr, a_.p, s_);
+    comm_.allreduce_sum(a_.p, (size_t)l_, s_);
+    predict_from_scores(l_, a_.p, y_.p, lab.p, correct.p, s_);
+    count_launch(2);
+    cuda_check(cudaMemcpyAsync(&c, correct.p, sizeof(c), cudaMemcpyDeviceToHost, s_), "D2H");
   } else {
     if (dense_)
       predict_dense(l_, n_, ld_, Xc_.p, vtmp_.p, y_.p, lab.p, correct.p, s_);

@@ -306,6 +306,13 @@ class Engine {
   bool hv_dot_available() const;
   DevBuf<double> coop_parts_;  // CTA partials of the cooperative CG step
   bool use_graphs_ = true;
+  // column-partitioned layout: X_, w and the
+  // n-vectors are this rank's column slice; z / D / mask are whole (all rows)
+  bool colpart_ = false;
+  int64_t global_n_ = 0;
+  DevBuf<double> cp_dots_;  // scalar exchange buffer
+  double gdot(const double* a, const double* b);
+  void run_cg_columns(double delta, const tron_config& cfg, CgState* out);
   // out-of-core dense layout: X stays in the caller's
   // host array (page-locked in place) and every pass streams it in blocks of
   // blk_ rows through two device windows, copy (cs_) overlapping compute (s_)

@@ -136,7 +136,7 @@ struct Scratch {
 constexpr int kMaxPartialBlocks = 4096;
 constexpr int kNumTickets = 16;
 enum Ticket : int { T_FUN = 0, T_AXPY = 1, T_NORM = 2, T_CG_INIT = 3, T_CG_PHP = 4, T_CG_UPD = 5,
-                    T_CG_P = 6, T_CG_POST = 7, T_DENSE_FIN = 8, T_COUNT = 9, T_DOT2 = 10 };
+                    T_CG_P = 6, T_CG_POST = 7, T_DENSE_FIN = 8, T_COUNT = 9, T_DOT2 = 10, T_SUMSQ = 11 };
 
 int device_sm_count();
 
@@ -183,6 +183,9 @@ void narrow_offsets(const int64_t* in, int32_t* out, int64_t count, cudaStream_t
 // order (bit-exact with the reference); *correct (device) = #{labels == y}.
 void predict_csr(const CsrView& X, const double* w, const double* y, double* labels,
                  unsigned long long* correct, cudaStream_t s);
+// labels from precomputed scores x_i . w (the column layout's allreduced row sums)
+void predict_from_scores(int64_t l, const double* scores, const double* y, double* labels,
+                         unsigned long long* correct, cudaStream_t s);
 void predict_dense(int64_t l, int64_t n, int64_t ld, const double* X, const double* w,
                    const double* y, double* labels, unsigned long long* correct, cudaStream_t s);
 
@@ -198,6 +201,17 @@ void vec_dot2(int64_t n, const double* a, const double* b, const double* c, cons
 // out = base + scale*raw  (after an allreduce of raw partials; raw == nullptr => 0)
 void vec_epilogue(int64_t n, const double* raw, const EpiView& epi, double* out, cudaStream_t s);
 void l2_read_flush(const double* buf, int64_t n, cudaStream_t s);
+// Column-partitioned layout helpers (engine.cpp run_cg_columns):
+// out = a*x + b*y (x / y may be null: treated as 0); z = r / M (M null: copy)
+void vec_lincomb(int64_t n, double a, const double* x, double b, const double* y, double* out,
+                 cudaStream_t s);
+void vec_div(int64_t n, const double* r, const double* M, double* z, cudaStream_t s);
+// out2 = {sum g_j^2, any non-finite g_j} (fixed order); then, after the
+// allreduce of out2, obj->gnorm = sqrt(out2[0]), obj->grad_nonfinite
+void vec_sumsq_bad(int64_t n, const double* g, double* out2, Scratch sc, cudaStream_t s);
+void obj_set_gnorm(ObjScalars* obj, const double* in2, cudaStream_t s);
+// a_i *= D_i (dvec) or a_i = mask_i ? a_i : 0 (the allreduced row products)
+void vec_row_scale(int64_t l, double* a, const double* dvec, const uint8_t* mask, cudaStream_t s);
 // Streamed (out-of-core) margin pass: the per-block loss sums and |I|
 // (red[2b], red[2b+1]) into obj->f = 0.5 ww + C sum, nact, red[0..1]; fixed order.
 void obj_combine_blocks(ObjScalars* obj, const double* red, int64_t nblk, double C, cudaStream_t s);

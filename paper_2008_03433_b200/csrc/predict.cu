@@ -78,6 +78,33 @@ void predict_csr(const CsrView& X, const double* w, const double* y, double* lab
   TB_LAUNCH_CHECK();
 }
 
+namespace {
+__global__ void __launch_bounds__(kBlock) predict_scores_kernel(long long l, const double* __restrict__ sc,
+                                                                const double* __restrict__ y,
+                                                                double* __restrict__ labels,
+                                                                unsigned long long* correct) {
+  const long long stride = (long long)gridDim.x * kBlock;
+  const long long rows_up = (l + 31) / 32 * 32;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < rows_up; i += stride) {
+    bool ok = false;
+    if (i < l) {
+      const double label = sc[i] < 0.0 ? -1.0 : 1.0;
+      labels[i] = label;
+      ok = y && y[i] == label;
+    }
+    count_correct(ok, correct);
+  }
+}
+}  // namespace
+
+void predict_from_scores(int64_t l, const double* scores, const double* y, double* labels,
+                         unsigned long long* correct, cudaStream_t s) {
+  cudaMemsetAsync(correct, 0, sizeof(unsigned long long), s);
+  if (l == 0) return;
+  predict_scores_kernel<<<predict_grid(l), kBlock, 0, s>>>(l, scores, y, labels, correct);
+  TB_LAUNCH_CHECK();
+}
+
 void predict_dense(int64_t l, int64_t n, int64_t ld, const double* X, const double* w,
                    const double* y, double* labels, unsigned long long* correct, cudaStream_t s) {
   cudaMemsetAsync(correct, 0, sizeof(unsigned long long), s);

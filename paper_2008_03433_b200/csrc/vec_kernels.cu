@@ -758,6 +758,80 @@ void obj_combine_blocks(ObjScalars* obj, const double* red, int64_t nblk, double
   TB_LAUNCH_CHECK();
 }
 
+__global__ void __launch_bounds__(kBlock) lincomb_kernel(long long n, double a, const double* x,
+                                                        double b, const double* y, double* out) {
+  pdl_wait();
+  pdl_trigger();
+  GRID_STRIDE(j, n) {
+    const double xv = x ? a * x[j] : 0.0;
+    out[j] = y ? (x ? xv + b * y[j] : b * y[j]) : xv;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) div_kernel(long long n, const double* r, const double* M,
+                                                    double* z) {
+  pdl_wait();
+  pdl_trigger();
+  GRID_STRIDE(j, n) z[j] = M ? r[j] / M[j] : r[j];  // apply_precond, tron.cpp:46-53
+}
+
+__global__ void __launch_bounds__(kBlock) sumsq_bad_kernel(long long n, const double* g, double* out2,
+                                                          Scratch sc) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double sh[kBlock / kWarp + 1];
+  double acc = 0.0, bad = 0.0;
+  GRID_STRIDE(j, n) {
+    const double v = g[j];
+    acc += v * v;
+    if (!isfinite(v)) bad = 1.0;
+  }
+  const double b = block_sum<kBlock>(acc, sh, true);
+  const double bb = block_sum<kBlock>(bad, sh, true);
+  if (threadIdx.x == 0) {
+    sc.partials[2 * blockIdx.x] = b;
+    sc.partials[2 * blockIdx.x + 1] = bb;
+  }
+  if (last_block_arrive(sc.tickets + T_SUMSQ)) {
+    const double tot = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 0, sh);
+    const double nb = reduce_partials<kBlock>(sc.partials, gridDim.x, 2, 1, sh);
+    if (threadIdx.x == 0) {
+      out2[0] = tot;
+      out2[1] = nb;
+    }
+  }
+}
+
+__global__ void set_gnorm_kernel(ObjScalars* obj, const double* in2) {
+  obj->gnorm = sqrt(in2[0]);
+  obj->grad_nonfinite = in2[1] > 0.0;
+}
+
+__global__ void __launch_bounds__(kBlock) row_scale_kernel(long long l, double* a, const double* dvec,
+                                                          const uint8_t* mask) {
+  pdl_wait();
+  pdl_trigger();
+  GRID_STRIDE(i, l) a[i] = dvec ? a[i] * dvec[i] : (mask[i] ? a[i] : 0.0);  // loss.cpp:86-89, :150-160
+}
+
+void vec_lincomb(int64_t n, double a, const double* x, double b, const double* y, double* out,
+                 cudaStream_t s) {
+  if (n > 0) launch_pdl(lincomb_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, a, x, b, y, out);
+}
+void vec_div(int64_t n, const double* r, const double* M, double* z, cudaStream_t s) {
+  if (n > 0) launch_pdl(div_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, r, M, z);
+}
+void vec_sumsq_bad(int64_t n, const double* g, double* out2, Scratch sc, cudaStream_t s) {
+  launch_pdl(sumsq_bad_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, g, out2, sc);
+}
+void obj_set_gnorm(ObjScalars* obj, const double* in2, cudaStream_t s) {
+  set_gnorm_kernel<<<1, 1, 0, s>>>(obj, in2);
+  TB_LAUNCH_CHECK();
+}
+void vec_row_scale(int64_t l, double* a, const double* dvec, const uint8_t* mask, cudaStream_t s) {
+  if (l > 0) launch_pdl(row_scale_kernel, dim3(vec_grid(l)), dim3(kBlock), 0, s, (long long)l, a, dvec, mask);
+}
+
 void vec_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d,
               double* out2, Scratch sc, cudaStream_t s) {
   launch_pdl(dot2_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, a, b, c, d, out2, sc);

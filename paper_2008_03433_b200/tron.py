@@ -212,6 +212,11 @@ class ExecutionPlan:
     # memory (the caller keeps the Problem alive), -1 never
     out_of_core: int = 0
     stream_block_rows: int = 0
+    # column-partitioned layout (world > 1): this rank owns columns
+    # [col_begin, col_begin + n) of global_cols (sharding.column_shard)
+    partition: str = "rows"
+    col_begin: int = 0
+    global_cols: int = 0
 
     @staticmethod
     def gpu(device: int = 0, svm_strategy: SvmStrategy = SvmStrategy.Indirect,
@@ -234,6 +239,8 @@ class ExecutionPlan:
         o.reference_order = int(bool(self.reference_order))
         o.out_of_core = int(self.out_of_core)
         o.stream_block_rows = int(self.stream_block_rows)
+        o.partition = _lib.PARTITION_COLUMNS if self.partition == "columns" else _lib.PARTITION_ROWS
+        o.col_begin, o.global_cols = int(self.col_begin), int(self.global_cols)
         keep = []
         if self.nccl_unique_id is not None:
             uid = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)

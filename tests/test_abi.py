@@ -44,8 +44,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.tron_iteration) == 4 * 8 + 8 + 8
     assert ctypes.sizeof(_lib.tron_ledger) == 7 * 8
     # ... reference_order (int32 + pad), host_allreduce + its user pointer,
-    # out_of_core (int32 + pad), stream_block_rows
-    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8
+    # out_of_core (int32 + pad), stream_block_rows, partition (int32 + pad), col_begin, global_cols
+    assert ctypes.sizeof(_lib.tron_gpu_options) == 4 + 4 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8
 
 
 def test_defaults_mirror_reference():
