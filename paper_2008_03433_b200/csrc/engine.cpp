@@ -664,6 +664,19 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
     e->idx_tmp_.alloc((l + 1023) / 1024 + 2);
     e->count_.alloc(1);
   }
+  {  // Gram mode (TRON_B200_DENSE_GRAM=0 keeps the tall-skinny passes)
+    const char* gm = std::getenv("TRON_B200_DENSE_GRAM");
+    const bool off = gm && gm[0] == '0';
+    if (!off && !e->ro_ && !e->ooc_ && n > 0 && n <= (uint64_t)kDenseMaxN &&
+        !(loss == TRON_LOSS_L2SVM && e->svm_strategy_ == TRON_SVM_GATHERED)) {
+      AllocScope scope(e->s_);
+      e->gram_ = true;
+      if (e->svm_strategy_ == TRON_SVM_AUTO) e->svm_strategy_ = TRON_SVM_INDIRECT;  // G is compact already
+      for (auto& S : e->slot_) S.gram.alloc((size_t)n * n);
+      e->gram_parts_.alloc((size_t)gram_grid((int64_t)l) * n * n);
+      cuda_check(cudaStreamSynchronize(e->s_), "gram buffers");
+    }
+  }
   if (e->ro_) {
     AllocScope scope(e->s_);
     if (dense_make_map_box(&e->xmap128_, e->Xc_.p, e->ld_, (int64_t)l, (int64_t)n, 128) != 0)
@@ -987,6 +1000,7 @@ void Engine::gradient_into(const Slot& S, double* out) {
   }
   if (dense_) {
     dense_vector(-1, nullptr, epi, out, &S);  // partials from the fused margin pass
+    if (gram_) gram_slot(S);                  // the Hessian of this iterate, once per commit
   } else {
     UView u;
     if (loss_ == TRON_LOSS_LOGISTIC) {
@@ -1235,6 +1249,16 @@ void Engine::row_products(const double* v, const double* dvec, const uint8_t* ma
   count_launch(K);
 }
 
+// G = sum_i c_i x_i x_i^T of slot S (c = its mask or D), summed over the
+// shards when row-sharded (one n*n exchange per commit, none per Hv).
+void Engine::gram_slot(const Slot& S) {
+  const bool svm = loss_ == TRON_LOSS_L2SVM;
+  dense_gram(l_, n_, ld_, Xc_.p, svm ? S.mask.p : nullptr, svm ? nullptr : S.dvec.p, gram_parts_.p,
+             S.gram.p, s_);
+  count_launch(2);
+  if (comm_.active()) comm_.allreduce_sum(S.gram.p, (size_t)n_ * n_, s_);
+}
+
 void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   const Slot& S = slot_[cand_ ^ 1];
   EpiView epi;
@@ -1248,6 +1272,11 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
   }
   if (ro_) {
     ro_accum_slot(RO_HV, S, v, epi, out);
+    return;
+  }
+  if (dense_ && gram_) {  // v + s G v
+    gram_hv(n_, S.gram.p, v, epi.scale, out, s_);
+    count_launch(1);
     return;
   }
   if (dense_) {
@@ -1322,6 +1351,9 @@ void Engine::precond_kernels(const Slot& S) {
   epi.scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
   if (ro_) {
     ro_accum_slot(RO_PRECOND, S, nullptr, epi, M_.p);
+  } else if (dense_ && gram_) {
+    gram_precond(n_, S.gram.p, epi.scale, M_.p, s_);
+    count_launch(1);
   } else if (dense_) {
     const int saved = cand_;
     cand_ = (int)(&S - slot_) ^ 1;  // dense_vector reads the committed slot_[cand_ ^ 1]
@@ -1410,7 +1442,11 @@ void Engine::capture_cg_body(int k, const CgVectors& v, Cond cond) {
     ro_cg_step(v, st_d_, cond, s_);
     count_launch(1);
   } else if (small_engine_) {
-    if (dense_ && !comm_.active() && !ooc_) {  // sharded / streamed: through hv_kernels
+    if (dense_ && gram_) {  // hp = p + s G p inside the step kernel
+      const double scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
+      cg_small_step_gram(v, slot_[k].gram.p, scale, st_d_, cond, s_);
+      count_launch(1);
+    } else if (dense_ && !comm_.active() && !ooc_) {  // sharded / streamed: through hv_kernels
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;
       const double scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;

@@ -180,6 +180,7 @@ class Engine {
     DevBuf<double> gparts;  // dense: gradient partials from this slot's margin pass
     DevBuf<int32_t> idx;    // reference order: this slot's active set I (ascending)
     DevBuf<long long> cnt;  // ... and |I| (device)
+    DevBuf<double> gram;    // dense Gram mode: this slot's Hessian sum_i c_i x_i x_i^T (n x n)
     double f = 0.0;
     long long nact = 0;
     bool valid = false;
@@ -306,6 +307,11 @@ class Engine {
   bool hv_dot_available() const;
   DevBuf<double> coop_parts_;  // CTA partials of the cooperative CG step
   bool use_graphs_ = true;
+  // dense problems (n <= 64): the Hessian as an n x n matrix formed once per
+  // commit (gram.cu); Hv / the preconditioner then read G instead of X
+  bool gram_ = false;
+  DevBuf<double> gram_parts_;
+  void gram_slot(const Slot& S);
   // column-partitioned layout: X_, w and the
   // n-vectors are this rank's column slice; z / D / mask are whole (all rows)
   bool colpart_ = false;

@@ -323,6 +323,20 @@ void compact_mask(int64_t l, const uint8_t* mask, int32_t* idx, int32_t* tmp, lo
 void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int32_t* idx,
                   double* Xg, int64_t ldg, cudaStream_t s);
 
+// ---- the dense Hessian as an n x n matrix (gram.cu), n <= 64 ----------------
+// G = sum_i c_i x_i x_i^T, c = mask (SVM, dvec null) or dvec (LR); partials
+// >= gram_grid(l) * n * n doubles.  Deterministic.
+int gram_grid(int64_t l);
+void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
+                const double* dvec, double* partials, double* G, cudaStream_t s);
+// out = v + scale * G v (row j of G dotted with v in index order)
+void gram_hv(int64_t n, const double* G, const double* v, double scale, double* out, cudaStream_t s);
+// M_j = 1 + scale * G_jj (loss.cpp:176-188)
+void gram_precond(int64_t n, const double* G, double scale, double* M, cudaStream_t s);
+// The small-n CG step with hp = p + scale * G p formed first.
+void cg_small_step_gram(const CgVectors& v, const double* G, double scale, CgState* st, Cond cond,
+                        cudaStream_t s);
+
 // ---- reference-order reductions for the dense L2-SVM (refexact.cu) --------
 // Bit-for-bit the reference's arithmetic: 64 sequential block sums + the
 // pairwise tree (parallel.hpp:14-34), serial n-length dots.  n <= kRoMaxN.

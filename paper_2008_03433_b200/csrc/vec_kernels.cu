@@ -440,14 +440,23 @@ template <int SPLIT>
 __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
                                                                     const double* partials,
                                                                     int nparts, double scale,
-                                                                    CgState* st, Cond cond) {
+                                                                    CgState* st, Cond cond,
+                                                                    const double* gram) {
   pdl_wait();
   pdl_trigger();
   __shared__ double sh[kSmallBlock / kWarp + 1];
   __shared__ double s_part[kSmallBlock];
   __shared__ int s_flag;
   const long long n = v.n;
-  if (partials) {
+  if (gram) {
+    // hp = p + scale * G p (gram.cu: the dense Hessian of the committed iterate)
+    for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
+      double t = 0.0;
+      for (long long k = 0; k < n; ++k) t += gram[j * n + k] * v.p[k];
+      v.hp[j] = v.p[j] + scale * t;
+    }
+    __syncthreads();
+  } else if (partials) {
     // hp_j = p_j + scale * sum_b partials[b*n + j], fixed order (SPLIT lanes per j)
     const int per = kSmallBlock / SPLIT;  // coordinates handled per pass
     for (long long j0 = 0; j0 < n; j0 += per) {
@@ -855,15 +864,23 @@ void cg_small_init(const CgVectors& v, CgState* st, Cond cond, cudaStream_t s) {
 
 void cg_small_step(const CgVectors& v, const double* partials, int nparts, double scale,
                    CgState* st, Cond cond, cudaStream_t s) {
+  const double* no_gram = nullptr;
   if (v.n <= 32)
     launch_pdl(cg_small_step_kernel<16>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
-               st, cond);
+               st, cond, no_gram);
   else if (v.n <= 64)
     launch_pdl(cg_small_step_kernel<8>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
-               st, cond);
+               st, cond, no_gram);
   else
     launch_pdl(cg_small_step_kernel<1>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
-               st, cond);
+               st, cond, no_gram);
+}
+
+void cg_small_step_gram(const CgVectors& v, const double* G, double scale, CgState* st, Cond cond,
+                        cudaStream_t s) {
+  const double* no_parts = nullptr;
+  launch_pdl(cg_small_step_kernel<8>, dim3(1), dim3(kSmallBlock), 0, s, v, no_parts, 0, scale, st, cond,
+             G);
 }
 
 namespace {
