@@ -575,8 +575,32 @@ def main():
     kt = ev.bench_kernels(reps=20, flush_l2=True)
     ab = algorithmic_bytes(p)
     peak, peak_kind = load_peaks()
-    achieved = ab["hv"] / (kt["hv_ms"] / 1e3) / 1e9
+    mode = ev.mode()
     trans_gbs = ab["transposed"] / (kt["transposed_ms"] / 1e3) / 1e9
+    n_evals = res.trace.objective_evaluations
+    if p.X.layout == "dense" and mode["gram"]:
+        # Hessian as an n x n matrix per commit (gram.cu): the CG's Hv no longer
+        # reads X; the passes over X are the fused margin pass (one per
+        # evaluation) and the Gram pass (one per evaluation, speculative with
+        # the gradient).  The roofline object describes the larger of the two.
+        l, n = p.X.rows, p.X.cols
+        fwd_bytes, gram_bytes = 8 * l * n + 17 * l, 8 * l * n + l
+        if kt["grad_ms"] >= kt["forward_ms"]:
+            kern, kbytes, kms = "Gram pass G = sum_i c_i x_i x_i^T (gram.cu; once per commit)", gram_bytes, kt["grad_ms"]
+        else:
+            kern, kbytes, kms = "fused margin pass (dense_pass FWD: margins, mask, f, gradient partials)", fwd_bytes, kt["forward_ms"]
+        achieved = kbytes / (kms / 1e3) / 1e9
+        share = n_evals * kms / (t_step * 1e3) if t_step > 0 else None
+        gram_extra = {"gram_pass_ms": kt["grad_ms"], "gram_fp64_tflops": l * n * (n + 1) / (kt["grad_ms"] / 1e3) / 1e12,
+                      "hv_from_gram_us": kt["hv_ms"] * 1e3,
+                      "tall_skinny_hv_pass_ms": kt["transposed_ms"], "tall_skinny_hv_gbs": trans_gbs}
+    else:
+        kern = ("Hessian-vector product (CSR D*Xv + CSC segmented X^T u)" if p.X.layout == "csr"
+                else "Hessian-vector product (dense tall-skinny TMA pass, one read of X)")
+        kbytes, kms = ab["hv"], kt["hv_ms"]
+        achieved = kbytes / (kms / 1e3) / 1e9
+        share = res.hessian_products * kms / (t_step * 1e3) if t_step > 0 else None
+        gram_extra = {}
 
     # ---- e2e through the public API, every step: make_evaluator from the
     # caller's PAGEABLE numpy arrays (H2D + on-device CSC build / transpose),
@@ -634,17 +658,16 @@ def main():
         "objective": res.objective, "converged": res.converged,
         "outer_iterations": len(res.trace.iterations), "hessian_products": res.hessian_products,
         "hv_per_s": res.hessian_products / t_step if t_step > 0 else None,
-        "roofline": {"bound": "hbm",
-                     "kernel": ("Hessian-vector product (CSR D*Xv + CSC segmented X^T u)" if p.X.layout == "csr"
-                                else "Hessian-vector product (dense tall-skinny TMA pass, one read of X)"),
+        "roofline": {"bound": "hbm", "kernel": kern,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs: copy read+write GB/s)",
-                     "traffic": read_traffic(args.workload),
-                     "algorithmic_bytes_per_launch": ab["hv"], "avg_launch_ms": kt["hv_ms"],
-                     "launch_timing": "CUDA events around each Hv launch on the solver stream, 256 MiB "
+                     "traffic": read_traffic(args.workload + ("-gram" if gram_extra else "")),
+                     "algorithmic_bytes_per_launch": kbytes, "avg_launch_ms": kms,
+                     "launch_timing": "CUDA events around each launch on the solver stream, 256 MiB "
                                       "read-based L2 eviction before each, mean of 20, after the timed solves",
-                     "hv_share_of_step": res.hessian_products * kt["hv_ms"] / (t_step * 1e3) if t_step > 0 else None,
-                     "transposed_only_gbs": trans_gbs, "kernel_ms": kt},
+                     "share_of_step": share,
+                     "transposed_only_gbs": trans_gbs, "kernel_ms": kt, **gram_extra},
+        "mode": mode,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes(p),
                 "d2h_bytes_per_step": int(8 * p.X.cols + 64),

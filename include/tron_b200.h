@@ -210,6 +210,13 @@ int tron_gpu_reset_ledger(tron_gpu_ctx *ctx);
  * pass, [3] the gradient.  flush_l2 evicts the L2 between launches by
  * reading a 256 MiB buffer (nothing dirty is left to write back). */
 int tron_gpu_bench_kernels(tron_gpu_ctx *ctx, int reps, int flush_l2, double out_ms[4]);
+/* How this context runs its hot path (bit set): TRON_MODE_GRAM (dense: the
+ * Hessian as an n x n matrix per commit), TRON_MODE_OUT_OF_CORE (X streamed from
+ * host memory), TRON_MODE_COLUMNS (column-partitioned), TRON_MODE_DEVICE_LOOP
+ * (the solve is one graph launch), TRON_MODE_SHARDED (row shards). */
+enum { TRON_MODE_GRAM = 1, TRON_MODE_OUT_OF_CORE = 2, TRON_MODE_COLUMNS = 4, TRON_MODE_DEVICE_LOOP = 8,
+       TRON_MODE_SHARDED = 16 };
+int tron_gpu_mode(tron_gpu_ctx *ctx, uint32_t *flags);
 /* Device bytes held by the context (matrix copies + vectors). */
 int tron_gpu_memory_bytes(tron_gpu_ctx *ctx, uint64_t *bytes);
 /* Number of kernel launches issued by this context since creation. */

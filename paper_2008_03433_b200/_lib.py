@@ -24,6 +24,7 @@ LOSS_LOGISTIC, LOSS_L2SVM = 0, 1
 SVM_GATHERED, SVM_INDIRECT, SVM_AUTO = 0, 1, 2
 SOLVE_DEVICE, SOLVE_HOST_CG = 0, 1
 PARTITION_ROWS, PARTITION_COLUMNS = 0, 1
+MODE_GRAM, MODE_OUT_OF_CORE, MODE_COLUMNS, MODE_DEVICE_LOOP, MODE_SHARDED = 1, 2, 4, 8, 16
 
 
 class tron_config(ctypes.Structure):
@@ -102,6 +103,7 @@ SIGNATURES = [
     ("tron_gpu_reset_ledger", c_int, [c_void_p]),
     ("tron_gpu_bench_kernels", c_int, [c_void_p, c_int, c_int, PD]),
     ("tron_gpu_memory_bytes", c_int, [c_void_p, PU64]),
+    ("tron_gpu_mode", c_int, [c_void_p, POINTER(ctypes.c_uint32)]),
     ("tron_gpu_launch_count", c_int, [c_void_p, PU64]),
     ("tron_gpu_synchronize", c_int, [c_void_p]),
     ("tron_gpu_nccl_unique_id", c_int, [c_void_p]),

@@ -484,6 +484,12 @@ int tron_gpu_bench_kernels(tron_gpu_ctx* ctx, int reps, int flush_l2, double out
   });
 }
 
+int tron_gpu_mode(tron_gpu_ctx* ctx, uint32_t* flags) {
+  NEED_CTX(ctx);
+  if (flags) *flags = ctx->engine->mode_flags();
+  return TRON_OK;
+}
+
 int tron_gpu_memory_bytes(tron_gpu_ctx* ctx, uint64_t* bytes) {
   NEED_CTX(ctx);
   *bytes = ctx->engine->memory_bytes();

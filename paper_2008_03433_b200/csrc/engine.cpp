@@ -673,7 +673,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       e->gram_ = true;
       if (e->svm_strategy_ == TRON_SVM_AUTO) e->svm_strategy_ = TRON_SVM_INDIRECT;  // G is compact already
       for (auto& S : e->slot_) S.gram.alloc((size_t)n * n);
-      e->gram_parts_.alloc((size_t)gram_grid((int64_t)l) * n * n);
+      e->gram_parts_.alloc((size_t)gram_grid((int64_t)l, (int64_t)n) * n * n);
       cuda_check(cudaStreamSynchronize(e->s_), "gram buffers");
     }
   }
@@ -731,6 +731,12 @@ void Engine::screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_
   cuda_check(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, s_), "D2H");
   synchronize();
   if (h[0] != ~0ull || h[1] != ~0ull) report((uint64_t)h[0], (uint64_t)h[1]);
+}
+
+uint32_t Engine::mode_flags() const {
+  return (gram_ ? TRON_MODE_GRAM : 0) | (ooc_ ? TRON_MODE_OUT_OF_CORE : 0) |
+         (colpart_ ? TRON_MODE_COLUMNS : 0) | (device_loop_ok() ? TRON_MODE_DEVICE_LOOP : 0) |
+         (comm_.active() && !colpart_ ? TRON_MODE_SHARDED : 0);
 }
 
 uint64_t Engine::memory_bytes() const {

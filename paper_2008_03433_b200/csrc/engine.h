@@ -163,6 +163,7 @@ class Engine {
   tron_ledger ledger{};
   uint64_t launches = 0;
   uint64_t memory_bytes() const;
+  uint32_t mode_flags() const;
   void synchronize();
 
   // Device-side building blocks (also used by the host-CG adapter).

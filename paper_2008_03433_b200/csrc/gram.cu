@@ -10,14 +10,13 @@
 // X of a P1 solve become 4.  The preconditioner diagonal (loss.cpp:176-188) is
 // 1 + s G_jj.
 //
-// gram_kernel: CTAs stride over 128-row tiles of the column-major X.  A tile
-// and its row weights are staged in shared memory; thread (b, ph) owns the 4x4
-// block b of the upper triangle (NB (NB+1) / 2 blocks, NB = ceil(n/4)) over the
-// rows r = ph (mod P) of the tile, 16 register accumulators, 8 shared loads per
-// 16 FMAs (explicit __fma_rn: the build's -fmad=false would split them; G is not
-// a reference quantity, so the fused rounding costs no parity).  The P row phases are combined in a fixed order, the CTA writes its
-// full n x n partial (mirrored), and gram_finalize sums the CTA partials in
-// index order: deterministic.
+// gram_kernel: CTAs stride over 128-row tiles of the column-major X, staged in
+// shared memory (weights applied); the FP64 tensor cores (DMMA m8n8k4) form
+// the tile's G blocks, 8 warps splitting the tile's 32 k-steps; the warps'
+// partials are added in warp order, the CTA writes its n x n partial, and
+// gram_finalize sums the CTA partials in index order: deterministic.  (DMMA
+// fuses multiply and add: G is not a reference quantity, so the rounding costs
+// no parity.)
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,94 +24,127 @@ namespace tb {
 
 namespace {
 
+// Tile of 128 rows staged column-major with a padded stride (132 = 4 mod 16
+// doubles: the DMMA fragment loads below hit distinct banks in each half-warp).
 constexpr int kGramRows = 128;
-constexpr int kGramStride = kGramRows + 1;  // padded columns: spreads the blocks over the banks
-constexpr int kGramThreads = 256;
+constexpr int kGramStride = 132;
+constexpr int kGramThreads = 256;  // 8 warps; warp w takes the k-steps w, w+8, ... of a tile
 
-__global__ void __launch_bounds__(kGramThreads) gram_kernel(long long l, int n, long long ld,
-                                                           const double* __restrict__ X,
-                                                           const uint8_t* __restrict__ mask,
-                                                           const double* __restrict__ dvec,
-                                                           double* __restrict__ partials) {
+// mma.sync m8n8k4 f64 (DMMA): D(8x8) += A(8x4) B(4x8); per lane one A and one
+// B element and two accumulators (row g = lane/4, columns 2t, 2t+1, t = lane%4).
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// G = T^T C T over the tiles T (rows of X) with C = diag(c): the n columns in
+// NB groups of 8; for a k-step of four rows one fragment per group serves as
+// B (block column) and, times the row weight c_r, as A (block row) -- NB
+// loads feed NB (NB+1)/2 DMMAs.  Tiles are double-buffered with cp.async: the
+// next tile's rows and weights are in flight while this one is multiplied.
+template <int NB, bool MASK>
+__global__ void __launch_bounds__(kGramThreads, NB <= 5 ? 2 : 1) gram_kernel(long long l, int n, long long ld,
+                                                              const double* __restrict__ X,
+                                                              const uint8_t* __restrict__ mask,
+                                                              const double* __restrict__ dvec,
+                                                              double* __restrict__ partials) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) double gs[];  // [NB*4][kGramStride] tile, then [kGramRows] weights
-  const int NB = (n + 3) >> 2;
-  const int NC = NB * 4;
-  double* cs = gs + (size_t)NC * kGramStride;
-  const int nblk = NB * (NB + 1) / 2;
-  const int P = kGramThreads / nblk;  // row phases per block (>= 1 for n <= 64)
-  const int tid = threadIdx.x;
-  const bool worker = tid < nblk * P;
-  const int b = worker ? tid / P : 0, ph = worker ? tid % P : 0;
-  // block b -> (bj, bk), bj <= bk, row-major over the upper triangle
-  int bj = 0, rem = b;
-  while (rem >= NB - bj) {
-    rem -= NB - bj;
-    ++bj;
-  }
-  const int bk = bj + rem;
-  double acc[4][4];
+  constexpr int NC = NB * 8;
+  constexpr int NP = NB * (NB + 1) / 2;
+  constexpr int TILE = NC * kGramStride;  // doubles per staged tile
+  extern __shared__ __align__(16) double gs[];
+  // buffer b: the tile at gs + b * TILE, its row weights (MASK: 128 bytes of the
+  // 0/1 mask, else 128 doubles of D) at gs + 2 * TILE + b * kGramRows
+  auto Tb = [&](int b) { return gs + b * TILE; };
+  auto Wb = [&](int b) { return reinterpret_cast<unsigned char*>(gs + 2 * TILE + b * kGramRows); };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[NP][2];
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
-
-  const long long ntiles = (l + kGramRows - 1) / kGramRows;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long r0 = t * kGramRows;
-    __syncthreads();  // the previous tile is consumed
-    for (int e = tid; e < NC * kGramRows; e += kGramThreads) {
-      const int j = e / kGramRows, r = e % kGramRows;
-      const long long i = r0 + r;
-      gs[j * kGramStride + r] = (j < n && i < l) ? __ldg(X + (long long)j * ld + i) : 0.0;
+  for (int p = 0; p < NP; ++p) acc[p][0] = acc[p][1] = 0.0;
+  // columns past n read column 0 (their rows of G are never written out)
+  auto stage = [&](long long tile, int b) {
+    const long long r0 = tile * kGramRows;
+    for (int e = tid; e < NC * (kGramRows / 2); e += kGramThreads) {
+      const int j = e / (kGramRows / 2), r = 2 * (e % (kGramRows / 2));
+      cp16(Tb(b) + j * kGramStride + r, X + (long long)(j < n ? j : 0) * ld + r0 + r);
     }
-    for (int r = tid; r < kGramRows; r += kGramThreads) {
-      const long long i = r0 + r;
-      cs[r] = i < l ? (mask ? (mask[i] ? 1.0 : 0.0) : dvec[i]) : 0.0;
+    if (MASK) {
+      if (tid < kGramRows / 16) cp16(Wb(b) + 16 * tid, mask + r0 + 16 * tid);
+    } else {
+      if (tid < kGramRows / 2) cp16(Wb(b) + 16 * tid, dvec + r0 + 2 * tid);
+    }
+  };
+  // X, mask and D are padded with zeros to whole 256-row tiles, so the
+  // 128-row tiles need no row guard
+  const long long ntiles = (l + kGramRows - 1) / kGramRows;
+  long long tile = blockIdx.x;
+  if (tile < ntiles) stage(tile, 0);
+  cp_commit();
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, b ^ 1);
+    cp_commit();
+    cp_wait<1>();     // this tile's copies (this thread's) have landed
+    __syncthreads();  // ... and every thread's
+    const double* T = Tb(b);
+    for (int ks = warp; ks < kGramRows / 4; ks += kGramThreads / 32) {
+      const int rr = ks * 4 + t;
+      const double c = MASK ? (Wb(b)[rr] ? 1.0 : 0.0) : reinterpret_cast<const double*>(Wb(b))[rr];
+      double fb[NB], fa[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        fb[q] = T[(q * 8 + g) * kGramStride + rr];
+        fa[q] = c * fb[q];
+      }
+      int p = 0;
+#pragma unroll
+      for (int c1 = 0; c1 < NB; ++c1)
+#pragma unroll
+        for (int c2 = c1; c2 < NB; ++c2) dmma(acc[p++], fa[c1], fb[c2]);
+    }
+    __syncthreads();  // the buffer is restaged two tiles later
+  }
+  cp_wait<0>();
+  // the 8 warps' partial blocks, added in warp order
+  __syncthreads();
+  double* red = gs;  // [NP][64]
+  for (int w = 0; w < kGramThreads / 32; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int idx = p * 64 + g * 8 + 2 * t + h;
+          red[idx] = w == 0 ? acc[p][h] : red[idx] + acc[p][h];
+        }
     }
     __syncthreads();
-    if (worker) {
-      const double* A = gs + (size_t)(4 * bj) * kGramStride;
-      const double* B = gs + (size_t)(4 * bk) * kGramStride;
-      for (int r = ph; r < kGramRows; r += P) {
-        const double c = cs[r];
-        double a[4], bb[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) a[p] = c * A[p * kGramStride + r];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) bb[q] = B[q * kGramStride + r];
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[p][q] = __fma_rn(a[p], bb[q], acc[p][q]);  // (no -fmad here)
-      }
-    }
   }
-  // phases of each block, in order (reuse the tile's shared memory)
-  __syncthreads();
-  double* red = gs;  // [nblk*P][16]
-  if (worker)
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) red[(size_t)tid * 16 + p * 4 + q] = acc[p][q];
-  __syncthreads();
   double* out = partials + (size_t)blockIdx.x * n * n;
-  for (int e = tid; e < nblk * 16; e += kGramThreads) {
-    const int bb = e / 16, pq = e % 16, p = pq / 4, q = pq % 4;
-    double s = 0.0;
-    for (int h = 0; h < P; ++h) s += red[(size_t)(bb * P + h) * 16 + pq];
-    int jj = 0, rr = bb;
-    while (rr >= NB - jj) {
-      rr -= NB - jj;
-      ++jj;
+  for (int e = tid; e < NP * 64; e += kGramThreads) {
+    const int p = e / 64, gi = (e % 64) / 8, ci = e % 8;
+    int c1 = 0, rem = p;
+    while (rem >= NB - c1) {
+      rem -= NB - c1;
+      ++c1;
     }
-    const int kk = jj + rr;
-    const int j = 4 * jj + p, k = 4 * kk + q;
+    const int c2 = c1 + rem;
+    const int j = c1 * 8 + gi, k = c2 * 8 + ci;
     if (j < n && k < n) {
-      out[j * n + k] = s;
-      out[k * n + j] = s;  // diagonal blocks write each entry twice, with the same bits
+      out[j * n + k] = red[e];
+      if (c1 != c2) out[k * n + j] = red[e];  // the lower triangle mirrors the upper
     }
   }
 }
@@ -153,23 +185,47 @@ void gram_precond(int64_t n, const double* G, double scale, double* M, cudaStrea
   TB_LAUNCH_CHECK();
 }
 
-int gram_grid(int64_t l) {
+int gram_grid(int64_t l, int64_t n) {
   const int64_t tiles = (l + kGramRows - 1) / kGramRows;
-  int64_t g = (int64_t)device_sm_count() * 3;
+  int64_t g = (int64_t)device_sm_count() * (n <= 40 ? 2 : 1);  // resident CTAs of 8 warps per SM
   if (g > tiles) g = tiles;
   return (int)(g > 0 ? g : 1);
 }
 
+namespace {
+template <int NB, bool W>
+void launch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
+                 const double* dvec, double* partials, int grid, cudaStream_t s) {
+  const size_t tile = ((size_t)2 * NB * 8 * kGramStride + 2 * kGramRows) * sizeof(double);
+  const size_t red = (size_t)(NB * (NB + 1) / 2) * 64 * sizeof(double);
+  const size_t bytes = tile > red ? tile : red;
+  ensure_max_dynamic_smem((const void*)gram_kernel<NB, W>, (int)bytes);
+  launch_pdl(gram_kernel<NB, W>, dim3(grid), dim3(kGramThreads), bytes, s, (long long)l, (int)n,
+             (long long)ld, X, mask, dvec, partials);
+}
+template <bool W>
+void dispatch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
+                   const double* dvec, double* partials, int grid, cudaStream_t s) {
+  switch ((n + 7) / 8) {
+    case 1: launch_gram<1, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 2: launch_gram<2, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 3: launch_gram<3, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 4: launch_gram<4, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 5: launch_gram<5, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 6: launch_gram<6, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 7: launch_gram<7, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    default: launch_gram<8, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+  }
+}
+}  // namespace
+
 void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
                 const double* dvec, double* partials, double* G, cudaStream_t s) {
-  const int NB = (int)((n + 3) / 4);
-  const size_t smem = ((size_t)NB * 4 * kGramStride + kGramRows) * sizeof(double);
-  const size_t red = (size_t)kGramThreads * 16 * sizeof(double);
-  const size_t bytes = smem > red ? smem : red;
-  ensure_max_dynamic_smem((const void*)gram_kernel, (int)bytes);
-  const int grid = gram_grid(l);
-  launch_pdl(gram_kernel, dim3(grid), dim3(kGramThreads), bytes, s, (long long)l, (int)n, (long long)ld,
-             X, mask, dvec, partials);
+  const int grid = gram_grid(l, n);
+  if (mask)
+    dispatch_gram<true>(l, n, ld, X, mask, dvec, partials, grid, s);
+  else
+    dispatch_gram<false>(l, n, ld, X, mask, dvec, partials, grid, s);
   gram_finalize_kernel<<<(int)((n * n + 255) / 256), 256, 0, s>>>((int)n, partials, grid, G);
   TB_LAUNCH_CHECK();
 }

@@ -325,8 +325,8 @@ void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int3
 
 // ---- the dense Hessian as an n x n matrix (gram.cu), n <= 64 ----------------
 // G = sum_i c_i x_i x_i^T, c = mask (SVM, dvec null) or dvec (LR); partials
-// >= gram_grid(l) * n * n doubles.  Deterministic.
-int gram_grid(int64_t l);
+// >= gram_grid(l, n) * n * n doubles.  Deterministic.
+int gram_grid(int64_t l, int64_t n);
 void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
                 const double* dvec, double* partials, double* G, cudaStream_t s);
 // out = v + scale * G v (row j of G dotted with v in index order)

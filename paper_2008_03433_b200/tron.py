@@ -523,6 +523,15 @@ class GpuEvaluator:
         lib.tron_gpu_launch_count(self._h, ctypes.byref(c))
         return c.value
 
+    def mode(self) -> dict:
+        """How this context runs (tron_gpu_mode): gram / out_of_core / columns /
+        device_loop / sharded."""
+        f = ctypes.c_uint32()
+        _raise(lib.tron_gpu_mode(self._h, ctypes.byref(f)))
+        names = {"gram": _lib.MODE_GRAM, "out_of_core": _lib.MODE_OUT_OF_CORE, "columns": _lib.MODE_COLUMNS,
+                 "device_loop": _lib.MODE_DEVICE_LOOP, "sharded": _lib.MODE_SHARDED}
+        return {k: bool(f.value & b) for k, b in names.items()}
+
     def memory_bytes(self) -> int:
         c = ctypes.c_uint64()
         lib.tron_gpu_memory_bytes(self._h, ctypes.byref(c))
