@@ -12,19 +12,23 @@ from paper_2008_03433_b200 import ExecutionPlan, LossKind, TrustRegionConfig, ma
 pytestmark = pytest.mark.gpu
 LR, SVM = LossKind.Logistic, LossKind.L2Svm
 
+# (name, problem, loss, well-conditioned): the SYNTH-v1 dense problems carry
+# column scales over 2 decades, so w is determined only to ~1e-5 at the eps a
+# test can afford; for them the solves are compared on the objective and the
+# counts, for the equal-scale problems on w as well.
 CASES = [
-    ("svm-synth", lambda: synth.synth_dense(1, 200_000, 40), SVM),
-    ("svm-ragged", lambda: synth.synth_dense(5, 77_777, 37), SVM),
-    ("svm-n64", lambda: synth.synth_dense(3, 30_000, 64), SVM),
-    ("svm-n1", lambda: synth.synth_dense(4, 5_000, 1), SVM),
-    ("lr-testgen", lambda: synth.testgen_dense_problem(2001, 3000, 20, 1.0), LR),
-    ("lr-synth", lambda: synth.synth_dense(2, 100_000, 40), LR),
+    ("svm-synth", lambda: synth.synth_dense(1, 200_000, 40), SVM, False),
+    ("svm-ragged", lambda: synth.synth_dense(5, 77_777, 37, decades=0.0), SVM, True),
+    ("svm-n64", lambda: synth.synth_dense(3, 30_000, 64, decades=0.0), SVM, True),
+    ("svm-n1", lambda: synth.testgen_dense_problem(4, 5_000, 1, 1.0), SVM, True),
+    ("lr-testgen", lambda: synth.testgen_dense_problem(2001, 3000, 20, 1.0), LR, True),
+    ("lr-synth", lambda: synth.synth_dense(2, 100_000, 40), LR, False),
 ]
 
 
 @pytest.mark.parametrize("case", range(len(CASES)))
 def test_gram_evaluator_matches_oracle(port, case):
-    name, make, loss = CASES[case]
+    name, make, loss, _ = CASES[case]
     p = make()
     n = p.X.cols
     w = synth.testgen_random_vector(8, n, 0.1)
@@ -45,7 +49,7 @@ def test_gram_evaluator_matches_oracle(port, case):
 @pytest.mark.parametrize("precond", [False, True])
 @pytest.mark.parametrize("case", range(len(CASES)))
 def test_gram_solve_matches_traversal_and_reference(ref, monkeypatch, case, precond):
-    name, make, loss = CASES[case]
+    name, make, loss, conditioned = CASES[case]
     p = make()
     cfg = TrustRegionConfig(eps=1e-3, use_preconditioner=precond)
     out = {}
@@ -54,16 +58,17 @@ def test_gram_solve_matches_traversal_and_reference(ref, monkeypatch, case, prec
         with make_evaluator(p, loss, ExecutionPlan.gpu()) as ev:
             r = ev.solve(cfg)
             act = ev.committed_state().active if loss == SVM else None
+            assert ev.mode()["gram"] == (mode == "1")
         out[mode] = (r, act)
     (a, act_a), (b, act_b) = out["1"], out["0"]
     w_ref, t_ref = ref.solve(p, 0 if loss == LR else 1, cfg)
     for r in (a, b):
-        assert rel_err(r.objective, t_ref["objective"]) <= 1e-6 and rel_err(r.w, w_ref) <= 1e-6, name
-    ca = [it.cg_iters for it in a.trace.iterations]
-    cr = [it["cg_iters"] for it in t_ref["iterations"]]
-    assert len(ca) == len(cr) and all(abs(x - y) <= 1 for x, y in zip(ca, cr)), (ca, cr)
-    if act_a is not None:
-        assert act_a.size == act_b.size or rel_err(a.w, b.w) > 0
+        assert rel_err(r.objective, t_ref["objective"]) <= 1e-7, name
+        if conditioned:
+            assert rel_err(r.w, w_ref) <= 1e-6, name
+        c = [it.cg_iters for it in r.trace.iterations]
+        cr = [it["cg_iters"] for it in t_ref["iterations"]]
+        assert len(c) == len(cr) and all(abs(x - y) <= 1 for x, y in zip(c, cr)), (name, c, cr)
 
 
 def test_gram_sharded_matches(monkeypatch):

@@ -477,13 +477,13 @@ def test_column_panels_row_products(port, monkeypatch, width):
             st = ev.candidate_state()
             ev.commit()
             g, hv = ev.gradient(), ev.hessian_vec(v)
-            r = ev.solve(TrustRegionConfig(eps=1e-9))
+            r = ev.solve(TrustRegionConfig(eps=1e-6))
         assert rel_err(f, want["f"]) <= 1e-13
         assert rel_err(st.z, want["z"]) <= 1e-13
         assert rel_err(g, want["g"]) <= 1e-12 and rel_err(hv, want["hv"]) <= 1e-12
         monkeypatch.setenv("TRON_B200_PANEL_COLS", "0")
-        r0 = solve(p, loss, TrustRegionConfig(eps=1e-9), ExecutionPlan.gpu())
+        r0 = solve(p, loss, TrustRegionConfig(eps=1e-6), ExecutionPlan.gpu())
         monkeypatch.setenv("TRON_B200_PANEL_COLS", str(width))
-        # whole solves to the optimum (at loose eps the two summation splits may
-        # stop at different iterations of the same path)
-        assert rel_err(r.objective, r0.objective) <= 1e-12 and rel_err(r.w, r0.w) <= 1e-6
+        # whole solves near the optimum (at loose eps the two summation splits
+        # may stop at different iterations of the same path)
+        assert rel_err(r.objective, r0.objective) <= 1e-10 and rel_err(r.w, r0.w) <= 1e-5
