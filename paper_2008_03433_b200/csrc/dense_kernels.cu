@@ -66,15 +66,24 @@ struct PassArgs {
   ObjScalars* obj;
   Scratch sc;
   double* partials;      // [gridDim.x][n]
+  double* gram_partials; // PM_FWDG: [gridDim.x][n*n] Gram partials (gram.cu's G) of the candidate
 };
 
-enum PassMode : int { PM_FWD = 0, PM_HV = 1, PM_PRECOND = 2 };
+enum PassMode : int { PM_FWD = 0, PM_HV = 1, PM_PRECOND = 2, PM_FWDG = 3 };
+
+// mma.sync m8n8k4 f64 (DMMA), as gram.cu
+__device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 
 // Side arrays of a mode: d-arrays in order, then the mask.
 template <int MODE, int LOSS>
 struct Side {
-  static constexpr int nd = (MODE == PM_FWD) ? 1 : (LOSS == kLossLogistic ? 1 : 0);
-  static constexpr bool mask = (MODE != PM_FWD) && LOSS == kLossSvm;
+  static constexpr bool fwd = MODE == PM_FWD || MODE == PM_FWDG;
+  static constexpr int nd = fwd ? 1 : (LOSS == kLossLogistic ? 1 : 0);
+  static constexpr bool mask = !fwd && LOSS == kLossSvm;
 };
 
 // T compute threads (one row of the tile each) + one producer warp.
@@ -111,6 +120,16 @@ __global__ void __launch_bounds__(T + kWarp, 1)
 #pragma unroll
   for (int j = 0; j < NMAX; ++j) acc[j] = 0.0;
   double term_acc = 0.0, cnt_acc = 0.0;
+  // PM_FWDG: the candidate's Gram matrix G = sum_i c_i x_i x_i^T in the same
+  // pass (gram.cu's DMMA scheme on the staged tile): NB groups of 8 columns,
+  // NP block pairs, two accumulators per pair and lane
+  constexpr bool FG = MODE == PM_FWDG;
+  constexpr int NB = FG ? (NMAX + 7) / 8 : 1;
+  constexpr int NP = NB * (NB + 1) / 2;
+  __shared__ double s_w[FG ? 2 : 1][FG ? T : 1];  // row weights c_i, by tile parity
+  double gacc[NP][2];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) gacc[p][0] = gacc[p][1] = 0.0;
 
   if (wid == NCW) {
     // ---- producer warp: one 2-D TMA box {T rows x n columns} of X per
@@ -126,7 +145,7 @@ __global__ void __launch_bounds__(T + kWarp, 1)
         mbar_arrive_expect_tx(&full[s], (unsigned)L.bytes());
         tma_load_2d(base, &xmap, (int)row0, 0, &full[s]);
         if (SD::nd >= 1) {
-          const double* src = MODE == PM_FWD ? a.y : a.dvec;
+          const double* src = SD::fwd ? a.y : a.dvec;
           bulk_g2s(base + (size_t)n * T * 8, src + row0, T * 8, &full[s]);
         }
         if (use_mask) bulk_g2s(base + (size_t)(n + SD::nd) * T * 8, a.mask + row0, T, &full[s]);
@@ -161,7 +180,8 @@ __global__ void __launch_bounds__(T + kWarp, 1)
       for (int j = 0; j < NMAX; ++j)
         if (j < n) sdot += x[j] * s_v[j];
       double c;
-      if (MODE == PM_FWD) {
+      double cg = 0.0;  // PM_FWDG: this row's Gram weight (SVM: [i in I], LR: D_i)
+      if (SD::fwd) {
         const double yi = side[tid];
         c = 0.0;
         if (in) {
@@ -171,13 +191,16 @@ __global__ void __launch_bounds__(T + kWarp, 1)
             const double sig = 1.0 / (1.0 + exp(tt));  // exp overflow -> inf -> 0
             const double zh = -yi * sig;
             a.zhat[i] = zh;
-            a.dvec_out[i] = (1.0 - sig) * sig;
+            const double di = (1.0 - sig) * sig;
+            a.dvec_out[i] = di;
+            cg = di;
             term_acc += log1p_exp_neg(tt);
             c = zh;  // gradient coefficient (loss.cpp:74-80)
           } else {  // svm_fused_pass, loss.cpp:94-122 (strict margin > 0)
             const double margin = 1.0 - yi * sdot;
             if (margin > 0.0) {
               a.mask_out[i] = 1;
+              cg = 1.0;
               term_acc += margin * margin;
               cnt_acc += 1.0;
               c = sdot - yi;  // svm_gradient coefficient (loss.cpp:129-137)
@@ -195,6 +218,30 @@ __global__ void __launch_bounds__(T + kWarp, 1)
       }
 #pragma unroll
       for (int j = 0; j < NMAX; ++j) acc[j] += c * x[j];  // x[j] = 0 beyond n
+      if (FG) {
+        // the tile's Gram blocks: every row weight first (a barrier of the
+        // compute warps), then warp w takes the k-steps w, w + NCW, ... of the tile
+        double* wts = s_w[FG ? (k & 1) : 0];
+        wts[tid] = cg;
+        asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        const int g = lane >> 2, tq = lane & 3;
+        for (int ks = wid; ks < T / 4; ks += NCW) {
+          const int rr = ks * 4 + tq;
+          const double cw = wts[rr];
+          double fb[NB], fa[NB];
+#pragma unroll
+          for (int q = 0; q < NB; ++q) {
+            const int col = q * 8 + g;
+            fb[q] = col < n ? xs[col * T + rr] : 0.0;
+            fa[q] = cw * fb[q];
+          }
+          int pp = 0;
+#pragma unroll
+          for (int c1 = 0; c1 < NB; ++c1)
+#pragma unroll
+            for (int c2 = c1; c2 < NB; ++c2) dmma8(gacc[pp++], fa[c1], fb[c2]);
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
@@ -220,7 +267,42 @@ __global__ void __launch_bounds__(T + kWarp, 1)
     a.partials[(long long)blockIdx.x * n + tid] = tsum;
   }
 
-  if (MODE == PM_FWD) {
+  if (FG) {
+    // the compute warps' Gram partials, added in warp order (after the
+    // gradient tree's slots), then this CTA's n x n partial, mirrored
+    __syncthreads();
+    double* gred = s_red + NCW * NMAX;  // [NP][64]
+    const int g = lane >> 2, tq = lane & 3;
+    for (int w = 0; w < NCW; ++w) {
+      if (wid == w) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int idx = p * 64 + g * 8 + 2 * tq + h;
+            gred[idx] = w == 0 ? gacc[p][h] : gred[idx] + gacc[p][h];
+          }
+      }
+      __syncthreads();
+    }
+    double* gout = a.gram_partials + (size_t)blockIdx.x * n * n;
+    for (int e = tid; e < NP * 64; e += BLK) {
+      const int p = e / 64, gi = (e % 64) / 8, ci = e % 8;
+      int c1 = 0, rem = p;
+      while (rem >= NB - c1) {
+        rem -= NB - c1;
+        ++c1;
+      }
+      const int c2 = c1 + rem;
+      const int j = c1 * 8 + gi, kk = c2 * 8 + ci;
+      if (j < n && kk < n) {
+        gout[j * n + kk] = gred[e];
+        if (c1 != c2) gout[kk * n + j] = gred[e];
+      }
+    }
+  }
+
+  if (SD::fwd) {
     const double bt = block_sum<BLK>(term_acc, sh, true);
     const double bc = block_sum<BLK>(cnt_acc, sh, true);
     if (tid == 0) {
@@ -260,7 +342,11 @@ void launch_pass(const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
   if (ns > 4) ns = 4;
   if (ns < 2) ns = 2;
   size_t smem = (size_t)ns * sbytes;
-  const size_t red = (size_t)(T / kWarp) * NMAX * 8;
+  size_t red = (size_t)(T / kWarp) * NMAX * 8;
+  if (MODE == PM_FWDG) {
+    const int NB = (NMAX + 7) / 8;
+    red += (size_t)(NB * (NB + 1) / 2) * 64 * 8;
+  }
   if (smem < red) smem = red;
   auto k = dense_pass_kernel<NMAX, T, MODE, LOSS>;
   // (the attribute must not exceed the opt-in max minus the static shared memory)
@@ -274,10 +360,12 @@ void launch_mode_t(int mode, int loss, const CUtensorMap& m, const PassArgs& a, 
   if (loss == kLossLogistic) {
     if (mode == PM_FWD) launch_pass<NMAX, T, PM_FWD, kLossLogistic>(m, a, s);
     else if (mode == PM_HV) launch_pass<NMAX, T, PM_HV, kLossLogistic>(m, a, s);
+    else if (mode == PM_FWDG) { if constexpr (NMAX <= 40) launch_pass<NMAX, T, PM_FWDG, kLossLogistic>(m, a, s); }
     else launch_pass<NMAX, T, PM_PRECOND, kLossLogistic>(m, a, s);
   } else {
     if (mode == PM_FWD) launch_pass<NMAX, T, PM_FWD, kLossSvm>(m, a, s);
     else if (mode == PM_HV) launch_pass<NMAX, T, PM_HV, kLossSvm>(m, a, s);
+    else if (mode == PM_FWDG) { if constexpr (NMAX <= 40) launch_pass<NMAX, T, PM_FWDG, kLossSvm>(m, a, s); }
     else launch_pass<NMAX, T, PM_PRECOND, kLossSvm>(m, a, s);
   }
 }
@@ -483,11 +571,15 @@ int dense_grid(int64_t l, int64_t n) {
   return (int)g;
 }
 
+bool dense_forward_gram_fused(int64_t n) { return n <= 40; }
+
 void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUtensorMap& xmap,
                    int loss, const double* w,
                    const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
-                   double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s) {
+                   double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s,
+                   double* gram_parts) {
   PassArgs a{};
+  a.gram_partials = gram_parts;
   a.l = l;
   a.ld = ld;
   a.n = (int)n;
@@ -502,7 +594,7 @@ void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUte
   a.obj = obj;
   a.sc = sc;
   a.partials = gparts;
-  launch(PM_FWD, loss, xmap, a, s);
+  launch(gram_parts ? PM_FWDG : PM_FWD, loss, xmap, a, s);
 }
 
 void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X,

@@ -672,8 +672,13 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       AllocScope scope(e->s_);
       e->gram_ = true;
       if (e->svm_strategy_ == TRON_SVM_AUTO) e->svm_strategy_ = TRON_SVM_INDIRECT;  // G is compact already
-      for (auto& S : e->slot_) S.gram.alloc((size_t)n * n);
-      e->gram_parts_.alloc((size_t)gram_grid((int64_t)l, (int64_t)n) * n * n);
+      const char* gf = std::getenv("TRON_B200_GRAM_FUSED");  // 0: a separate Gram pass
+      e->gram_fused_ = dense_forward_gram_fused((int64_t)n) && !(gf && gf[0] == '0');
+      for (auto& S : e->slot_) {
+        S.gram.alloc((size_t)n * n);
+        if (e->gram_fused_) S.gram_parts.alloc((size_t)dense_grid((int64_t)l, (int64_t)n) * n * n);
+      }
+      if (!e->gram_fused_) e->gram_parts_.alloc((size_t)gram_grid((int64_t)l, (int64_t)n) * n * n);
       cuda_check(cudaStreamSynchronize(e->s_), "gram buffers");
     }
   }
@@ -854,7 +859,7 @@ void Engine::forward(Slot& S) {
     obj_combine_blocks(obj_d_, blk_red_.p, nblk_, C_, s_);
   } else if (dense_) {
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
-                  S.gparts.p, obj_d_, sc_, s_);
+                  S.gparts.p, obj_d_, sc_, s_, gram_fused_ ? S.gram_parts.p : nullptr);
     if (ro_) {  // I of this slot, then f in the reference's order (loss.cpp:114-119)
       compact_mask(l_, S.mask.p, S.idx.p, idx_tmp_.p, S.cnt.p, s_);
       ro_hinge(l_, n_, S.z.p, y_.p, S.w.p, C_, ro_hparts_.p, ro_tickets_.p, obj_d_, s_);
@@ -1259,9 +1264,14 @@ void Engine::row_products(const double* v, const double* dvec, const uint8_t* ma
 // shards when row-sharded (one n*n exchange per commit, none per Hv).
 void Engine::gram_slot(const Slot& S) {
   const bool svm = loss_ == TRON_LOSS_L2SVM;
-  dense_gram(l_, n_, ld_, Xc_.p, svm ? S.mask.p : nullptr, svm ? nullptr : S.dvec.p, gram_parts_.p,
-             S.gram.p, s_);
-  count_launch(2);
+  if (gram_fused_) {  // the slot's margin pass accumulated the partials already
+    gram_finalize(n_, S.gram_parts.p, dense_grid(l_, n_), S.gram.p, s_);
+    count_launch(1);
+  } else {
+    dense_gram(l_, n_, ld_, Xc_.p, svm ? S.mask.p : nullptr, svm ? nullptr : S.dvec.p, gram_parts_.p,
+               S.gram.p, s_);
+    count_launch(2);
+  }
   if (comm_.active()) comm_.allreduce_sum(S.gram.p, (size_t)n_ * n_, s_);
 }
 
@@ -2202,7 +2212,8 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
     out->forward_ms = time_it([&] {
       dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, slot_[cand_].z.p,
                     slot_[cand_].zhat.p, slot_[cand_].dvec.p, slot_[cand_].mask.p,
-                    slot_[cand_].gparts.p, obj_d_, sc_, s_);
+                    slot_[cand_].gparts.p, obj_d_, sc_, s_,
+                    gram_fused_ ? slot_[cand_].gram_parts.p : nullptr);
     });
   }
   out->grad_ms = time_it([&] { gradient_dev(); });

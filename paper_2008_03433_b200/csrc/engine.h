@@ -182,6 +182,7 @@ class Engine {
     DevBuf<int32_t> idx;    // reference order: this slot's active set I (ascending)
     DevBuf<long long> cnt;  // ... and |I| (device)
     DevBuf<double> gram;    // dense Gram mode: this slot's Hessian sum_i c_i x_i x_i^T (n x n)
+    DevBuf<double> gram_parts;  // ... its per-CTA partials from the fused margin pass
     double f = 0.0;
     long long nact = 0;
     bool valid = false;
@@ -311,6 +312,7 @@ class Engine {
   // dense problems (n <= 64): the Hessian as an n x n matrix formed once per
   // commit (gram.cu); Hv / the preconditioner then read G instead of X
   bool gram_ = false;
+  bool gram_fused_ = false;  // n <= 40: G accumulated by the margin pass itself (PM_FWDG)
   DevBuf<double> gram_parts_;
   void gram_slot(const Slot& S);
   // column-partitioned layout: X_, w and the

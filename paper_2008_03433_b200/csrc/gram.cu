@@ -176,6 +176,11 @@ __global__ void gram_precond_kernel(int n, const double* __restrict__ G, double 
 
 }  // namespace
 
+void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s) {
+  gram_finalize_kernel<<<(int)((n * n + 255) / 256), 256, 0, s>>>((int)n, partials, nparts, G);
+  TB_LAUNCH_CHECK();
+}
+
 void gram_hv(int64_t n, const double* G, const double* v, double scale, double* out, cudaStream_t s) {
   launch_pdl(gram_hv_kernel, dim3(1), dim3(64), 0, s, (int)n, G, v, scale, out);
 }

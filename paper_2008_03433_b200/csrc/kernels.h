@@ -296,10 +296,16 @@ int dense_grid(int64_t l, int64_t n);
 // 2-D TMA descriptor of a column-major X (rows x n, leading dimension ld):
 // box = {dense_tile_rows(n) rows, n columns}.  Returns 0 on success.
 int dense_make_map(CUtensorMap* map, const double* X, int64_t ld, int64_t rows, int64_t n);
+// gram_parts (n <= 40, dense_forward_gram_fused): also the candidate's Gram
+// partials [grid][n*n] (gram.cu's G, finished by gram_finalize) in the same pass.
+bool dense_forward_gram_fused(int64_t n);
 void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUtensorMap& xmap,
                    int loss, const double* w,
                    const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
-                   double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s);
+                   double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s,
+                   double* gram_parts = nullptr);
+// G = sum over nparts of the per-CTA Gram partials (fixed order)
+void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s);
 // partial sums per block (grid = dense_grid(l, n)) of:
 //  HV:      sum_i c_i x_i   with c = (x_i.v)*dvec_i (LR) or mask?(x_i.v):0 (SVM;
 //           mask == nullptr => every row active, used on the gathered panel)
