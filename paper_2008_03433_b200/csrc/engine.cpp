@@ -672,8 +672,12 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       AllocScope scope(e->s_);
       e->gram_ = true;
       if (e->svm_strategy_ == TRON_SVM_AUTO) e->svm_strategy_ = TRON_SVM_INDIRECT;  // G is compact already
-      const char* gf = std::getenv("TRON_B200_GRAM_FUSED");  // 0: a separate Gram pass
-      e->gram_fused_ = dense_forward_gram_fused((int64_t)n) && !(gf && gf[0] == '0');
+      // TRON_B200_GRAM_FUSED=1: G accumulated by the margin pass itself.  Measured
+      // slower (P1: 2.95 ms fused vs 1.17 + 1.63 ms separate): one 9-warp CTA per
+      // SM alternates the row phase and the DMMA phase, where the separate Gram
+      // kernel keeps 16 warps per SM on the FP64 tensor pipe.
+      const char* gf = std::getenv("TRON_B200_GRAM_FUSED");
+      e->gram_fused_ = dense_forward_gram_fused((int64_t)n) && gf && gf[0] == '1';
       for (auto& S : e->slot_) {
         S.gram.alloc((size_t)n * n);
         if (e->gram_fused_) S.gram_parts.alloc((size_t)dense_grid((int64_t)l, (int64_t)n) * n * n);

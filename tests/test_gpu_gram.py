@@ -81,3 +81,26 @@ def test_gram_sharded_matches(monkeypatch):
     with make_evaluator(p, SVM, ExecutionPlan.gpu()) as ev:
         r0 = ev.solve(TrustRegionConfig(eps=1e-3))
     assert np.array_equal(r1.w, r0.w) and r1.objective == r0.objective
+
+
+@pytest.mark.parametrize("case", [0, 1, 4])
+def test_gram_fused_margin_pass(port, monkeypatch, case):
+    """The opt-in fused margin + Gram pass (TRON_B200_GRAM_FUSED=1, n <= 40)."""
+    monkeypatch.setenv("TRON_B200_GRAM_FUSED", "1")
+    name, make, loss, _ = CASES[case]
+    p = make()
+    n = p.X.cols
+    w = synth.testgen_random_vector(8, n, 0.1)
+    v = synth.testgen_random_vector(9, n, 1.0)
+    want = port.svm(p, w, v) if loss == SVM else port.logistic(p, w, v)
+    with make_evaluator(p, loss, ExecutionPlan.gpu()) as ev:
+        ev.eval_candidate(w)
+        ev.commit()
+        assert rel_err(ev.hessian_vec(v), want["hv"]) <= 1e-12, name
+        assert rel_err(ev.precond_diagonal(), want["M"]) <= 1e-12, name
+        r = ev.solve(TrustRegionConfig(eps=1e-3))
+    monkeypatch.setenv("TRON_B200_GRAM_FUSED", "0")
+    with make_evaluator(p, loss, ExecutionPlan.gpu()) as ev:
+        r0 = ev.solve(TrustRegionConfig(eps=1e-3))
+    assert rel_err(r.objective, r0.objective) <= 1e-9
+    assert [it.cg_iters for it in r.trace.iterations] == [it.cg_iters for it in r0.trace.iterations]
