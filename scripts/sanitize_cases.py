@@ -7,8 +7,10 @@ Engines covered: single-block CG (n <= 4096, dense and sparse), the 8-CTA
 cluster CG step (4096 < n <= 262144), the cooperative grid CG step
 (n > 262144, with the p.Hp / ||g|| fused into the segmented emission), the
 reference-order dense L2-SVM, the Gathered L2-SVM (dense panel and CSR X_I
-with its CSC copy), the preconditioner, predict, and the staged-u segmented
-product (>= 128 nonzeros per column entry).  Each solve is checked against
+with its CSC copy), the preconditioner, predict, the staged-u segmented
+product (>= 128 nonzeros per column entry), the dense Gram pass (DMMA; the
+default for dense), the tall-skinny traversal, out-of-core streaming and
+column panels.  Each solve is checked against
 the C oracle so a sanitizer-clean run is also a correct one.
 """
 import os
@@ -60,7 +62,14 @@ cases = [
     ("dense SVM precond", synth.synth_dense(2, 3000, 40), SVM, gpu(), dict(precond=True)),
     ("dense SVM reference order", synth.synth_dense(1, 5000, 40), SVM, gpu(reference_order=True), {}),
     ("dense LR", synth.testgen_dense_problem(1001, 50, 5, 1.0), LR, gpu(), dict(eps=1e-8)),
+    ("dense SVM out-of-core streaming", synth.synth_dense(1, 5000, 40, decades=0.0), SVM,
+     gpu(out_of_core=1, stream_block_rows=1024), dict(eps=1e-8)),
+    ("dense SVM tall-skinny (no Gram)", synth.synth_dense(1, 5000, 40), SVM, gpu(), dict(eps=1e-8)),
+    ("sparse LR column panels", synth.synth_sparse(13, 600, 9000, 20), LR, gpu(), {}),
 ]
+# per-case environment (applied before the case's context is created)
+ENV = {"dense SVM tall-skinny (no Gram)": {"TRON_B200_DENSE_GRAM": "0"},
+       "sparse LR column panels": {"TRON_B200_PANEL_COLS": "2000"}}
 if sys.argv[1:] == ["--count"]:
     print(len(cases))
     sys.exit(0)
@@ -70,6 +79,10 @@ bad = 0
 for i, (name, p, loss, plan, kw) in enumerate(cases):
     if only and i not in only:
         continue
+    for k, v in ENV.get(name, {}).items():
+        os.environ[k] = v
     bad += not check(name, p, loss, plan, **kw)
+    for k in ENV.get(name, {}):
+        os.environ.pop(k)
 print("sanitize cases:", "all ok" if bad == 0 else f"{bad} mismatches")
 sys.exit(1 if bad else 0)
