@@ -105,10 +105,37 @@ def host_description():
     return {"cpu_model": model, "nproc": os.cpu_count(), "usable_cores": cpu_cores(), "mem_gb": mem_gb}
 
 
+def _nvml_sampler_proc(device_uuid, device_index, conn, stop, go):
+    """Child process: SM clocks + throttle-reason bits every 20 ms while `go` is
+    set (the timed region), until `stop`; then the samples through `conn`.  A separate process shares no GIL
+    with the timed loop (an in-process sampler thread delayed the return of
+    1-2 ms solves by holding the GIL across NVML calls)."""
+    rows = []
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByUUID(device_uuid) if device_uuid else nv.nvmlDeviceGetHandleByIndex(device_index)
+        except Exception:
+            h = nv.nvmlDeviceGetHandleByIndex(device_index)
+        get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not stop.is_set():
+            if go.is_set():
+                try:
+                    rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                 float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), int(get(h))))
+                except Exception:
+                    pass
+            stop.wait(0.02)
+    except Exception:
+        pass
+    conn.send(rows)
+    conn.close()
+
+
 class ClockSampler:
-    """SM clocks + throttle reasons sampled during the timed region, in process
-    through NVML (no nvidia-smi subprocess: forking the benchmark process every
-    sample stalled short solves); nvidia-smi only if NVML is unavailable."""
+    """SM clocks + throttle reasons sampled during the timed region, by an NVML
+    child process (nvidia-smi only if NVML is unavailable)."""
 
     # nvmlClocksEventReasons bits
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
@@ -120,34 +147,13 @@ class ClockSampler:
     def __init__(self, device=0):
         self.device = device
         self.rows = []  # (sm_mhz, max_mhz, set of reasons)
-        self._stop = threading.Event()
-        self._t = None
-        self._nvml = None
+        self.source = "nvml"
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = None
-            try:
-                import torch
-                uuid = str(torch.cuda.get_device_properties(device).uuid)
-                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
-            except Exception:
-                h = pynvml.nvmlDeviceGetHandleByIndex(device)
-            self._nvml = (pynvml, h)
+            import pynvml  # noqa: F401
         except Exception:
-            self._nvml = None
+            self.source = "nvidia-smi"
 
-    def _sample_nvml(self):
-        nv, h = self._nvml
-        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        try:
-            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-        except AttributeError:
-            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-        return float(sm), float(mx), {name for b, name in self.REASONS.items() if bits & b}
-
-    def _sample_smi(self):
+    def _smi(self):
         out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
                               "--format=csv,noheader,nounits"], capture_output=True, text=True,
                              timeout=5).stdout.strip()
@@ -155,22 +161,43 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         return float(r[0]), float(r[1]), {n for n, v in zip(names, r[3:7]) if v.lower() == "active"}
 
-    def _run(self):
-        while not self._stop.is_set():
+    def __enter__(self):
+        if self.source == "nvml":
+            import multiprocessing as mp
+            uuid = None
             try:
-                self.rows.append(self._sample_nvml() if self._nvml else self._sample_smi())
+                import torch
+                u = str(torch.cuda.get_device_properties(self.device).uuid)
+                uuid = u if u.startswith("GPU-") else "GPU-" + u
             except Exception:
                 pass
-            self._stop.wait(0.25)
-
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+            ctx = mp.get_context("spawn")
+            self._rx, tx = ctx.Pipe(duplex=False)
+            self._stop, self._go = ctx.Event(), ctx.Event()
+            self._proc = ctx.Process(target=_nvml_sampler_proc,
+                                     args=(uuid, self.device, tx, self._stop, self._go), daemon=True)
+            self._proc.start()
+            time.sleep(1.0)  # the child has initialised NVML before the timed region starts
+            self._go.set()
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.source == "nvml":
+            self._go.clear()
+            self._stop.set()
+            try:
+                if self._rx.poll(30):
+                    raw = self._rx.recv()
+                    self.rows = [(a, b, {nm for bit, nm in self.REASONS.items() if r & bit}) for a, b, r in raw]
+            except Exception:
+                pass
+            self._proc.join(timeout=10)
+        if not self.rows:
+            try:
+                self.rows = [self._smi()]
+                self.source = "nvidia-smi (after the timed region)"
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
@@ -178,7 +205,7 @@ class ClockSampler:
         reasons = set().union(*(r[2] for r in self.rows))
         return {"sm_mhz": float(np.median([r[0] for r in self.rows])),
                 "sm_max_mhz": max(r[1] for r in self.rows), "reasons": sorted(reasons),
-                "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
+                "samples": len(self.rows), "source": self.source}
 
 
 # ---------------------------------------------------------------------------- oracle-side data
