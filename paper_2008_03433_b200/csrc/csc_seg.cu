@@ -46,13 +46,7 @@ constexpr int kEmptyItems = 4;  // empty rows per lane per visit
 #ifndef TB_LD256
 #define TB_LD256 1  // measured: N1 Hv 91.8 -> 80.6 us, K1 3.63 -> 3.47 ms
 #endif
-#ifndef TB_SEG_SINGLE
-#define TB_SEG_SINGLE 0
-#endif
-#ifndef TB_SEG_BLOCKS
-#define TB_SEG_BLOCKS (TB_SEG_SINGLE ? 4 : 2)
-#endif
-constexpr int kSegBlocksPerSm = TB_SEG_BLOCKS;
+constexpr int kSegBlocksPerSm = 2;  // 128 registers: 16 warps per SM (seg_dot_slots counts on it)
 __device__ __forceinline__ void ld4d_ef(const double* p, double& a, double& b, double& c, double& d) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0, %1, %2, %3}, [%4];"
                : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
@@ -352,18 +346,7 @@ __device__ __forceinline__ void seg_body(const CsrView& A, const SegView& S, con
         if (EPI == EPI_VEC && E.dot_parts) dacc.add(E, bb[m], o);
       }
   }
-#if TB_SEG_SINGLE
-  // one chunk at a time (no register pipeline): latency hidden by more warps
-  (void)seg_walk;
-  for (; t < nch; t += W) {
-    LaneChunk c;
-    load_chunk(A, S, t, lane, rank_of(t), c);
-    gather_chunk<UK, SQ, EPI, STAGED, COH>(U, E, su, c);
-    process_chunk<SQ, EPI, STAGED, COH>(A, S, E, out, t, c, lane, ebuf, dacc);
-  }
-#else
   if (t < nch) seg_walk(t);
-#endif
   if (EPI == EPI_VEC && E.dot_parts) {  // warp partial, fixed order
     const double a = warp_sum(dacc.acc), b = warp_sum(dacc.bad);
     if (lane == 0) {
