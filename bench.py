@@ -544,18 +544,25 @@ def main():
 
     p_full, loss = product_problem(args.workload, rows=args.rows)
     p, row_begin = shard(p_full, rank, world) if world > 1 else (p_full, 0)
-    plan = ExecutionPlan.gpu(device=local_rank)
-    if world > 1:
-        uid = None
-        if rank == 0:
-            buf = ctypes.create_string_buffer(128)
-            if _lib.lib.tron_gpu_nccl_unique_id(buf) != 0:
-                raise RuntimeError(_lib.last_error())
-            uid = buf.raw
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        plan.rank, plan.world, plan.nccl_unique_id = rank, world, obj[0]
-        plan.row_begin, plan.global_rows = row_begin, p_full.X.rows
+
+    def make_plan():
+        """The rank's plan; N > 1: a fresh NCCL unique id (rank 0's, broadcast)
+        for every context -- an id serves one communicator."""
+        pl = ExecutionPlan.gpu(device=local_rank)
+        if world > 1:
+            uid = None
+            if rank == 0:
+                buf = ctypes.create_string_buffer(128)
+                if _lib.lib.tron_gpu_nccl_unique_id(buf) != 0:
+                    raise RuntimeError(_lib.last_error())
+                uid = buf.raw
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            pl.rank, pl.world, pl.nccl_unique_id = rank, world, obj[0]
+            pl.row_begin, pl.global_rows = row_begin, p_full.X.rows
+        return pl
+
+    plan = make_plan()
     cfg = TrustRegionConfig(eps=args.eps)
 
     torch.cuda.set_device(local_rank)
@@ -635,9 +642,10 @@ def main():
     def e2e_time(prob, reps):
         ts = []
         for _ in range(reps):
+            pl = make_plan()  # (N > 1: its id broadcast happens before the timer)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            with make_evaluator(prob, loss, plan) as ev2:
+            with make_evaluator(prob, loss, pl) as ev2:
                 ev2.solve(cfg)
             ts.append(time.perf_counter() - t0)
         return max_over_ranks(float(np.median(ts)))
