@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TRON train time to eps (s)"
+FP64_TENSOR_TFLOPS = 45.0  # B200 nominal (no measured FP64 figure in MEASURED_PEAKS.json)
 UNIT = "s"
 SEED = 1
 TEST_SEED = 2  # held-out rows for the prediction parity check
@@ -619,19 +620,29 @@ def main():
         # the gradient).  The roofline object describes the larger of the two.
         l, n = p.X.rows, p.X.cols
         fwd_bytes, gram_bytes = 8 * l * n + 17 * l, 8 * l * n + l
+        gram_flops = l * n * (n + 1)  # the upper triangle of sum_i c_i x_i x_i^T, 2 flops per product
         if kt["grad_ms"] >= kt["forward_ms"]:
-            kern, kbytes, kms = "Gram pass G = sum_i c_i x_i x_i^T (gram.cu; once per commit)", gram_bytes, kt["grad_ms"]
+            # bound by the FP64 tensor pipe (ncu: math-pipe throttle), HBM a close second
+            kern, kbytes, kms = "Gram pass G = sum_i c_i x_i x_i^T (gram.cu, DMMA; once per commit)", gram_bytes, kt["grad_ms"]
+            bound, unit = "tensor", "TFLOP/s"
+            achieved = gram_flops / (kms / 1e3) / 1e12
+            peak, peak_kind = FP64_TENSOR_TFLOPS, ("fallback: B200 FP64 tensor 45 TFLOPS "
+                                                   "(/opt/skills/guides/blackwell_cuda_programming.md:52)")
         else:
             kern, kbytes, kms = "fused margin pass (dense_pass FWD: margins, mask, f, gradient partials)", fwd_bytes, kt["forward_ms"]
-        achieved = kbytes / (kms / 1e3) / 1e9
+            bound, unit = "hbm", "GB/s"
+            achieved = kbytes / (kms / 1e3) / 1e9
         share = n_evals * kms / (t_step * 1e3) if t_step > 0 else None
-        gram_extra = {"gram_pass_ms": kt["grad_ms"], "gram_fp64_tflops": l * n * (n + 1) / (kt["grad_ms"] / 1e3) / 1e12,
+        gram_extra = {"gram_pass_ms": kt["grad_ms"], "gram_pass_hbm_gbs": gram_bytes / (kt["grad_ms"] / 1e3) / 1e9,
+                      "gram_pass_fp64_tflops": gram_flops / (kt["grad_ms"] / 1e3) / 1e12,
+                      "margin_pass_ms": kt["forward_ms"], "margin_pass_gbs": fwd_bytes / (kt["forward_ms"] / 1e3) / 1e9,
                       "hv_from_gram_us": kt["hv_ms"] * 1e3,
                       "tall_skinny_hv_pass_ms": kt["transposed_ms"], "tall_skinny_hv_gbs": trans_gbs}
     else:
         kern = ("Hessian-vector product (CSR D*Xv + CSC segmented X^T u)" if p.X.layout == "csr"
                 else "Hessian-vector product (dense tall-skinny TMA pass, one read of X)")
         kbytes, kms = ab["hv"], kt["hv_ms"]
+        bound, unit = "hbm", "GB/s"
         achieved = kbytes / (kms / 1e3) / 1e9
         share = res.hessian_products * kms / (t_step * 1e3) if t_step > 0 else None
         gram_extra = {}
@@ -693,9 +704,10 @@ def main():
         "objective": res.objective, "converged": res.converged,
         "outer_iterations": len(res.trace.iterations), "hessian_products": res.hessian_products,
         "hv_per_s": res.hessian_products / t_step if t_step > 0 else None,
-        "roofline": {"bound": "hbm", "kernel": kern,
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs: copy read+write GB/s)",
+        "roofline": {"bound": bound, "kernel": kern,
+                     "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                     "peak_source": (peak_kind if bound == "tensor" else
+                                     f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs: copy read+write GB/s)"),
                      "traffic": read_traffic(args.workload + ("-gram" if gram_extra else "")),
                      "algorithmic_bytes_per_launch": kbytes, "avg_launch_ms": kms,
                      "launch_timing": "CUDA events around each launch on the solver stream, 256 MiB "
