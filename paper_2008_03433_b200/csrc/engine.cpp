@@ -127,6 +127,23 @@ Comm::~Comm() {
   if (stage_) tron_host_free(stage_);
 }
 
+void Comm::allreduce_sum(const double* send, double* recv, size_t count, cudaStream_t s) {
+  if (count == 0) return;
+  if (!active()) {
+    if (send != recv)
+      cuda_check(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
+    return;
+  }
+  if (host_fn_) {
+    if (send != recv)
+      cuda_check(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, s), "D2D");
+    allreduce_sum(recv, count, s);
+    return;
+  }
+  nccl_check(g_nccl.AllReduce(send, recv, count, ncclFloat64, ncclSum, (ncclComm_t)comm_, s),
+             "ncclAllReduce");
+}
+
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
   if (!active() || count == 0) return;
   if (host_fn_) {
@@ -680,6 +697,9 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       e->gram_fused_ = dense_forward_gram_fused((int64_t)n) && gf && gf[0] == '1';
       for (auto& S : e->slot_) {
         S.gram.alloc((size_t)n * n);
+        if (e->comm_.active()) S.gram_local.alloc((size_t)n * n);
+        S.gram_stale.alloc(1);
+        cuda_check(cudaMemsetAsync(S.gram_stale.p, 0, sizeof(int), e->s_), "memset");
         if (e->gram_fused_) S.gram_parts.alloc((size_t)dense_grid((int64_t)l, (int64_t)n) * n * n);
       }
       if (!e->gram_fused_) e->gram_parts_.alloc((size_t)gram_grid((int64_t)l, (int64_t)n) * n * n);
@@ -1015,7 +1035,10 @@ void Engine::gradient_into(const Slot& S, double* out) {
   }
   if (dense_) {
     dense_vector(-1, nullptr, epi, out, &S);  // partials from the fused margin pass
-    if (gram_) gram_slot(S);                  // the Hessian of this iterate, once per commit
+    if (gram_) {  // the Hessian of this iterate: formed when first needed (ensure_gram)
+      cuda_check(cudaMemsetAsync(S.gram_stale.p, 0xff, sizeof(int), s_), "memset");
+      if (gram_fused_) gram_slot(S);  // (the fused pass's partials are already there)
+    }
   } else {
     UView u;
     if (loss_ == TRON_LOSS_LOGISTIC) {
@@ -1266,6 +1289,22 @@ void Engine::row_products(const double* v, const double* dvec, const uint8_t* ma
 
 // G = sum_i c_i x_i x_i^T of slot S (c = its mask or D), summed over the
 // shards when row-sharded (one n*n exchange per commit, none per Hv).
+// G of slot S for its current iterate.  Lazily: an accepted step marks the new
+// committed slot's G stale, and it is formed right before the CG that needs
+// it -- so the last iterate of a solve (converged) and rejected candidates
+// never pay for a Gram pass.  The kernels check the flag on the device.
+void Engine::ensure_gram(const Slot& S) {
+  if (!gram_ || gram_fused_) return;
+  const bool svm = loss_ == TRON_LOSS_L2SVM;
+  const bool shard = comm_.active();
+  dense_gram(l_, n_, ld_, Xc_.p, svm ? S.mask.p : nullptr, svm ? nullptr : S.dvec.p, gram_parts_.p,
+             shard ? S.gram_local.p : S.gram.p, s_, S.gram_stale.p);
+  count_launch(2);
+  // row shards: G = sum of the ranks' parts, out of place, so repeating it
+  // when nothing was stale changes nothing (every rank makes the same calls)
+  if (shard) comm_.allreduce_sum(S.gram_local.p, S.gram.p, (size_t)n_ * n_, s_);
+}
+
 void Engine::gram_slot(const Slot& S) {
   const bool svm = loss_ == TRON_LOSS_L2SVM;
   if (gram_fused_) {  // the slot's margin pass accumulated the partials already
@@ -1295,6 +1334,7 @@ void Engine::hv_kernels(const double* v, double* out, bool with_dot) {
     return;
   }
   if (dense_ && gram_) {  // v + s G v
+    ensure_gram(S);
     gram_hv(n_, S.gram.p, v, epi.scale, out, s_);
     count_launch(1);
     return;
@@ -1372,6 +1412,7 @@ void Engine::precond_kernels(const Slot& S) {
   if (ro_) {
     ro_accum_slot(RO_PRECOND, S, nullptr, epi, M_.p);
   } else if (dense_ && gram_) {
+    ensure_gram(S);
     gram_precond(n_, S.gram.p, epi.scale, M_.p, s_);
     count_launch(1);
   } else if (dense_) {
@@ -1442,7 +1483,8 @@ void Engine::state_svm(int which, double* z, int64_t* active, uint64_t cap, uint
 // device-resident truncated CG (tron.cpp:37-108)
 // ----------------------------------------------------------------------------
 // CG initialisation (d = 0, r = -g, p = M^-1 r) into the current capture.
-void Engine::capture_cg_init(const CgVectors& v, Cond cond) {
+void Engine::capture_cg_init(int k, const CgVectors& v, Cond cond) {
+  if (dense_ && gram_) ensure_gram(slot_[k]);  // the committed iterate's G (if stale)
   if (ro_)
     ro_cg_init(v, st_d_, cond, s_);
   else if (small_engine_)
@@ -1543,7 +1585,7 @@ void Engine::build_graph(int k, bool use_m) {
   const uint64_t saved_launches = launches;
 
   begin_capture(s_, graph);
-  capture_cg_init(v, cond);
+  capture_cg_init(k, v, cond);
   cudaGraph_t body = add_conditional(s_, (cudaGraphConditionalHandle)cond.h, cudaGraphCondTypeWhile);
   cuda_check(cudaStreamEndCapture(s_, &graph), "end capture");
 
@@ -1715,7 +1757,7 @@ void Engine::run_cg(double delta, const tron_config& cfg, CgState* out) {
   // host-driven loop (host data plane, or TRON_B200_NO_GRAPH / NCCL_GRAPH=0):
   // the graph's kernels, launched one iteration at a time
   Cond none;
-  capture_cg_init(v, none);
+  capture_cg_init(k, v, none);
   read_cg(out);
   while (out->cont) {
     capture_cg_body(k, v, none);
@@ -2014,7 +2056,7 @@ void Engine::build_solve_graph(bool use_m) {
     if (use_m) precond_kernels(slot_[k]);  // recomputed per iteration: same bits as cached
     tr_prep(ss, st_d_, s_);
     count_launch(1);
-    capture_cg_init(v, ck);
+    capture_cg_init(k, v, ck);
     cudaGraph_t W = add_conditional(s_, (cudaGraphConditionalHandle)ck.h, cudaGraphCondTypeWhile);
     const int saved = cand_;
     cand_ = k ^ 1;
@@ -2220,7 +2262,11 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
                     gram_fused_ ? slot_[cand_].gram_parts.p : nullptr);
     });
   }
-  out->grad_ms = time_it([&] { gradient_dev(); });
+  // (Gram mode: the gradient plus the committed iterate's G, formed afresh)
+  out->grad_ms = time_it([&] {
+    gradient_dev();
+    if (dense_ && gram_) ensure_gram(slot_[cand_ ^ 1]);
+  });
   slot_[cand_].valid = false;  // forward timing overwrote the candidate slot
   cudaEventDestroy(a);
   cudaEventDestroy(b);

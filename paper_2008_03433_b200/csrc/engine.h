@@ -111,6 +111,8 @@ class Comm {
   void init(const tron_gpu_options& opt);
   ~Comm();
   void allreduce_sum(double* buf, size_t count, cudaStream_t s);
+  // out-of-place (idempotent: recv = sum of the ranks' send)
+  void allreduce_sum(const double* send, double* recv, size_t count, cudaStream_t s);
   bool active() const { return world > 1 || forced; }
   bool host() const { return host_fn_ != nullptr && world > 1; }
   bool forced = false;  // one-rank communicator forced on (TRON_B200_FORCE_NCCL=1)
@@ -183,6 +185,8 @@ class Engine {
     DevBuf<long long> cnt;  // ... and |I| (device)
     DevBuf<double> gram;    // dense Gram mode: this slot's Hessian sum_i c_i x_i x_i^T (n x n)
     DevBuf<double> gram_parts;  // ... its per-CTA partials from the fused margin pass
+    DevBuf<int> gram_stale;     // 1: the slot's iterate changed since G was formed
+    DevBuf<double> gram_local;  // row-sharded: this rank's part of G (allreduced into gram)
     double f = 0.0;
     long long nact = 0;
     bool valid = false;
@@ -207,7 +211,8 @@ class Engine {
   void build_graph(int slot, bool use_m);
   void launch_cg_graph(int slot, bool use_m);
   // CG pieces captured into the current stream capture (committed slot k)
-  void capture_cg_init(const CgVectors& v, Cond cond);
+  void capture_cg_init(int k, const CgVectors& v, Cond cond);
+  void ensure_gram(const Slot& S);  // G of slot S, formed only when stale
   void capture_cg_body(int k, const CgVectors& v, Cond cond);
   void precond_kernels(const Slot& S);
   // device-resident outer loop (trloop.cu): one graph per use_m

@@ -26,9 +26,18 @@ namespace {
 
 // Tile of 128 rows staged column-major with a padded stride (132 = 4 mod 16
 // doubles: the DMMA fragment loads below hit distinct banks in each half-warp).
-constexpr int kGramRows = 128;
-constexpr int kGramStride = 132;
-constexpr int kGramThreads = 256;  // 8 warps; warp w takes the k-steps w, w+8, ... of a tile
+#ifndef TB_GRAM_ROWS
+#define TB_GRAM_ROWS 128
+#endif
+#ifndef TB_GRAM_THREADS
+#define TB_GRAM_THREADS 256
+#endif
+#ifndef TB_GRAM_CTAS
+#define TB_GRAM_CTAS 2  // resident CTAs per SM (n <= 40)
+#endif
+constexpr int kGramRows = TB_GRAM_ROWS;
+constexpr int kGramStride = kGramRows + 4;  // = 4 (mod 16) doubles
+constexpr int kGramThreads = TB_GRAM_THREADS;  // warp w takes the k-steps w, w + warps, ... of a tile
 
 // mma.sync m8n8k4 f64 (DMMA): D(8x8) += A(8x4) B(4x8); per lane one A and one
 // B element and two accumulators (row g = lane/4, columns 2t, 2t+1, t = lane%4).
@@ -53,13 +62,15 @@ __device__ __forceinline__ void cp_wait() {
 // loads feed NB (NB+1)/2 DMMAs.  Tiles are double-buffered with cp.async: the
 // next tile's rows and weights are in flight while this one is multiplied.
 template <int NB, bool MASK>
-__global__ void __launch_bounds__(kGramThreads, NB <= 5 ? 2 : 1) gram_kernel(long long l, int n, long long ld,
+__global__ void __launch_bounds__(kGramThreads, NB <= 5 ? TB_GRAM_CTAS : 1) gram_kernel(long long l, int n, long long ld,
                                                               const double* __restrict__ X,
                                                               const uint8_t* __restrict__ mask,
                                                               const double* __restrict__ dvec,
-                                                              double* __restrict__ partials) {
+                                                              double* __restrict__ partials,
+                                                              const int* __restrict__ stale) {
   pdl_wait();
   pdl_trigger();
+  if (stale && *stale == 0) return;  // G of this iterate is current
   constexpr int NC = NB * 8;
   constexpr int NP = NB * (NB + 1) / 2;
   constexpr int TILE = NC * kGramStride;  // doubles per staged tile
@@ -149,13 +160,18 @@ __global__ void __launch_bounds__(kGramThreads, NB <= 5 ? 2 : 1) gram_kernel(lon
   }
 }
 
-__global__ void gram_finalize_kernel(int n, const double* __restrict__ partials, int nparts,
-                                     double* __restrict__ G) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+// One CTA: every thread reads the stale flag before thread 0 clears it.
+__global__ void __launch_bounds__(1024) gram_finalize_kernel(int n, const double* __restrict__ partials,
+                                                            int nparts, double* __restrict__ G,
+                                                            int* stale) {
+  if (stale && *stale == 0) return;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     double s = 0.0;
     for (int b = 0; b < nparts; ++b) s += partials[(size_t)b * n * n + e];
     G[e] = s;
   }
+  __syncthreads();
+  if (stale && threadIdx.x == 0) *stale = 0;
 }
 
 __global__ void gram_hv_kernel(int n, const double* __restrict__ G, const double* __restrict__ v,
@@ -177,7 +193,7 @@ __global__ void gram_precond_kernel(int n, const double* __restrict__ G, double 
 }  // namespace
 
 void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s) {
-  gram_finalize_kernel<<<(int)((n * n + 255) / 256), 256, 0, s>>>((int)n, partials, nparts, G);
+  gram_finalize_kernel<<<1, 1024, 0, s>>>((int)n, partials, nparts, G, nullptr);
   TB_LAUNCH_CHECK();
 }
 
@@ -192,12 +208,13 @@ void gram_precond(int64_t n, const double* G, double scale, double* M, cudaStrea
 
 int gram_grid(int64_t l, int64_t n) {
   const int64_t tiles = (l + kGramRows - 1) / kGramRows;
-  int64_t g = (int64_t)device_sm_count() * (n <= 40 ? 2 : 1);  // resident CTAs of 8 warps per SM
+  int64_t g = (int64_t)device_sm_count() * (n <= 40 ? TB_GRAM_CTAS : 1);  // resident CTAs per SM
   if (g > tiles) g = tiles;
   return (int)(g > 0 ? g : 1);
 }
 
 namespace {
+thread_local int* stale_g = nullptr;  // dense_gram's stale flag for launch_gram
 template <int NB, bool W>
 void launch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
                  const double* dvec, double* partials, int grid, cudaStream_t s) {
@@ -206,7 +223,7 @@ void launch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_
   const size_t bytes = tile > red ? tile : red;
   ensure_max_dynamic_smem((const void*)gram_kernel<NB, W>, (int)bytes);
   launch_pdl(gram_kernel<NB, W>, dim3(grid), dim3(kGramThreads), bytes, s, (long long)l, (int)n,
-             (long long)ld, X, mask, dvec, partials);
+             (long long)ld, X, mask, dvec, partials, (const int*)stale_g);
 }
 template <bool W>
 void dispatch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
@@ -225,14 +242,16 @@ void dispatch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint
 }  // namespace
 
 void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
-                const double* dvec, double* partials, double* G, cudaStream_t s) {
+                const double* dvec, double* partials, double* G, cudaStream_t s, int* stale) {
+  stale_g = stale;
   const int grid = gram_grid(l, n);
   if (mask)
     dispatch_gram<true>(l, n, ld, X, mask, dvec, partials, grid, s);
   else
     dispatch_gram<false>(l, n, ld, X, mask, dvec, partials, grid, s);
-  gram_finalize_kernel<<<(int)((n * n + 255) / 256), 256, 0, s>>>((int)n, partials, grid, G);
+  gram_finalize_kernel<<<1, 1024, 0, s>>>((int)n, partials, grid, G, stale);
   TB_LAUNCH_CHECK();
+  stale_g = nullptr;
 }
 
 }  // namespace tb

@@ -333,8 +333,11 @@ void dense_gather(int64_t nI, int64_t n, const double* X, int64_t ld, const int3
 // G = sum_i c_i x_i x_i^T, c = mask (SVM, dvec null) or dvec (LR); partials
 // >= gram_grid(l, n) * n * n doubles.  Deterministic.
 int gram_grid(int64_t l, int64_t n);
+// stale (device int, nullable): when it reads 0 the kernels return at once (G is
+// current); the finalize clears it -- so the launch can sit unconditionally in a
+// graph and cost ~10 us when nothing changed.
 void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
-                const double* dvec, double* partials, double* G, cudaStream_t s);
+                const double* dvec, double* partials, double* G, cudaStream_t s, int* stale = nullptr);
 // out = v + scale * G v (row j of G dotted with v in index order)
 void gram_hv(int64_t n, const double* G, const double* v, double scale, double* out, cudaStream_t s);
 // M_j = 1 + scale * G_jj (loss.cpp:176-188)
