@@ -214,44 +214,41 @@ int gram_grid(int64_t l, int64_t n) {
 }
 
 namespace {
-thread_local int* stale_g = nullptr;  // dense_gram's stale flag for launch_gram
 template <int NB, bool W>
 void launch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
-                 const double* dvec, double* partials, int grid, cudaStream_t s) {
+                 const double* dvec, double* partials, const int* stale, int grid, cudaStream_t s) {
   const size_t tile = ((size_t)2 * NB * 8 * kGramStride + 2 * kGramRows) * sizeof(double);
   const size_t red = (size_t)(NB * (NB + 1) / 2) * 64 * sizeof(double);
   const size_t bytes = tile > red ? tile : red;
   ensure_max_dynamic_smem((const void*)gram_kernel<NB, W>, (int)bytes);
   launch_pdl(gram_kernel<NB, W>, dim3(grid), dim3(kGramThreads), bytes, s, (long long)l, (int)n,
-             (long long)ld, X, mask, dvec, partials, (const int*)stale_g);
+             (long long)ld, X, mask, dvec, partials, stale);
 }
 template <bool W>
 void dispatch_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
-                   const double* dvec, double* partials, int grid, cudaStream_t s) {
+                   const double* dvec, double* partials, const int* stale, int grid, cudaStream_t s) {
   switch ((n + 7) / 8) {
-    case 1: launch_gram<1, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    case 2: launch_gram<2, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    case 3: launch_gram<3, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    case 4: launch_gram<4, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    case 5: launch_gram<5, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    case 6: launch_gram<6, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    case 7: launch_gram<7, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
-    default: launch_gram<8, W>(l, n, ld, X, mask, dvec, partials, grid, s); break;
+    case 1: launch_gram<1, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    case 2: launch_gram<2, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    case 3: launch_gram<3, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    case 4: launch_gram<4, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    case 5: launch_gram<5, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    case 6: launch_gram<6, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    case 7: launch_gram<7, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
+    default: launch_gram<8, W>(l, n, ld, X, mask, dvec, partials, stale, grid, s); break;
   }
 }
 }  // namespace
 
 void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t* mask,
                 const double* dvec, double* partials, double* G, cudaStream_t s, int* stale) {
-  stale_g = stale;
   const int grid = gram_grid(l, n);
   if (mask)
-    dispatch_gram<true>(l, n, ld, X, mask, dvec, partials, grid, s);
+    dispatch_gram<true>(l, n, ld, X, mask, dvec, partials, stale, grid, s);
   else
-    dispatch_gram<false>(l, n, ld, X, mask, dvec, partials, grid, s);
+    dispatch_gram<false>(l, n, ld, X, mask, dvec, partials, stale, grid, s);
   gram_finalize_kernel<<<1, 1024, 0, s>>>((int)n, partials, grid, G, stale);
   TB_LAUNCH_CHECK();
-  stale_g = nullptr;
 }
 
 }  // namespace tb
