@@ -2235,6 +2235,7 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
     return total / std::max(reps, 1);
   };
   cuda_check(cudaMemcpyAsync(vtmp_.p, g_.p, n_ * 8, cudaMemcpyDeviceToDevice, s_), "D2D");
+  if (dense_ && gram_) ensure_gram(slot_[cand_ ^ 1]);  // Hv times the product from a current G
   out->hv_ms = time_it([&] { hv_kernels(vtmp_.p, otmp_.p); });
   const Slot& S = slot_[cand_ ^ 1];
   if (!dense_) {
