@@ -397,8 +397,20 @@ def cpu_baseline(args, p_full, res, ev, loss, cfg, plan, act_gpu=None):
         v, sample = modelled_reference_solve(ref, p_full, args.workload, threads)
         out.update(value=v, sample=sample)
         try:
-            out["parity"] = json.load(open(os.path.join(ROOT, PARITY_FILES[args.workload])))["parity"]
+            rec = json.load(open(os.path.join(ROOT, PARITY_FILES[args.workload])))
+            out["parity"] = rec["parity"]
             out["parity"]["source"] = PARITY_FILES[args.workload] + " (full-size run, same generator)"
+            # the measured full reference solve behind the model (same SYNTH-v1 input)
+            secs = rec.get("reference_solve_s") or rec.get("reference", {}).get("seconds")
+            if secs:
+                out["full_solve_measured_s"] = secs
+                out["full_solve_measured_where"] = (f"{PARITY_FILES[args.workload]}: ExecutionPlan::parallel("
+                                                    f"{rec.get('threads', '?')}) "
+                                                    + ("on this pool's GPU box" if args.workload == "Q1"
+                                                       else "in the build container (8 cores)"))
+            if "tight" in rec:
+                out["parity"]["tight_eps"] = {k: rec["tight"][k] for k in ("eps", "rel_objective", "rel_w")
+                                              if k in rec["tight"]}
         except Exception:
             pass
         return out
