@@ -122,12 +122,18 @@ SolveResult solve(LossEvaluator& evaluator, const TrustRegionConfig& cfg,
 
 // ---- the B200 evaluator (BackendKind "gpu") ----
 enum class LossKind { Logistic, L2Svm };
-enum class SvmStrategy { Gathered, Indirect };
+enum class SvmStrategy { Gathered, Indirect, Auto };
 
 struct GpuPlan {
   int device = 0;
   SvmStrategy svm_strategy = SvmStrategy::Indirect;
   std::size_t gathered_budget_bytes = std::size_t{2} << 30;
+  bool reference_order = false;  // dense L2-SVM: every reduction in the reference's order
+  int out_of_core = 0;           // dense: 0 auto, 1 stream X from host memory, -1 never
+  std::size_t stream_block_rows = 0;
+  // Everything else (row / column shards, NCCL id, host allreduce): the full C
+  // options; when set they are used as given (device / strategy above ignored).
+  const tron_gpu_options* options = nullptr;
   tron_ledger ledger{};
 };
 
