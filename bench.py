@@ -530,6 +530,9 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--rows", type=int, default=None,
                     help="first ROWS rows of the workload only (tests; the config says so)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="N > 1 data plane: NCCL (one GPU per rank) or the host allreduce over the gloo "
+                         "group (ranks may share a GPU: a functional check of the N > 1 flow)")
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -558,10 +561,18 @@ def main():
     p_full, loss = product_problem(args.workload, rows=args.rows)
     p, row_begin = shard(p_full, rank, world) if world > 1 else (p_full, 0)
 
+    device = local_rank % max(torch.cuda.device_count(), 1)
+
     def make_plan():
         """The rank's plan; N > 1: a fresh NCCL unique id (rank 0's, broadcast)
-        for every context -- an id serves one communicator."""
-        pl = ExecutionPlan.gpu(device=local_rank)
+        for every context -- an id serves one communicator -- or the host
+        data plane over the gloo group."""
+        pl = ExecutionPlan.gpu(device=device)
+        if world > 1 and args.comm == "host":
+            pl.rank, pl.world = rank, world
+            pl.row_begin, pl.global_rows = row_begin, p_full.X.rows
+            pl.host_allreduce = lambda buf: dist.all_reduce(torch.from_numpy(buf))
+            return pl
         if world > 1:
             uid = None
             if rank == 0:
@@ -578,7 +589,7 @@ def main():
     plan = make_plan()
     cfg = TrustRegionConfig(eps=args.eps)
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(device)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def evict_l2():  # read-based: leaves nothing dirty to write back inside the step
@@ -604,7 +615,7 @@ def main():
 
     launches0 = ev.launch_count()
     wall, dev_ms, res = [], [], None
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(device)
     barrier()
     with sampler:
         for _ in range(args.steps):
@@ -709,7 +720,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (SYNTH-v1 generator, seed {SEED}; SURVEY.md §8(d))",
         "config": workload_config(args.workload, args.eps, args.rows),
-        "parallelism": f"row-sharded x{world} (NCCL allreduce of partials)" if world > 1 else "1 GPU",
+        "parallelism": (f"row-sharded x{world} ({'NCCL' if args.comm == 'nccl' else 'host/gloo'} allreduce of "
+                        "partials)") if world > 1 else "1 GPU",
         "timing": ("value: host wall time of each solve call (returns with w on the host), mean over "
                    "steps, max over ranks; device_s: CUDA-event time of the same solves"),
         "device_s": t_dev, "wall_s_min": max_over_ranks(float(np.min(wall))) if world > 1 else float(np.min(wall)),
