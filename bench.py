@@ -534,6 +534,12 @@ def main():
                     help="N > 1 data plane: NCCL (one GPU per rank) or the host allreduce over the gloo "
                          "group (ranks may share a GPU: a functional check of the N > 1 flow)")
     args = ap.parse_args()
+    if os.environ.get("TRON_BENCH_WATCHDOG") and "WORLD_SIZE" in os.environ:
+        # debugging: every thread's stack after N s into gpurun_out/hang_rank<R>.txt, then exit
+        import faulthandler
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        _wd = open(os.path.join(ROOT, "gpurun_out", f"hang_rank{os.environ.get('RANK', '0')}.txt"), "w")
+        faulthandler.dump_traceback_later(int(os.environ["TRON_BENCH_WATCHDOG"]), exit=True, file=_wd)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args)
@@ -708,6 +714,9 @@ def main():
         # (N > 1: rank 0 alone, the other ranks wait at the closing barrier)
         cpu = cpu_baseline(args, p_full, res, ev, loss, cfg, plan, act_gpu=act_all)
 
+    # (every collective happens before the ranks part: the other ranks wait at
+    # the closing barrier while rank 0 assembles the line)
+    wall_min = max_over_ranks(float(np.min(wall)))
     if rank != 0:
         ev.close()
         barrier()
@@ -724,7 +733,7 @@ def main():
                         "partials)") if world > 1 else "1 GPU",
         "timing": ("value: host wall time of each solve call (returns with w on the host), mean over "
                    "steps, max over ranks; device_s: CUDA-event time of the same solves"),
-        "device_s": t_dev, "wall_s_min": max_over_ranks(float(np.min(wall))) if world > 1 else float(np.min(wall)),
+        "device_s": t_dev, "wall_s_min": wall_min,
         "objective": res.objective, "converged": res.converged,
         "outer_iterations": len(res.trace.iterations), "hessian_products": res.hessian_products,
         "hv_per_s": res.hessian_products / t_step if t_step > 0 else None,
