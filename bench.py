@@ -645,12 +645,15 @@ def main():
     if p.X.layout == "dense" and mode["gram"]:
         # Hessian as an n x n matrix per commit (gram.cu): the CG's Hv no longer
         # reads X; the passes over X are the fused margin pass (one per
-        # evaluation) and the Gram pass (one per evaluation, speculative with
-        # the gradient).  The roofline object describes the larger of the two.
+        # evaluation; gram_delta: it also adds the rows that changed side to the
+        # committed G) and the Gram pass (gram_delta: at w0 only; else once per
+        # committed iterate that runs a CG).  The roofline object describes the
+        # one with the larger share of the solve.
         l, n = p.X.rows, p.X.cols
-        fwd_bytes, gram_bytes = 8 * l * n + 17 * l, 8 * l * n + l
+        fwd_bytes, gram_bytes = 8 * l * n + (18 if mode.get("gram_delta") else 17) * l, 8 * l * n + l
         gram_flops = l * n * (n + 1)  # the upper triangle of sum_i c_i x_i x_i^T, 2 flops per product
-        if kt["grad_ms"] >= kt["forward_ms"]:
+        n_gram = 1 if mode.get("gram_delta") else max(1, res.trace.accepted_steps)
+        if n_gram * kt["grad_ms"] >= n_evals * kt["forward_ms"]:
             # bound by the FP64 tensor pipe (ncu: math-pipe throttle), HBM a close second
             kern, kbytes, kms = "Gram pass G = sum_i c_i x_i x_i^T (gram.cu, DMMA; once per commit)", gram_bytes, kt["grad_ms"]
             bound, unit = "tensor", "TFLOP/s"
@@ -661,8 +664,9 @@ def main():
             kern, kbytes, kms = "fused margin pass (dense_pass FWD: margins, mask, f, gradient partials)", fwd_bytes, kt["forward_ms"]
             bound, unit = "hbm", "GB/s"
             achieved = kbytes / (kms / 1e3) / 1e9
-        share = n_evals * kms / (t_step * 1e3) if t_step > 0 else None
-        gram_extra = {"gram_pass_ms": kt["grad_ms"], "gram_pass_hbm_gbs": gram_bytes / (kt["grad_ms"] / 1e3) / 1e9,
+        share = (n_gram if bound == "tensor" else n_evals) * kms / (t_step * 1e3) if t_step > 0 else None
+        gram_extra = {"gram_delta": bool(mode.get("gram_delta")), "gram_passes_per_solve": n_gram,
+                      "gram_pass_ms": kt["grad_ms"], "gram_pass_hbm_gbs": gram_bytes / (kt["grad_ms"] / 1e3) / 1e9,
                       "gram_pass_fp64_tflops": gram_flops / (kt["grad_ms"] / 1e3) / 1e12,
                       "margin_pass_ms": kt["forward_ms"], "margin_pass_gbs": fwd_bytes / (kt["forward_ms"] / 1e3) / 1e9,
                       "hv_from_gram_us": kt["hv_ms"] * 1e3,

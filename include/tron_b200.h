@@ -213,9 +213,11 @@ int tron_gpu_bench_kernels(tron_gpu_ctx *ctx, int reps, int flush_l2, double out
 /* How this context runs its hot path (bit set): TRON_MODE_GRAM (dense: the
  * Hessian as an n x n matrix per commit), TRON_MODE_OUT_OF_CORE (X streamed from
  * host memory), TRON_MODE_COLUMNS (column-partitioned), TRON_MODE_DEVICE_LOOP
- * (the solve is one graph launch), TRON_MODE_SHARDED (row shards). */
+ * (the solve is one graph launch), TRON_MODE_SHARDED (row shards),
+ * TRON_MODE_GRAM_DELTA (L2-SVM Gram mode: each candidate's G is the committed
+ * G plus the rows that changed side, accumulated by its margin pass). */
 enum { TRON_MODE_GRAM = 1, TRON_MODE_OUT_OF_CORE = 2, TRON_MODE_COLUMNS = 4, TRON_MODE_DEVICE_LOOP = 8,
-       TRON_MODE_SHARDED = 16 };
+       TRON_MODE_SHARDED = 16, TRON_MODE_GRAM_DELTA = 32 };
 int tron_gpu_mode(tron_gpu_ctx *ctx, uint32_t *flags);
 /* Device bytes held by the context (matrix copies + vectors). */
 int tron_gpu_memory_bytes(tron_gpu_ctx *ctx, uint64_t *bytes);

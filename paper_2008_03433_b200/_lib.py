@@ -24,7 +24,7 @@ LOSS_LOGISTIC, LOSS_L2SVM = 0, 1
 SVM_GATHERED, SVM_INDIRECT, SVM_AUTO = 0, 1, 2
 SOLVE_DEVICE, SOLVE_HOST_CG = 0, 1
 PARTITION_ROWS, PARTITION_COLUMNS = 0, 1
-MODE_GRAM, MODE_OUT_OF_CORE, MODE_COLUMNS, MODE_DEVICE_LOOP, MODE_SHARDED = 1, 2, 4, 8, 16
+MODE_GRAM, MODE_OUT_OF_CORE, MODE_COLUMNS, MODE_DEVICE_LOOP, MODE_SHARDED, MODE_GRAM_DELTA = 1, 2, 4, 8, 16, 32
 
 
 class tron_config(ctypes.Structure):

@@ -66,10 +66,18 @@ struct PassArgs {
   ObjScalars* obj;
   Scratch sc;
   double* partials;      // [gridDim.x][n]
-  double* gram_partials; // PM_FWDG: [gridDim.x][n*n] Gram partials (gram.cu's G) of the candidate
+  double* gram_partials; // PM_FWDG: [gridDim.x][n*n] Gram partials (gram.cu's G) of the candidate;
+                         // PM_FWDD: the partials of its change against the reference slot
+  const int* ref_stale;  // PM_FWDD: the reference slot's Gram flag (0: its G matches a.mask)
 };
 
-enum PassMode : int { PM_FWD = 0, PM_HV = 1, PM_PRECOND = 2, PM_FWDG = 3 };
+// PM_FWDD (L2-SVM): the margin pass also accumulates
+//   Delta = sum_i (m_i - m_ref_i) x_i x_i^T
+// over the rows whose active bit differs from the reference slot's mask
+// (a.mask), so that the candidate's Gram matrix is G_ref + Delta
+// (gram_delta_finalize) instead of a fresh pass over X: between commits only
+// 6-11% of P1's rows change sides (profiles/active_churn_P1.jsonl, scripts/active_churn.py).
+enum PassMode : int { PM_FWD = 0, PM_HV = 1, PM_PRECOND = 2, PM_FWDG = 3, PM_FWDD = 4 };
 
 // mma.sync m8n8k4 f64 (DMMA), as gram.cu
 __device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
@@ -81,21 +89,31 @@ __device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
 // Side arrays of a mode: d-arrays in order, then the mask.
 template <int MODE, int LOSS>
 struct Side {
-  static constexpr bool fwd = MODE == PM_FWD || MODE == PM_FWDG;
+  static constexpr bool fwd = MODE == PM_FWD || MODE == PM_FWDG || MODE == PM_FWDD;
   static constexpr int nd = fwd ? 1 : (LOSS == kLossLogistic ? 1 : 0);
-  static constexpr bool mask = !fwd && LOSS == kLossSvm;
+  static constexpr bool mask = (!fwd && LOSS == kLossSvm) || MODE == PM_FWDD;  // (FWDD: the reference mask)
 };
 
-// T compute threads (one row of the tile each) + one producer warp.
+// TB_DENSE_PRODUCER_WARP=1: a dedicated producer warp issues the copies.
+// Default: thread 0 issues them -- the first stages up front, then each stage
+// again as soon as every warp has released it -- so the CTA is 8 warps, not 9,
+// and a thread may hold 255 registers instead of 168 (the register file is
+// split over the four sub-partitions: 3 warps of one CTA shared one of them).
+#ifndef TB_DENSE_PRODUCER_WARP
+#define TB_DENSE_PRODUCER_WARP 0
+#endif
+constexpr int kProdWarps = TB_DENSE_PRODUCER_WARP ? 1 : 0;
+
+// T compute threads (one row of the tile each) [+ one producer warp].
 template <int NMAX, int T, int MODE, int LOSS>
-__global__ void __launch_bounds__(T + kWarp, 1)
+__global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
     dense_pass_kernel(const __grid_constant__ CUtensorMap xmap, PassArgs a, int nstages) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long full[4], empty[4];
   __shared__ double s_v[NMAX];
-  constexpr int BLK = T + kWarp;
+  constexpr int BLK = T + kProdWarps * kWarp;
   constexpr int NCW = T / kWarp;  // compute warps
   __shared__ double sh[BLK / kWarp + 1];
   using SD = Side<MODE, LOSS>;
@@ -124,31 +142,68 @@ __global__ void __launch_bounds__(T + kWarp, 1)
   // pass (gram.cu's DMMA scheme on the staged tile): NB groups of 8 columns,
   // NP block pairs, two accumulators per pair and lane
   constexpr bool FG = MODE == PM_FWDG;
-  constexpr int NB = FG ? (NMAX + 7) / 8 : 1;
+  constexpr bool FD = MODE == PM_FWDD;
+  constexpr int NB = (FG || FD) ? (NMAX + 7) / 8 : 1;
   constexpr int NP = NB * (NB + 1) / 2;
   __shared__ double s_w[FG ? 2 : 1][FG ? T : 1];  // row weights c_i, by tile parity
-  double gacc[NP][2];
+  // PM_FWDD: the tile's changed rows, compacted kDR at a time into a
+  // column-major block (stride kDS = 4 mod 16 doubles: conflict-free DMMA
+  // fragment loads), their weights +-1, and the per-warp counts by tile parity
+  constexpr int kDR = 64, kDS = kDR + 4;
+  __shared__ double s_cb[FD ? NMAX * kDS : 1];
+  __shared__ double s_cw[FD ? kDR : 1];
+  __shared__ int s_cnt[FD ? 2 : 1][FD ? NCW : 1];
+  // (no delta against a reference whose G is not current: the pass is plain FWD)
+  const bool dodelta = FD && *a.ref_stale == 0;
+  double gacc[FD ? 1 : NP][2];  // (FWDD: dacc below)
 #pragma unroll
-  for (int p = 0; p < NP; ++p) gacc[p][0] = gacc[p][1] = 0.0;
+  for (int p = 0; p < (FD ? 1 : NP); ++p) gacc[p][0] = gacc[p][1] = 0.0;
+  // PM_FWDD: warp w owns the block pairs w, w + NCW, ... of the Delta (two
+  // accumulators per pair and lane, summed over every k-step of every round
+  // in order: deterministic, and only NPW pairs' registers per thread)
+  constexpr int NPW = FD ? (NP + NCW - 1) / NCW : 1;
+  double dacc[NPW][2];
+  int dc1[NPW], dc2[NPW];
+#pragma unroll
+  for (int q = 0; q < NPW; ++q) {
+    dacc[q][0] = dacc[q][1] = 0.0;
+    int pp = wid + q * NCW, c1 = 0;
+    if (pp >= NP) pp = -1;
+    int rem = pp < 0 ? 0 : pp;
+    while (rem >= NB - c1) {
+      rem -= NB - c1;
+      ++c1;
+    }
+    dc1[q] = pp < 0 ? -1 : c1;
+    dc2[q] = c1 + rem;
+  }
 
-  if (wid == NCW) {
-    // ---- producer warp: one 2-D TMA box {T rows x n columns} of X per
-    // tile plus the per-row side arrays, into stage k % nstages
+  // one 2-D TMA box {T rows x n columns} of X per tile plus the per-row side
+  // arrays, into stage k % nstages (one thread)
+  auto issue = [&](long long k) {
+    const long long t = blockIdx.x + k * gridDim.x;
+    const int s = (int)(k % nstages);
+    unsigned char* base = smem + (size_t)s * sbytes;
+    const long long row0 = t * T;
+    mbar_arrive_expect_tx(&full[s], (unsigned)L.bytes());
+    tma_load_2d(base, &xmap, (int)row0, 0, &full[s]);
+    if (SD::nd >= 1) {
+      const double* src = SD::fwd ? a.y : a.dvec;
+      bulk_g2s(base + (size_t)n * T * 8, src + row0, T * 8, &full[s]);
+    }
+    if (use_mask) bulk_g2s(base + (size_t)(n + SD::nd) * T * 8, a.mask + row0, T, &full[s]);
+  };
+  if (!kProdWarps && tid == 0)
+    for (long long k = 0; k < nstages && blockIdx.x + k * gridDim.x < ntiles; ++k) issue(k);
+  if (kProdWarps && wid == NCW) {
+    // ---- producer warp
     if (lane == 0) {
       for (long long k = 0;; ++k) {
         const long long t = blockIdx.x + k * gridDim.x;
         if (t >= ntiles) break;
         const int s = (int)(k % nstages);
         if (k >= nstages) mbar_wait_parity(&empty[s], (unsigned)(((k / nstages) - 1) & 1));
-        unsigned char* base = smem + (size_t)s * sbytes;
-        const long long row0 = t * T;
-        mbar_arrive_expect_tx(&full[s], (unsigned)L.bytes());
-        tma_load_2d(base, &xmap, (int)row0, 0, &full[s]);
-        if (SD::nd >= 1) {
-          const double* src = SD::fwd ? a.y : a.dvec;
-          bulk_g2s(base + (size_t)n * T * 8, src + row0, T * 8, &full[s]);
-        }
-        if (use_mask) bulk_g2s(base + (size_t)(n + SD::nd) * T * 8, a.mask + row0, T, &full[s]);
+        issue(k);
       }
     }
   } else {
@@ -242,9 +297,59 @@ __global__ void __launch_bounds__(T + kWarp, 1)
             for (int c2 = c1; c2 < NB; ++c2) dmma8(gacc[pp++], fa[c1], fb[c2]);
         }
       }
+      if (FD && dodelta) {
+        // this row's change of side: +1 entered I, -1 left it, 0 unchanged
+        const double cdel = in ? cg - (ms[tid] ? 1.0 : 0.0) : 0.0;
+        const bool ch = cdel != 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ch);
+        int* cnt = s_cnt[FD ? (k & 1) : 0];
+        if (lane == 0) cnt[wid] = __popc(bal);
+        asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        int pos = __popc(bal & ((1u << lane) - 1u)), tot = 0;
+        for (int w = 0; w < NCW; ++w) {
+          const int c2 = cnt[w];
+          pos += w < wid ? c2 : 0;
+          tot += c2;
+        }
+        const int g = lane >> 2, tq = lane & 3;
+        for (int r0 = 0; r0 < tot; r0 += kDR) {
+          const int nr = tot - r0 < kDR ? tot - r0 : kDR, nr4 = (nr + 3) & ~3;
+          if (ch && pos >= r0 && pos < r0 + kDR) {
+            const int q = pos - r0;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + q] = j < n ? xs[j * T + tid] : 0.0;  // (the staged row)
+            s_cw[q] = cdel;
+          }
+          if (tid < nr4 - nr) {  // the last k-step's padding rows: weight 0, finite values
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + nr + tid] = 0.0;
+            s_cw[nr + tid] = 0.0;
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+          for (int ks = 0; ks < nr4 / 4; ++ks) {
+            const int rr = ks * 4 + tq;
+            const double cw = s_cw[rr];
+#pragma unroll
+            for (int q = 0; q < NPW; ++q) {
+              if (dc1[q] >= 0) {
+                const double fa = cw * s_cb[(dc1[q] * 8 + g) * kDS + rr];
+                const double fb = s_cb[(dc2[q] * 8 + g) * kDS + rr];
+                dmma8(dacc[q], fa, fb);
+              }
+            }
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");  // the block is restaged next
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    if (!kProdWarps && wid == 0 && blockIdx.x + (k + nstages) * gridDim.x < ntiles) {
+      // refill stage s once every warp has released it
+      mbar_wait_parity(&empty[s], (unsigned)((k / nstages) & 1));
+      if (lane == 0) issue(k + nstages);
+      __syncwarp();
+    }
   }
   }
   __syncthreads();  // all stages consumed; the producer has no copy in flight
@@ -267,23 +372,34 @@ __global__ void __launch_bounds__(T + kWarp, 1)
     a.partials[(long long)blockIdx.x * n + tid] = tsum;
   }
 
-  if (FG) {
+  if (FG || (FD && dodelta)) {
     // the compute warps' Gram partials, added in warp order (after the
     // gradient tree's slots), then this CTA's n x n partial, mirrored
     __syncthreads();
     double* gred = s_red + NCW * NMAX;  // [NP][64]
     const int g = lane >> 2, tq = lane & 3;
-    for (int w = 0; w < NCW; ++w) {
-      if (wid == w) {
+    if (FD) {  // each pair has one owner warp
+      if (wid < NCW) {
 #pragma unroll
-        for (int p = 0; p < NP; ++p)
+        for (int q = 0; q < NPW; ++q)
+          if (dc1[q] >= 0)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int idx = p * 64 + g * 8 + 2 * tq + h;
-            gred[idx] = w == 0 ? gacc[p][h] : gred[idx] + gacc[p][h];
-          }
+            for (int h = 0; h < 2; ++h) gred[(wid + q * NCW) * 64 + g * 8 + 2 * tq + h] = dacc[q][h];
       }
       __syncthreads();
+    } else {
+      for (int w = 0; w < NCW; ++w) {
+        if (wid == w) {
+#pragma unroll
+          for (int p = 0; p < NP; ++p)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int idx = p * 64 + g * 8 + 2 * tq + h;
+              gred[idx] = w == 0 ? gacc[p][h] : gred[idx] + gacc[p][h];
+            }
+        }
+        __syncthreads();
+      }
     }
     double* gout = a.gram_partials + (size_t)blockIdx.x * n * n;
     for (int e = tid; e < NP * 64; e += BLK) {
@@ -343,7 +459,7 @@ void launch_pass(const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
   if (ns < 2) ns = 2;
   size_t smem = (size_t)ns * sbytes;
   size_t red = (size_t)(T / kWarp) * NMAX * 8;
-  if (MODE == PM_FWDG) {
+  if (MODE == PM_FWDG || MODE == PM_FWDD) {
     const int NB = (NMAX + 7) / 8;
     red += (size_t)(NB * (NB + 1) / 2) * 64 * 8;
   }
@@ -352,7 +468,7 @@ void launch_pass(const CUtensorMap& m, const PassArgs& a, cudaStream_t s) {
   // (the attribute must not exceed the opt-in max minus the static shared memory)
   ensure_max_dynamic_smem((const void*)k, (int)smem);
   const int grid = dense_grid(a.l, a.n);
-  launch_pdl(k, dim3(grid), dim3(T + kWarp), smem, s, m, a, ns);
+  launch_pdl(k, dim3(grid), dim3(T + kProdWarps * kWarp), smem, s, m, a, ns);
 }
 
 template <int NMAX, int T>
@@ -366,6 +482,7 @@ void launch_mode_t(int mode, int loss, const CUtensorMap& m, const PassArgs& a, 
     if (mode == PM_FWD) launch_pass<NMAX, T, PM_FWD, kLossSvm>(m, a, s);
     else if (mode == PM_HV) launch_pass<NMAX, T, PM_HV, kLossSvm>(m, a, s);
     else if (mode == PM_FWDG) { if constexpr (NMAX <= 40) launch_pass<NMAX, T, PM_FWDG, kLossSvm>(m, a, s); }
+    else if (mode == PM_FWDD) { if constexpr (NMAX <= 40) launch_pass<NMAX, T, PM_FWDD, kLossSvm>(m, a, s); }
     else launch_pass<NMAX, T, PM_PRECOND, kLossSvm>(m, a, s);
   }
 }
@@ -572,14 +689,17 @@ int dense_grid(int64_t l, int64_t n) {
 }
 
 bool dense_forward_gram_fused(int64_t n) { return n <= 40; }
+bool dense_forward_gram_delta(int64_t n) { return n <= 40; }
 
 void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUtensorMap& xmap,
                    int loss, const double* w,
                    const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
                    double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s,
-                   double* gram_parts) {
+                   double* gram_parts, const uint8_t* mask_ref, const int* ref_stale) {
   PassArgs a{};
   a.gram_partials = gram_parts;
+  a.mask = mask_ref;
+  a.ref_stale = ref_stale;
   a.l = l;
   a.ld = ld;
   a.n = (int)n;
@@ -594,7 +714,7 @@ void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUte
   a.obj = obj;
   a.sc = sc;
   a.partials = gparts;
-  launch(gram_parts ? PM_FWDG : PM_FWD, loss, xmap, a, s);
+  launch(gram_parts ? (mask_ref ? PM_FWDD : PM_FWDG) : PM_FWD, loss, xmap, a, s);
 }
 
 void dense_accum(int kind, int64_t l, int64_t n, int64_t ld, const double* X,

@@ -695,12 +695,21 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       // kernel keeps 16 warps per SM on the FP64 tensor pipe.
       const char* gf = std::getenv("TRON_B200_GRAM_FUSED");
       e->gram_fused_ = dense_forward_gram_fused((int64_t)n) && gf && gf[0] == '1';
+      // L2-SVM: the candidate's G from the committed slot's and the rows that
+      // changed side, accumulated by the margin pass (TRON_B200_GRAM_DELTA=0: a
+      // fresh Gram pass per commit)
+      const char* gd = std::getenv("TRON_B200_GRAM_DELTA");
+      e->gram_delta_ = loss == TRON_LOSS_L2SVM && !e->gram_fused_ && dense_forward_gram_delta((int64_t)n) &&
+                       !(gd && gd[0] == '0');
+      static const int kFlagsInit[4] = {1, 0, 0, 0};  // no slot's G is current yet
       for (auto& S : e->slot_) {
         S.gram.alloc((size_t)n * n);
         if (e->comm_.active()) S.gram_local.alloc((size_t)n * n);
-        S.gram_stale.alloc(1);
-        cuda_check(cudaMemsetAsync(S.gram_stale.p, 0, sizeof(int), e->s_), "memset");
+        S.gram_flags.alloc(4);
+        cuda_check(cudaMemcpyAsync(S.gram_flags.p, kFlagsInit, sizeof(kFlagsInit), cudaMemcpyHostToDevice, e->s_),
+                   "H2D");
         if (e->gram_fused_) S.gram_parts.alloc((size_t)dense_grid((int64_t)l, (int64_t)n) * n * n);
+        if (e->gram_delta_) S.gram_dparts.alloc((size_t)dense_grid((int64_t)l, (int64_t)n) * n * n);
       }
       if (!e->gram_fused_) e->gram_parts_.alloc((size_t)gram_grid((int64_t)l, (int64_t)n) * n * n);
       cuda_check(cudaStreamSynchronize(e->s_), "gram buffers");
@@ -765,7 +774,7 @@ void Engine::screen(const int32_t* ptr, const int32_t* idx, int64_t rows, int64_
 uint32_t Engine::mode_flags() const {
   return (gram_ ? TRON_MODE_GRAM : 0) | (ooc_ ? TRON_MODE_OUT_OF_CORE : 0) |
          (colpart_ ? TRON_MODE_COLUMNS : 0) | (device_loop_ok() ? TRON_MODE_DEVICE_LOOP : 0) |
-         (comm_.active() && !colpart_ ? TRON_MODE_SHARDED : 0);
+         (comm_.active() && !colpart_ ? TRON_MODE_SHARDED : 0) | (gram_delta_ ? TRON_MODE_GRAM_DELTA : 0);
 }
 
 uint64_t Engine::memory_bytes() const {
@@ -882,8 +891,20 @@ void Engine::forward(Slot& S) {
     });
     obj_combine_blocks(obj_d_, blk_red_.p, nblk_, C_, s_);
   } else if (dense_) {
+    // the other slot: the committed iterate whose G the candidate's updates
+    const Slot& R = &S == &slot_[0] ? slot_[1] : slot_[0];
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
-                  S.gparts.p, obj_d_, sc_, s_, gram_fused_ ? S.gram_parts.p : nullptr);
+                  S.gparts.p, obj_d_, sc_, s_,
+                  gram_fused_ ? S.gram_parts.p : gram_delta_ ? S.gram_dparts.p : nullptr,
+                  gram_delta_ ? R.mask.p : nullptr, gram_delta_ ? R.gram_flags.p : nullptr);
+    if (gram_delta_) {  // G of this slot = G of R + the change (or flagged stale)
+      const bool shard = comm_.active();
+      gram_delta_finalize(n_, S.gram_dparts.p, dense_grid(l_, n_), shard ? R.gram_local.p : R.gram.p,
+                          R.gram_flags.p, shard ? S.gram_local.p : S.gram.p, S.gram_flags.p, s_);
+      count_launch(1);
+    } else if (gram_ && !gram_fused_) {  // formed when first needed (ensure_gram)
+      cuda_check(cudaMemsetAsync(S.gram_flags.p, 0xff, sizeof(int), s_), "memset");
+    }
     if (ro_) {  // I of this slot, then f in the reference's order (loss.cpp:114-119)
       compact_mask(l_, S.mask.p, S.idx.p, idx_tmp_.p, S.cnt.p, s_);
       ro_hinge(l_, n_, S.z.p, y_.p, S.w.p, C_, ro_hparts_.p, ro_tickets_.p, obj_d_, s_);
@@ -1035,10 +1056,8 @@ void Engine::gradient_into(const Slot& S, double* out) {
   }
   if (dense_) {
     dense_vector(-1, nullptr, epi, out, &S);  // partials from the fused margin pass
-    if (gram_) {  // the Hessian of this iterate: formed when first needed (ensure_gram)
-      cuda_check(cudaMemsetAsync(S.gram_stale.p, 0xff, sizeof(int), s_), "memset");
-      if (gram_fused_) gram_slot(S);  // (the fused pass's partials are already there)
-    }
+    // (gram mode: the margin pass left this slot's G current or flagged stale)
+    if (gram_fused_) gram_slot(S);  // (the fused pass's partials are already there)
   } else {
     UView u;
     if (loss_ == TRON_LOSS_LOGISTIC) {
@@ -1289,16 +1308,18 @@ void Engine::row_products(const double* v, const double* dvec, const uint8_t* ma
 
 // G = sum_i c_i x_i x_i^T of slot S (c = its mask or D), summed over the
 // shards when row-sharded (one n*n exchange per commit, none per Hv).
-// G of slot S for its current iterate.  Lazily: an accepted step marks the new
-// committed slot's G stale, and it is formed right before the CG that needs
-// it -- so the last iterate of a solve (converged) and rejected candidates
-// never pay for a Gram pass.  The kernels check the flag on the device.
+// G of slot S for its current iterate.  Lazily: a margin pass leaves its
+// slot's G current (L2-SVM: the committed slot's G plus the rows that changed
+// side, dense_pass PM_FWDD) or flagged stale, and a stale G is formed right
+// before the CG that needs it -- so the last iterate of a solve (converged) and
+// rejected candidates never pay for a Gram pass.  The kernels check the flag
+// on the device.
 void Engine::ensure_gram(const Slot& S) {
   if (!gram_ || gram_fused_) return;
   const bool svm = loss_ == TRON_LOSS_L2SVM;
   const bool shard = comm_.active();
   dense_gram(l_, n_, ld_, Xc_.p, svm ? S.mask.p : nullptr, svm ? nullptr : S.dvec.p, gram_parts_.p,
-             shard ? S.gram_local.p : S.gram.p, s_, S.gram_stale.p);
+             shard ? S.gram_local.p : S.gram.p, s_, S.gram_flags.p);
   count_launch(2);
   // row shards: G = sum of the ranks' parts, out of place, so repeating it
   // when nothing was stale changes nothing (every rank makes the same calls)
@@ -2260,13 +2281,17 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
       dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, slot_[cand_].z.p,
                     slot_[cand_].zhat.p, slot_[cand_].dvec.p, slot_[cand_].mask.p,
                     slot_[cand_].gparts.p, obj_d_, sc_, s_,
-                    gram_fused_ ? slot_[cand_].gram_parts.p : nullptr);
+                    gram_fused_ ? slot_[cand_].gram_parts.p : gram_delta_ ? slot_[cand_].gram_dparts.p : nullptr,
+                    gram_delta_ ? S.mask.p : nullptr, gram_delta_ ? S.gram_flags.p : nullptr);
     });
   }
   // (Gram mode: the gradient plus the committed iterate's G, formed afresh)
   out->grad_ms = time_it([&] {
     gradient_dev();
-    if (dense_ && gram_) ensure_gram(slot_[cand_ ^ 1]);
+    if (dense_ && gram_ && !gram_fused_) {
+      cuda_check(cudaMemsetAsync(S.gram_flags.p, 0xff, sizeof(int), s_), "memset");
+      ensure_gram(S);
+    }
   });
   slot_[cand_].valid = false;  // forward timing overwrote the candidate slot
   cudaEventDestroy(a);

@@ -185,7 +185,8 @@ class Engine {
     DevBuf<long long> cnt;  // ... and |I| (device)
     DevBuf<double> gram;    // dense Gram mode: this slot's Hessian sum_i c_i x_i x_i^T (n x n)
     DevBuf<double> gram_parts;  // ... its per-CTA partials from the fused margin pass
-    DevBuf<int> gram_stale;     // 1: the slot's iterate changed since G was formed
+    DevBuf<int> gram_flags;     // gram.cu's flags: [0] != 0: G does not match the slot's mask
+    DevBuf<double> gram_dparts; // L2-SVM: the margin pass's partials of G - G(other slot)
     DevBuf<double> gram_local;  // row-sharded: this rank's part of G (allreduced into gram)
     double f = 0.0;
     long long nact = 0;
@@ -318,6 +319,7 @@ class Engine {
   // commit (gram.cu); Hv / the preconditioner then read G instead of X
   bool gram_ = false;
   bool gram_fused_ = false;  // n <= 40: G accumulated by the margin pass itself (PM_FWDG)
+  bool gram_delta_ = false;  // L2-SVM, n <= 40: G = G(other slot) + the rows that changed side
   DevBuf<double> gram_parts_;
   void gram_slot(const Slot& S);
   // column-partitioned layout: X_, w and the

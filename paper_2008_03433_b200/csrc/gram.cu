@@ -160,19 +160,62 @@ __global__ void __launch_bounds__(kGramThreads, NB <= 5 ? TB_GRAM_CTAS : 1) gram
   }
 }
 
-// One CTA: every thread reads the stale flag before thread 0 clears it.
-__global__ void __launch_bounds__(1024) gram_finalize_kernel(int n, const double* __restrict__ partials,
-                                                            int nparts, double* __restrict__ G,
-                                                            int* stale) {
-  if (stale && *stale == 0) return;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+// G = sum of the per-CTA partials: one warp per element, its lanes striding
+// over the partials in index order, then the fixed butterfly (deterministic).
+// flags (nullable; gram_flags layout): every CTA reads flags[0] first and
+// returns when G is current; the last CTA to finish clears it (a ticket in
+// flags[2]), so no CTA can see the flag cleared before reading it.
+__global__ void __launch_bounds__(256) gram_finalize_kernel(int n, const double* __restrict__ partials,
+                                                           int nparts, double* __restrict__ G, int* flags) {
+  if (flags && flags[0] == 0) return;
+  const int nn = n * n;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (e < nn) {
     double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += partials[(size_t)b * n * n + e];
-    G[e] = s;
+    for (int b = lane; b < nparts; b += 32) s += partials[(size_t)b * nn + e];
+    s = warp_sum(s);
+    if (lane == 0) G[e] = s;
   }
-  __syncthreads();
-  if (stale && threadIdx.x == 0) *stale = 0;
+  if (flags) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(flags + 2, 1) == (int)gridDim.x - 1) {
+        flags[0] = 0;  // G matches the slot's mask
+        flags[1] = 0;  // ... and was formed from scratch
+        flags[2] = 0;
+      }
+    }
+  }
 }
+
+// G_out = G_ref + sum of the per-CTA Delta partials of the margin pass
+// (dense_pass PM_FWDD), when G_ref is current; the output flag says whether
+// G_out is.  Every kGramDeltaChain-th update forms G from scratch instead
+// (the flag stays set), so rounding cannot drift over a long solve.
+constexpr int kGramDeltaChain = 16;
+__global__ void __launch_bounds__(256) gram_delta_finalize_kernel(int n, const double* __restrict__ parts,
+                                                                 int nparts, const double* __restrict__ Gref,
+                                                                 const int* __restrict__ ref_flags,
+                                                                 double* __restrict__ Gout, int* out_flags) {
+  pdl_wait();
+  pdl_trigger();
+  const bool ok = ref_flags[0] == 0 && ref_flags[1] < kGramDeltaChain;
+  const int nn = n * n;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (ok && e < nn) {
+    double s = 0.0;
+    for (int b = lane; b < nparts; b += 32) s += parts[(size_t)b * nn + e];
+    s = warp_sum(s);
+    if (lane == 0) Gout[e] = Gref[e] + s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out_flags[0] = ok ? 0 : 1;
+    out_flags[1] = ok ? ref_flags[1] + 1 : 0;
+  }
+}
+
+int finalize_grid(int64_t n) { return (int)((n * n * 32 + 255) / 256); }
 
 __global__ void gram_hv_kernel(int n, const double* __restrict__ G, const double* __restrict__ v,
                                double scale, double* __restrict__ out) {
@@ -193,8 +236,14 @@ __global__ void gram_precond_kernel(int n, const double* __restrict__ G, double 
 }  // namespace
 
 void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s) {
-  gram_finalize_kernel<<<1, 1024, 0, s>>>((int)n, partials, nparts, G, nullptr);
+  gram_finalize_kernel<<<finalize_grid(n), 256, 0, s>>>((int)n, partials, nparts, G, nullptr);
   TB_LAUNCH_CHECK();
+}
+
+void gram_delta_finalize(int64_t n, const double* parts, int nparts, const double* Gref, const int* ref_flags,
+                         double* Gout, int* out_flags, cudaStream_t s) {
+  launch_pdl(gram_delta_finalize_kernel, dim3(finalize_grid(n)), dim3(256), 0, s, (int)n, parts, nparts, Gref,
+             ref_flags, Gout, out_flags);
 }
 
 void gram_hv(int64_t n, const double* G, const double* v, double scale, double* out, cudaStream_t s) {
@@ -247,7 +296,7 @@ void dense_gram(int64_t l, int64_t n, int64_t ld, const double* X, const uint8_t
     dispatch_gram<true>(l, n, ld, X, mask, dvec, partials, stale, grid, s);
   else
     dispatch_gram<false>(l, n, ld, X, mask, dvec, partials, stale, grid, s);
-  gram_finalize_kernel<<<1, 1024, 0, s>>>((int)n, partials, grid, G, stale);
+  gram_finalize_kernel<<<finalize_grid(n), 256, 0, s>>>((int)n, partials, grid, G, stale);
   TB_LAUNCH_CHECK();
 }
 

@@ -303,7 +303,18 @@ void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUte
                    int loss, const double* w,
                    const double* y, double C, double* z, double* zhat, double* dvec, uint8_t* mask,
                    double* gparts, ObjScalars* obj, Scratch sc, cudaStream_t s,
-                   double* gram_parts = nullptr);
+                   double* gram_parts = nullptr, const uint8_t* mask_ref = nullptr,
+                   const int* ref_stale = nullptr);
+// L2-SVM, n <= 40 (dense_forward_gram_delta): with gram_parts AND mask_ref the
+// pass accumulates instead the partials [grid][n*n] of
+//   Delta = sum_i (m_i - mask_ref_i) x_i x_i^T
+// over the rows that changed side -- skipped (plain FWD) when *ref_stale != 0 --
+// and gram_delta_finalize forms G = G_ref + Delta.
+bool dense_forward_gram_delta(int64_t n);
+// Gram flags (int[4] per slot): [0] != 0: G does not match the slot's mask;
+// [1] delta updates since G was formed from scratch; [2] finalize ticket.
+void gram_delta_finalize(int64_t n, const double* parts, int nparts, const double* Gref, const int* ref_flags,
+                         double* Gout, int* out_flags, cudaStream_t s);
 // G = sum over nparts of the per-CTA Gram partials (fixed order)
 void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s);
 // partial sums per block (grid = dense_grid(l, n)) of:

@@ -525,11 +525,12 @@ class GpuEvaluator:
 
     def mode(self) -> dict:
         """How this context runs (tron_gpu_mode): gram / out_of_core / columns /
-        device_loop / sharded."""
+        device_loop / sharded / gram_delta."""
         f = ctypes.c_uint32()
         _raise(lib.tron_gpu_mode(self._h, ctypes.byref(f)))
         names = {"gram": _lib.MODE_GRAM, "out_of_core": _lib.MODE_OUT_OF_CORE, "columns": _lib.MODE_COLUMNS,
-                 "device_loop": _lib.MODE_DEVICE_LOOP, "sharded": _lib.MODE_SHARDED}
+                 "device_loop": _lib.MODE_DEVICE_LOOP, "sharded": _lib.MODE_SHARDED,
+                 "gram_delta": _lib.MODE_GRAM_DELTA}
         return {k: bool(f.value & b) for k, b in names.items()}
 
     def memory_bytes(self) -> int:
