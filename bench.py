@@ -650,21 +650,30 @@ def main():
         # committed iterate that runs a CG).  The roofline object describes the
         # one with the larger share of the solve.
         l, n = p.X.rows, p.X.cols
-        fwd_bytes, gram_bytes = 8 * l * n + (18 if mode.get("gram_delta") else 17) * l, 8 * l * n + l
+        fwd_bytes = 8 * l * n + (18 if mode.get("gram_delta") else 17) * l
+        gram_bytes = fwd_bytes if mode.get("gram_delta") else 8 * l * n + l
         gram_flops = l * n * (n + 1)  # the upper triangle of sum_i c_i x_i x_i^T, 2 flops per product
         n_gram = 1 if mode.get("gram_delta") else max(1, res.trace.accepted_steps)
-        if n_gram * kt["grad_ms"] >= n_evals * kt["forward_ms"]:
+        delta = bool(mode.get("gram_delta"))
+        n_fwd = n_evals - 1 if delta else n_evals  # (delta: the first margin pass is the Gram pass)
+        if n_gram * kt["grad_ms"] >= n_fwd * kt["forward_ms"]:
             # bound by the FP64 tensor pipe (ncu: math-pipe throttle), HBM a close second
-            kern, kbytes, kms = "Gram pass G = sum_i c_i x_i x_i^T (gram.cu, DMMA; once per commit)", gram_bytes, kt["grad_ms"]
+            kern = ("first margin pass, forming the whole G = sum_i c_i x_i x_i^T on the FP64 tensor cores "
+                    "(dense_pass PM_FWDD, empty reference)" if delta else
+                    "Gram pass G = sum_i c_i x_i x_i^T (gram.cu, DMMA; once per commit)")
+            kbytes, kms = gram_bytes, kt["grad_ms"]
             bound, unit = "tensor", "TFLOP/s"
             achieved = gram_flops / (kms / 1e3) / 1e12
             peak, peak_kind = FP64_TENSOR_TFLOPS, ("fallback: B200 FP64 tensor 45 TFLOPS "
                                                    "(/opt/skills/guides/blackwell_cuda_programming.md:52)")
         else:
-            kern, kbytes, kms = "fused margin pass (dense_pass FWD: margins, mask, f, gradient partials)", fwd_bytes, kt["forward_ms"]
+            kern = ("fused margin pass (dense_pass FWDD: margins, mask, f, gradient partials, and the rows "
+                    "that changed side added to the committed G)" if delta else
+                    "fused margin pass (dense_pass FWD: margins, mask, f, gradient partials)")
+            kbytes, kms = fwd_bytes, kt["forward_ms"]
             bound, unit = "hbm", "GB/s"
             achieved = kbytes / (kms / 1e3) / 1e9
-        share = (n_gram if bound == "tensor" else n_evals) * kms / (t_step * 1e3) if t_step > 0 else None
+        share = (n_gram if bound == "tensor" else n_fwd) * kms / (t_step * 1e3) if t_step > 0 else None
         gram_extra = {"gram_delta": bool(mode.get("gram_delta")), "gram_passes_per_solve": n_gram,
                       "gram_pass_ms": kt["grad_ms"], "gram_pass_hbm_gbs": gram_bytes / (kt["grad_ms"] / 1e3) / 1e9,
                       "gram_pass_fp64_tflops": gram_flops / (kt["grad_ms"] / 1e3) / 1e12,

@@ -207,8 +207,11 @@ int tron_gpu_reset_ledger(tron_gpu_ctx *ctx);
  * context's stream) over `reps` launches on the committed state of
  * out_ms[0] whole Hv product, [1] the transposed product alone (CSC merge
  * SpMV, or the dense tall-skinny accumulation), [2] the forward margin
- * pass, [3] the gradient.  flush_l2 evicts the L2 between launches by
- * reading a 256 MiB buffer (nothing dirty is left to write back). */
+ * pass, [3] the gradient (dense Gram mode: plus the committed iterate's G
+ * formed afresh -- by the Gram pass, or with TRON_MODE_GRAM_DELTA by a margin
+ * pass against an empty reference, like a solve's first pass).  flush_l2
+ * evicts the L2 between launches by reading a 256 MiB buffer (nothing dirty is
+ * left to write back). */
 int tron_gpu_bench_kernels(tron_gpu_ctx *ctx, int reps, int flush_l2, double out_ms[4]);
 /* How this context runs its hot path (bit set): TRON_MODE_GRAM (dense: the
  * Hessian as an n x n matrix per commit), TRON_MODE_OUT_OF_CORE (X streamed from

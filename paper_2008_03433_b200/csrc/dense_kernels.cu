@@ -77,6 +77,9 @@ struct PassArgs {
 // (a.mask), so that the candidate's Gram matrix is G_ref + Delta
 // (gram_delta_finalize) instead of a fresh pass over X: between commits only
 // 6-11% of P1's rows change sides (profiles/active_churn_P1.jsonl, scripts/active_churn.py).
+// When G_ref is not current (or the chain of updates is due for a refresh)
+// the pass is a plain FWD and the candidate's G is left stale (formed afresh
+// by ensure_gram if a CG needs it).
 enum PassMode : int { PM_FWD = 0, PM_HV = 1, PM_PRECOND = 2, PM_FWDG = 3, PM_FWDD = 4 };
 
 // mma.sync m8n8k4 f64 (DMMA), as gram.cu
@@ -153,8 +156,7 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
   __shared__ double s_cb[FD ? NMAX * kDS : 1];
   __shared__ double s_cw[FD ? kDR : 1];
   __shared__ int s_cnt[FD ? 2 : 1][FD ? NCW : 1];
-  // (no delta against a reference whose G is not current: the pass is plain FWD)
-  const bool dodelta = FD && *a.ref_stale == 0;
+  const bool dodelta = FD && !gram_ref_is_empty(a.ref_stale);
   double gacc[FD ? 1 : NP][2];  // (FWDD: dacc below)
 #pragma unroll
   for (int p = 0; p < (FD ? 1 : NP); ++p) gacc[p][0] = gacc[p][1] = 0.0;

@@ -701,6 +701,10 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       const char* gd = std::getenv("TRON_B200_GRAM_DELTA");
       e->gram_delta_ = loss == TRON_LOSS_L2SVM && !e->gram_fused_ && dense_forward_gram_delta((int64_t)n) &&
                        !(gd && gd[0] == '0');
+      // a solve's starting point: its margin pass forms the whole G as well
+      // (TRON_B200_GRAM_FIRST=separate: a plain margin pass, then the Gram pass)
+      const char* gfirst = std::getenv("TRON_B200_GRAM_FIRST");
+      e->gram_first_fused_ = e->gram_delta_ && !(gfirst && std::string(gfirst) == "separate");
       static const int kFlagsInit[4] = {1, 0, 0, 0};  // no slot's G is current yet
       for (auto& S : e->slot_) {
         S.gram.alloc((size_t)n * n);
@@ -893,12 +897,21 @@ void Engine::forward(Slot& S) {
   } else if (dense_) {
     // the other slot: the committed iterate whose G the candidate's updates
     const Slot& R = &S == &slot_[0] ? slot_[1] : slot_[0];
+    const bool shard = comm_.active();
+    // delta mode, a solve's starting point: G formed whole by this pass (PM_FWDG)
+    const bool whole = gram_delta_ && gram_full_next_;
+    gram_full_next_ = false;
+    const bool upd = gram_delta_ && !whole;  // PM_FWDD against R
     dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, S.z.p, S.zhat.p, S.dvec.p, S.mask.p,
                   S.gparts.p, obj_d_, sc_, s_,
                   gram_fused_ ? S.gram_parts.p : gram_delta_ ? S.gram_dparts.p : nullptr,
-                  gram_delta_ ? R.mask.p : nullptr, gram_delta_ ? R.gram_flags.p : nullptr);
-    if (gram_delta_) {  // G of this slot = G of R + the change (or flagged stale)
-      const bool shard = comm_.active();
+                  upd ? R.mask.p : nullptr, upd ? R.gram_flags.p : nullptr);
+    if (whole) {
+      cuda_check(cudaMemsetAsync(S.gram_flags.p, 0xff, sizeof(int), s_), "memset");
+      gram_finalize(n_, S.gram_dparts.p, dense_grid(l_, n_), shard ? S.gram_local.p : S.gram.p, s_,
+                    S.gram_flags.p);
+      count_launch(1);
+    } else if (upd) {  // G of this slot = G of R + the change (or flagged stale)
       gram_delta_finalize(n_, S.gram_dparts.p, dense_grid(l_, n_), shard ? R.gram_local.p : R.gram.p,
                           R.gram_flags.p, shard ? S.gram_local.p : S.gram.p, S.gram_flags.p, s_);
       count_launch(1);
@@ -1851,6 +1864,11 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
   }
   const char* trace_env = std::getenv("TRON_B200_TRACE");
   const bool device_loop = device_loop_ok() && !(trace_env && trace_env[0] == '1');
+  if (gram_delta_) {
+    // every solve forms its own G: nothing carries over from an earlier solve
+    for (auto& S : slot_) cuda_check(cudaMemsetAsync(S.gram_flags.p, 0xff, sizeof(int), s_), "memset");
+    gram_full_next_ = gram_first_fused_;
+  }
   // device loop: the starting point's margin pass and gradient in one round trip
   double f = eval_candidate_dev(nullptr, /*read=*/!device_loop);
   if (device_loop) {
@@ -2285,12 +2303,22 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
                     gram_delta_ ? S.mask.p : nullptr, gram_delta_ ? S.gram_flags.p : nullptr);
     });
   }
-  // (Gram mode: the gradient plus the committed iterate's G, formed afresh)
+  // Gram mode: the gradient plus the committed iterate's G formed afresh -- by
+  // the Gram pass, or (delta mode, TRON_B200_GRAM_FIRST fused) by the margin
+  // pass that forms G whole, as a solve's first pass does
   out->grad_ms = time_it([&] {
     gradient_dev();
     if (dense_ && gram_ && !gram_fused_) {
-      cuda_check(cudaMemsetAsync(S.gram_flags.p, 0xff, sizeof(int), s_), "memset");
-      ensure_gram(S);
+      if (gram_delta_ && gram_first_fused_) {
+        Slot& C = slot_[cand_];
+        dense_forward(l_, n_, ld_, Xc_.p, xmap_, kLossSvm, S.w.p, y_.p, C_, C.z.p, C.zhat.p, C.dvec.p, C.mask.p,
+                      C.gparts.p, obj_d_, sc_, s_, C.gram_dparts.p);
+        cuda_check(cudaMemsetAsync(C.gram_flags.p, 0xff, sizeof(int), s_), "memset");
+        gram_finalize(n_, C.gram_dparts.p, dense_grid(l_, n_), C.gram.p, s_, C.gram_flags.p);
+      } else {
+        cuda_check(cudaMemsetAsync(S.gram_flags.p, 0xff, sizeof(int), s_), "memset");
+        ensure_gram(S);
+      }
     }
   });
   slot_[cand_].valid = false;  // forward timing overwrote the candidate slot

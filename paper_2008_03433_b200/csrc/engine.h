@@ -320,6 +320,8 @@ class Engine {
   bool gram_ = false;
   bool gram_fused_ = false;  // n <= 40: G accumulated by the margin pass itself (PM_FWDG)
   bool gram_delta_ = false;  // L2-SVM, n <= 40: G = G(other slot) + the rows that changed side
+  bool gram_first_fused_ = false;  // delta mode: a solve's first margin pass forms G whole (PM_FWDG)
+  bool gram_full_next_ = false;    // ... armed by solve_device for its starting point
   DevBuf<double> gram_parts_;
   void gram_slot(const Slot& S);
   // column-partitioned layout: X_, w and the

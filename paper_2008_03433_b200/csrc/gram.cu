@@ -190,17 +190,15 @@ __global__ void __launch_bounds__(256) gram_finalize_kernel(int n, const double*
 }
 
 // G_out = G_ref + sum of the per-CTA Delta partials of the margin pass
-// (dense_pass PM_FWDD), when G_ref is current; the output flag says whether
-// G_out is.  Every kGramDeltaChain-th update forms G from scratch instead
-// (the flag stays set), so rounding cannot drift over a long solve.
-constexpr int kGramDeltaChain = 16;
+// (dense_pass PM_FWDD) when the reference can be updated; otherwise (the pass
+// skipped the Delta) G_out is flagged stale.
 __global__ void __launch_bounds__(256) gram_delta_finalize_kernel(int n, const double* __restrict__ parts,
                                                                  int nparts, const double* __restrict__ Gref,
                                                                  const int* __restrict__ ref_flags,
                                                                  double* __restrict__ Gout, int* out_flags) {
   pdl_wait();
   pdl_trigger();
-  const bool ok = ref_flags[0] == 0 && ref_flags[1] < kGramDeltaChain;
+  const bool ok = !gram_ref_is_empty(ref_flags);
   const int nn = n * n;
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (ok && e < nn) {
@@ -235,8 +233,8 @@ __global__ void gram_precond_kernel(int n, const double* __restrict__ G, double 
 
 }  // namespace
 
-void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s) {
-  gram_finalize_kernel<<<finalize_grid(n), 256, 0, s>>>((int)n, partials, nparts, G, nullptr);
+void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s, int* flags) {
+  gram_finalize_kernel<<<finalize_grid(n), 256, 0, s>>>((int)n, partials, nparts, G, flags);
   TB_LAUNCH_CHECK();
 }
 

@@ -313,10 +313,17 @@ void dense_forward(int64_t l, int64_t n, int64_t ld, const double* X, const CUte
 bool dense_forward_gram_delta(int64_t n);
 // Gram flags (int[4] per slot): [0] != 0: G does not match the slot's mask;
 // [1] delta updates since G was formed from scratch; [2] finalize ticket.
+// A reference G that is stale, or has had kGramDeltaChain updates (so rounding
+// cannot drift), is not updated: the candidate's G is then formed afresh.
+constexpr int kGramDeltaChain = 16;
+__host__ __device__ inline bool gram_ref_is_empty(const int* flags) {
+  return flags[0] != 0 || flags[1] >= kGramDeltaChain;
+}
 void gram_delta_finalize(int64_t n, const double* parts, int nparts, const double* Gref, const int* ref_flags,
                          double* Gout, int* out_flags, cudaStream_t s);
 // G = sum over nparts of the per-CTA Gram partials (fixed order)
-void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s);
+void gram_finalize(int64_t n, const double* partials, int nparts, double* G, cudaStream_t s,
+                   int* flags = nullptr);  // flags: computed only if flags[0] != 0, then cleared
 // partial sums per block (grid = dense_grid(l, n)) of:
 //  HV:      sum_i c_i x_i   with c = (x_i.v)*dvec_i (LR) or mask?(x_i.v):0 (SVM;
 //           mask == nullptr => every row active, used on the gathered panel)
