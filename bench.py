@@ -22,6 +22,7 @@ The reference arm never maps the product library: its inputs come from the
 SYNTH-v1 generator inside oracle/_ref (the reference's own testgen::Rng).
 """
 import argparse
+import gc
 import json
 import os
 import socket
@@ -623,6 +624,7 @@ def main():
     wall, dev_ms, res = [], [], None
     sampler = ClockSampler(device)
     barrier()
+    gc.disable()  # (as timeit does: a collector pause is host noise, not the solve)
     with sampler:
         for _ in range(args.steps):
             evict_l2()
@@ -630,6 +632,7 @@ def main():
             res = ev.solve(cfg)  # returns with w in host memory
             wall.append(time.perf_counter() - t0)
             dev_ms.append(res.device_ms)
+    gc.enable()
     barrier()
     launches = ev.launch_count() - launches0
     t_step = max_over_ranks(float(np.mean(wall)))
@@ -677,6 +680,9 @@ def main():
         gram_extra = {"gram_delta": bool(mode.get("gram_delta")), "gram_passes_per_solve": n_gram,
                       "gram_pass_ms": kt["grad_ms"], "gram_pass_hbm_gbs": gram_bytes / (kt["grad_ms"] / 1e3) / 1e9,
                       "gram_pass_fp64_tflops": gram_flops / (kt["grad_ms"] / 1e3) / 1e12,
+                      "margin_pass_what": ("a candidate pass at the iterate before the last commit against the committed G: "
+                                           "it adds the rows of the last commit's change (P1: 1.8% of rows; the solve's "
+                                           "earlier passes change 6-11%)" if delta else "margin pass at the committed w"),
                       "margin_pass_ms": kt["forward_ms"], "margin_pass_gbs": fwd_bytes / (kt["forward_ms"] / 1e3) / 1e9,
                       "hv_from_gram_us": kt["hv_ms"] * 1e3,
                       "tall_skinny_hv_pass_ms": kt["transposed_ms"], "tall_skinny_hv_gbs": trans_gbs}
@@ -746,7 +752,7 @@ def main():
                         "partials)") if world > 1 else "1 GPU",
         "timing": ("value: host wall time of each solve call (returns with w on the host), mean over "
                    "steps, max over ranks; device_s: CUDA-event time of the same solves"),
-        "device_s": t_dev, "wall_s_min": wall_min,
+        "device_s": t_dev, "wall_s_min": wall_min, "wall_ms_steps": [round(x * 1e3, 3) for x in wall],
         "objective": res.objective, "converged": res.converged,
         "outer_iterations": len(res.trace.iterations), "hessian_products": res.hessian_products,
         "hv_per_s": res.hessian_products / t_step if t_step > 0 else None,
@@ -754,7 +760,9 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                      "peak_source": (peak_kind if bound == "tensor" else
                                      f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs: copy read+write GB/s)"),
-                     "traffic": read_traffic(args.workload + ("-gram" if gram_extra else "")),
+                     "traffic": read_traffic(args.workload + ("" if not gram_extra else
+                                                             "-gram-delta" if gram_extra.get("gram_delta") and bound == "hbm"
+                                                             else "-gram")),
                      "algorithmic_bytes_per_launch": kbytes, "avg_launch_ms": kms,
                      "launch_timing": "CUDA events around each launch on the solver stream, 256 MiB "
                                       "read-based L2 eviction before each, mean of 20, after the timed solves",

@@ -2295,8 +2295,12 @@ void Engine::bench_kernels(int reps, bool flush_l2, KernelTimes* out) {
     out->transposed_ms = time_it([&] {
       dense_accum(DA_HV, l_, n_, ld_, Xc_.p, xmap_, loss, vtmp_.p, S.dvec.p, S.mask.p, parts_.p, s_);
     });
+    // delta mode: the candidate slot's own iterate (after a solve: the one
+    // before the last commit) against the committed G -- a pass that updates G
+    // by the rows of the last commit's change, not a no-change pass
+    const double* wf = gram_delta_ ? slot_[cand_].w.p : S.w.p;
     out->forward_ms = time_it([&] {
-      dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, S.w.p, y_.p, C_, slot_[cand_].z.p,
+      dense_forward(l_, n_, ld_, Xc_.p, xmap_, loss, wf, y_.p, C_, slot_[cand_].z.p,
                     slot_[cand_].zhat.p, slot_[cand_].dvec.p, slot_[cand_].mask.p,
                     slot_[cand_].gparts.p, obj_d_, sc_, s_,
                     gram_fused_ ? slot_[cand_].gram_parts.p : gram_delta_ ? slot_[cand_].gram_dparts.p : nullptr,

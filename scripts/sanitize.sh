@@ -7,7 +7,7 @@ mkdir -p gpurun_out/san
 N=$(python scripts/sanitize_cases.py --count)
 : > gpurun_out/san/summary.txt
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
-  for i in $(seq 0 $((N-1))); do
+  for i in ${CASES:-$(seq 0 $((N-1)))}; do
     log=gpurun_out/san/${tool}_$i.log
     extra=""
     [ "$tool" = synccheck ] && extra="--num-cuda-barriers 4096"

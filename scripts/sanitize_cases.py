@@ -66,10 +66,14 @@ cases = [
      gpu(out_of_core=1, stream_block_rows=1024), dict(eps=1e-8)),
     ("dense SVM tall-skinny (no Gram)", synth.synth_dense(1, 5000, 40), SVM, gpu(), dict(eps=1e-8)),
     ("sparse LR column panels", synth.synth_sparse(13, 600, 9000, 20), LR, gpu(), {}),
+    ("dense SVM Gram: separate first pass", synth.synth_dense(1, 5000, 40), SVM, gpu(), dict(eps=1e-8)),
+    ("dense SVM Gram: no incremental update", synth.synth_dense(1, 5000, 40), SVM, gpu(), dict(eps=1e-8)),
 ]
 # per-case environment (applied before the case's context is created)
 ENV = {"dense SVM tall-skinny (no Gram)": {"TRON_B200_DENSE_GRAM": "0"},
-       "sparse LR column panels": {"TRON_B200_PANEL_COLS": "2000"}}
+       "sparse LR column panels": {"TRON_B200_PANEL_COLS": "2000"},
+       "dense SVM Gram: separate first pass": {"TRON_B200_GRAM_FIRST": "separate"},
+       "dense SVM Gram: no incremental update": {"TRON_B200_GRAM_DELTA": "0"}}
 if sys.argv[1:] == ["--count"]:
     print(len(cases))
     sys.exit(0)
