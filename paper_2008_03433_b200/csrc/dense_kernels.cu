@@ -273,6 +273,31 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
           c = use_mask ? (ms[tid] ? sdot : 0.0) : sdot;
         if (!in) c = 0.0;
       }
+      // PM_FWDD, part 1: this row's change of side (+1 entered I, -1 left it,
+      // 0 unchanged), its place among the tile's changed rows, and -- for the
+      // first kDR of them -- the row into the block straight from the registers
+      bool fd_ch = false;
+      int fd_pos = 0, fd_tot = 0;
+      double fd_cdel = 0.0;
+      if (FD && dodelta) {
+        fd_cdel = in ? cg - (ms[tid] ? 1.0 : 0.0) : 0.0;
+        fd_ch = fd_cdel != 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, fd_ch);
+        int* cnt = s_cnt[FD ? (k & 1) : 0];
+        if (lane == 0) cnt[wid] = __popc(bal);
+        asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        fd_pos = __popc(bal & ((1u << lane) - 1u));
+        for (int w = 0; w < NCW; ++w) {
+          const int c2 = cnt[w];
+          fd_pos += w < wid ? c2 : 0;
+          fd_tot += c2;
+        }
+        if (fd_ch && fd_pos < kDR) {
+#pragma unroll
+          for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + fd_pos] = x[j];  // (zeros beyond n)
+          s_cw[fd_pos] = fd_cdel;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NMAX; ++j) acc[j] += c * x[j];  // x[j] = 0 beyond n
       if (FG) {
@@ -300,27 +325,17 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
         }
       }
       if (FD && dodelta) {
-        // this row's change of side: +1 entered I, -1 left it, 0 unchanged
-        const double cdel = in ? cg - (ms[tid] ? 1.0 : 0.0) : 0.0;
-        const bool ch = cdel != 0.0;
-        const unsigned bal = __ballot_sync(0xffffffffu, ch);
-        int* cnt = s_cnt[FD ? (k & 1) : 0];
-        if (lane == 0) cnt[wid] = __popc(bal);
-        asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
-        int pos = __popc(bal & ((1u << lane) - 1u)), tot = 0;
-        for (int w = 0; w < NCW; ++w) {
-          const int c2 = cnt[w];
-          pos += w < wid ? c2 : 0;
-          tot += c2;
-        }
+        // part 2: the block's rows times themselves on the FP64 tensor cores,
+        // kDR rows per round (rounds past the first restage their rows from
+        // the tile: the registers are gone by then)
         const int g = lane >> 2, tq = lane & 3;
-        for (int r0 = 0; r0 < tot; r0 += kDR) {
-          const int nr = tot - r0 < kDR ? tot - r0 : kDR, nr4 = (nr + 3) & ~3;
-          if (ch && pos >= r0 && pos < r0 + kDR) {
-            const int q = pos - r0;
+        for (int r0 = 0; r0 < fd_tot; r0 += kDR) {
+          const int nr = fd_tot - r0 < kDR ? fd_tot - r0 : kDR, nr4 = (nr + 3) & ~3;
+          if (r0 > 0 && fd_ch && fd_pos >= r0 && fd_pos < r0 + kDR) {
+            const int q = fd_pos - r0;
 #pragma unroll
-            for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + q] = j < n ? xs[j * T + tid] : 0.0;  // (the staged row)
-            s_cw[q] = cdel;
+            for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + q] = j < n ? xs[j * T + tid] : 0.0;
+            s_cw[q] = fd_cdel;
           }
           if (tid < nr4 - nr) {  // the last k-step's padding rows: weight 0, finite values
 #pragma unroll
