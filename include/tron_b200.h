@@ -172,6 +172,13 @@ int tron_gpu_hessian_vec(tron_gpu_ctx *ctx, const double *v, double *out);
 /* quadratic_model(g, hv, d) (tron.hpp:83; tron.cpp:31-35) with g the committed
  * gradient and hv this context's Hessian: *q = g.d + 0.5 d.(H d). */
 int tron_gpu_quadratic_model(tron_gpu_ctx *ctx, const double *d, double *q);
+/* Row shards (replicated state is bitwise identical on every
+ * rank): this context's checksum of its committed w -- the wrap-around sum of
+ * the 64-bit patterns as four 16-bit chunks, order-independent.  With
+ * TRON_B200_CHECK_REPLICAS=1 a sharded solve compares the ranks' checksums of
+ * w, f and delta after every outer iteration (device loop: after the solve)
+ * and fails with TRON_ERR_LOGIC when they differ. */
+int tron_gpu_replica_checksum(tron_gpu_ctx *ctx, double out[4]);
 /* LossEvaluator::precond_diagonal (tron.hpp:124; backend.cpp:200-214/292-306). */
 int tron_gpu_precond_diagonal(tron_gpu_ctx *ctx, double *m);
 

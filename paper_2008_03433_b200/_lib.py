@@ -92,6 +92,7 @@ SIGNATURES = [
     ("tron_gpu_hessian_vec", c_int, [c_void_p, PD, PD]),
     ("tron_gpu_precond_diagonal", c_int, [c_void_p, PD]),
     ("tron_gpu_quadratic_model", c_int, [c_void_p, PD, PD]),
+    ("tron_gpu_replica_checksum", c_int, [c_void_p, PD]),
     ("tron_gpu_state_lr", c_int, [c_void_p, c_int, PD, PD, PD]),
     ("tron_gpu_state_svm", c_int, [c_void_p, c_int, PD, PI64, c_uint64, PU64]),
     ("tron_gpu_truncated_cg", c_int, [c_void_p, c_double, POINTER(tron_config), PD, PI32, PU64,

@@ -375,6 +375,12 @@ int tron_gpu_quadratic_model(tron_gpu_ctx* ctx, const double* d, double* q) {
   });
 }
 
+int tron_gpu_replica_checksum(tron_gpu_ctx* ctx, double out[4]) {
+  NEED_CTX(ctx);
+  if (!out) return fail(TRON_ERR_ARGUMENT, "replica_checksum: out is null");
+  return guarded([&] { ctx->engine->replica_checksum_host(out); });
+}
+
 int tron_gpu_precond_diagonal(tron_gpu_ctx* ctx, double* m) {
   tb::NvtxRange nvtx_range("tron_gpu_precond_diagonal");
   NEED_CTX(ctx);

@@ -22,6 +22,11 @@
 
 namespace tb {
 
+static bool env_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '1';
+}
+
 [[noreturn]] void raise(int status, const std::string& msg) { throw StatusError(status, msg); }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -409,6 +414,7 @@ std::unique_ptr<Engine> Engine::create_csr(int loss, uint64_t l, uint64_t n, con
     e->budget_ = opt.gathered_budget_bytes;
     e->row_begin_ = opt.row_begin;
     e->comm_.init(opt);
+    e->replica_check_ = env_flag("TRON_B200_CHECK_REPLICAS");
     if (opt.partition == TRON_PARTITION_COLUMNS && e->comm_.active()) {
       if (opt.global_cols < n || opt.col_begin + n > opt.global_cols)
         raise(TRON_ERR_ARGUMENT, "column partition: [col_begin, col_begin + n) must lie in global_cols");
@@ -574,6 +580,7 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
   e->budget_ = opt.gathered_budget_bytes;
   e->row_begin_ = opt.row_begin;
   e->comm_.init(opt);
+  e->replica_check_ = env_flag("TRON_B200_CHECK_REPLICAS");
   e->ld_ = dense_ld((int64_t)l);
   {  // out-of-core streaming when X does not fit (or when asked to)
     // (no usable device: decided as in-memory; creation then reports the
@@ -945,6 +952,33 @@ void Engine::forward(Slot& S) {
                 s_);
   }
   count_launch(1);
+}
+
+void Engine::replica_checksum_host(double out4[4]) {
+  if (!rc_.p) rc_.alloc(8);
+  replica_checksum(n_, slot_[cand_ ^ 1].w.p, 0.0, 0.0, rc_.p, s_);
+  double h[8];
+  cuda_check(cudaMemcpyAsync(h, rc_.p, sizeof(h), cudaMemcpyDeviceToHost, s_), "D2H");
+  cuda_check(cudaStreamSynchronize(s_), "sync");
+  for (int c = 0; c < 4; ++c) out4[c] = h[c];
+}
+
+// Replicated state must be bitwise identical on every rank: a
+// checksum of w (committed), f and delta summed over the ranks with its
+// squares; "all equal" <=> world * sum(h^2) == sum(h)^2 for each 16-bit chunk
+// (exact in doubles), which every rank evaluates on the same sums.
+void Engine::check_replicas(double f, double delta, uint64_t iter) {
+  if (!replica_check_ || !comm_.active() || colpart_) return;  // (column shards hold different w)
+  if (!rc_.p) rc_.alloc(8);
+  replica_checksum(n_, slot_[cand_ ^ 1].w.p, f, delta, rc_.p, s_);
+  comm_.allreduce_sum(rc_.p, 8, s_);
+  double h[8];
+  cuda_check(cudaMemcpyAsync(h, rc_.p, sizeof(h), cudaMemcpyDeviceToHost, s_), "D2H");
+  cuda_check(cudaStreamSynchronize(s_), "sync");
+  for (int c = 0; c < 4; ++c)
+    if ((double)comm_.world * h[4 + c] != h[c] * h[c])
+      raise(TRON_ERR_LOGIC, "replicas diverged: the ranks' w / f / delta differ after outer iteration " +
+                                std::to_string(iter));
 }
 
 double Engine::eval_candidate_dev(const double* d_step, bool read) {
@@ -1924,6 +1958,8 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
       finish(status);
       raise(status, what);
     }
+    // (the device loop's delta stays on the device: the check covers w and f)
+    check_replicas(info->objective, 0.0, info->n_iterations);
     finish(TRON_OK);
     return;
   }
@@ -2045,9 +2081,11 @@ void Engine::solve_device(const tron_config& cfg, const double* w0, double* w_ou
       gnorm = gnorm_;
       if (gnorm <= cfg.eps * gnorm0) {
         info->converged = 1;
+        check_replicas(f, delta, info->n_iterations);
         break;
       }
     }
+    check_replicas(f, delta, info->n_iterations);
   }
   finish(TRON_OK);
 }

@@ -152,6 +152,8 @@ class Engine {
   void hessian_vec_host(const double* v, double* out);
   void precond_host(double* m);
   double quadratic_model_host(const double* d);
+  // this replica's checksum of the committed w (replica_checksum's four chunks)
+  void replica_checksum_host(double out4[4]);
   void state_lr(int which, double* z, double* zhat, double* dvec);
   void state_svm(int which, double* z, int64_t* active, uint64_t cap, uint64_t* n_active);
   void truncated_cg(double delta, const tron_config& cfg, double* d, int32_t* exit_kind,
@@ -319,6 +321,11 @@ class Engine {
   // commit (gram.cu); Hv / the preconditioner then read G instead of X
   bool gram_ = false;
   bool gram_fused_ = false;  // n <= 40: G accumulated by the margin pass itself (PM_FWDG)
+  // TRON_B200_CHECK_REPLICAS=1 (row shards): after every outer iteration (the
+  // device loop: after the solve) the ranks compare checksums of w, f and delta
+  bool replica_check_ = false;
+  DevBuf<double> rc_;
+  void check_replicas(double f, double delta, uint64_t iter);
   bool gram_delta_ = false;  // L2-SVM, n <= 40: G = G(other slot) + the rows that changed side
   bool gram_first_fused_ = false;  // delta mode: a solve's first margin pass forms G whole (PM_FWDG)
   bool gram_full_next_ = false;    // ... armed by solve_device for its starting point

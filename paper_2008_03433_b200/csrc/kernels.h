@@ -210,6 +210,9 @@ void vec_div(int64_t n, const double* r, const double* M, double* z, cudaStream_
 // allreduce of out2, obj->gnorm = sqrt(out2[0]), obj->grad_nonfinite
 void vec_sumsq_bad(int64_t n, const double* g, double* out2, Scratch sc, cudaStream_t s);
 void obj_set_gnorm(ObjScalars* obj, const double* in2, cudaStream_t s);
+// out8[0..3] = 16-bit chunks of the wrap-around sum of the bit patterns of w,
+// f and delta; out8[4..7] their squares (replica check of the row shards)
+void replica_checksum(int64_t n, const double* w, double f, double delta, double* out8, cudaStream_t s);
 // a_i *= D_i (dvec) or a_i = mask_i ? a_i : 0 (the allreduced row products)
 void vec_row_scale(int64_t l, double* a, const double* dvec, const uint8_t* mask, cudaStream_t s);
 // Streamed (out-of-core) margin pass: the per-block loss sums and |I|

@@ -833,6 +833,39 @@ void vec_div(int64_t n, const double* r, const double* M, double* z, cudaStream_
 void vec_sumsq_bad(int64_t n, const double* g, double* out2, Scratch sc, cudaStream_t s) {
   launch_pdl(sumsq_bad_kernel, dim3(vec_grid(n)), dim3(kBlock), 0, s, (long long)n, g, out2, sc);
 }
+namespace {
+// Replica checksum: the wrap-around sum of the 64-bit patterns of w, f and
+// delta (integer addition: the same in any order), as four 16-bit chunks and
+// their squares -- exact in doubles, so after a sum over the ranks every rank
+// can test "all equal" as world * sum(h^2) == sum(h)^2.
+__global__ void __launch_bounds__(256) replica_checksum_kernel(long long n, const double* __restrict__ w,
+                                                               double f, double delta, double* out8) {
+  __shared__ unsigned long long sh[256];
+  unsigned long long s = 0;
+  for (long long i = threadIdx.x; i < n; i += 256) s += (unsigned long long)__double_as_longlong(w[i]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long t = sh[0] + (unsigned long long)__double_as_longlong(f) * 3ull +
+                                 (unsigned long long)__double_as_longlong(delta) * 5ull;
+    for (int c = 0; c < 4; ++c) {
+      const double h = (double)((t >> (16 * c)) & 0xffffull);
+      out8[c] = h;
+      out8[4 + c] = h * h;
+    }
+  }
+}
+}  // namespace
+
+void replica_checksum(int64_t n, const double* w, double f, double delta, double* out8, cudaStream_t s) {
+  replica_checksum_kernel<<<1, 256, 0, s>>>((long long)n, w, f, delta, out8);
+  TB_LAUNCH_CHECK();
+}
+
 void obj_set_gnorm(ObjScalars* obj, const double* in2, cudaStream_t s) {
   set_gnorm_kernel<<<1, 1, 0, s>>>(obj, in2);
   TB_LAUNCH_CHECK();

@@ -432,6 +432,13 @@ class GpuEvaluator:
         _raise(lib.tron_gpu_quadratic_model(self._h, _ptr(d, ctypes.c_double), ctypes.byref(q)))
         return q.value
 
+    def replica_checksum(self) -> np.ndarray:
+        """Checksum of the committed w (four 16-bit chunks of the wrap-around sum of
+        its bit patterns): equal on every row shard when the replicas agree."""
+        out = np.empty(4)
+        _raise(lib.tron_gpu_replica_checksum(self._h, _ptr(out, ctypes.c_double)))
+        return out
+
     def precond_diagonal(self) -> np.ndarray:
         out = np.empty(self.n)
         _raise(lib.tron_gpu_precond_diagonal(self._h, _ptr(out, ctypes.c_double)))

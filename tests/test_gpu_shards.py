@@ -58,6 +58,8 @@ def _worker(rank, port, names, q):
     from paper_2008_03433_b200.sharding import shard
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    # every sharded solve compares the ranks' w / f / delta after each outer iteration
+    os.environ["TRON_B200_CHECK_REPLICAS"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
         def allreduce(buf):
@@ -84,9 +86,10 @@ def _worker(rank, port, names, q):
                 m = ev.precond_diagonal()
                 res = ev.solve(TrustRegionConfig(eps=EPS.get(name, 1e-4)))
                 act = ev.committed_state().active if loss.name == "L2Svm" else None
+                csum = ev.replica_checksum()
             out[name] = dict(f=f, g=g, hv=hv, m=m, w=res.w, obj=res.objective,
                              cg=[it.cg_iters for it in res.trace.iterations], act=act,
-                             act_w=act_w)
+                             act_w=act_w, csum=csum)
         q.put((rank, out))
     except Exception as e:  # surfaced by the parent
         q.put((rank, repr(e)))
@@ -132,6 +135,7 @@ def test_two_shards_compose(sharded, ref, name):
         assert rel_err(r["hv"], hv) <= 1e-13
         assert rel_err(r["m"], m) <= 1e-13
     assert np.array_equal(a["w"].view(np.uint64), b["w"].view(np.uint64))
+    assert np.array_equal(a["csum"], b["csum"])  # (and the per-iteration checks passed)
     assert a["obj"] == b["obj"] and a["cg"] == b["cg"]
     assert rel_err(a["obj"], res.objective) <= 1e-10
     assert rel_err(a["w"], res.w) <= 1e-7
@@ -144,3 +148,22 @@ def test_two_shards_compose(sharded, ref, name):
         assert np.array_equal(np.concatenate([a["act_w"], b["act_w"]]), act_w)
         glob = np.concatenate([a["act"], b["act"]])
         assert np.all(np.diff(glob) > 0) and abs(glob.size - act.size) <= 0.001 * act.size
+
+
+def test_replica_checksum_sees_one_ulp():
+    """The replica checksum (tron_gpu_replica_checksum) of the committed w: equal
+    for equal w, different after a one-ulp change of one coordinate."""
+    from paper_2008_03433_b200 import ExecutionPlan, make_evaluator, synth
+    p, loss = _problems()["sparse-svm"]
+    w = synth.testgen_random_vector(5, p.X.cols, 0.05)
+    w2 = w.copy()
+    w2[17] = np.nextafter(w2[17], np.inf)
+    with make_evaluator(p, loss, ExecutionPlan.gpu()) as ev:
+        sums = []
+        for x in (w, w, w2):
+            ev.eval_candidate(x)
+            ev.commit()
+            sums.append(ev.replica_checksum())
+    assert np.array_equal(sums[0], sums[1])
+    assert not np.array_equal(sums[0], sums[2])
+    assert all(0 <= h < 65536 and h == int(h) for h in sums[0])
