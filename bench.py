@@ -107,7 +107,7 @@ def host_description():
     return {"cpu_model": model, "nproc": os.cpu_count(), "usable_cores": cpu_cores(), "mem_gb": mem_gb}
 
 
-def _nvml_sampler_proc(device_uuid, device_index, conn, stop, go):
+def _nvml_sampler_proc(device_uuid, device_index, conn, stop, go, ready):
     """Child process: SM clocks + throttle-reason bits every 20 ms while `go` is
     set (the timed region), until `stop`; then the samples through `conn`.  A separate process shares no GIL
     with the timed loop (an in-process sampler thread delayed the return of
@@ -121,6 +121,12 @@ def _nvml_sampler_proc(device_uuid, device_index, conn, stop, go):
         except Exception:
             h = nv.nvmlDeviceGetHandleByIndex(device_index)
         get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        # every query once before the timed region: a first call can hold the
+        # driver for tens of ms (it stalled the second timed solve)
+        nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get(h)
+        ready.set()
         while not stop.is_set():
             if go.is_set():
                 try:
@@ -131,6 +137,7 @@ def _nvml_sampler_proc(device_uuid, device_index, conn, stop, go):
             stop.wait(0.02)
     except Exception:
         pass
+    ready.set()
     conn.send(rows)
     conn.close()
 
@@ -164,6 +171,9 @@ class ClockSampler:
         return float(r[0]), float(r[1]), {n for n, v in zip(names, r[3:7]) if v.lower() == "active"}
 
     def __enter__(self):
+        if os.environ.get("TRON_BENCH_NO_SAMPLER") == "1":  # (diagnostics: one nvidia-smi read at the end)
+            self.source = "nvidia-smi"
+            return self
         if self.source == "nvml":
             import multiprocessing as mp
             uuid = None
@@ -175,11 +185,12 @@ class ClockSampler:
                 pass
             ctx = mp.get_context("spawn")
             self._rx, tx = ctx.Pipe(duplex=False)
-            self._stop, self._go = ctx.Event(), ctx.Event()
+            self._stop, self._go, ready = ctx.Event(), ctx.Event(), ctx.Event()
             self._proc = ctx.Process(target=_nvml_sampler_proc,
-                                     args=(uuid, self.device, tx, self._stop, self._go), daemon=True)
+                                     args=(uuid, self.device, tx, self._stop, self._go, ready), daemon=True)
             self._proc.start()
-            time.sleep(1.0)  # the child has initialised NVML before the timed region starts
+            ready.wait(60)  # NVML initialised and every query made once before the timed region
+            time.sleep(0.1)
             self._go.set()
         return self
 

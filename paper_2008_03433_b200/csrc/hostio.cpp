@@ -91,6 +91,14 @@ void* pinned_pool_get(size_t bytes) {
   void* p = nullptr;
   cuda_check(cudaMallocHost(&p, cap), "cudaMallocHost");
   g_pool_live.emplace_back(p, cap);
+  // a spare of the same size: a caller holding one result while the next solve
+  // asks for another (every repeated solve) then never waits on page-locking
+  // (cudaMallocHost: ~1-5 ms) -- the second timed solve of bench.py did
+  void* spare = nullptr;
+  if (cap <= (size_t(64) << 20) && cudaMallocHost(&spare, cap) == cudaSuccess)
+    g_pool_free.emplace_back(cap, spare);
+  else
+    cudaGetLastError();
   return p;
 }
 
