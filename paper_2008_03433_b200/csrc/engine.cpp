@@ -705,6 +705,10 @@ std::unique_ptr<Engine> Engine::create_dense(int loss, uint64_t l, uint64_t n,
       // L2-SVM: the candidate's G from the committed slot's and the rows that
       // changed side, accumulated by the margin pass (TRON_B200_GRAM_DELTA=0: a
       // fresh Gram pass per commit)
+      // the CG of a Gram-mode context in one launch (TRON_B200_GRAM_CG_LOOP=0:
+      // one launch per iteration)
+      const char* gl = std::getenv("TRON_B200_GRAM_CG_LOOP");
+      e->gram_cg_loop_ = !(gl && gl[0] == '0');
       const char* gd = std::getenv("TRON_B200_GRAM_DELTA");
       e->gram_delta_ = loss == TRON_LOSS_L2SVM && !e->gram_fused_ && dense_forward_gram_delta((int64_t)n) &&
                        !(gd && gd[0] == '0');
@@ -1559,7 +1563,7 @@ void Engine::capture_cg_init(int k, const CgVectors& v, Cond cond) {
     cg_small_init(v, st_d_, cond, s_);
   else
     cg_large_init(v, st_d_, sc_, cond, s_);
-  count_launch(1);
+  count_launch(small_engine_ && dense_ && gram_ && gram_cg_loop_ ? 2 : 1);  // (+ the looped CG, if it runs)
 }
 
 // One CG iteration with slot k committed (Hv of p, then the step kernel that
@@ -1574,8 +1578,14 @@ void Engine::capture_cg_body(int k, const CgVectors& v, Cond cond) {
   } else if (small_engine_) {
     if (dense_ && gram_) {  // hp = p + s G p inside the step kernel
       const double scale = loss_ == TRON_LOSS_LOGISTIC ? C_ : 2.0 * C_;
-      cg_small_step_gram(v, slot_[k].gram.p, scale, st_d_, cond, s_);
-      count_launch(1);
+      if (gram_cg_loop_) {
+        // every iteration in this one launch (the WHILE node then runs once);
+        // counted with the CG's init: body_kernels_ stays 0
+        cg_small_gram_loop(v, slot_[k].gram.p, scale, st_d_, cond, s_);
+      } else {
+        cg_small_step_gram(v, slot_[k].gram.p, scale, st_d_, cond, s_);
+        count_launch(1);
+      }
     } else if (dense_ && !comm_.active() && !ooc_) {  // sharded / streamed: through hv_kernels
       const Slot& S = slot_[k];
       const int loss = loss_ == TRON_LOSS_LOGISTIC ? kLossLogistic : kLossSvm;

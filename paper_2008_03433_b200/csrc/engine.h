@@ -326,6 +326,7 @@ class Engine {
   bool replica_check_ = false;
   DevBuf<double> rc_;
   void check_replicas(double f, double delta, uint64_t iter);
+  bool gram_cg_loop_ = false;  // Gram mode: the whole CG loop is one kernel (cg_small_gram_loop)
   bool gram_delta_ = false;  // L2-SVM, n <= 40: G = G(other slot) + the rows that changed side
   bool gram_first_fused_ = false;  // delta mode: a solve's first margin pass forms G whole (PM_FWDG)
   bool gram_full_next_ = false;    // ... armed by solve_device for its starting point

@@ -364,6 +364,10 @@ void gram_hv(int64_t n, const double* G, const double* v, double scale, double* 
 // M_j = 1 + scale * G_jj (loss.cpp:176-188)
 void gram_precond(int64_t n, const double* G, double scale, double* M, cudaStream_t s);
 // The small-n CG step with hp = p + scale * G p formed first.
+// Gram mode, n <= 64: every iteration of the CG (after cg_small_init) in one
+// launch, G in shared memory; leaves st / cond as the last step would.
+void cg_small_gram_loop(const CgVectors& v, const double* G, double scale, CgState* st, Cond cond,
+                        cudaStream_t s);
 void cg_small_step_gram(const CgVectors& v, const double* G, double scale, CgState* st, Cond cond,
                         cudaStream_t s);
 

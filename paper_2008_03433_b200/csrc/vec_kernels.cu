@@ -436,17 +436,13 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_init_kernel(CgVectors v,
   if (!s_cont) small_finish(v, st, sh);
 }
 
+// One CG iteration of the small engine (tron.cpp:64-106) on one block:
+// hp (from G, or the per-CTA Hv partials), p.Hp, the step, the boundary case,
+// r, beta, p; returns whether the CG continues.
 template <int SPLIT>
-__global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
-                                                                    const double* partials,
-                                                                    int nparts, double scale,
-                                                                    CgState* st, Cond cond,
-                                                                    const double* gram) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double sh[kSmallBlock / kWarp + 1];
-  __shared__ double s_part[kSmallBlock];
-  __shared__ int s_flag;
+__device__ __forceinline__ bool small_step(CgVectors v, const double* partials, int nparts, double scale,
+                                           CgState* st, Cond cond, const double* gram, double* sh,
+                                           double* s_part, int* s_flag) {
   const long long n = v.n;
   if (gram) {
     // hp = p + scale * G p (gram.cu: the dense Hessian of the committed iterate)
@@ -482,8 +478,8 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
   if (threadIdx.x == 0) {
     st->iters += 1;
     st->php = php;
-    s_flag = !(php > 0.0);
-    if (s_flag) {
+    (*s_flag) = !(php > 0.0);
+    if ((*s_flag)) {
       st->fail = 1;
       st->cont = 0;
       set_cond(cond, 0);
@@ -492,7 +488,7 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
     }
   }
   __syncthreads();
-  if (s_flag) return;
+  if ((*s_flag)) return false;
   const double alpha = st->alpha;
   double dd = 0.0;
   for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
@@ -533,7 +529,7 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
     }
     __syncthreads();
     small_finish(v, st, sh);
-    return;
+    return false;
   }
   double rz = 0.0, rr = 0.0;
   for (long long j = threadIdx.x; j < n; j += kSmallBlock) {
@@ -554,12 +550,47 @@ __global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
     st->rz = rz;
     st->rnorm = sqrt(rr);
     st->exit_kind = kCgMaxIters;
-    s_flag = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
-    st->cont = s_flag;
-    set_cond(cond, s_flag);
+    (*s_flag) = (st->iters < st->max_iters) && !(st->rnorm <= st->stop);
+    st->cont = (*s_flag);
+    set_cond(cond, (*s_flag));
   }
   __syncthreads();
-  if (!s_flag) small_finish(v, st, sh);
+  if (!(*s_flag)) small_finish(v, st, sh);
+  return (*s_flag) != 0;
+}
+
+template <int SPLIT>
+__global__ void __launch_bounds__(kSmallBlock) cg_small_step_kernel(CgVectors v,
+                                                                    const double* partials,
+                                                                    int nparts, double scale,
+                                                                    CgState* st, Cond cond,
+                                                                    const double* gram) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double sh[kSmallBlock / kWarp + 1];
+  __shared__ double s_part[kSmallBlock];
+  __shared__ int s_flag;
+  small_step<SPLIT>(v, partials, nparts, scale, st, cond, gram, sh, s_part, &s_flag);
+}
+
+// Gram mode (n <= 64): the whole CG loop in one launch -- G staged in shared
+// memory once, then iterations until the step says stop (the WHILE node
+// around it then runs once); the iterations are those of cg_small_step_kernel.
+__global__ void __launch_bounds__(kSmallBlock) cg_small_gram_loop_kernel(CgVectors v, double scale,
+                                                                         CgState* st, Cond cond,
+                                                                         const double* gram) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double sh[kSmallBlock / kWarp + 1];
+  __shared__ double s_part[kSmallBlock];
+  __shared__ int s_flag;
+  __shared__ double sG[64 * 64];
+  const long long nn = v.n * v.n;
+  for (long long e = threadIdx.x; e < nn; e += kSmallBlock) sG[e] = gram[e];
+  __syncthreads();
+  if (!st->cont) return;  // (the init found r already small enough)
+  while (small_step<8>(v, nullptr, 0, scale, st, cond, sG, sh, s_part, &s_flag)) {
+  }
 }
 
 }  // namespace
@@ -907,6 +938,11 @@ void cg_small_step(const CgVectors& v, const double* partials, int nparts, doubl
   else
     launch_pdl(cg_small_step_kernel<1>, dim3(1), dim3(kSmallBlock), 0, s, v, partials, nparts, scale,
                st, cond, no_gram);
+}
+
+void cg_small_gram_loop(const CgVectors& v, const double* G, double scale, CgState* st, Cond cond,
+                        cudaStream_t s) {
+  launch_pdl(cg_small_gram_loop_kernel, dim3(1), dim3(kSmallBlock), 0, s, v, scale, st, cond, G);
 }
 
 void cg_small_step_gram(const CgVectors& v, const double* G, double scale, CgState* st, Cond cond,
