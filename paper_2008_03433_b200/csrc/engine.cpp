@@ -959,7 +959,10 @@ void Engine::forward(Slot& S) {
 }
 
 void Engine::replica_checksum_host(double out4[4]) {
-  if (!rc_.p) rc_.alloc(8);
+  if (!rc_.p) {
+    AllocScope scope(s_);
+    rc_.alloc(8);
+  }
   replica_checksum(n_, slot_[cand_ ^ 1].w.p, 0.0, 0.0, rc_.p, s_);
   double h[8];
   cuda_check(cudaMemcpyAsync(h, rc_.p, sizeof(h), cudaMemcpyDeviceToHost, s_), "D2H");
@@ -973,7 +976,10 @@ void Engine::replica_checksum_host(double out4[4]) {
 // (exact in doubles), which every rank evaluates on the same sums.
 void Engine::check_replicas(double f, double delta, uint64_t iter) {
   if (!replica_check_ || !comm_.active() || colpart_) return;  // (column shards hold different w)
-  if (!rc_.p) rc_.alloc(8);
+  if (!rc_.p) {
+    AllocScope scope(s_);
+    rc_.alloc(8);
+  }
   replica_checksum(n_, slot_[cand_ ^ 1].w.p, f, delta, rc_.p, s_);
   comm_.allreduce_sum(rc_.p, 8, s_);
   double h[8];
