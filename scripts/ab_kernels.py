@@ -8,7 +8,7 @@ sys.path.insert(0, ROOT)
 from paper_2008_03433_b200 import ExecutionPlan, LossKind, TrustRegionConfig, make_evaluator, synth
 W = sys.argv[1]
 tag = sys.argv[2] if len(sys.argv) > 2 else ""
-p = synth.make_shape(W)
+p = synth.make_shape(W, rows=int(os.environ["ROWS"]) if os.environ.get("ROWS") else None)
 loss = LossKind.Logistic if synth.SHAPES[W]["loss"] == "logistic" else LossKind.L2Svm
 with make_evaluator(p, loss, ExecutionPlan.gpu()) as ev:
     cfg = TrustRegionConfig(eps=0.01)
