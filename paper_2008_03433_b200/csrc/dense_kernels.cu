@@ -4,11 +4,12 @@
 // multiple of 256 rows, padding zeroed).  Every pass is one stream over X
 // through a TMA bulk-copy pipeline:
 //
-//  * a persistent CTA (one per SM) walks 256-row tiles t = blockIdx.x,
+//  * a persistent 8-warp CTA (one per SM) walks 256-row tiles t = blockIdx.x,
 //    blockIdx.x + gridDim.x, ...;
-//  * warp 0 issues one `cp.async.bulk` per column (2 KB contiguous each)
-//    plus the per-row side arrays the pass needs (y, D, mask, ...) into a
-//    shared-memory stage, completing on that stage's mbarrier;
+//  * thread 0 issues one 2-D tensor-map box (the tile's rows x n columns)
+//    plus bulk copies of the per-row side arrays the pass needs (y, D, mask,
+//    ...) into a shared-memory stage, completing on that stage's mbarrier, and
+//    refills a stage as soon as every warp has released it;
 //  * 2-4 stages are in flight, so the bytes outstanding per SM are set by
 //    shared memory (80-160 KB), not by registers -- the limiter of the
 //    register-blocked thread-per-row kernel this replaces (255 regs, 12%
@@ -24,7 +25,9 @@
 //
 // The margin pass also accumulates the gradient partials of the candidate
 // (loss.cpp:74-80 / :129-137) -- free under the HBM bound -- so commit()
-// never re-reads X.
+// never re-reads X; in Gram mode it also forms the whole Gram matrix (FWDG,
+// a solve's starting point) or adds the rows that changed side to the
+// committed one (FWDD, every candidate: gram.cu).
 #include "common.cuh"
 #include "kernels.h"
 

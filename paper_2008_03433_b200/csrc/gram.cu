@@ -4,11 +4,13 @@
 // and logistic_hessian_vec (loss.cpp:82-92) out = v + C sum_i D_i (x_i . v) x_i:
 // both are v + s G v with G = sum_i c_i x_i x_i^T (c = the active-set mask or D)
 // fixed between commits.  For the tall-skinny dense problems (P1 / Q1: n = 40,
-// l = 2.3e7 / 2.15e8) G is formed once per commit -- one pass over X, on the
-// FP64 FMA pipes -- and every Hessian product of the truncated CG becomes a
-// 40 x 40 matrix-vector product inside the CG step kernel: the 25 passes over
-// X of a P1 solve become 4.  The preconditioner diagonal (loss.cpp:176-188) is
-// 1 + s G_jj.
+// l = 2.3e7 / 2.15e8) G is formed once per commit on the FP64 tensor cores,
+// and every Hessian product of the truncated CG becomes a 40 x 40
+// matrix-vector product inside the CG kernel (cg_small_gram_loop): the 29
+// passes over X of a P1 solve become 4.  For the L2-SVM the margin passes keep
+// G current themselves (dense_kernels.cu FWDG / FWDD + gram_delta_finalize
+// below); gram_kernel serves LR, n > 40 and stale references.  The
+// preconditioner diagonal (loss.cpp:176-188) is 1 + s G_jj.
 //
 // gram_kernel: CTAs stride over 128-row tiles of the column-major X, staged in
 // shared memory (weights applied); the FP64 tensor cores (DMMA m8n8k4) form
