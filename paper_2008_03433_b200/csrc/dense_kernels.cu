@@ -156,9 +156,12 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
   // column-major block (stride kDS = 4 mod 16 doubles: conflict-free DMMA
   // fragment loads), their weights +-1, and the per-warp counts by tile parity
   constexpr int kDR = 64, kDS = kDR + 4;
-  __shared__ double s_cb[FD ? NMAX * kDS : 1];
-  __shared__ double s_cw[FD ? kDR : 1];
+  // (two blocks by tile parity: a tile's rows are multiplied during the next
+  // tile, after its count barrier -- one CTA barrier per tile)
+  __shared__ double s_cb[FD ? 2 : 1][FD ? NMAX * kDS : 1];
+  __shared__ double s_cw[FD ? 2 : 1][FD ? kDR : 1];
   __shared__ int s_cnt[FD ? 2 : 1][FD ? NCW : 1];
+  int pend = 0;  // PM_FWDD: rows (whole k-steps) of the previous tile waiting in its block
   const bool dodelta = FD && !gram_ref_is_empty(a.ref_stale);
   double gacc[FD ? 1 : NP][2];  // (FWDD: dacc below)
 #pragma unroll
@@ -169,6 +172,22 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
   constexpr int NPW = FD ? (NP + NCW - 1) / NCW : 1;
   double dacc[NPW][2];
   int dc1[NPW], dc2[NPW];
+  // the rows of a block (rows4: whole k-steps) times themselves: this warp's pairs
+  auto delta_rows = [&](const double* cb, const double* cw, int rows4) {
+    const int g = lane >> 2, tq = lane & 3;
+    for (int ks = 0; ks < rows4 / 4; ++ks) {
+      const int rr = ks * 4 + tq;
+      const double w = cw[rr];
+#pragma unroll
+      for (int q = 0; q < NPW; ++q) {
+        if (dc1[q] >= 0) {
+          const double fa = w * cb[(dc1[q] * 8 + g) * kDS + rr];
+          const double fb = cb[(dc2[q] * 8 + g) * kDS + rr];
+          dmma8(dacc[q], fa, fb);
+        }
+      }
+    }
+  };
 #pragma unroll
   for (int q = 0; q < NPW; ++q) {
     dacc[q][0] = dacc[q][1] = 0.0;
@@ -212,6 +231,7 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
       }
     }
   } else {
+  long long last_k = 0;
   for (long long k = 0;; ++k) {
     const long long t = blockIdx.x + k * gridDim.x;
     if (t >= ntiles) break;
@@ -295,10 +315,20 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
           fd_pos += w < wid ? c2 : 0;
           fd_tot += c2;
         }
-        if (fd_ch && fd_pos < kDR) {
+        if (fd_tot <= kDR) {  // (else the rounds of part 2)
+          double* cb = s_cb[FD ? (k & 1) : 0];
+          double* cw = s_cw[FD ? (k & 1) : 0];
+          if (fd_ch) {
 #pragma unroll
-          for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + fd_pos] = x[j];  // (zeros beyond n)
-          s_cw[fd_pos] = fd_cdel;
+            for (int j = 0; j < NMAX; ++j) cb[j * kDS + fd_pos] = x[j];  // (zeros beyond n)
+            cw[fd_pos] = fd_cdel;
+          }
+          const int t4 = (fd_tot + 3) & ~3;
+          if (tid < t4 - fd_tot) {  // the last k-step's padding rows: weight 0, finite values
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) cb[j * kDS + fd_tot + tid] = 0.0;
+            cw[fd_tot + tid] = 0.0;
+          }
         }
       }
 #pragma unroll
@@ -328,37 +358,35 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
         }
       }
       if (FD && dodelta) {
-        // part 2: the block's rows times themselves on the FP64 tensor cores,
-        // kDR rows per round (rounds past the first restage their rows from
-        // the tile: the registers are gone by then)
-        const int g = lane >> 2, tq = lane & 3;
-        for (int r0 = 0; r0 < fd_tot; r0 += kDR) {
-          const int nr = fd_tot - r0 < kDR ? fd_tot - r0 : kDR, nr4 = (nr + 3) & ~3;
-          if (r0 > 0 && fd_ch && fd_pos >= r0 && fd_pos < r0 + kDR) {
-            const int q = fd_pos - r0;
+        // part 2: the PREVIOUS tile's block on the FP64 tensor cores (every
+        // warp wrote its rows before this tile's count barrier; the block is
+        // rewritten only after the next one), then this tile's rows wait
+        if (pend > 0) delta_rows(s_cb[FD ? ((k + 1) & 1) : 0], s_cw[FD ? ((k + 1) & 1) : 0], pend);
+        pend = 0;
+        if (fd_tot <= kDR) {
+          pend = (fd_tot + 3) & ~3;
+        } else {
+          // more than kDR rows changed in this tile (rare): rounds now, from the
+          // stage (the registers are gone), with barriers
+          double* cb = s_cb[FD ? (k & 1) : 0];
+          double* cw = s_cw[FD ? (k & 1) : 0];
+          for (int r0 = 0; r0 < fd_tot; r0 += kDR) {
+            const int nr = fd_tot - r0 < kDR ? fd_tot - r0 : kDR, nr4 = (nr + 3) & ~3;
+            if (fd_ch && fd_pos >= r0 && fd_pos < r0 + kDR) {
+              const int q = fd_pos - r0;
 #pragma unroll
-            for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + q] = j < n ? xs[j * T + tid] : 0.0;
-            s_cw[q] = fd_cdel;
-          }
-          if (tid < nr4 - nr) {  // the last k-step's padding rows: weight 0, finite values
-#pragma unroll
-            for (int j = 0; j < NMAX; ++j) s_cb[j * kDS + nr + tid] = 0.0;
-            s_cw[nr + tid] = 0.0;
-          }
-          asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
-          for (int ks = 0; ks < nr4 / 4; ++ks) {
-            const int rr = ks * 4 + tq;
-            const double cw = s_cw[rr];
-#pragma unroll
-            for (int q = 0; q < NPW; ++q) {
-              if (dc1[q] >= 0) {
-                const double fa = cw * s_cb[(dc1[q] * 8 + g) * kDS + rr];
-                const double fb = s_cb[(dc2[q] * 8 + g) * kDS + rr];
-                dmma8(dacc[q], fa, fb);
-              }
+              for (int j = 0; j < NMAX; ++j) cb[j * kDS + q] = j < n ? xs[j * T + tid] : 0.0;
+              cw[q] = fd_cdel;
             }
+            if (tid < nr4 - nr) {
+#pragma unroll
+              for (int j = 0; j < NMAX; ++j) cb[j * kDS + nr + tid] = 0.0;
+              cw[nr + tid] = 0.0;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+            delta_rows(cb, cw, nr4);
+            asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");  // the block is restaged next
           }
-          asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");  // the block is restaged next
         }
       }
     }
@@ -370,6 +398,11 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
       if (lane == 0) issue(k + nstages);
       __syncwarp();
     }
+    last_k = k;
+  }
+  if (FD && dodelta && pend > 0) {  // the last tile's rows
+    asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+    delta_rows(s_cb[FD ? (last_k & 1) : 0], s_cw[FD ? (last_k & 1) : 0], pend);
   }
   }
   __syncthreads();  // all stages consumed; the producer has no copy in flight
