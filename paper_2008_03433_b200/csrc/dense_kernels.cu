@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
   for (long long k = 0;; ++k) {
     const long long t = blockIdx.x + k * gridDim.x;
     if (t >= ntiles) break;
+    int fd_tot_k = 0;  // PM_FWDD: this tile's changed rows
     const int s = (int)(k % nstages);
     mbar_wait_parity(&full[s], (unsigned)((k / nstages) & 1));
     const double* xs = reinterpret_cast<const double*>(smem + (size_t)s * sbytes);
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
           fd_pos += w < wid ? c2 : 0;
           fd_tot += c2;
         }
+        fd_tot_k = fd_tot;
         if (fd_tot <= kDR) {  // (else the rounds of part 2)
           double* cb = s_cb[FD ? (k & 1) : 0];
           double* cw = s_cw[FD ? (k & 1) : 0];
@@ -358,14 +360,9 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
         }
       }
       if (FD && dodelta) {
-        // part 2: the PREVIOUS tile's block on the FP64 tensor cores (every
-        // warp wrote its rows before this tile's count barrier; the block is
-        // rewritten only after the next one), then this tile's rows wait
-        if (pend > 0) delta_rows(s_cb[FD ? ((k + 1) & 1) : 0], s_cw[FD ? ((k + 1) & 1) : 0], pend);
-        pend = 0;
-        if (fd_tot <= kDR) {
-          pend = (fd_tot + 3) & ~3;
-        } else {
+        if (fd_tot > kDR) {
+          if (pend > 0) delta_rows(s_cb[FD ? ((k + 1) & 1) : 0], s_cw[FD ? ((k + 1) & 1) : 0], pend);
+          pend = 0;
           // more than kDR rows changed in this tile (rare): rounds now, from the
           // stage (the registers are gone), with barriers
           double* cb = s_cb[FD ? (k & 1) : 0];
@@ -390,6 +387,11 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
         }
       }
     }
+    int pend_now = 0;  // PM_FWDD: the previous tile's rows, multiplied after this stage's release
+    if (FD && dodelta) {
+      pend_now = pend;
+      pend = fd_tot_k <= kDR ? ((fd_tot_k + 3) & ~3) : 0;
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     if (!kProdWarps && wid == 0 && blockIdx.x + (k + nstages) * gridDim.x < ntiles) {
@@ -398,6 +400,10 @@ __global__ void __launch_bounds__(T + kProdWarps * kWarp, 1)
       if (lane == 0) issue(k + nstages);
       __syncwarp();
     }
+    // PM_FWDD, part 2: the PREVIOUS tile's block on the FP64 tensor cores
+    // (every warp wrote its rows before this tile's count barrier; the block is
+    // rewritten only after the next one), off the stage
+    if (pend_now > 0) delta_rows(s_cb[FD ? ((k + 1) & 1) : 0], s_cw[FD ? ((k + 1) & 1) : 0], pend_now);
     last_k = k;
   }
   if (FD && dodelta && pend > 0) {  // the last tile's rows
