@@ -235,7 +235,10 @@ void cg_large_init(const CgVectors& v, CgState* st, Scratch sc, Cond cond,
 
 // Mid-n CG engine (kSmallCgMaxN < n <= kClusterCgMaxN): one kernel per iteration
 // on a cluster of 8 CTAs (vector phases + scalars; the exit's q(d), ||d|| included).
-constexpr int64_t kClusterCgMaxN = 262144;
+// Beyond ~32k coordinates the cooperative grid step is faster: eight SMs'
+// bandwidth bounds the cluster's vector passes (scripts/cg_engine_sweep.py:
+// n = 47236 0.93 vs 0.89 ms, n = 200000 1.24 vs 0.97 ms per solve).
+constexpr int64_t kClusterCgMaxN = 32768;
 // One large-n CG iteration as a single cooperative kernel (vec_kernels.cu);
 // parts: 8 * cg_coop_grid() doubles.  Ends the loop itself (no post kernel).
 int cg_coop_grid();

@@ -252,7 +252,7 @@ def test_device_cg_matches_host_cg(port, case, precond):
 
 
 # the CG engines on the same mid-size problem: single cluster kernel per step
-# (default for 4096 < n <= 262144), the cooperative large-n step (default above),
+# (default for 4096 < n <= 32768), the cooperative large-n step (default above),
 # and the host-driven loop (no graph), each against the host restatement
 @pytest.mark.parametrize("engine", ["cluster", "coop", "nograph"])
 @pytest.mark.parametrize("precond", [False, True])

@@ -132,7 +132,7 @@ def test_synth_n1_full_size_evaluator(ref):
 
 @pytest.mark.parametrize("loss,precond", [(0, False), (1, False), (1, True)])
 def test_large_n_sparse_solve_cooperative_engine(ref, loss, precond):
-    """n > 262144 runs the cooperative CG step (one grid kernel per
+    """n > 32768 runs the cooperative CG step (one grid kernel per
     iteration, p.Hp from the Hv emission) and the emission-fused gradient
     norm: sparse LR and sparse L2-SVM (indirect strategy), with and without
     the preconditioner, against the reference solver."""
