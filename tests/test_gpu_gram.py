@@ -168,3 +168,24 @@ def test_gram_delta_solve_equals_fresh(monkeypatch, precond):
     assert rel_err(a.objective, b.objective) <= 1e-12
     assert rel_err(a.w, b.w) <= 1e-9
     assert np.array_equal(act_a, act_b)
+
+
+def test_gram_delta_many_rows_change(port):
+    """More than a block of rows (64) changing side in a tile -- the update's
+    round-by-round path: from w = 0 (every row active) to a w that turns about
+    half of the rows inactive, then back; Hv, M and the active set against the
+    oracle after each commit."""
+    n = 40
+    p = synth.synth_dense(12, 30_000, n, decades=0.0)
+    v = synth.testgen_random_vector(9, n, 1.0)
+    w_far = synth.testgen_random_vector(21, n, 2.0)
+    with make_evaluator(p, SVM, ExecutionPlan.gpu()) as ev:
+        for w in (np.zeros(n), w_far, np.zeros(n), 0.5 * w_far):
+            ev.eval_candidate(w)
+            ev.commit()
+            want = port.svm(p, w, v)
+            assert rel_err(ev.hessian_vec(v), want["hv"]) <= 1e-12
+            assert rel_err(ev.precond_diagonal(), want["M"]) <= 1e-12
+            act = ev.committed_state().active
+            assert np.array_equal(act, np.asarray(want["active"]))
+        assert 0.2 < act.size / p.X.rows < 0.9  # (a real change of side happened)
