@@ -313,6 +313,11 @@ int device_sm_count() {
 }
 
 int choose_group(int64_t rows, int64_t nnz) {
+  static const int forced = [] {  // TRON_B200_CSR_G=2/4/8/16/32: A/B of the lanes per row
+    const char* e = std::getenv("TRON_B200_CSR_G");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   const double mean = rows > 0 ? (double)nnz / (double)rows : 0.0;
   if (mean >= 96) return 32;
   if (mean >= 32) return 16;
