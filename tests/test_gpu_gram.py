@@ -189,3 +189,20 @@ def test_gram_delta_many_rows_change(port):
             act = ev.committed_state().active
             assert np.array_equal(act, np.asarray(want["active"]))
         assert 0.2 < act.size / p.X.rows < 0.9  # (a real change of side happened)
+
+
+@pytest.mark.parametrize("rows", [1, 7, 300, 2049])
+def test_gram_delta_small_row_counts(ref, rows):
+    """Fewer rows than one tile, or than one tile per SM (CTAs without a tile),
+    through the whole-G first pass, the updates and the one-launch CG: the solve
+    against the reference solver (counts +-1, objective to 1e-7)."""
+    p = synth.synth_dense(13, rows, 40, decades=0.0)
+    cfg = TrustRegionConfig(eps=1e-3)
+    with make_evaluator(p, SVM, ExecutionPlan.gpu()) as ev:
+        assert ev.mode()["gram_delta"]
+        r = ev.solve(cfg)
+    w_ref, t_ref = ref.solve(p, 1, cfg)
+    assert rel_err(r.objective, t_ref["objective"]) <= 1e-7
+    c = [it.cg_iters for it in r.trace.iterations]
+    cr = [it["cg_iters"] for it in t_ref["iterations"]]
+    assert len(c) == len(cr) and all(abs(x - y) <= 1 for x, y in zip(c, cr)), (c, cr)
