@@ -57,3 +57,27 @@ def test_reference_arm_other_ranks_exit_without_work():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
                          capture_output=True, text=True, env=env, timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_no_collective_after_the_ranks_part():
+    """N > 1: every collective of the own arm happens before rank 0 parts from
+    the others (they wait at the closing barrier).  A max_over_ranks inside
+    rank 0's JSON line once deadlocked every multi-rank run; this reads main()'s
+    source after the split and finds no collective there."""
+    import ast
+    import inspect
+    import bench
+    src = inspect.getsource(bench.main)
+    tree = ast.parse(src)
+    fn = tree.body[0]
+    # the statement `if rank != 0: ... return 0` in main's body
+    split = next(i for i, st in enumerate(fn.body)
+                 if isinstance(st, ast.If) and ast.unparse(st.test).replace(" ", "") == "rank!=0")
+    def collectives(stmts):
+        mod = ast.Module(body=stmts, type_ignores=[])
+        names = [ast.unparse(n.func) for n in ast.walk(mod) if isinstance(n, ast.Call)]
+        return sorted(c for c in names if c in ("max_over_ranks", "barrier") or c.startswith("dist."))
+    # rank 0 after the split: only its side of the closing barrier, the same
+    # calls the other ranks make in the split's branch
+    assert collectives(fn.body[split + 1:]) == collectives(fn.body[split].body)
+    assert collectives(fn.body[split].body) == ["barrier", "dist.destroy_process_group"]
